@@ -1,0 +1,115 @@
+"""ctypes binding of libplexus_b200.so (include/plexus_b200.h).
+
+The library is the product: there is no Python or CPU fallback. Loading
+fails loudly when the shared object is missing; every call raises the
+reference's exception type when the C ABI returns an error.
+"""
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libplexus_b200.so")
+
+PK_OK, PK_ERR_CONTRACT, PK_ERR_CUDA, PK_ERR_NCCL, PK_ERR_MEMORY, PK_ERR_TRAINING = range(6)
+PK_MODE_PARITY, PK_MODE_FAST = 0, 1
+
+
+class ContractError(RuntimeError):
+    """plexuskit::ContractError (common.hpp:16-20)."""
+
+
+class MemoryError_(RuntimeError):
+    """plexuskit::MemoryError (common.hpp:22-26)."""
+
+
+class TrainingError(RuntimeError):
+    """plexuskit::TrainingError (trainer.hpp:26-29)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class NcclError(RuntimeError):
+    pass
+
+
+_ERRORS = {PK_ERR_CONTRACT: ContractError, PK_ERR_CUDA: CudaError, PK_ERR_NCCL: NcclError,
+           PK_ERR_MEMORY: MemoryError_, PK_ERR_TRAINING: TrainingError}
+
+
+class pk_csr(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_uint64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+class pk_csr_owned(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_uint64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+P = C.c_void_p
+I64 = C.c_int64
+U64 = C.c_uint64
+U32 = C.c_uint32
+INT = C.c_int
+DBL = C.c_double
+U64P = C.POINTER(C.c_uint64)
+I64P = C.POINTER(C.c_int64)
+
+# name -> (restype, argtypes); mirrors include/plexus_b200.h
+SIGNATURES = {
+    "pk_last_error": (C.c_char_p, []),
+    "pk_abi_version": (INT, []),
+    "pk_device_sm_count": (INT, [INT]),
+    "pk_spmm_rows_f32": (INT, [C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64, U64P, P]),
+    "pk_spmm_f32": (INT, [C.POINTER(pk_csr), P, I64, I64, I64, P, I64, U64P, P]),
+    "pk_spmm_plan_create": (INT, [C.POINTER(pk_csr), I64, P, C.POINTER(P)]),
+    "pk_spmm_plan_destroy": (INT, [P]),
+    "pk_spmm_plan_rows_f32": (INT, [P, C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64,
+                                    U64P, P]),
+    "pk_spmm_plan_info": (INT, [P, I64P, I64P]),
+    "pk_gemm_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),
+    "pk_relu_forward_f32": (INT, [P, I64, I64, I64, P, I64, P]),
+    "pk_relu_backward_f32": (INT, [P, I64, P, I64, I64, I64, P, I64, P]),
+    "pk_softmax_ce_sums_f32": (INT, [P, I64, I64, I64, P, P, P, I64, P, P]),
+    "pk_scale_by_count_f32": (INT, [P, I64, I64, I64, P, P]),
+    "pk_adam_step_f32": (INT, [P, P, P, P, I64, U64, DBL, DBL, DBL, DBL, P]),
+    "pk_csr_transpose": (INT, [C.POINTER(pk_csr), C.POINTER(pk_csr_owned), P]),
+    "pk_csr_block": (INT, [C.POINTER(pk_csr), I64, I64, I64, I64, C.POINTER(pk_csr_owned), P]),
+    "pk_normalize_adjacency": (INT, [I64, P, U64, INT, C.POINTER(pk_csr_owned), P]),
+    "pk_permute_csr": (INT, [C.POINTER(pk_csr), P, P, C.POINTER(pk_csr_owned), P]),
+    "pk_csr_free": (None, [C.POINTER(pk_csr_owned)]),
+    "pk_permutation_pair_host": (INT, [U64, U64, P, P]),
+    "pk_rmat_edges": (INT, [INT, U64, DBL, DBL, DBL, U64, P, U64P, P]),
+    "pk_rmat_features": (INT, [U64, I64, I64, P, I64, P]),
+    "pk_degree_quantile_labels": (INT, [P, U64, I64, U32, P, P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libplexus_b200.so; raise if it is not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                f"g.build()'` (no CPU fallback exists)")
+        lib_ = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib_, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib_
+    return _lib
+
+
+def call(name, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc not in (None, PK_OK):
+        msg = lib().pk_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, RuntimeError)(msg)
+    return rc

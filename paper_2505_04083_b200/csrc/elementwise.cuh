@@ -1,0 +1,32 @@
+// Internal interface of the fused elementwise kernels (elementwise.cu).
+#pragma once
+
+#include "pk_common.cuh"
+
+namespace pk {
+
+void relu_forward_launch(const float* q, i64 ldq, i64 rows, i64 cols, float* out, i64 ldo,
+                         cudaStream_t st);
+void relu_backward_launch(const float* q, i64 ldq, const float* df, i64 lddf, i64 rows,
+                          i64 cols, float* out, i64 ldo, cudaStream_t st);
+
+struct CeWorkspace {
+  DevBuf<double> partial;
+  DevBuf<u32> bad;  // set when a masked-in label is out of range
+};
+
+// sums = {loss_sum, count, correct} as doubles on the device.
+void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
+                    const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
+                    cudaStream_t st);
+void scale_by_count_launch(float* d, i64 ldd, i64 rows, i64 cols, const double* sums,
+                           cudaStream_t st);
+
+struct AdamScalars {
+  float b1, b2, omb1, omb2, bias1, bias2, lr, eps;
+};
+AdamScalars adam_scalars(u64 step, double lr, double beta1, double beta2, double eps);
+void adam_launch(float* p, const float* g, float* m, float* v, i64 n, const AdamScalars& s,
+                 cudaStream_t st);
+
+}  // namespace pk

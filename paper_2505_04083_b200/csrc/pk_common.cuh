@@ -1,0 +1,117 @@
+// Shared plumbing for the sm_100a kernels: status codes, the thread-local
+// error string behind pk_last_error(), CUDA checks and a small device
+// allocation helper. Exceptions never cross the C ABI: every extern "C"
+// entry point wraps its body in pk_guard().
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "plexus_b200.h"
+
+namespace pk {
+
+using u8 = uint8_t;
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i64 = int64_t;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// Reference ContractError wording (common.hpp:47-49).
+inline void check(bool ok, const std::string& msg) {
+  if (!ok) throw Error(PK_ERR_CONTRACT, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation)
+    throw Error(PK_ERR_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+  throw Error(PK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PK_CUDA(x) ::pk::cuda_check((x), #x)
+#define PK_LAUNCH(what) ::pk::cuda_check(cudaGetLastError(), what)
+
+void set_last_error(const std::string& msg);
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return PK_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return PK_ERR_MEMORY;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return PK_ERR_CUDA;
+  }
+}
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+inline std::string shape(i64 r, i64 c) {
+  return std::to_string(r) + "x" + std::to_string(c);
+}
+
+// Device buffer owned by RAII; used for workspaces.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p, n = o.n;
+    o.p = nullptr, o.n = 0;
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) PK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* release_ownership() {
+    T* q = p;
+    p = nullptr;
+    n = 0;
+    return q;
+  }
+};
+
+inline int sm_count() {
+  static thread_local int cached = -1;
+  if (cached < 0) {
+    int dev = 0;
+    PK_CUDA(cudaGetDevice(&dev));
+    PK_CUDA(cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return cached;
+}
+
+inline unsigned ceil_div(u64 a, u64 b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+}  // namespace pk

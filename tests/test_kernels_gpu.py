@@ -1,0 +1,294 @@
+"""Parity of the sm_100a kernels against the CPU oracle (bit-exact where the
+reference semantics allow it). Calls go through the C ABI
+(libplexus_b200.so) via paper_2505_04083_b200.kernels.
+
+Reference cases mirrored: proj/tests/test_kernels.cpp (identity / row swap /
+flop counter / shape errors / random_csr vs dense / gemm 2x2 / transpose
+flags / relu / cross entropy / masked rows).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ref, restate
+
+pytestmark = pytest.mark.gpu
+
+
+def _k():
+    from paper_2505_04083_b200 import kernels
+    return kernels
+
+
+def random_csr(rows, cols, density, rng):
+    """test_helpers.hpp:31-45 shape of random_csr (numpy RNG; sorted cols)."""
+    mask = rng.random((rows, cols)) < density
+    r, c = np.nonzero(mask)
+    v = rng.uniform(-2, 2, size=r.size).astype(np.float32)
+    rp = np.zeros(rows + 1, np.uint64)
+    np.add.at(rp, r + 1, 1)
+    rp = np.cumsum(rp).astype(np.uint64)
+    return rp, c.astype(np.uint32), v
+
+
+def skewed_csr(rows, cols, rng, hubs=((0, 9000), (7, 5000))):
+    """Power-law-ish rows plus explicit hub rows (RMAT skew)."""
+    lens = np.minimum(rng.zipf(1.6, size=rows), cols).astype(np.int64)
+    for r, l in hubs:
+        if r < rows:
+            lens[r] = min(l, cols)
+    rp = np.zeros(rows + 1, np.uint64)
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate([np.sort(rng.choice(cols, size=l, replace=False)) for l in lens]
+                        ).astype(np.uint32) if lens.sum() else np.zeros(0, np.uint32)
+    v = rng.uniform(-1, 1, size=ci.size).astype(np.float32)
+    return rp, ci, v
+
+
+def dev_csr(rows, cols, rp, ci, v):
+    return _k().DeviceCsr.from_host(rows, cols, rp, ci, v)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_bitwise(got, want):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert got.shape == want.shape
+    diff = np.nonzero(bits(got) != bits(want))
+    assert diff[0].size == 0, f"{diff[0].size} elements differ, first at {tuple(d[0] for d in diff)}"
+
+
+# ---------------------------------------------------------------------------
+# SpMM
+
+def test_spmm_identity_and_row_swap(cuda):
+    k = _k()
+    eye = dev_csr(3, 3, np.array([0, 1, 2, 3]), np.array([0, 1, 2]), np.ones(3, np.float32))
+    x = torch.tensor([[1, 2], [3, 4], [5, 6]], dtype=torch.float32, device=cuda)
+    assert torch.equal(k.spmm(eye, x), x)
+    sw = dev_csr(2, 2, np.array([0, 1, 2]), np.array([1, 0]), np.ones(2, np.float32))
+    x2 = torch.tensor([[1, 2], [3, 4]], dtype=torch.float32, device=cuda)
+    assert k.spmm(sw, x2).tolist() == [[3, 4], [1, 2]]
+
+
+def test_spmm_flops_and_shape_error(cuda):
+    k = _k()
+    a = dev_csr(2, 2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]),
+                np.array([1, 2, 3, 4], np.float32))
+    fl = [0]
+    k.spmm(a, torch.zeros(2, 2, device=cuda), flops=fl)
+    assert fl[0] == 16
+    bad = dev_csr(2, 3, np.array([0, 1, 1]), np.array([2]), np.array([5], np.float32))
+    with pytest.raises(k.ContractError):
+        k.spmm(bad, torch.zeros(2, 2, device=cuda))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 8, 13, 16, 25, 32, 47, 50, 64, 100, 128, 256, 301])
+def test_spmm_bitwise_random(cuda, d):
+    rng = np.random.default_rng(d)
+    rows, cols = 300, 257
+    rp, ci, v = random_csr(rows, cols, 0.08, rng)
+    x = rng.uniform(-1, 1, size=(cols, d)).astype(np.float32)
+    want = restate.spmm_rows(rp, ci, v, x, 0, rows)
+    a = dev_csr(rows, cols, rp, ci, v)
+    got = _k().spmm(a, torch.from_numpy(x).to(cuda)).cpu().numpy()
+    assert_bitwise(got, want)
+
+
+@pytest.mark.parametrize("d,ld", [(50, 52), (100, 100), (128, 132), (13, 16), (47, 48)])
+def test_spmm_bitwise_padded_ld_and_row_range(cuda, d, ld):
+    rng = np.random.default_rng(100 + d)
+    rows, cols = 500, 400
+    rp, ci, v = skewed_csr(rows, cols, rng, hubs=((3, 350),))
+    x = rng.uniform(-1, 1, size=(cols, d)).astype(np.float32)
+    xs = torch.zeros(cols, ld, device=cuda)
+    xs[:, :d] = torch.from_numpy(x).to(cuda)
+    a = dev_csr(rows, cols, rp, ci, v)
+    r0, r1 = 37, 411
+    out = torch.full((r1 - r0, ld), 7.0, device=cuda)
+    fl = [0]
+    _k().spmm_rows(a, xs[:, :d], r0, r1, flops=fl, out=out[:, :d])
+    want = restate.spmm_rows(rp, ci, v, x, r0, r1)
+    assert_bitwise(out[:, :d].cpu().numpy(), want)
+    assert torch.all(out[:, d:] == 7.0)  # padding untouched
+    assert fl[0] == 2 * int(rp[r1] - rp[r0]) * d
+
+
+@pytest.mark.parametrize("d", [16, 50, 100, 128, 256])
+def test_spmm_hub_path_bitwise(cuda, d):
+    """Hub CTAs (cp.async ring + sequential consumer) match the reference
+    chain exactly; force a low threshold so several rows take that path."""
+    rng = np.random.default_rng(7 + d)
+    rows, cols = 2000, 20000
+    rp, ci, v = skewed_csr(rows, cols, rng, hubs=((0, 15000), (5, 9000), (1999, 4097),
+                                                   (1000, 33), (77, 2)))
+    x = rng.uniform(-1, 1, size=(cols, d)).astype(np.float32)
+    a = dev_csr(rows, cols, rp, ci, v)
+    plan = _k().SpmmPlan(a, hub_threshold=30)
+    hubs, thr = plan.info()
+    assert thr == 30 and hubs >= 4
+    xt = torch.from_numpy(x).to(cuda)
+    got = _k().spmm(a, xt, plan=plan).cpu().numpy()
+    want = restate.spmm_rows(rp, ci, v, x, 0, rows)
+    assert_bitwise(got, want)
+    # a row range through the same plan
+    got2 = _k().spmm_rows(a, xt, 3, 1500, plan=plan).cpu().numpy()
+    assert_bitwise(got2, want[3:1500])
+
+
+def test_spmm_matches_reference_binary(cuda):
+    """Against the compiled reference itself (oracle/_ref), not only the
+    restatement."""
+    rng = np.random.default_rng(3)
+    rows, cols, d = 64, 64, 16
+    rp, ci, v = random_csr(rows, cols, 0.15, rng)
+    x = rng.uniform(-1, 1, size=(cols, d)).astype(np.float32)
+    want, fl = ref.spmm_rows(rows, cols, rp, ci, v, x)
+    got = _k().spmm(dev_csr(rows, cols, rp, ci, v), torch.from_numpy(x).to(cuda))
+    assert_bitwise(got.cpu().numpy(), want)
+
+
+def test_spmm_empty_rows_and_zero_extent(cuda):
+    k = _k()
+    a = dev_csr(4, 3, np.array([0, 0, 2, 2, 3]), np.array([0, 2, 1]),
+                np.array([1, 2, 3], np.float32))
+    x = torch.arange(6, dtype=torch.float32, device=cuda).reshape(3, 2)
+    got = k.spmm(a, x).cpu().numpy()
+    assert got.tolist() == [[0, 0], [0 + 8, 1 + 10], [0, 0], [6, 9]]
+    z = k.spmm(a, torch.zeros(3, 0, device=cuda))
+    assert tuple(z.shape) == (4, 0)
+    e = dev_csr(0, 3, np.array([0]), np.zeros(0, np.uint32), np.zeros(0, np.float32))
+    assert tuple(k.spmm(e, x).shape) == (0, 2)
+
+
+# ---------------------------------------------------------------------------
+# GEMM
+
+def test_gemm_known_answers(cuda):
+    k = _k()
+    b1 = torch.tensor([[1, 2], [3, 4]], dtype=torch.float32, device=cuda)
+    b2 = torch.tensor([[5, 6], [7, 8]], dtype=torch.float32, device=cuda)
+    assert k.gemm(b1, b2).tolist() == [[19, 22], [43, 50]]
+    a = torch.tensor([[1, 2, 3], [4, 5, 6]], dtype=torch.float32, device=cuda)
+    fl = [0]
+    assert torch.equal(k.gemm(a, torch.eye(3, device=cuda), flops=fl), a)
+    assert fl[0] == 2 * 2 * 3 * 3
+    with pytest.raises(k.ContractError):
+        k.gemm(a, a)
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("m,n,kk", [(5, 7, 4), (130, 47, 100), (67, 256, 129), (1, 1, 1),
+                                    (200, 13, 3000)])
+def test_gemm_parity_bitwise(cuda, ta, tb, m, n, kk):
+    rng = np.random.default_rng(m * 7 + n + kk)
+    a = rng.uniform(-1, 1, size=(kk, m) if ta else (m, kk)).astype(np.float32)
+    b = rng.uniform(-1, 1, size=(n, kk) if tb else (kk, n)).astype(np.float32)
+    want = restate.gemm(a, b, ta, tb)
+    got = _k().gemm(torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda), ta, tb)
+    assert_bitwise(got.cpu().numpy(), want)
+
+
+def test_gemm_tall_reduction_parity(cuda):
+    """dW shape: (dQ^T H)^T with K = adjacency rows (engine.hpp:233-235)."""
+    rng = np.random.default_rng(5)
+    K, f, w = 20000, 50, 24
+    h = rng.uniform(-1, 1, size=(K, f)).astype(np.float32)
+    dq = rng.uniform(-1, 1, size=(K, w)).astype(np.float32)
+    want = restate.gemm(h, dq, True, False)  # serial form H^T dQ
+    got = _k().gemm(torch.from_numpy(h).to(cuda), torch.from_numpy(dq).to(cuda), True, False)
+    assert_bitwise(got.cpu().numpy(), want)
+    want_rw, _ = ref.gemm(dq, h, True, False)  # engine rewrite (dQ^T H), transposed
+    assert_bitwise(got.cpu().numpy(), want_rw.T)
+
+
+def test_gemm_fast_mode_tolerance(cuda):
+    k = _k()
+    rng = np.random.default_rng(9)
+    for (m, n, kk, ta, tb) in [(4096, 128, 100, False, False), (256, 47, 30000, True, False),
+                               (5000, 100, 256, False, True)]:
+        a = rng.uniform(-1, 1, size=(kk, m) if ta else (m, kk)).astype(np.float32)
+        b = rng.uniform(-1, 1, size=(n, kk) if tb else (kk, n)).astype(np.float32)
+        want = (a.T.astype(np.float64) if ta else a.astype(np.float64)) @ (
+            b.T.astype(np.float64) if tb else b.astype(np.float64))
+        got = k.gemm(torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda), ta, tb,
+                     mode=k.PK_MODE_FAST).cpu().numpy().astype(np.float64)
+        rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+        assert rel <= 1e-5, (m, n, kk, ta, tb, rel)
+
+
+def test_gemm_zero_k_writes_zeros(cuda):
+    k = _k()
+    out = k.gemm(torch.zeros(13, 0, device=cuda), torch.zeros(7, 0, device=cuda), False, True)
+    assert tuple(out.shape) == (13, 7) and torch.count_nonzero(out) == 0
+
+
+# ---------------------------------------------------------------------------
+# elementwise
+
+def test_relu_bitwise(cuda):
+    k = _k()
+    rng = np.random.default_rng(1)
+    q = rng.uniform(-1, 1, size=(333, 47)).astype(np.float32)
+    q[0, :3] = [0.0, -0.0, np.float32(1e-45)]
+    df = rng.uniform(-1, 1, size=q.shape).astype(np.float32)
+    qt, dft = torch.from_numpy(q).to(cuda), torch.from_numpy(df).to(cuda)
+    assert_bitwise(k.relu_forward(qt).cpu().numpy(), restate.relu_forward(q))
+    assert_bitwise(k.relu_backward(qt, dft).cpu().numpy(), restate.relu_backward(q, df))
+    with pytest.raises(k.ContractError):
+        k.relu_backward(qt, torch.zeros(2, 2, device=cuda))
+
+
+def test_cross_entropy_known_answer(cuda):
+    k = _k()
+    logits = torch.zeros(1, 2, device=cuda)
+    loss, dl = k.softmax_cross_entropy(logits, torch.tensor([0], dtype=torch.int32, device=cuda),
+                                       torch.tensor([1], dtype=torch.uint8, device=cuda))
+    assert abs(loss - np.log(2.0)) <= 1e-7
+    assert dl.cpu().tolist() == [[-0.5, 0.5]]
+    with pytest.raises(k.ContractError):
+        k.softmax_cross_entropy(torch.eye(2, device=cuda),
+                                torch.tensor([0, 1], dtype=torch.int32, device=cuda),
+                                torch.zeros(2, dtype=torch.uint8, device=cuda))
+
+
+@pytest.mark.parametrize("c", [3, 16, 47, 172])
+def test_cross_entropy_vs_oracle(cuda, c):
+    k = _k()
+    rng = np.random.default_rng(c)
+    rows = 4099
+    logits = rng.normal(0, 3, size=(rows, c)).astype(np.float32)
+    logits[5, :] = 1.0  # all ties -> argmax 0
+    labels = rng.integers(0, c, size=rows).astype(np.uint32)
+    mask = (rng.random(rows) < 0.8).astype(np.uint8)
+    ls, cnt, cor, d = restate.ce_sums(logits, labels, mask)
+    s = k.softmax_cross_entropy_sums(torch.from_numpy(logits).to(cuda),
+                                     torch.from_numpy(labels.view(np.int32)).to(cuda),
+                                     torch.from_numpy(mask).to(cuda))
+    assert s.count == cnt and s.correct == cor
+    assert abs(s.loss_sum - ls) / abs(ls) <= 1e-6
+    dg = s.dlogits.cpu().numpy()
+    assert np.linalg.norm(dg - d) / np.linalg.norm(d) <= 1e-6
+    assert np.all(dg[mask == 0] == 0)
+
+
+def test_adam_bitwise(cuda):
+    k = _k()
+    rng = np.random.default_rng(2)
+    shape = (611, 50)
+    p = rng.uniform(-1, 1, size=shape).astype(np.float32)
+    m = np.zeros(shape, np.float32)
+    v = np.zeros(shape, np.float32)
+    pt = torch.from_numpy(p.copy()).to(cuda)
+    st = k.AdamState.like(pt)
+    for step in range(1, 6):
+        g = rng.uniform(-1, 1, size=shape).astype(np.float32)
+        restate.adam_step(p, g, m, v, step)
+        k.adam_step(pt, torch.from_numpy(g).to(cuda), st)
+        assert_bitwise(pt.cpu().numpy(), p)
+        assert_bitwise(st.m.cpu().numpy(), m)
+        assert_bitwise(st.v.cpu().numpy(), v)
