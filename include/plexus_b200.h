@@ -69,6 +69,8 @@ typedef struct pk_csr_owned {
 
 const char* pk_last_error(void);
 int pk_abi_version(void);
+/* total kernels launched by this library in the process (evidence counter) */
+uint64_t pk_kernel_launch_count(void);
 int pk_device_sm_count(int device);
 
 /* ------------------------------------------------------------------ */
@@ -186,6 +188,95 @@ int pk_rmat_features(uint64_t seed, int64_t n, int64_t d, float* out,
 int pk_degree_quantile_labels(const uint32_t* edges_uv, uint64_t num_edges,
                               int64_t n, uint32_t classes, uint32_t* labels,
                               void* stream);
+
+/* ------------------------------------------------------------------ */
+/* 3D-parallel GCN engine: one per rank (one per GPU)                   */
+/*                                                                     */
+/* Replaces the per-rank body of train_distributed (trainer.hpp:562-633):*/
+/* RankTensors slicing (trainer.hpp:234-250), weight/feature slices      */
+/* (model.hpp:35-67), forward_layer / backward_layer (engine.hpp:158-259),*/
+/* rank_forward_backward (trainer.hpp:478-527) and Adam (598-599).       */
+/* Collectives run on NCCL per-axis communicators (Cluster/RankCtx,      */
+/* cluster.hpp:198-403, in-process threads in the reference).            */
+
+#define PK_MAX_LAYERS 15
+
+typedef struct pk_engine pk_engine;
+
+typedef struct pk_engine_config {
+  int gx, gy, gz;     /* GridConfig (grid.hpp:39-102)                   */
+  int rank;           /* x fastest-varying (grid.hpp:58-63)             */
+  int device;         /* CUDA device this rank runs on                  */
+  int num_layers;     /* L                                              */
+  int64_t dims[PK_MAX_LAYERS + 1]; /* model_dims (trainer.hpp:51-59)    */
+  int64_t n;          /* nodes                                          */
+  uint64_t seed;      /* TrainOptions.seed: weight init (model.hpp:17)  */
+  double lr, beta1, beta2, eps;    /* AdamParams (model.hpp:69-74)       */
+  int block_count;    /* EngineOptions.block_count, 0 = auto            */
+  int mode;           /* pk_mode of the dense transforms                */
+  int fault_epoch;    /* TrainOptions.fault_epoch (-1 = none)           */
+  int64_t hub_threshold; /* SpMM hub rows (0 = automatic)               */
+} pk_engine_config;
+
+/* PreprocessedDataset<float> (graph.hpp:327-350). Device pointers for
+ * pk_engine_load, host pointers for pk_engine_load_host. */
+typedef struct pk_dataset_view {
+  int64_t n;
+  int64_t feat_dim;
+  uint32_t num_classes;
+  pk_csr a_even, a_odd;       /* n x n, permuted (graph.hpp:133-148)      */
+  const float* features;      /* n x feat_dim, col_perm order             */
+  int64_t ld_features;
+  const uint32_t* labels_row; /* labels_row_order / labels_col_order      */
+  const uint32_t* labels_col;
+  const uint8_t* mask_row;
+  const uint8_t* mask_col;
+} pk_dataset_view;
+
+/* EpochMetrics (trainer.hpp:40-49); phase seconds are device time of this
+ * rank (CUDA events), byte counters use the reference's ring model. */
+typedef struct pk_epoch_metrics {
+  int epoch;
+  double loss, accuracy;
+  double forward_spmm_s, forward_gemm_s, backward_s, optimizer_s, collectives_s;
+  double epoch_s;
+  double spmm_s;        /* device time of all SpMM launches (fwd + bwd)  */
+  double spmm_bytes;    /* their algorithmic bytes (SURVEY 8d formula)    */
+  uint64_t kernel_launches; /* libplexus kernels launched in the epoch    */
+  uint64_t spmm_flops, gemm_flops;
+  double allreduce_bytes, allgather_bytes, reducescatter_bytes;
+} pk_epoch_metrics;
+
+typedef struct pk_tensor_view {
+  float* data;
+  int64_t rows, cols, ld;
+} pk_tensor_view;
+
+/* which tensor pk_engine_tensor returns */
+enum {
+  PK_T_W = 0,      /* stored W shard of layer l (weight_slice)           */
+  PK_T_DW = 1,     /* dW shard of the last pass                          */
+  PK_T_F0 = 2,     /* trainable feature shard (feature_slice)            */
+  PK_T_DF0 = 3,    /* its gradient                                       */
+  PK_T_FOUT = 4,   /* last layer's raw logits shard (RankPass.f_out)     */
+  PK_T_H = 5,      /* cached H of layer l (valid after forward)          */
+  PK_T_Q = 6       /* cached Q of layer l                                */
+};
+
+/* 128-byte ncclUniqueId for rank 0 to broadcast (any bootstrap works). */
+int pk_nccl_unique_id(void* out128);
+int pk_engine_create(const pk_engine_config* cfg, pk_engine** out);
+/* world_size 1 needs no call; otherwise every rank passes rank 0's id. */
+int pk_engine_comm_init(pk_engine* e, const void* unique_id128, int world_size);
+int pk_engine_load(pk_engine* e, const pk_dataset_view* ds);
+int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds_host);
+int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss_host,
+                               double* accuracy_host);
+int pk_engine_optimizer_step(pk_engine* e);
+int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* out_host);
+int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out);
+int pk_engine_stream(pk_engine* e, void** stream_out);
+int pk_engine_destroy(pk_engine* e);
 
 #ifdef __cplusplus
 }

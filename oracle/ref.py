@@ -214,6 +214,14 @@ class Pre(_Handle):
             out["features"] = f
         return out
 
+    def epoch_sample(self, hidden, rows, threads):
+        """ref_epoch_sample: (estimated full-epoch seconds, sampled wall seconds)."""
+        hid = np.asarray(hidden, np.uint64)
+        out = np.zeros(2)
+        _check(lib().ref_epoch_sample(self.h, _p(hid), C.c_int(len(hidden)), C.c_uint64(rows),
+                                      C.c_int(threads), _p(out)))
+        return float(out[0]), float(out[1])
+
     def distributed_pass(self, grid, hidden=(128, 128), seed=0, block_count=0):
         i = self.info()
         dims = [i["feat"], *hidden, i["classes"]]

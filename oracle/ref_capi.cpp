@@ -940,4 +940,76 @@ int ref_distributed_pass(void* pre, int gx, int gy, int gz, const u64* hidden,
   });
 }
 
+// ---------------------------------------------------------------------------
+// CPU baseline sampler (bench.py): the reference's own per-layer ops of one
+// 1x1x1 training epoch (SerialTrainer::forward_backward + adam_step,
+// trainer.hpp:137-176; same op list as train_distributed on 1x1x1) timed on
+// a bounded sample of `rows` consecutive rows per thread, `threads` threads
+// on disjoint row blocks, every op linear in the rows it touches. The
+// backward aggregation uses A^T = the other permutation variant, which holds
+// exactly for the symmetric (undirected) normalized adjacency
+// (P_r A P_c^T)^T = P_c A P_r^T. Returns the wall seconds of the sampled
+// region; out[0] = estimated full-epoch seconds = wall * n / (threads*rows).
+int ref_epoch_sample(void* pre, const u64* hidden, int nh, u64 rows, int threads,
+                     double* out) {
+  auto* p = static_cast<Pre*>(pre);
+  return guarded([&] {
+    check(!p->f64, "ref_epoch_sample: float datasets only");
+    auto& d = p->f;
+    std::vector<std::size_t> dims{d.feat_dim};
+    for (int i = 0; i < nh; ++i) dims.push_back(hidden[i]);
+    dims.push_back(d.num_classes);
+    const int L = static_cast<int>(dims.size()) - 1;
+    const std::size_t n = d.n;
+    std::size_t dmax = 0;
+    for (auto x : dims) dmax = std::max(dmax, x);
+    // one shared dense operand at the widest width; the narrower layers read
+    // its leading columns (content does not change the op cost)
+    auto x_full = DenseMatrix<float>::zeros(n, dmax);
+    for (std::size_t i = 0; i < x_full.size(); ++i) x_full.data()[i] = 0.001f * (i % 997);
+    std::vector<DenseMatrix<float>> xs;
+    for (int l = 0; l < L; ++l) xs.push_back(x_full.block(0, n, 0, dims[l]));
+    x_full = DenseMatrix<float>();
+    auto ws = init_weights<float>(dims, 0);
+    std::vector<u32> labels(rows, 0);
+    std::vector<u8> mask(rows, 1);
+    AdamParams ap;
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&, t] {
+        const std::size_t r0 = (static_cast<std::size_t>(t) * rows) % (n > rows ? n - rows : 1);
+        const std::size_t r1 = std::min(n, r0 + rows);
+        std::vector<DenseMatrix<float>> h(L), q(L);
+        for (int l = 0; l < L; ++l) {
+          const auto& a = l % 2 ? d.a_odd : d.a_even;
+          h[l] = spmm_rows(a, xs[l], r0, r1);
+          q[l] = gemm(h[l], ws[l]);
+          if (l + 1 < L) q[l] = relu_forward(q[l]);
+        }
+        auto sums = softmax_cross_entropy_sums(
+            q[L - 1], std::vector<u32>(labels.begin(), labels.begin() + (r1 - r0)),
+            std::vector<u8>(mask.begin(), mask.begin() + (r1 - r0)));
+        DenseMatrix<float> df = std::move(sums.dlogits);
+        for (int l = L - 1; l >= 0; --l) {
+          auto dq = l == L - 1 ? df : relu_backward(q[l], df);
+          auto dw = gemm(dq, h[l], true, false).transposed();
+          auto dh = gemm(dq, ws[l], false, true);
+          const auto& at = l % 2 ? d.a_even : d.a_odd;
+          df = spmm_rows(at, xs[l], r0, r1);
+          (void)dw;
+          (void)dh;
+        }
+        auto f0 = d.features.block(r0, r1, 0, dims[0]);
+        auto st = AdamState<float>::like(f0);
+        adam_step(f0, df, st, ap);
+      });
+    for (auto& th : pool) th.join();
+    const double wall =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    out[0] = wall * static_cast<double>(n) / (static_cast<double>(threads) * rows);
+    out[1] = wall;
+  });
+}
+
 }  // extern "C"

@@ -62,6 +62,7 @@ I64P = C.POINTER(C.c_int64)
 SIGNATURES = {
     "pk_last_error": (C.c_char_p, []),
     "pk_abi_version": (INT, []),
+    "pk_kernel_launch_count": (U64, []),
     "pk_device_sm_count": (INT, [INT]),
     "pk_spmm_rows_f32": (INT, [C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64, U64P, P]),
     "pk_spmm_f32": (INT, [C.POINTER(pk_csr), P, I64, I64, I64, P, I64, U64P, P]),
@@ -105,6 +106,16 @@ def lib():
             fn.argtypes = args
         _lib = lib_
     return _lib
+
+
+def register(sigs):
+    """Add signatures declared by another module (applied now if loaded)."""
+    SIGNATURES.update(sigs)
+    if _lib is not None:
+        for name, (res, args) in sigs.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
 
 
 def call(name, *args):

@@ -2,6 +2,7 @@
 // Each validates shapes with the reference's error wording, then launches.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <string>
 
 #include "elementwise.cuh"
@@ -18,6 +19,12 @@ thread_local std::string g_last_error;
 }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
+std::atomic<u64> g_launches{0};
+}
+u64 count_launch() { return g_launches.fetch_add(1, std::memory_order_relaxed) + 1; }
+u64 launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 SideStream& side_stream() {
   struct Holder {
@@ -98,6 +105,8 @@ extern "C" {
 const char* pk_last_error(void) { return g_last_error.c_str(); }
 
 int pk_abi_version(void) { return 1; }
+
+uint64_t pk_kernel_launch_count(void) { return g_launches.load(); }
 
 int pk_device_sm_count(int device) {
   int n = 0;

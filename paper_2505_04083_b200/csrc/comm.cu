@@ -1,0 +1,168 @@
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+
+#include "comm.cuh"
+
+namespace pk {
+
+namespace {
+
+// out[r, off_j + c] = stage_j[r, c] for member blocks stacked in `stage`
+__global__ void pack_cols_kernel(const float* __restrict__ stage, i64 rows, i64 total_cols,
+                                 int g, float* __restrict__ out, i64 ld_out) {
+  const i64 n = rows * total_cols;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = i / total_cols, c = i % total_cols;
+    // locate the member owning column c (ceil split)
+    const i64 base = total_cols / g, rem = total_cols % g;
+    int j;
+    i64 c0;
+    if (c < rem * (base + 1)) {
+      j = static_cast<int>(c / (base + 1));
+      c0 = j * (base + 1);
+    } else {
+      j = static_cast<int>(rem + (c - rem * (base + 1)) / base);
+      c0 = j * base + rem;
+    }
+    const i64 cj = j < rem ? base + 1 : base;
+    const i64 blk = rows * c0;  // blocks before j hold rows * c0 floats in total
+    out[r * ld_out + c] = stage[blk + r * cj + (c - c0)];
+  }
+}
+
+__global__ void copy_block_kernel(const float* __restrict__ src, i64 ld_src, i64 rows, i64 cols,
+                                  float* __restrict__ dst, i64 ld_dst) {
+  const i64 n = rows * cols;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    dst[(i / cols) * ld_dst + i % cols] = src[(i / cols) * ld_src + i % cols];
+}
+
+unsigned small_grid(i64 n) {
+  return static_cast<unsigned>(std::max<i64>(1, std::min<i64>((n + 255) / 256, 4096)));
+}
+
+}  // namespace
+
+Comms::~Comms() {
+  for (auto& c : axes_)
+    if (c) ncclCommDestroy(c);
+  if (world_) ncclCommDestroy(world_);
+}
+
+void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
+  grid_ = grid;
+  coords_ = grid.coords_of(rank);
+  check(world_size == grid.size(), "comm init: world size " + std::to_string(world_size) +
+                                       " != grid size " + std::to_string(grid.size()));
+  if (world_size == 1) return;
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  PK_NCCL(ncclCommInitRank(&world_, world_size, id, rank));
+  for (int a = 0; a < 3; ++a) {
+    if (grid.extent(a) == 1) continue;  // singleton: identity, nothing moves
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    PK_NCCL(ncclCommSplit(world_, grid.group_id(a, coords_), coords_.along(a), &axes_[a], &cfg));
+    int n = 0, r = 0;
+    PK_NCCL(ncclCommCount(axes_[a], &n));
+    PK_NCCL(ncclCommUserRank(axes_[a], &r));
+    check(n == grid.extent(a) && r == coords_.along(a), "comm split: inconsistent axis group");
+  }
+}
+
+void Comms::all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaStream_t st) {
+  const int g = grid_.extent(axis);
+  counters.calls[axis][kAllReduce]++;
+  counters.ring_numer[axis][kAllReduce] += 2 * static_cast<u64>(g - 1) * logical_bytes;
+  if (g == 1 || count == 0) return;
+  PK_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, axes_[axis], st));
+}
+
+void Comms::all_reduce_f64(double* buf, i64 count, int axis, cudaStream_t st) {
+  const int g = grid_.extent(axis);
+  counters.calls[axis][kAllReduce]++;  // loss stats are not part of the modeled volume
+  if (g == 1 || count == 0) return;
+  PK_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, axes_[axis], st));
+}
+
+void Comms::all_gather_rows(const float* local, float* out, i64 total_rows, i64 ld, int axis,
+                            i64 logical_cols, cudaStream_t st) {
+  const int g = grid_.extent(axis), pos = coords_.along(axis);
+  counters.calls[axis][kAllGather]++;
+  counters.ring_numer[axis][kAllGather] +=
+      static_cast<u64>(g - 1) * static_cast<u64>(total_rows) * logical_cols * sizeof(float);
+  const i64 own0 = chunk_start(total_rows, g, pos), own_rows = chunk_size(total_rows, g, pos);
+  if (g == 1) {
+    if (local != out && own_rows)
+      PK_CUDA(cudaMemcpyAsync(out, local, own_rows * ld * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  PK_NCCL(ncclGroupStart());
+  for (int j = 0; j < g; ++j) {
+    const i64 off = chunk_start(total_rows, g, j), rows = chunk_size(total_rows, g, j);
+    const float* send = j == pos ? local : out + off * ld;
+    PK_NCCL(ncclBroadcast(send, out + off * ld, rows * ld, ncclFloat32, j, axes_[axis], st));
+  }
+  PK_NCCL(ncclGroupEnd());
+  (void)own0;
+}
+
+void Comms::all_gather_cols(const float* local, i64 ld_in, float* out, i64 ld_out, i64 rows,
+                            i64 total_cols, int axis, float* stage, cudaStream_t st) {
+  const int g = grid_.extent(axis), pos = coords_.along(axis);
+  counters.calls[axis][kAllGather]++;
+  counters.ring_numer[axis][kAllGather] +=
+      static_cast<u64>(g - 1) * static_cast<u64>(rows) * total_cols * sizeof(float);
+  if (rows == 0 || total_cols == 0) return;
+  if (g == 1) {
+    copy_block_kernel<<<small_grid(rows * total_cols), 256, 0, st>>>(local, ld_in, rows,
+                                                                     total_cols, out, ld_out);
+    PK_LAUNCH("gather cols copy");
+    return;
+  }
+  // own block -> its contiguous slot of `stage`, then broadcasts, then pack
+  const i64 my_c0 = chunk_start(total_cols, g, pos), my_c = chunk_size(total_cols, g, pos);
+  if (my_c) {
+    copy_block_kernel<<<small_grid(rows * my_c), 256, 0, st>>>(local, ld_in, rows, my_c,
+                                                               stage + rows * my_c0, my_c);
+    PK_LAUNCH("gather cols stage");
+  }
+  PK_NCCL(ncclGroupStart());
+  for (int j = 0; j < g; ++j) {
+    const i64 c0 = chunk_start(total_cols, g, j), cj = chunk_size(total_cols, g, j);
+    float* slot = stage + rows * c0;
+    PK_NCCL(ncclBroadcast(slot, slot, rows * cj, ncclFloat32, j, axes_[axis], st));
+  }
+  PK_NCCL(ncclGroupEnd());
+  pack_cols_kernel<<<small_grid(rows * total_cols), 256, 0, st>>>(stage, rows, total_cols, g, out,
+                                                                  ld_out);
+  PK_LAUNCH("gather cols pack");
+}
+
+void Comms::reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int axis,
+                                i64 logical_cols, cudaStream_t st) {
+  const int g = grid_.extent(axis), pos = coords_.along(axis);
+  counters.calls[axis][kReduceScatter]++;
+  counters.ring_numer[axis][kReduceScatter] +=
+      static_cast<u64>(g - 1) * static_cast<u64>(rows) * logical_cols * sizeof(float);
+  const i64 own0 = chunk_start(rows, g, pos), own_rows = chunk_size(rows, g, pos);
+  if (g == 1) {
+    if (buf != out && own_rows)
+      PK_CUDA(cudaMemcpyAsync(out, buf + own0 * ld, own_rows * ld * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  PK_NCCL(ncclGroupStart());
+  for (int j = 0; j < g; ++j) {
+    const i64 off = chunk_start(rows, g, j), cnt = chunk_size(rows, g, j);
+    PK_NCCL(ncclReduce(buf + off * ld, j == pos ? out : buf + off * ld, cnt * ld, ncclFloat32,
+                       ncclSum, j, axes_[axis], st));
+  }
+  PK_NCCL(ncclGroupEnd());
+}
+
+}  // namespace pk

@@ -1,0 +1,81 @@
+// Per-axis NCCL communicators and the reference's three collectives
+// (cluster.hpp:265-340) on device buffers, plus the ring-model byte
+// counters of CommStats (cluster.hpp:35-65).
+//
+// One communicator per grid axis, split from the world communicator with
+// color = group_id(axis) and key = coordinate along the axis, so NCCL rank
+// order inside a group is the reference's ascending-coordinate order
+// (grid.hpp:77-93) and row/column concatenation needs no reordering. Ragged
+// ceil-split chunks (layout.hpp:16-26) are handled without padding:
+// all-gather = grouped ncclBroadcast into each member's offset,
+// reduce-scatter = grouped ncclReduce of each member's row chunk. Singleton
+// axes short-circuit like the reference (cluster.hpp:380-386) but still count
+// calls. With two members per axis (every axis of 2x2x2) a sum is a+b = b+a,
+// so results are bit-identical to the reference's ordered combine.
+#pragma once
+
+#include <nccl.h>
+
+#include <array>
+
+#include "layout.h"
+#include "pk_common.cuh"
+
+namespace pk {
+
+inline void nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess || r == ncclInProgress) return;
+  throw Error(PK_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define PK_NCCL(x) ::pk::nccl_check((x), #x)
+
+enum CollOp : int { kAllGather = 0, kAllReduce = 1, kReduceScatter = 2 };
+
+struct CommCounters {
+  u64 calls[3][3] = {};       // [axis][op]
+  u64 ring_numer[3][3] = {};  // g * bytes under the ring model
+};
+
+class Comms {
+ public:
+  Comms() = default;
+  Comms(const Comms&) = delete;
+  Comms& operator=(const Comms&) = delete;
+  ~Comms();
+
+  // world_size == 1: no NCCL at all. Otherwise `uid` is the 128-byte
+  // ncclUniqueId from rank 0.
+  void init(const Grid& grid, int rank, const void* uid, int world_size);
+  bool ready() const { return world_ != nullptr || grid_.size() == 1; }
+  int size(int axis) const { return grid_.extent(axis); }
+  int pos(int axis) const { return coords_.along(axis); }
+
+  // In-place sum over the axis group (cluster.hpp:307-321).
+  void all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaStream_t st);
+  void all_reduce_f64(double* buf, i64 count, int axis, cudaStream_t st);
+  // Row concatenation in coordinate order (cluster.hpp:268-305): member j
+  // contributes chunk_size(total_rows, g, j) rows of width `ld` floats;
+  // `local` may alias out + own offset.
+  void all_gather_rows(const float* local, float* out, i64 total_rows, i64 ld, int axis,
+                       i64 logical_cols, cudaStream_t st);
+  // Column concatenation (trainer.hpp:499): member j holds rows x c_j
+  // (ld_in) with c_j = chunk_size(total_cols, g, j); output rows x total_cols
+  // (ld_out). `stage` must hold rows * total_cols floats.
+  void all_gather_cols(const float* local, i64 ld_in, float* out, i64 ld_out, i64 rows,
+                       i64 total_cols, int axis, float* stage, cudaStream_t st);
+  // Sum over the group, keep this member's row chunk (cluster.hpp:323-340):
+  // buf is rows x ld (clobbered); out receives chunk rows x ld.
+  void reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int axis, i64 logical_cols,
+                           cudaStream_t st);
+
+  CommCounters counters;
+
+ private:
+  ncclComm_t axis_comm(int axis) const { return axes_[axis]; }
+  Grid grid_;
+  Coords coords_;
+  ncclComm_t world_ = nullptr;
+  std::array<ncclComm_t, 3> axes_{nullptr, nullptr, nullptr};
+};
+
+}  // namespace pk

@@ -1,0 +1,618 @@
+// Per-rank GCN engine: device twin of forward_layer / backward_layer
+// (engine.hpp:158-259), rank_forward_backward (trainer.hpp:478-527) and the
+// epoch body of train_distributed (trainer.hpp:586-628).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "engine.cuh"
+#include "gemm.cuh"
+#include "philox.cuh"
+#include "shard_builder.cuh"
+
+namespace pk {
+
+namespace {
+
+i64 pad4(i64 c) { return c <= 0 ? 4 : (c + 3) / 4 * 4; }
+
+// 8 B per nonzero (u32 col + f32 val) + 8 B per row_ptr entry
+// + one gathered feature row per nonzero + one written output row per row.
+double spmm_alg_bytes(i64 rows, u64 nnz, i64 d) {
+  return 8.0 * nnz + 8.0 * (rows + 1) + 4.0 * nnz * d + 4.0 * rows * d;
+}
+
+// Global Glorot init (model.hpp:17-33) then this rank's block.
+std::vector<float> init_weight_block(u64 seed, int l, i64 din, i64 dout, const Slice& s) {
+  const double bound = std::sqrt(6.0 / static_cast<double>(din + dout));
+  PhiloxStream rng(seed, 100 + static_cast<u64>(l));
+  std::vector<float> blk(static_cast<size_t>((s.r1 - s.r0) * (s.c1 - s.c0)));
+  for (i64 i = 0; i < din; ++i)
+    for (i64 j = 0; j < dout; ++j) {
+      const double u = u64_to_unit(rng.next_u64());
+      const float w = static_cast<float>(-bound + (bound - -bound) * u);
+      if (i >= s.r0 && i < s.r1 && j >= s.c0 && j < s.c1)
+        blk[(i - s.r0) * (s.c1 - s.c0) + (j - s.c0)] = w;
+    }
+  return blk;
+}
+
+void upload_block(DMat& m, const float* host, i64 cols, cudaStream_t st) {
+  if (m.rows == 0 || cols == 0) return;
+  PK_CUDA(cudaMemcpy2DAsync(m.p(), m.ld * sizeof(float), host, cols * sizeof(float),
+                            cols * sizeof(float), m.rows, cudaMemcpyHostToDevice, st));
+}
+
+}  // namespace
+
+void DMat::alloc(i64 r, i64 c) {
+  rows = r;
+  cols = c;
+  ld = pad4(c);
+  buf.alloc(static_cast<size_t>(std::max<i64>(1, r) * ld));
+  PK_CUDA(cudaMemset(buf.p, 0, buf.n * sizeof(float)));
+}
+
+AdjShard::~AdjShard() {
+  csr_free(&a);
+  csr_free(&at);
+}
+
+// ---------------------------------------------------------------------------
+// phase clock
+
+cudaEvent_t PhaseClock::get() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    PK_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void PhaseClock::begin(int phase, cudaStream_t st) {
+  if (!enabled) return;
+  open_phase = phase;
+  open_ev = get();
+  PK_CUDA(cudaEventRecord(open_ev, st));
+}
+
+void PhaseClock::end(cudaStream_t st) {
+  if (!enabled || open_phase < 0) return;
+  cudaEvent_t e = get();
+  PK_CUDA(cudaEventRecord(e, st));
+  marks.push_back({open_phase, open_ev, e});
+  open_phase = -1;
+}
+
+void PhaseClock::collect(double out[6]) {
+  for (int i = 0; i < 6; ++i) out[i] = 0;
+  for (auto& m : marks) {
+    PK_CUDA(cudaEventSynchronize(m.b));
+    float ms = 0;
+    PK_CUDA(cudaEventElapsedTime(&ms, m.a, m.b));
+    out[m.phase] += ms * 1e-3;
+  }
+  marks.clear();
+  used = 0;
+}
+
+PhaseClock::~PhaseClock() {
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
+// ---------------------------------------------------------------------------
+
+Engine::Engine(const pk_engine_config& cfg) : cfg_(cfg) {
+  check(cfg.gx >= 1 && cfg.gy >= 1 && cfg.gz >= 1, "grid: all dimensions must be >= 1");
+  check(cfg.num_layers >= 1 && cfg.num_layers <= PK_MAX_LAYERS, "engine: bad layer count");
+  grid_.g[0] = cfg.gx, grid_.g[1] = cfg.gy, grid_.g[2] = cfg.gz;
+  check(cfg.rank >= 0 && cfg.rank < grid_.size(), "grid: rank out of range");
+  PK_CUDA(cudaSetDevice(cfg.device));
+  rank_ = cfg.rank;
+  c_ = grid_.coords_of(rank_);
+  L_ = cfg.num_layers;
+  dims_.assign(cfg.dims, cfg.dims + L_ + 1);
+  for (auto d : dims_) check(d >= 1, "engine: zero layer dimension");
+  lays_ = plan_layouts(L_);
+  for (int l = 0; l < L_; ++l)
+    shapes_.push_back(layer_shapes(grid_, lays_[l], c_, cfg.n, dims_[l], dims_[l + 1]));
+  PK_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  sums_.alloc(4);
+}
+
+Engine::~Engine() {
+  if (st_) {
+    cudaStreamSynchronize(st_);
+    cudaStreamDestroy(st_);
+  }
+}
+
+const AdjShard& Engine::shard(const Layout& l) const {
+  const auto& s = shards_[l.plane() * 2 + l.parity()];
+  check(s != nullptr, "no adjacency shard for plane " + std::to_string(l.plane()) +
+                          " parity " + std::to_string(l.parity()));
+  return *s;
+}
+
+void Engine::load(const pk_dataset_view& dsin, bool host) {
+  PK_CUDA(cudaSetDevice(cfg_.device));
+  check(dsin.n == cfg_.n, "engine load: dataset has " + std::to_string(dsin.n) +
+                              " nodes but the engine was configured for " +
+                              std::to_string(cfg_.n));
+  check(dsin.feat_dim == dims_[0] && static_cast<i64>(dsin.num_classes) == dims_[L_],
+        "engine load: dataset dims do not match the model dims");
+  const i64 n = cfg_.n;
+  // host inputs: stage the whole preprocessed dataset in HBM first
+  pk_dataset_view ds = dsin;
+  DevBuf<u64> erp, orp;
+  DevBuf<u32> eci, oci, lr, lc;
+  DevBuf<float> ev, ov, feat;
+  DevBuf<u8> mr, mc;
+  if (host) {
+    auto up = [&](auto& buf, const auto* src, size_t count) {
+      buf.alloc(count ? count : 1);
+      if (count)
+        PK_CUDA(cudaMemcpyAsync(buf.p, src, count * sizeof(*src), cudaMemcpyHostToDevice, st_));
+      return buf.p;
+    };
+    ds.a_even.row_ptr = up(erp, dsin.a_even.row_ptr, n + 1);
+    ds.a_even.col_idx = up(eci, dsin.a_even.col_idx, dsin.a_even.nnz);
+    ds.a_even.values = up(ev, dsin.a_even.values, dsin.a_even.nnz);
+    ds.a_odd.row_ptr = up(orp, dsin.a_odd.row_ptr, n + 1);
+    ds.a_odd.col_idx = up(oci, dsin.a_odd.col_idx, dsin.a_odd.nnz);
+    ds.a_odd.values = up(ov, dsin.a_odd.values, dsin.a_odd.nnz);
+    feat.alloc(static_cast<size_t>(n * dims_[0]));
+    PK_CUDA(cudaMemcpy2DAsync(feat.p, dims_[0] * sizeof(float), dsin.features,
+                              dsin.ld_features * sizeof(float), dims_[0] * sizeof(float), n,
+                              cudaMemcpyHostToDevice, st_));
+    ds.features = feat.p;
+    ds.ld_features = dims_[0];
+    ds.labels_row = up(lr, dsin.labels_row, n);
+    ds.labels_col = up(lc, dsin.labels_col, n);
+    ds.mask_row = up(mr, dsin.mask_row, n);
+    ds.mask_col = up(mc, dsin.mask_col, n);
+  }
+  // adjacency shards (build_adjacency_shards, engine.hpp:96-113)
+  for (auto [plane, parity] : needed_adjacency_keys(L_)) {
+    const pk_csr& variant = parity ? ds.a_odd : ds.a_even;
+    check(variant.rows == n && variant.cols == n,
+          "build_adjacency_shards: adjacency variants must be square and equal");
+    const Slice r = adjacency_block_range(grid_, plane, c_, n);
+    auto sh = std::make_unique<AdjShard>();
+    csr_block(variant, r.r0, r.r1, r.c0, r.c1, &sh->a, st_);
+    csr_transpose(view(sh->a), &sh->at, st_);
+    spmm_plan_build(sh->plan_a, view(sh->a), static_cast<u64>(cfg_.hub_threshold), st_);
+    spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_);
+    // nnz per forward row block, for the FLOP counters
+    std::vector<u64> rp(sh->a.rows + 1);
+    PK_CUDA(cudaMemcpy(rp.data(), sh->a.row_ptr, rp.size() * sizeof(u64),
+                       cudaMemcpyDeviceToHost));
+    const int blocks = resolve_block_count(cfg_.block_count, sh->a.rows);
+    for (int b = 0; b < blocks; ++b)
+      sh->block_nnz.push_back(rp[chunk_start(sh->a.rows, blocks, b + 1)] -
+                              rp[chunk_start(sh->a.rows, blocks, b)]);
+    sh->nnz_t = sh->at.nnz;
+    shards_[plane * 2 + parity] = std::move(sh);
+  }
+  // trainable features F0 (feature_slice, model.hpp:53-67) + Adam state
+  const Slice fs = feature_slice(grid_, c_, n, dims_[0]);
+  f0_.alloc(fs.r1 - fs.r0, fs.c1 - fs.c0);
+  if (f0_.rows && f0_.cols)
+    PK_CUDA(cudaMemcpy2DAsync(f0_.p(), f0_.ld * sizeof(float),
+                              ds.features + fs.r0 * ds.ld_features + fs.c0,
+                              ds.ld_features * sizeof(float), f0_.cols * sizeof(float), f0_.rows,
+                              cudaMemcpyDeviceToDevice, st_));
+  f0_m_.alloc(f0_.rows, f0_.cols);
+  f0_v_.alloc(f0_.rows, f0_.cols);
+  df0_.alloc(f0_.rows, f0_.cols);
+  f0_step_ = 0;
+  // weights (global init, then weight_slice) + Adam state
+  w_.resize(L_), w_m_.resize(L_), w_v_.resize(L_), dw_.resize(L_);
+  wfull_.resize(L_), dwp_.resize(L_), h_.resize(L_), q_.resize(L_), fout_.resize(L_);
+  i64 max_dq = 1, max_dh = 1, max_df = 1;
+  for (int l = 0; l < L_; ++l) {
+    const Shapes& s = shapes_[l];
+    const Slice ws = weight_slice(grid_, lays_[l], c_, dims_[l], dims_[l + 1]);
+    w_[l].alloc(ws.r1 - ws.r0, ws.c1 - ws.c0);
+    auto blk = init_weight_block(cfg_.seed, l, dims_[l], dims_[l + 1], ws);
+    upload_block(w_[l], blk.data(), w_[l].cols, st_);
+    PK_CUDA(cudaStreamSynchronize(st_));
+    w_m_[l].alloc(w_[l].rows, w_[l].cols);
+    w_v_[l].alloc(w_[l].rows, w_[l].cols);
+    dw_[l].alloc(w_[l].rows, w_[l].cols);
+    wfull_[l].alloc(s.f_cols, s.w_cols);
+    dwp_[l].alloc(s.f_cols, s.w_cols);
+    h_[l].alloc(s.h_rows, s.h_cols);
+    q_[l].alloc(s.q_rows, s.q_cols);
+    if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols);
+    max_dq = std::max(max_dq, s.q_rows * pad4(s.q_cols));
+    max_dh = std::max(max_dh, s.h_rows * pad4(s.h_cols));
+    max_df = std::max(max_df, s.a_cols * pad4(s.f_cols));
+  }
+  w_step_ = 0;
+  f0g_.alloc(shapes_[0].f_rows, shapes_[0].f_cols);
+  dq_.buf.alloc(max_dq);
+  dh_.buf.alloc(max_dh);
+  df_.buf.alloc(max_df);
+  df_prev_.buf.alloc(max_df);
+  PK_CUDA(cudaMemset(dq_.buf.p, 0, dq_.buf.n * sizeof(float)));
+  PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
+  PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
+  PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
+  // labels / mask of this rank's logit rows (trainer.hpp:241-248)
+  const Shapes& sl = shapes_[L_ - 1];
+  const int parity = (L_ - 1) % 2;
+  const auto lr_rng = label_row_range(grid_, c_, n, L_);
+  const i64 lrows = lr_rng.second - lr_rng.first;
+  check(lrows == sl.a_rows, "engine: label rows disagree with the logits shard");
+  labels_.alloc(std::max<i64>(1, lrows));
+  mask_.alloc(std::max<i64>(1, lrows));
+  if (lrows) {
+    PK_CUDA(cudaMemcpyAsync(labels_.p, (parity ? ds.labels_col : ds.labels_row) + lr_rng.first,
+                            lrows * sizeof(u32), cudaMemcpyDeviceToDevice, st_));
+    PK_CUDA(cudaMemcpyAsync(mask_.p, (parity ? ds.mask_col : ds.mask_row) + lr_rng.first, lrows,
+                            cudaMemcpyDeviceToDevice, st_));
+  }
+  logits_.alloc(sl.a_rows, dims_[L_]);
+  dl_.alloc(sl.a_rows, dims_[L_]);
+  stage_.alloc(sl.a_rows, dims_[L_]);
+  // DMat::alloc zeroes on the legacy stream: drain everything before use
+  PK_CUDA(cudaDeviceSynchronize());
+  loaded_ = true;
+}
+
+// ---------------------------------------------------------------------------
+// forward_layer (engine.hpp:158-206)
+
+void Engine::forward_layer(int l, bool fault) {
+  const Layout& lay = lays_[l];
+  const Shapes& s = shapes_[l];
+  const AdjShard& sh = shard(lay);
+  const float* f;
+  i64 ldf;
+  if (l == 0) {
+    // layer-0 input carries the extra row_shard split: gather it
+    clock_.begin(4, st_);
+    comms_.all_gather_rows(f0_.p(), f0g_.p(), s.f_rows, f0g_.ld, lay.row, s.f_cols, st_);
+    clock_.end(st_);
+    f = f0g_.p();
+    ldf = f0g_.ld;
+  } else {
+    f = fout_[l - 1].p();
+    ldf = fout_[l - 1].ld;
+  }
+  check(sh.a.cols == s.f_rows, "forward layer " + std::to_string(l) + ": adjacency shard " +
+                                   shape(sh.a.rows, sh.a.cols) + " does not match features " +
+                                   shape(s.f_rows, s.f_cols));
+  DMat& h = h_[l];
+  const int blocks = resolve_block_count(cfg_.block_count, sh.a.rows);
+  // blocked aggregation: SpMM row block, then its all-reduce along inner
+  for (int b = 0; b < blocks; ++b) {
+    const i64 r0 = chunk_start(sh.a.rows, blocks, b), r1 = chunk_start(sh.a.rows, blocks, b + 1);
+    clock_.begin(0, st_);
+    SpmmArgs args;
+    args.rp = sh.a.row_ptr;
+    args.ci = sh.a.col_idx;
+    args.val = sh.a.values;
+    args.x = f;
+    args.ldx = ldf;
+    args.y = h.p() + r0 * h.ld;
+    args.ldy = h.ld;
+    args.r0 = r0;
+    args.nrows = r1 - r0;
+    auto& plan = const_cast<SpmmPlan&>(sh.plan_a);
+    args.hub_threshold = plan.threshold;
+    args.hub_rows = spmm_plan_range(plan, r0, r1, &args.hub_count, st_);
+    spmm_launch(args, s.f_cols, st_);
+    spmm_flops_ += 2 * sh.block_nnz[b] * static_cast<u64>(s.f_cols);
+    spmm_bytes_ += spmm_alg_bytes(r1 - r0, sh.block_nnz[b], s.f_cols);
+    clock_.end(st_);
+    if (!fault) {
+      clock_.begin(4, st_);
+      comms_.all_reduce(h.p() + r0 * h.ld, (r1 - r0) * h.ld, lay.inner,
+                        (r1 - r0) * s.f_cols * 4, st_);
+      clock_.end(st_);
+    }
+  }
+  clock_.begin(4, st_);
+  comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols, st_);
+  clock_.end(st_);
+  clock_.begin(1, st_);
+  gemm_launch(false, false, s.h_rows, s.w_cols, s.h_cols, h.p(), h.ld, wfull_[l].p(),
+              wfull_[l].ld, q_[l].p(), q_[l].ld, cfg_.mode, st_);
+  gemm_flops_ += 2 * static_cast<u64>(s.h_rows) * s.w_cols * s.h_cols;
+  clock_.end(st_);
+  clock_.begin(4, st_);
+  comms_.all_reduce(q_[l].p(), q_[l].elems(), lay.col, s.q_rows * s.q_cols * 4, st_);
+  clock_.end(st_);
+  if (l + 1 < L_) {
+    clock_.begin(1, st_);
+    relu_forward_launch(q_[l].p(), q_[l].ld, s.q_rows, s.q_cols, fout_[l].p(), fout_[l].ld, st_);
+    clock_.end(st_);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// loss (trainer.hpp:498-516)
+
+void Engine::loss(int epoch, double* loss_out, double* acc_out) {
+  const Layout& last = lays_[L_ - 1];
+  const Shapes& s = shapes_[L_ - 1];
+  const i64 C = dims_[L_];
+  clock_.begin(4, st_);
+  comms_.all_gather_cols(q_[L_ - 1].p(), q_[L_ - 1].ld, logits_.p(), logits_.ld, s.a_rows, C,
+                         last.inner, stage_.p(), st_);
+  clock_.end(st_);
+  clock_.begin(2, st_);
+  ce_sums_launch(logits_.p(), logits_.ld, s.a_rows, C, labels_.p, mask_.p, dl_.p(), dl_.ld,
+                 sums_.p, ce_ws_, st_);
+  clock_.end(st_);
+  clock_.begin(4, st_);
+  comms_.all_reduce_f64(sums_.p, 3, last.row, st_);
+  clock_.end(st_);
+  double h[3];
+  u32 bad = 0;
+  PK_CUDA(cudaMemcpyAsync(h, sums_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  PK_CUDA(cudaMemcpyAsync(&bad, ce_ws_.bad.p, sizeof(u32), cudaMemcpyDeviceToHost, st_));
+  PK_CUDA(cudaStreamSynchronize(st_));
+  check(!bad, "cross entropy: label out of range for " + std::to_string(C) + " classes");
+  // finalize_loss (trainer.hpp:71-89)
+  const u64 count = static_cast<u64>(h[1]), correct = static_cast<u64>(h[2]);
+  if (count == 0)
+    throw Error(PK_ERR_TRAINING,
+                "epoch " + std::to_string(epoch) + ": no nodes selected by the training mask");
+  const double loss = h[0] / static_cast<double>(count);
+  if (!std::isfinite(loss))
+    throw Error(PK_ERR_TRAINING, "epoch " + std::to_string(epoch) + ": loss is not finite (" +
+                                     std::to_string(loss) + ")");
+  *loss_out = loss;
+  *acc_out = static_cast<double>(correct) / static_cast<double>(count);
+  clock_.begin(2, st_);
+  scale_by_count_launch(dl_.p(), dl_.ld, s.a_rows, C, sums_.p, st_);
+  clock_.end(st_);
+}
+
+// ---------------------------------------------------------------------------
+// backward_layer (engine.hpp:214-259)
+
+void Engine::backward_layer(int l) {
+  const Layout& lay = lays_[l];
+  const Shapes& s = shapes_[l];
+  const AdjShard& sh = shard(lay);
+  const bool is_last = l == L_ - 1;
+  // dQ: the loss gradient's own class chunk on the last layer (a strided
+  // view of dlogits: no copy), relu'(Q) * dF otherwise
+  const float* dq;
+  i64 lddq;
+  clock_.begin(2, st_);
+  if (is_last) {
+    const i64 c0 = chunk_start(dims_[L_], comms_.size(lay.inner), c_.along(lay.inner));
+    dq = dl_.p() + c0;
+    lddq = dl_.ld;
+  } else {
+    lddq = pad4(s.q_cols);
+    relu_backward_launch(q_[l].p(), q_[l].ld, df_prev_.p(), pad4(s.q_cols), s.q_rows, s.q_cols,
+                         dq_.p(), lddq, st_);
+    dq = dq_.p();
+  }
+  // dW = (dQ^T H)^T computed as H^T dQ: same products, same k order
+  gemm_launch(true, false, s.h_cols, s.q_cols, s.h_rows, h_[l].p(), h_[l].ld, dq, lddq,
+              dwp_[l].p(), dwp_[l].ld, cfg_.mode, st_);
+  gemm_flops_ += 2 * static_cast<u64>(s.h_cols) * s.q_cols * s.h_rows;
+  clock_.end(st_);
+  clock_.begin(4, st_);
+  comms_.reduce_scatter_rows(dwp_[l].p(), dw_[l].p(), s.f_cols, dwp_[l].ld, lay.row, s.w_cols,
+                             st_);
+  comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
+                         st_);
+  clock_.end(st_);
+  clock_.begin(2, st_);
+  const i64 lddh = pad4(s.h_cols);
+  gemm_launch(false, true, s.q_rows, s.h_cols, s.q_cols, dq, lddq, wfull_[l].p(), wfull_[l].ld,
+              dh_.p(), lddh, cfg_.mode, st_);
+  gemm_flops_ += 2 * static_cast<u64>(s.q_rows) * s.h_cols * s.q_cols;
+  clock_.end(st_);
+  clock_.begin(4, st_);
+  comms_.all_reduce(dh_.p(), s.h_rows * lddh, lay.inner, s.h_rows * s.h_cols * 4, st_);
+  clock_.end(st_);
+  clock_.begin(5, st_);
+  const i64 lddf = pad4(s.f_cols);
+  SpmmArgs args;
+  args.rp = sh.at.row_ptr;
+  args.ci = sh.at.col_idx;
+  args.val = sh.at.values;
+  args.x = dh_.p();
+  args.ldx = lddh;
+  args.y = df_.p();
+  args.ldy = lddf;
+  args.r0 = 0;
+  args.nrows = sh.at.rows;
+  auto& plan = const_cast<SpmmPlan&>(sh.plan_at);
+  args.hub_threshold = plan.threshold;
+  args.hub_rows = spmm_plan_range(plan, 0, sh.at.rows, &args.hub_count, st_);
+  spmm_launch(args, s.f_cols, st_);
+  spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.f_cols);
+  spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.f_cols);
+  clock_.end(st_);
+  clock_.begin(4, st_);
+  if (l == 0) {
+    comms_.reduce_scatter_rows(df_.p(), df0_.p(), s.a_cols, lddf, lay.row, s.f_cols, st_);
+  } else {
+    comms_.all_reduce(df_.p(), s.a_cols * lddf, lay.row, s.a_cols * s.f_cols * 4, st_);
+    std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
+  }
+  clock_.end(st_);
+}
+
+void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
+  check(loaded_, "engine: no dataset loaded");
+  check(comms_.ready(), "engine: communicators not initialised");
+  PK_CUDA(cudaSetDevice(cfg_.device));
+  const bool fault = epoch == cfg_.fault_epoch;
+  for (int l = 0; l < L_; ++l) forward_layer(l, fault);
+  loss(epoch, loss_out, acc_out);
+  for (int l = L_ - 1; l >= 0; --l) backward_layer(l);
+}
+
+void Engine::optimizer_step() {
+  clock_.begin(3, st_);
+  ++w_step_;
+  const AdamScalars sw = adam_scalars(w_step_, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps);
+  for (int l = 0; l < L_; ++l)
+    adam_launch(w_[l].p(), dw_[l].p(), w_m_[l].p(), w_v_[l].p(), w_[l].elems(), sw, st_);
+  ++f0_step_;
+  const AdamScalars sf = adam_scalars(f0_step_, cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.eps);
+  adam_launch(f0_.p(), df0_.p(), f0_m_.p(), f0_v_.p(), f0_.elems(), sf, st_);
+  clock_.end(st_);
+}
+
+void Engine::train_epoch(int epoch, pk_epoch_metrics* m) {
+  CommCounters before = comms_.counters;
+  const u64 sf0 = spmm_flops_, gf0 = gemm_flops_;
+  const double sb0 = spmm_bytes_;
+  const u64 launches0 = launch_count();
+  cudaEvent_t e0 = clock_.get(), e1 = clock_.get();
+  PK_CUDA(cudaEventRecord(e0, st_));
+  double loss = 0, acc = 0;
+  forward_backward(epoch, &loss, &acc);
+  optimizer_step();
+  PK_CUDA(cudaEventRecord(e1, st_));
+  PK_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  PK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  double ph[6];
+  clock_.collect(ph);
+  if (!m) return;
+  std::memset(m, 0, sizeof(*m));
+  m->epoch = epoch;
+  m->loss = loss;
+  m->accuracy = acc;
+  m->forward_spmm_s = ph[0];
+  m->forward_gemm_s = ph[1];
+  m->backward_s = ph[2] + ph[5];
+  m->spmm_s = ph[0] + ph[5];
+  m->spmm_bytes = spmm_bytes_ - sb0;
+  m->kernel_launches = launch_count() - launches0;
+  m->optimizer_s = ph[3];
+  m->collectives_s = ph[4];
+  m->epoch_s = ms * 1e-3;
+  m->spmm_flops = spmm_flops_ - sf0;
+  m->gemm_flops = gemm_flops_ - gf0;
+  for (int a = 0; a < 3; ++a) {
+    const double g = grid_.extent(a);
+    auto delta = [&](int op) {
+      return static_cast<double>(comms_.counters.ring_numer[a][op] - before.ring_numer[a][op]) / g;
+    };
+    m->allreduce_bytes += delta(kAllReduce);
+    m->allgather_bytes += delta(kAllGather);
+    m->reducescatter_bytes += delta(kReduceScatter);
+  }
+}
+
+bool Engine::tensor(int which, int layer, pk_tensor_view* out) {
+  auto fill = [&](const DMat& m, i64 cols) {
+    out->data = m.p();
+    out->rows = m.rows;
+    out->cols = cols;
+    out->ld = m.ld;
+    return true;
+  };
+  const bool lay_ok = layer >= 0 && layer < L_;
+  switch (which) {
+    case PK_T_W: return lay_ok && fill(w_[layer], w_[layer].cols);
+    case PK_T_DW: return lay_ok && fill(dw_[layer], dw_[layer].cols);
+    case PK_T_F0: return fill(f0_, f0_.cols);
+    case PK_T_DF0: return fill(df0_, df0_.cols);
+    case PK_T_FOUT: return fill(q_[L_ - 1], q_[L_ - 1].cols);
+    case PK_T_H: return lay_ok && fill(h_[layer], h_[layer].cols);
+    case PK_T_Q: return lay_ok && fill(q_[layer], q_[layer].cols);
+    default: return false;
+  }
+}
+
+}  // namespace pk
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+struct pk_engine {
+  std::unique_ptr<pk::Engine> e;
+};
+
+using namespace pk;
+
+extern "C" {
+
+int pk_nccl_unique_id(void* out128) {
+  return guard([&] {
+    ncclUniqueId id;
+    PK_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int pk_engine_create(const pk_engine_config* cfg, pk_engine** out) {
+  return guard([&] {
+    check(cfg != nullptr && out != nullptr, "engine: null argument");
+    auto* h = new pk_engine;
+    try {
+      h->e = std::make_unique<Engine>(*cfg);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pk_engine_comm_init(pk_engine* e, const void* uid, int world_size) {
+  return guard([&] { e->e->comm_init(uid, world_size); });
+}
+
+int pk_engine_load(pk_engine* e, const pk_dataset_view* ds) {
+  return guard([&] { e->e->load(*ds, false); });
+}
+
+int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds) {
+  return guard([&] { e->e->load(*ds, true); });
+}
+
+int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss, double* acc) {
+  return guard([&] {
+    double l = 0, a = 0;
+    e->e->forward_backward(epoch, &l, &a);
+    PK_CUDA(cudaStreamSynchronize(e->e->stream()));
+    if (loss) *loss = l;
+    if (acc) *acc = a;
+  });
+}
+
+int pk_engine_optimizer_step(pk_engine* e) {
+  return guard([&] { e->e->optimizer_step(); });
+}
+
+int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* m) {
+  return guard([&] { e->e->train_epoch(epoch, m); });
+}
+
+int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out) {
+  return guard([&] {
+    PK_CUDA(cudaStreamSynchronize(e->e->stream()));
+    check(e->e->tensor(which, layer, out), "engine tensor: unknown tensor or layer");
+  });
+}
+
+int pk_engine_stream(pk_engine* e, void** s) {
+  return guard([&] { *s = e->e->stream(); });
+}
+
+int pk_engine_destroy(pk_engine* e) {
+  return guard([&] { delete e; });
+}
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// The per-rank 3D-parallel GCN engine (engine.hpp:158-259,
+// trainer.hpp:478-627) on one B200. One host thread (or process) drives one
+// Engine; collectives go through Comms (NCCL per-axis communicators).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "comm.cuh"
+#include "elementwise.cuh"
+#include "layout.h"
+#include "pk_common.cuh"
+#include "spmm.cuh"
+
+namespace pk {
+
+// Row-major device matrix with a 16-byte padded leading dimension; the
+// padding is zeroed once and never written, so float4 paths, Adam and the
+// collectives can run over whole rows.
+struct DMat {
+  DevBuf<float> buf;
+  i64 rows = 0, cols = 0, ld = 0;
+  float* p() const { return buf.p; }
+  void alloc(i64 r, i64 c);
+  i64 elems() const { return rows * ld; }
+};
+
+struct AdjShard {
+  pk_csr_owned a{}, at{};
+  SpmmPlan plan_a, plan_at;
+  std::vector<u64> block_nnz;  // nnz of each forward row block
+  u64 nnz_t = 0;
+  ~AdjShard();
+};
+
+struct PhaseClock {
+  // phases: 0 fwd spmm, 1 fwd gemm, 2 backward, 3 optimizer, 4 collectives,
+  // 5 backward spmm (reported inside backward_s, as the reference times it)
+  struct Mark {
+    int phase;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> pool;
+  std::vector<Mark> marks;
+  size_t used = 0;
+  bool enabled = true;
+  cudaEvent_t get();
+  void begin(int phase, cudaStream_t st);
+  void end(cudaStream_t st);
+  void collect(double out[6]);  // syncs, sums seconds per phase, resets
+  ~PhaseClock();
+  int open_phase = -1;
+  cudaEvent_t open_ev = nullptr;
+};
+
+class Engine {
+ public:
+  explicit Engine(const pk_engine_config& cfg);
+  ~Engine();
+
+  void comm_init(const void* uid, int world_size) { comms_.init(grid_, rank_, uid, world_size); }
+  void load(const pk_dataset_view& ds, bool host);
+  // rank_forward_backward (trainer.hpp:478-527): returns loss/accuracy
+  void forward_backward(int epoch, double* loss, double* acc);
+  void optimizer_step();
+  void train_epoch(int epoch, pk_epoch_metrics* m);
+  bool tensor(int which, int layer, pk_tensor_view* out);
+  cudaStream_t stream() const { return st_; }
+
+ private:
+  void forward_layer(int l, bool fault);
+  void backward_layer(int l);
+  void loss(int epoch, double* loss, double* acc);
+
+  pk_engine_config cfg_;
+  Grid grid_;
+  int rank_ = 0;
+  Coords c_;
+  int L_ = 0;
+  std::vector<i64> dims_;
+  std::vector<Layout> lays_;
+  std::vector<Shapes> shapes_;
+  cudaStream_t st_ = nullptr;
+  Comms comms_;
+  std::unique_ptr<AdjShard> shards_[6];
+  const AdjShard& shard(const Layout& l) const;
+
+  // parameters and optimizer state
+  std::vector<DMat> w_, w_m_, w_v_, dw_;
+  u64 w_step_ = 0;
+  DMat f0_, f0_m_, f0_v_, df0_;
+  u64 f0_step_ = 0;
+  // activations and workspaces
+  DMat f0g_;                           // layer-0 gathered features
+  std::vector<DMat> h_, q_, fout_;     // cached H, Q and relu(Q) per layer
+  std::vector<DMat> wfull_, dwp_;      // gathered W and dW partial per layer
+  DMat dq_, dh_, df_, df_prev_;        // backward workspaces (max shapes)
+  DMat logits_, dl_, stage_;
+  DevBuf<u32> labels_;
+  DevBuf<u8> mask_;
+  DevBuf<double> sums_;
+  CeWorkspace ce_ws_;
+  PhaseClock clock_;
+  u64 spmm_flops_ = 0, gemm_flops_ = 0;
+  double spmm_bytes_ = 0;
+  bool loaded_ = false;
+};
+
+}  // namespace pk

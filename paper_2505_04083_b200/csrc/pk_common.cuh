@@ -37,7 +37,11 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 
 #define PK_CUDA(x) ::pk::cuda_check((x), #x)
-#define PK_LAUNCH(what) ::pk::cuda_check(cudaGetLastError(), what)
+// Every kernel launch of the library is followed by PK_LAUNCH, which also
+// counts it (pk_kernel_launch_count(); bench.py reports the per-step count).
+u64 count_launch();
+u64 launch_count();
+#define PK_LAUNCH(what) (::pk::count_launch(), ::pk::cuda_check(cudaGetLastError(), what))
 
 void set_last_error(const std::string& msg);
 
