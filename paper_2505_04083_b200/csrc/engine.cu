@@ -191,7 +191,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     std::vector<u64> rp(sh->a.rows + 1);
     PK_CUDA(cudaMemcpy(rp.data(), sh->a.row_ptr, rp.size() * sizeof(u64),
                        cudaMemcpyDeviceToHost));
-    const int blocks = resolve_block_count(cfg_.block_count, sh->a.rows);
+    const int blocks = forward_blocks(sh->a.rows, plan_layouts(plane + 1).back());
     for (int b = 0; b < blocks; ++b)
       sh->block_nnz.push_back(rp[chunk_start(sh->a.rows, blocks, b + 1)] -
                               rp[chunk_start(sh->a.rows, blocks, b)]);
@@ -265,6 +265,12 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   loaded_ = true;
 }
 
+int Engine::forward_blocks(i64 rows, const Layout& lay) const {
+  if (cfg_.block_count > 0) return cfg_.block_count;
+  if (grid_.extent(lay.inner) == 1) return 1;
+  return static_cast<int>(std::max<i64>(1, std::min<i64>(4, rows / 65536)));
+}
+
 // ---------------------------------------------------------------------------
 // forward_layer (engine.hpp:158-206)
 
@@ -289,7 +295,7 @@ void Engine::forward_layer(int l, bool fault) {
                                    shape(sh.a.rows, sh.a.cols) + " does not match features " +
                                    shape(s.f_rows, s.f_cols));
   DMat& h = h_[l];
-  const int blocks = resolve_block_count(cfg_.block_count, sh.a.rows);
+  const int blocks = forward_blocks(sh.a.rows, lay);
   // blocked aggregation: SpMM row block, then its all-reduce along inner
   for (int b = 0; b < blocks; ++b) {
     const i64 r0 = chunk_start(sh.a.rows, blocks, b), r1 = chunk_start(sh.a.rows, blocks, b + 1);

@@ -71,6 +71,11 @@ class Engine {
   void forward_layer(int l, bool fault);
   void backward_layer(int l);
   void loss(int epoch, double* loss, double* acc);
+  // Forward row blocks of a plane's shard. The result is invariant to the
+  // block count (test_engine.cpp:190-213), so `block_count = 0` is free to
+  // pick for speed: one launch when no all-reduce follows, a few pipelined
+  // blocks otherwise. An explicit block_count is honoured.
+  int forward_blocks(i64 rows, const Layout& lay) const;
 
   pk_engine_config cfg_;
   Grid grid_;

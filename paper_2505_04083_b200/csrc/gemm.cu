@@ -26,9 +26,12 @@ constexpr int kBM = 64, kBN = 64, kBK = 16;
 
 template <bool TA, bool TB, bool EXACT>
 __global__ void __launch_bounds__(256)
-gemm_simt_kernel(i64 m, i64 n, i64 k_begin, i64 k_end, const float* __restrict__ a,
+gemm_simt_kernel(i64 m, i64 n, i64 k_total, i64 k_chunk, const float* __restrict__ a,
                  i64 lda, const float* __restrict__ b, i64 ldb, float* __restrict__ c,
                  i64 ldc) {
+  // split z covers k in [z*k_chunk, min(k_total, (z+1)*k_chunk))
+  const i64 k_begin = static_cast<i64>(blockIdx.z) * k_chunk;
+  const i64 k_end = min(k_total, k_begin + k_chunk);
   __shared__ float as[kBK][kBM + 4];
   __shared__ float bs[kBK][kBN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -162,11 +165,12 @@ __global__ void zero_kernel(float* c, i64 m, i64 n, i64 ldc) {
 }
 
 template <bool TA, bool TB, bool EXACT>
-void launch_simt(i64 m, i64 n, i64 kb, i64 ke, const float* a, i64 lda, const float* b,
+void launch_simt(i64 m, i64 n, i64 k, i64 k_chunk, const float* a, i64 lda, const float* b,
                  i64 ldb, float* c, i64 ldc, int splits, cudaStream_t st) {
   dim3 grid(ceil_div(n, kBN), ceil_div(m, kBM), splits);
   check(grid.y < 65536, "gemm: m too large for one launch");
-  gemm_simt_kernel<TA, TB, EXACT><<<grid, 256, 0, st>>>(m, n, kb, ke, a, lda, b, ldb, c, ldc);
+  gemm_simt_kernel<TA, TB, EXACT><<<grid, 256, 0, st>>>(m, n, k, k_chunk, a, lda, b, ldb, c,
+                                                         ldc);
   PK_LAUNCH("gemm simt kernel");
 }
 
@@ -181,7 +185,7 @@ void gemm_simt_dispatch(i64 m, i64 n, i64 k, const float* a, i64 lda, const floa
       gemm_tall_exact_kernel<TA, TB><<<grid, 256, 0, st>>>(m, n, k, a, lda, b, ldb, c, ldc);
       PK_LAUNCH("gemm tall exact kernel");
     } else {
-      launch_simt<TA, TB, true>(m, n, 0, k, a, lda, b, ldb, c, ldc, 1, st);
+      launch_simt<TA, TB, true>(m, n, k, k, a, lda, b, ldb, c, ldc, 1, st);
     }
     return;
   }
@@ -192,7 +196,7 @@ void gemm_simt_dispatch(i64 m, i64 n, i64 k, const float* a, i64 lda, const floa
     if (splits < 1) splits = 1;
   }
   if (splits == 1) {
-    launch_simt<TA, TB, false>(m, n, 0, k, a, lda, b, ldb, c, ldc, 1, st);
+    launch_simt<TA, TB, false>(m, n, k, k, a, lda, b, ldb, c, ldc, 1, st);
     return;
   }
   // each split covers a contiguous k range (multiple of kBK)
@@ -200,11 +204,7 @@ void gemm_simt_dispatch(i64 m, i64 n, i64 k, const float* a, i64 lda, const floa
   splits = static_cast<int>((k + chunk - 1) / chunk);
   static thread_local DevBuf<float> part;
   part.ensure(static_cast<size_t>(splits) * m * n);
-  for (int z = 0; z < splits; ++z) {
-    const i64 kb = z * chunk, ke = std::min(k, kb + chunk);
-    launch_simt<TA, TB, false>(m, n, kb, ke, a, lda, b, ldb,
-                               part.p + static_cast<i64>(z) * m * n, n, 1, st);
-  }
+  launch_simt<TA, TB, false>(m, n, k, chunk, a, lda, b, ldb, part.p, n, splits, st);
   splitk_reduce_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(part.p, splits, m, n, n, c, ldc);
   PK_LAUNCH("gemm split-k reduce");
 }
