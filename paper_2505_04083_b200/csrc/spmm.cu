@@ -75,75 +75,185 @@ __device__ __forceinline__ T ldg(const float* p) {
 
 constexpr int kThreads = 256;
 
+// Set (and reported once with printf) when a kernel bails out of a wait or
+// loop that should have terminated; read back by pk_spmm_watchdog().
+__device__ unsigned g_spmm_watchdog = 0;
+
 // ---------------------------------------------------------------------------
-// warp path
+// short-row path: persistent nnz-balanced stream
+//
+// [r0, r1) is cut into chunks of ~equal nonzeros (whole rows, empty rows
+// included). Each lane group grabs chunks from an atomic counter and walks
+// its chunk's nonzeros as one contiguous stream in windows of LANES entries:
+// the (col, val) window is a single coalesced load (the next one prefetched),
+// and U gathers are in flight regardless of where rows begin and end. Row
+// boundaries are tracked from a LANES-wide batch of row_ptr values; a row's
+// accumulator is stored the moment its last entry is consumed, so every
+// output element still sums its own k terms strictly in order.
+
+__global__ void spmm_partition_kernel(const u64* __restrict__ rp, i64 r0, i64 r1, int nchunks,
+                                      i64* __restrict__ bounds, int* __restrict__ counters,
+                                      int nslices) {
+  const i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (t < nslices) counters[t] = 0;
+  if (t > nchunks) return;
+  if (t == 0 || t == nchunks) {
+    bounds[t] = t == 0 ? r0 : r1;
+    return;
+  }
+  const u64 base = rp[r0], total = rp[r1] - base;
+  const u64 target = base + total / nchunks * t + (total % nchunks) * t / nchunks;
+  i64 lo = r0, hi = r1;  // first row with rp[row] >= target
+  while (lo < hi) {
+    const i64 mid = lo + (hi - lo) / 2;
+    if (rp[mid] < target)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  bounds[t] = lo;
+}
 
 template <int VEC, int LANES, int NV, int U>
-__global__ void __launch_bounds__(kThreads)
-spmm_warp_kernel(SpmmArgs args) {
+__device__ __forceinline__ void stream_rows(const SpmmArgs& a, i64 rs, i64 re, int lane,
+                                            unsigned gmask, int vbase, const bool (&valid)[NV]) {
   using V = typename Vec<VEC>::T;
-  const int lane = threadIdx.x % LANES;
-  const i64 group = static_cast<i64>(blockIdx.x) * (kThreads / LANES) + threadIdx.x / LANES;
-  const unsigned gmask =
-      LANES == 32 ? 0xffffffffu
-                  : (((1u << LANES) - 1u) << ((threadIdx.x % 32) / LANES * LANES));
-  const i64 row_begin = group * args.rows_per_group;
-  const i64 row_end = min(row_begin + static_cast<i64>(args.rows_per_group), args.nrows);
-  const int vbase = static_cast<int>(blockIdx.y) * (NV * LANES);
-  const u64 hub_t = args.hub_threshold;
+  const u64 hub_t = a.hub_threshold;
+  // ends[i] = rp[rb + 1 + i]: end of row rb + i
+  i64 rb = rs;
+  u64 ends = __ldg(a.rp + min(rb + 1 + lane, re));
+  u64 s = __ldg(a.rp + rs);
+  u64 e = __shfl_sync(gmask, ends, 0, LANES);
+  const u64 kend = __ldg(a.rp + re);
+  i64 r = rs;
+  V acc[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) acc[t] = Vec<VEC>::zero();
 
-  for (i64 rr = row_begin; rr < row_end; ++rr) {
-    const i64 r = args.r0 + rr;
-    const u64 s = __ldg(args.rp + r), e = __ldg(args.rp + r + 1);
-    if (e - s >= hub_t) continue;  // hub rows are owned by hub CTAs
-    V acc[NV];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) acc[t] = Vec<VEC>::zero();
-    bool valid[NV];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) valid[t] = vbase + t * LANES + lane < args.nvec;
-
-    for (u64 base = s; base < e; base += LANES) {
-      const u64 k = base + lane;
-      u32 c = 0;
-      float v = 0.f;
-      if (k < e) {
-        c = __ldcs(args.ci + k);
-        v = __ldcs(args.val + k);
-      }
-      const int cnt = static_cast<int>(min(static_cast<u64>(LANES), e - base));
-      int j = 0;
-      for (; j + U <= cnt; j += U) {
-        V xv[U][NV];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const u32 cj = __shfl_sync(gmask, c, j + u, LANES);
-          const float* xrow = args.x + static_cast<i64>(cj) * args.ldx;
-#pragma unroll
-          for (int t = 0; t < NV; ++t)
-            xv[u][t] = valid[t] ? ldg<V>(xrow + (vbase + t * LANES + lane) * VEC)
-                                : Vec<VEC>::zero();
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const float vj = __shfl_sync(gmask, v, j + u, LANES);
-#pragma unroll
-          for (int t = 0; t < NV; ++t) madd(acc[t], vj, xv[u][t]);
-        }
-      }
-      for (; j < cnt; ++j) {
-        const u32 cj = __shfl_sync(gmask, c, j, LANES);
-        const float vj = __shfl_sync(gmask, v, j, LANES);
-        const float* xrow = args.x + static_cast<i64>(cj) * args.ldx;
-#pragma unroll
-        for (int t = 0; t < NV; ++t)
-          if (valid[t]) madd(acc[t], vj, ldg<V>(xrow + (vbase + t * LANES + lane) * VEC));
-      }
-    }
-    float* yrow = args.y + rr * args.ldy;
+  auto store = [&](i64 row) {
+    float* yrow = a.y + (row - a.r0) * a.ldy;
 #pragma unroll
     for (int t = 0; t < NV; ++t)
       if (valid[t]) *reinterpret_cast<V*>(yrow + (vbase + t * LANES + lane) * VEC) = acc[t];
+  };
+  auto next_row = [&]() {
+    ++r;
+    s = e;
+    if (r < re) {
+      if (r - rb >= LANES) {
+        rb = r;
+        ends = __ldg(a.rp + min(rb + 1 + lane, re));
+      }
+      e = __shfl_sync(gmask, ends, static_cast<int>(r - rb), LANES);
+    }
+  };
+  // skip empty rows (store zeros) and hub rows (owned by hub CTAs); returns
+  // true when a hub was skipped, i.e. the nonzero stream jumps forward
+  auto settle = [&]() {
+    bool jumped = false;
+    while (r < re) {
+      if (s == e) {
+        store(r);  // acc is zero here
+        next_row();
+      } else if (e - s >= hub_t) {
+        next_row();
+        jumped = true;
+      } else {
+        break;
+      }
+    }
+    return jumped;
+  };
+
+  settle();
+  u64 kb = s;
+  u32 c = 0;
+  float v = 0.f;
+  if (r < re && kb + lane < kend) {
+    c = __ldcs(a.ci + kb + lane);
+    v = __ldcs(a.val + kb + lane);
+  }
+  // every window either consumes >= 1 entry or jumps forward, so a chunk
+  // takes at most (its nonzeros + its rows) windows
+  u64 guard = (kend - kb) + static_cast<u64>(re - rs) + 2;
+  while (r < re) {
+    if (guard-- == 0) {
+      if (atomicAdd(&g_spmm_watchdog, 1u) == 0)
+        printf("spmm stream watchdog: rows [%lld, %lld) stuck at row %lld kb %llu\n",
+               static_cast<long long>(rs), static_cast<long long>(re),
+               static_cast<long long>(r), static_cast<unsigned long long>(kb));
+      return;
+    }
+    // prefetch the next window
+    u32 cn = 0;
+    float vn = 0.f;
+    if (kb + LANES + lane < kend) {
+      cn = __ldcs(a.ci + kb + LANES + lane);
+      vn = __ldcs(a.val + kb + LANES + lane);
+    }
+    const int cnt = static_cast<int>(min(static_cast<u64>(LANES), kend - kb));
+    bool jumped = false;
+    for (int j = 0; j < cnt && !jumped && r < re; j += U) {
+      V xv[U][NV];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const u32 cj = __shfl_sync(gmask, c, (j + u) % LANES, LANES);
+        const float* xrow = a.x + static_cast<i64>(cj) * a.ldx;
+        const bool in = j + u < cnt;
+#pragma unroll
+        for (int t = 0; t < NV; ++t)
+          xv[u][t] = (valid[t] && in) ? ldg<V>(xrow + (vbase + t * LANES + lane) * VEC)
+                                      : Vec<VEC>::zero();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float vj = __shfl_sync(gmask, v, (j + u) % LANES, LANES);
+        if (j + u < cnt && !jumped && r < re) {
+#pragma unroll
+          for (int t = 0; t < NV; ++t) madd(acc[t], vj, xv[u][t]);
+          if (kb + j + u + 1 == e) {  // last entry of row r
+            store(r);
+#pragma unroll
+            for (int t = 0; t < NV; ++t) acc[t] = Vec<VEC>::zero();
+            next_row();
+            jumped = settle();
+          }
+        }
+      }
+    }
+    if (r >= re) break;
+    if (jumped) {  // restart the window at the next regular row
+      kb = s;
+      c = kb + lane < kend ? __ldcs(a.ci + kb + lane) : 0u;
+      v = kb + lane < kend ? __ldcs(a.val + kb + lane) : 0.f;
+    } else {
+      kb += cnt;
+      c = cn;
+      v = vn;
+    }
+  }
+}
+
+template <int VEC, int LANES, int NV, int U>
+__global__ void __launch_bounds__(kThreads)
+spmm_stream_kernel(SpmmArgs args, const i64* __restrict__ bounds, int nchunks,
+                   int* __restrict__ counters) {
+  const int lane = threadIdx.x % LANES;
+  const unsigned gmask =
+      LANES == 32 ? 0xffffffffu
+                  : (((1u << LANES) - 1u) << ((threadIdx.x % 32) / LANES * LANES));
+  const int vbase = static_cast<int>(blockIdx.y) * (NV * LANES);
+  bool valid[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) valid[t] = vbase + t * LANES + lane < args.nvec;
+  int* counter = counters + blockIdx.y;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(counter, 1);
+    t = __shfl_sync(gmask, t, 0, LANES);
+    if (t >= nchunks) break;
+    const i64 rs = bounds[t], re = bounds[t + 1];
+    if (rs < re) stream_rows<VEC, LANES, NV, U>(args, rs, re, lane, gmask, vbase, valid);
   }
 }
 
@@ -158,7 +268,6 @@ spmm_warp_kernel(SpmmArgs args) {
 
 constexpr int kHubBatch = 32;
 constexpr int kHubStages = 8;
-constexpr int kHubLoaders = kThreads / 32 - 1;
 
 __device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
@@ -171,17 +280,32 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
           static_cast<unsigned>(__cvta_generic_to_shared(bar)))
       : "memory");
 }
-__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+// Bounded wait: a protocol bug must surface as an error, never as a GPU that
+// spins until the job is killed. ~2^28 polls is seconds of wall time.
+__device__ __forceinline__ bool mbar_try(unsigned a, unsigned parity) {
+  unsigned ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  for (unsigned spins = 0; !mbar_try(a, parity); ++spins) {
+    if (spins == (1u << 28)) {
+      if (atomicAdd(&g_spmm_watchdog, 1u) == 0)
+        printf("spmm hub watchdog: block %d thread %d stuck on barrier parity %u\n",
+               blockIdx.x, threadIdx.x, parity);
+      return;
+    }
+  }
 }
 // arrive on `bar` once all of this thread's prior cp.async copies land
 __device__ __forceinline__ void cp_async_arrive(u64* bar) {
@@ -203,14 +327,41 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, bool pred
                  : "memory");
 }
 
+// Stage count per vector width: 6 stages of 16-B slices (96 KB) lets two hub
+// CTAs share an SM.
 template <int VEC>
-__global__ void __launch_bounds__(kThreads)
+constexpr int hub_stages() {
+  return VEC == 4 ? 6 : kHubStages;
+}
+// Loader warps = stages - 1. A loader may run ahead of the consumer by at
+// most its own stride of stages; with stride <= stages - 1 it can never
+// reach a ring slot two phases ahead, which mbarrier parity waits cannot
+// tell apart from the phase it is waiting for.
+template <int VEC>
+constexpr int hub_loaders() {
+  return hub_stages<VEC>() - 1;
+}
+template <int VEC>
+constexpr int hub_threads() {
+  return 32 * (hub_loaders<VEC>() + 1);
+}
+
+template <int VEC>
+size_t hub_smem_bytes() {
+  return static_cast<size_t>(hub_stages<VEC>()) * kHubBatch * (32 * VEC + 1) * sizeof(float);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(hub_threads<VEC>())
 spmm_hub_kernel(SpmmArgs args) {
   using V = typename Vec<VEC>::T;
   constexpr int kSliceVec = 32;  // vectors per slice (one per consumer lane)
+  constexpr int kStages = hub_stages<VEC>();
+  constexpr int kHubLoaders = hub_loaders<VEC>();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* ring = reinterpret_cast<V*>(smem_raw);  // [stage][batch][32]
-  __shared__ u64 full[kHubStages], empty[kHubStages];
+  V* ring = reinterpret_cast<V*>(smem_raw);  // [stage][batch][32] gathered slices
+  float* vring = reinterpret_cast<float*>(ring + kStages * kHubBatch * kSliceVec);  // [stage][batch]
+  __shared__ u64 full[kStages], empty[kStages];
 
   const int hb = blockIdx.x;
   if (hb >= args.hub_blocks) return;
@@ -224,7 +375,7 @@ spmm_hub_kernel(SpmmArgs args) {
   const u64 nb = (e - s + kHubBatch - 1) / kHubBatch;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kHubStages; ++i) {
+    for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 32);  // every loader lane arrives once per stage
       mbar_init(&empty[i], 1);  // consumer lane 0 releases
     }
@@ -233,18 +384,34 @@ spmm_hub_kernel(SpmmArgs args) {
   __syncthreads();
 
   if (warp > 0) {
-    // loaders: stage i handled by warp 1 + i % kHubLoaders
-    for (u64 i = warp - 1; i < nb; i += kHubLoaders) {
-      const int st = static_cast<int>(i % kHubStages);
-      const unsigned use = static_cast<unsigned>(i / kHubStages);
-      if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
+    // loaders: stage i handled by warp 1 + i % kHubLoaders. The column ids of
+    // the loader's next stage are fetched before it blocks on `empty`, so the
+    // index latency overlaps the wait.
+    u64 i = warp - 1;
+    u32 c_next = 0;
+    if (i < nb) {
       const u64 k = s + i * kHubBatch + lane;
-      const u32 c = k < e ? __ldcs(args.ci + k) : 0u;
+      c_next = k < e ? __ldcs(args.ci + k) : 0u;
+    }
+    for (; i < nb; i += kHubLoaders) {
+      const int st = static_cast<int>(i % kStages);
+      const unsigned use = static_cast<unsigned>(i / kStages);
+      const u32 c = c_next;
+      const u64 i2 = i + kHubLoaders;
+      if (i2 < nb) {
+        const u64 k2 = s + i2 * kHubBatch + lane;
+        c_next = k2 < e ? __ldcs(args.ci + k2) : 0u;
+      }
+      if (use > 0) mbar_wait(&empty[st], (use - 1) & 1);
       V* stage = ring + static_cast<size_t>(st) * kHubBatch * kSliceVec;
+      const u64 kbase = s + i * kHubBatch;
+      // the lane's own value rides the same async group as the gathers
+      cp_async<4>(vring + st * kHubBatch + lane, args.val + (kbase + lane < e ? kbase + lane : s),
+                  kbase + lane < e);
 #pragma unroll 8
       for (int j = 0; j < kHubBatch; ++j) {
         const u32 cj = __shfl_sync(0xffffffffu, c, j);
-        const bool ok = valid && (s + i * kHubBatch + j < e);
+        const bool ok = valid && (kbase + j < e);
         const float* src = args.x + static_cast<i64>(cj) * args.ldx + vcol * VEC;
         cp_async<sizeof(V)>(stage + j * kSliceVec + lane, ok ? src : args.x, ok);
       }
@@ -253,24 +420,17 @@ spmm_hub_kernel(SpmmArgs args) {
   } else {
     V acc = Vec<VEC>::zero();
     for (u64 i = 0; i < nb; ++i) {
-      const int st = static_cast<int>(i % kHubStages);
-      const unsigned use = static_cast<unsigned>(i / kHubStages);
-      const u64 k = s + i * kHubBatch + lane;
-      const float v = k < e ? __ldcs(args.val + k) : 0.f;
+      const int st = static_cast<int>(i % kStages);
+      const unsigned use = static_cast<unsigned>(i / kStages);
       const int cnt = static_cast<int>(min(static_cast<u64>(kHubBatch), e - s - i * kHubBatch));
       mbar_wait(&full[st], use & 1);
       const V* stage = ring + static_cast<size_t>(st) * kHubBatch * kSliceVec;
+      const float* vs = vring + st * kHubBatch;
       if (cnt == kHubBatch) {
 #pragma unroll
-        for (int j = 0; j < kHubBatch; ++j) {
-          const float vj = __shfl_sync(0xffffffffu, v, j);
-          madd(acc, vj, stage[j * kSliceVec + lane]);
-        }
+        for (int j = 0; j < kHubBatch; ++j) madd(acc, vs[j], stage[j * kSliceVec + lane]);
       } else {
-        for (int j = 0; j < cnt; ++j) {
-          const float vj = __shfl_sync(0xffffffffu, v, j);
-          madd(acc, vj, stage[j * kSliceVec + lane]);
-        }
+        for (int j = 0; j < cnt; ++j) madd(acc, vs[j], stage[j * kSliceVec + lane]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
@@ -282,25 +442,42 @@ spmm_hub_kernel(SpmmArgs args) {
   }
 }
 
-template <int VEC>
-size_t hub_smem_bytes() {
-  return static_cast<size_t>(kHubStages) * kHubBatch * 32 * VEC * sizeof(float);
-}
-
 // ---------------------------------------------------------------------------
 // launch selection
 
+struct StreamWorkspace {
+  DevBuf<i64> bounds;
+  DevBuf<int> counters;
+};
+
 template <int VEC, int LANES, int NV>
-void launch_warp(const SpmmArgs& a, cudaStream_t st) {
-  constexpr int U = NV >= 4 ? 2 : (NV == 2 ? 4 : 8);
+void launch_stream(const SpmmArgs& a, cudaStream_t st) {
+  constexpr int U0 = NV >= 4 ? 2 : (NV == 2 ? 4 : 8);
+  constexpr int U = U0 < LANES ? U0 : LANES;
+  auto kernel = spmm_stream_kernel<VEC, LANES, NV, U>;
   const int slices = ceil_div(a.nvec, NV * LANES);
-  const i64 groups = (a.nrows + a.rows_per_group - 1) / a.rows_per_group;
-  const i64 blocks = (groups + kThreads / LANES - 1) / (kThreads / LANES);
-  if (blocks <= 0) return;
-  check(blocks < (1ll << 31), "spmm: too many row blocks");
+  // ~1-2K nonzeros per chunk at the products shape; never more chunks than rows
+  const i64 nchunks64 = std::max<i64>(1, std::min<i64>(a.nrows, static_cast<i64>(sm_count()) * 512));
+  const int nchunks = static_cast<int>(nchunks64);
+  static thread_local StreamWorkspace ws;
+  ws.bounds.ensure(nchunks + 1);
+  ws.counters.ensure(std::max(slices, 1));
+  spmm_partition_kernel<<<ceil_div(nchunks + 1, 256), 256, 0, st>>>(a.rp, a.r0, a.r0 + a.nrows,
+                                                                    nchunks, ws.bounds.p,
+                                                                    ws.counters.p, slices);
+  PK_LAUNCH("spmm partition");
+  static thread_local int occ = 0;
+  if (occ == 0) {
+    PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0));
+    occ = std::max(occ, 1);
+  }
+  const i64 groups_per_block = kThreads / LANES;
+  const i64 blocks = std::max<i64>(
+      1, std::min<i64>(static_cast<i64>(sm_count()) * occ,
+                       (nchunks + groups_per_block - 1) / groups_per_block));
   dim3 grid(static_cast<unsigned>(blocks), slices);
-  spmm_warp_kernel<VEC, LANES, NV, U><<<grid, kThreads, 0, st>>>(a);
-  PK_LAUNCH("spmm warp kernel");
+  kernel<<<grid, kThreads, 0, st>>>(a, ws.bounds.p, nchunks, ws.counters.p);
+  PK_LAUNCH("spmm stream kernel");
 }
 
 template <int VEC>
@@ -314,7 +491,7 @@ void launch_hub(const SpmmArgs& a, cudaStream_t st) {
                                  static_cast<int>(smem)));
     attr_set = true;
   }
-  spmm_hub_kernel<VEC><<<a.hub_blocks, kThreads, smem, st>>>(a);
+  spmm_hub_kernel<VEC><<<a.hub_blocks, hub_threads<VEC>(), smem, st>>>(a);
   PK_LAUNCH("spmm hub kernel");
 }
 
@@ -332,17 +509,17 @@ void dispatch_vec(const SpmmArgs& a, cudaStream_t st) {
   }
   // lane-group width: smallest power of two covering the row's vectors
   if (nv <= 4)
-    launch_warp<VEC, 4, 1>(a, st);
+    launch_stream<VEC, 4, 1>(a, st);
   else if (nv <= 8)
-    launch_warp<VEC, 8, 1>(a, st);
+    launch_stream<VEC, 8, 1>(a, st);
   else if (nv <= 16)
-    launch_warp<VEC, 16, 1>(a, st);
+    launch_stream<VEC, 16, 1>(a, st);
   else if (nv <= 32)
-    launch_warp<VEC, 32, 1>(a, st);
+    launch_stream<VEC, 32, 1>(a, st);
   else if (nv <= 64)
-    launch_warp<VEC, 32, 2>(a, st);
+    launch_stream<VEC, 32, 2>(a, st);
   else
-    launch_warp<VEC, 32, 4>(a, st);  // wider rows split across blockIdx.y
+    launch_stream<VEC, 32, 4>(a, st);  // wider rows split across blockIdx.y
   if (a.hub_blocks > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
 }
 
@@ -366,11 +543,6 @@ void spmm_launch(SpmmArgs a, i64 d, cudaStream_t st) {
   // hub CTAs serve 32 vectors per slice
   a.hub_slices = ceil_div(a.nvec, 32);
   a.hub_blocks = a.hub_count * a.hub_slices;
-  if (a.rows_per_group <= 0) {
-    // enough groups for ~16 resident waves of short-row work
-    const i64 target_groups = static_cast<i64>(sm_count()) * 64 * 16;
-    a.rows_per_group = static_cast<int>(std::max<i64>(1, std::min<i64>(16, a.nrows / target_groups)));
-  }
   if (vec == 4)
     dispatch_vec<4>(a, st);
   else if (vec == 2)
