@@ -175,6 +175,10 @@ void pk_csr_free(pk_csr_owned* m);
 int pk_permutation_pair_host(uint64_t n, uint64_t seed, uint32_t* row_perm_host,
                              uint32_t* col_perm_host);
 
+/* Philox(seed, stream).permutation(n) (rng.hpp:57-66) on the host */
+int pk_philox_permutation_host(uint64_t n, uint64_t seed, uint64_t stream,
+                               uint32_t* out_host);
+
 /* synth_rmat edge draw (graph.hpp:291-322) on the device: Philox(seed, 5),
  * `scale` doubles per edge, self loops dropped (stable). Device output
  * buffer must hold 2*edges u32; *kept_host receives the kept count. */
@@ -277,6 +281,76 @@ int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* out_host);
 int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out);
 int pk_engine_stream(pk_engine* e, void** stream_out);
 int pk_engine_destroy(pk_engine* e);
+
+/* ------------------------------------------------------------------ */
+/* Performance model: picks the grid (perf_model.hpp:18-127,            */
+/* src/perf_model.cpp:33-229). Host-only; no device work.               */
+
+/* DatasetStats (perf_model.hpp:18-22) */
+typedef struct pk_dataset_stats {
+  int64_t n;
+  uint64_t nnz;
+  int num_dims;                       /* L + 1                          */
+  int64_t dims[PK_MAX_LAYERS + 1];
+} pk_dataset_stats;
+
+/* MachineParams (perf_model.hpp:24-29); reference defaults
+ * {4, 200e9, 25e9, 4}. */
+typedef struct pk_machine {
+  int g_node;
+  double beta_intra, beta_inter;
+  int bytes_per_scalar;
+} pk_machine;
+
+/* PerfCoefficients (perf_model.hpp:31-41) */
+typedef struct pk_perf_coeffs {
+  double c1, c2, c3, train_r2, train_rmse;
+} pk_perf_coeffs;
+
+/* ConfigPrediction (perf_model.hpp:98-104) */
+typedef struct pk_config_prediction {
+  int gx, gy, gz, clamped;
+  double spmm_seconds, comm_seconds, total_seconds;
+} pk_config_prediction;
+
+/* CollOp / CollectiveVolume (layout.hpp:105-121) */
+enum { PK_COLL_ALL_GATHER = 0, PK_COLL_ALL_REDUCE = 1, PK_COLL_REDUCE_SCATTER = 2 };
+typedef struct pk_collective_volume {
+  int layer, forward, op, axis; /* axis 0/1/2 = X/Y/Z                 */
+  uint64_t elems;               /* full buffer M (pre-scatter for RS) */
+} pk_collective_volume;
+
+/* default_coefficients (perf_model.hpp:38-40) */
+int pk_perf_default_coefficients(pk_perf_coeffs* out);
+/* comp_features (perf_model.cpp:33-56): 3 doubles */
+int pk_perf_comp_features(const pk_dataset_stats* stats, int gx, int gy, int gz,
+                          double* features3);
+/* predict_spmm_time (perf_model.cpp:58-64): negative -> 0, clamped = 1 */
+int pk_perf_predict_spmm(const double* features3, const pk_perf_coeffs* c,
+                         double* seconds, int* clamped);
+/* effective_bandwidth (perf_model.cpp:66-78) */
+int pk_perf_effective_bandwidth(int axis, int gx, int gy, int gz,
+                                const pk_machine* m, double* out);
+/* ring_collective_seconds (perf_model.cpp:80-85) */
+int pk_perf_ring_seconds(int op, double bytes, int g, double beta, double* out);
+/* predict_comm_time(...).total (perf_model.cpp:87-102) */
+int pk_perf_predict_comm(const pk_dataset_stats* stats, int gx, int gy, int gz,
+                         const pk_machine* m, double* total_seconds);
+/* training_collective_volumes (layout.hpp:123-157); out may be NULL to
+ * query the count */
+int pk_collective_volumes(int gx, int gy, int gz, const pk_dataset_stats* stats,
+                          pk_collective_volume* out, int cap, int* count);
+/* fit_regression (perf_model.cpp:104-166): features row-major count x 3 */
+int pk_perf_fit_regression(const double* features3, const double* seconds,
+                           int count, pk_perf_coeffs* out);
+/* enumerate_configs (grid.hpp:112-123): triples in (gx, gy) lexicographic
+ * order; gxyz may be NULL to query the count */
+int pk_enumerate_configs(int g, int* gxyz, int cap, int* count);
+/* rank_configs (perf_model.cpp:207-229): ascending total, ties by
+ * (gz, gx, gy) */
+int pk_perf_rank_configs(int g, const pk_dataset_stats* stats,
+                         const pk_machine* m, const pk_perf_coeffs* c,
+                         pk_config_prediction* out, int cap, int* count);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,7 @@ SIGNATURES = {
     "pk_permute_csr": (INT, [C.POINTER(pk_csr), P, P, C.POINTER(pk_csr_owned), P]),
     "pk_csr_free": (None, [C.POINTER(pk_csr_owned)]),
     "pk_permutation_pair_host": (INT, [U64, U64, P, P]),
+    "pk_philox_permutation_host": (INT, [U64, U64, U64, P]),
     "pk_rmat_edges": (INT, [INT, U64, DBL, DBL, DBL, U64, P, U64P, P]),
     "pk_rmat_features": (INT, [U64, I64, I64, P, I64, P]),
     "pk_degree_quantile_labels": (INT, [P, U64, I64, U32, P, P]),

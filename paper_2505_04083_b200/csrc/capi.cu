@@ -287,6 +287,16 @@ int pk_permutation_pair_host(uint64_t n, uint64_t seed, uint32_t* row_perm_host,
   });
 }
 
+int pk_philox_permutation_host(uint64_t n, uint64_t seed, uint64_t stream, uint32_t* out) {
+  return guard([&] {
+    // Philox::permutation (rng.hpp:57-66): identity, then Fisher-Yates from
+    // the top with rejection-sampled randint
+    PhiloxStream rng(seed, stream);
+    for (u64 i = 0; i < n; ++i) out[i] = static_cast<u32>(i);
+    for (u64 i = n; i > 1; --i) std::swap(out[i - 1], out[rng.randint(i)]);
+  });
+}
+
 int pk_rmat_edges(int scale, uint64_t edges, double a, double b, double c, uint64_t seed,
                   uint32_t* edges_uv, uint64_t* kept_host, void* stream) {
   return guard([&] {

@@ -1,13 +1,598 @@
-// tcgen05 3xTF32 GEMM tiles for the GCN dense transform (sm_100a).
-// Placeholder until the tensor-core path lands: every shape falls back to
-// the SIMT FFMA kernel in gemm.cu.
+// Tensor-core dense transforms of the GCN layer on sm_100a: tcgen05.mma
+// (kind::tf32) with fp32 accumulators in TMEM, 3xTF32 operand splitting.
+//
+// The reference multiplies in fp32 with a plain k-ascending loop
+// (kernels.hpp:64-92). TF32 alone (10-bit mantissa) misses the 1e-4
+// normwise budget (~3e-4 per GEMM), so every operand is
+// split x = hi + lo with hi = rna_tf32(x), lo = x - hi, and
+//     C = A_lo.B_hi + A_hi.B_lo + A_hi.B_hi
+// accumulated in TMEM (error ~2^-22 relative per product, i.e. fp32-level).
+//
+// Why the loads are register-staged and not TMA: the split has to happen
+// between HBM and the tensor core. Loader warps read fp32 tiles with 16-B
+// coalesced loads (the next k-stage's loads are in flight while the current
+// one is split and stored), write hi and lo into 128-B-swizzled shared
+// memory in the canonical UMMA layouts (K-major or MN-major, whichever the
+// operand's row-major storage gives without a transpose), and arrive on the
+// stage's mbarrier. One elected thread issues the MMAs; epilogue warps drain
+// the double-buffered TMEM accumulator with tcgen05.ld and store rows.
+//
+// Persistent CTAs walk a static tile schedule (m tile, n tile, k split). A
+// k split > 1 writes fp32 partials that a deterministic fixed-order reduce
+// combines (dW = H^T dQ reduces over all adjacency rows, engine.hpp:233-235).
+//
+// Operand forms (row-major storage, op = optional transpose):
+//   NN  Q  = H . W        A = H   (K-major)      B = W   (MN-major)
+//   NT  dH = dQ . W^T     A = dQ  (K-major)      B = W   (K-major)
+//   TN  dW = H^T . dQ     A = H^T (MN-major)     B = dQ  (MN-major)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
 #include "gemm.cuh"
+#include "pk_common.cuh"
 
 namespace pk {
 
-bool gemm_tc_launch(bool, bool, i64, i64, i64, const float*, i64, const float*, i64, float*,
-                    i64, cudaStream_t) {
-  return false;
+namespace {
+
+constexpr int kBM = 128;        // UMMA M (one CTA, cta_group::1)
+constexpr int kBK = 32;         // k per stage: one 128-B swizzle row of fp32
+constexpr int kLoaderWarps = 8;
+constexpr int kMmaWarp = kLoaderWarps;          // warp 8
+constexpr int kThreadsTc = 32 * (kLoaderWarps + 1 + 4);
+constexpr int kLoaderThreads = 32 * kLoaderWarps;
+
+__device__ unsigned g_gemm_watchdog = 0;
+
+// ---------------------------------------------------------------- PTX glue
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(u64* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// Bounded parity wait: a protocol error must surface as a flagged error, not
+// as a GPU that spins until the job is killed.
+__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+  const unsigned a = smem_u32(bar);
+  for (unsigned spins = 0;; ++spins) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spins == (1u << 26)) {
+      if (atomicAdd(&g_gemm_watchdog, 1u) == 0)
+        printf("gemm_tc watchdog: block %d thread %d stuck on barrier parity %u\n", blockIdx.x,
+               threadIdx.x, parity);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(u64* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_tf32(unsigned d_tmem, u64 adesc, u64 bdesc, unsigned idesc,
+                                            unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// 32 lanes x 32 bit, 8 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld8(unsigned taddr, float (&v)[8]) {
+  unsigned r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1"), 128-B swizzle.
+__device__ __forceinline__ u64 smem_desc(unsigned addr, unsigned lbo, unsigned sbo) {
+  u64 d = 0;
+  d |= static_cast<u64>((addr >> 4) & 0x3FFF);
+  d |= static_cast<u64>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<u64>((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (sm_100)
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: fp32 accumulate, tf32 A and B, M = 128.
+__host__ __device__ constexpr unsigned instr_desc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<unsigned>(a_mn) << 15) |
+         (static_cast<unsigned>(b_mn) << 16) | (static_cast<unsigned>(n >> 3) << 17) |
+         (static_cast<unsigned>(kBM >> 4) << 24);
+}
+
+// ------------------------------------------------------------ tile layouts
+//
+// K-major SW128 (rows = M or N index, 32 fp32 of k per 128-B row; 8-row
+// atoms of 1024 B): chunk c (k/4) of row r lives at r*128 + ((c ^ r%8) * 16).
+// k-step t (8 k) starts 32*t bytes into the tile; SBO = 1024.
+//
+// MN-major SW128 (k rows of 128-B atoms holding 32 consecutive M/N values):
+// k-group g = k/8 (one UMMA k-step), atom a = mn/32, row k%8, chunk (mn%32)/4
+// at g*ATOMS*1024 + a*1024 + (k%8)*128 + ((chunk ^ k%8) * 16). LBO = 1024
+// (next MN atom), SBO = ATOMS*1024 (next k-group).
+
+template <bool MN>
+struct OperandTile {
+  // rows: M/N extent stored in the tile (multiple of 8; MN-major: of 32)
+  static __device__ __forceinline__ unsigned offset(int mn, int k, int rows) {
+    if (!MN) {
+      const int c = k >> 2;
+      return static_cast<unsigned>(mn * 128 + ((c ^ (mn & 7)) << 4));
+    } else {
+      const int g = k >> 3, a = mn >> 5, c = (mn & 31) >> 2, r = k & 7;
+      return static_cast<unsigned>(g * (rows >> 5) * 1024 + a * 1024 + r * 128 + ((c ^ r) << 4));
+    }
+  }
+  static __device__ __forceinline__ u64 desc(unsigned base, int kstep, int rows) {
+    if (!MN) return smem_desc(base + 32u * kstep, 16u, 1024u);
+    const unsigned sbo = static_cast<unsigned>(rows >> 5) * 1024u;
+    return smem_desc(base + sbo * kstep, 1024u, sbo);
+  }
+};
+
+// One operand's view for the loaders. Storage is row-major `src[r * ld + c]`.
+//  K-major form: r = m/n index (extent `mn`), c = k index.
+//  MN-major form: r = k index, c = m/n index (extent `mn`).
+struct OperandSrc {
+  const float* p;
+  i64 ld;
+  i64 mn;      // extent of the M/N index
+  bool vec;    // base and ld allow 16-B loads
+};
+
+// chunk q of a stage -> (mn, k) inside the tile; 4 consecutive elements
+// along the storage-contiguous axis.
+template <bool MN, int ROWS>
+__device__ __forceinline__ void chunk_coords(int q, int& mn, int& k) {
+  if (!MN) {
+    mn = q >> 3;           // 8 chunks (128 B) per row of k
+    k = (q & 7) << 2;
+  } else {
+    constexpr int per_k = ROWS / 4;
+    k = q / per_k;
+    mn = (q % per_k) << 2;
+  }
+}
+
+template <bool MN>
+__device__ __forceinline__ float4 load_chunk(const OperandSrc& s, i64 mn0, int mn, i64 k0, int k,
+                                             i64 k_end) {
+  // global coordinates of the chunk's first element
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!MN) {
+    const i64 r = mn0 + mn, c = k0 + k;
+    if (r >= s.mn) return v;
+    const float* p = s.p + r * s.ld + c;
+    if (s.vec && c + 3 < k_end) return __ldg(reinterpret_cast<const float4*>(p));
+    if (c < k_end) v.x = __ldg(p);
+    if (c + 1 < k_end) v.y = __ldg(p + 1);
+    if (c + 2 < k_end) v.z = __ldg(p + 2);
+    if (c + 3 < k_end) v.w = __ldg(p + 3);
+  } else {
+    const i64 r = k0 + k, c = mn0 + mn;
+    if (r >= k_end) return v;
+    const float* p = s.p + r * s.ld + c;
+    if (s.vec && c + 3 < s.mn) return __ldg(reinterpret_cast<const float4*>(p));
+    if (c < s.mn) v.x = __ldg(p);
+    if (c + 1 < s.mn) v.y = __ldg(p + 1);
+    if (c + 2 < s.mn) v.z = __ldg(p + 2);
+    if (c + 3 < s.mn) v.w = __ldg(p + 3);
+  }
+  return v;
+}
+
+// Store hi and lo parts of a chunk. K-major: the 4 values are consecutive k
+// of one row -> one 16-B store. MN-major: 4 consecutive m/n of one k row ->
+// one 16-B store as well (the chunk never straddles a swizzle unit).
+template <bool MN, int ROWS>
+__device__ __forceinline__ void store_chunk(unsigned char* hi, unsigned char* lo, int mn, int k,
+                                            float4 v) {
+  float4 h, l;
+  h.x = tf32_rna(v.x), h.y = tf32_rna(v.y), h.z = tf32_rna(v.z), h.w = tf32_rna(v.w);
+  l.x = tf32_rna(v.x - h.x), l.y = tf32_rna(v.y - h.y);
+  l.z = tf32_rna(v.z - h.z), l.w = tf32_rna(v.w - h.w);
+  const unsigned off = OperandTile<MN>::offset(mn, k, ROWS);
+  *reinterpret_cast<float4*>(hi + off) = h;
+  *reinterpret_cast<float4*>(lo + off) = l;
+}
+
+struct TcParams {
+  OperandSrc a, b;
+  i64 m, n, k;
+  i64 k_chunk;      // k per split (multiple of kBK)
+  int m_tiles, n_tiles, splits;
+  float* c;         // output (splits == 1) or partials [split][m][ldc]
+  i64 ldc;
+  i64 split_stride; // elements between split partials
+};
+
+template <bool A_MN, bool B_MN, int BN, int STAGES>
+struct TcConfig {
+  static constexpr int kRowsB = B_MN ? ((BN + 31) / 32) * 32 : BN;  // stored N extent
+  static constexpr int kTileA = kBM * kBK * 4;                      // bytes, one of hi/lo
+  static constexpr int kTileB = kRowsB * kBK * 4;
+  static constexpr int kStage = 2 * kTileA + 2 * kTileB;
+  static constexpr int kChunksA = kBM * kBK / 4;
+  static constexpr int kChunksB = kRowsB * kBK / 4;
+  static constexpr int kPerThreadA = (kChunksA + kLoaderThreads - 1) / kLoaderThreads;
+  static constexpr int kPerThreadB = (kChunksB + kLoaderThreads - 1) / kLoaderThreads;
+  static constexpr int kTmemCols = BN <= 32 ? 64 : (BN <= 64 ? 128 : (BN <= 128 ? 256 : 512));
+  static constexpr int kAccStride = kTmemCols / 2;  // two accumulator buffers
+  static constexpr size_t kSmem = static_cast<size_t>(STAGES) * kStage + 1024;
+};
+
+template <bool A_MN, bool B_MN, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
+  using Cfg = TcConfig<A_MN, B_MN, BN, STAGES>;
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-B alignment for the swizzle atoms
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  __shared__ u64 full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ unsigned tmem_base;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kLoaderWarps);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "n"(Cfg::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem = tmem_base;
+
+  const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
+  auto tile_coords = [&](int t, int& mt, int& nt, int& sp) {
+    mt = t % p.m_tiles;
+    nt = (t / p.m_tiles) % p.n_tiles;
+    sp = t / (p.m_tiles * p.n_tiles);
+  };
+  auto k_range = [&](int sp, i64& kb, i64& ke) {
+    kb = static_cast<i64>(sp) * p.k_chunk;
+    ke = min(p.k, kb + p.k_chunk);
+  };
+
+  if (warp < kLoaderWarps) {
+    // ------------------------------------------------------------ loaders
+    const int lt = threadIdx.x;  // 0..255
+    int stage = 0;
+    unsigned phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int mt, nt, sp;
+      tile_coords(t, mt, nt, sp);
+      i64 kb, ke;
+      k_range(sp, kb, ke);
+      const i64 m0 = static_cast<i64>(mt) * kBM, n0 = static_cast<i64>(nt) * BN;
+      const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
+      float4 ra[Cfg::kPerThreadA], rb[Cfg::kPerThreadB];
+      auto load = [&](int kk) {
+        const i64 k0 = kb + static_cast<i64>(kk) * kBK;
+#pragma unroll
+        for (int i = 0; i < Cfg::kPerThreadA; ++i) {
+          const int q = lt + i * kLoaderThreads;
+          int mn, k;
+          chunk_coords<A_MN, kBM>(q, mn, k);
+          ra[i] = q < Cfg::kChunksA ? load_chunk<A_MN>(p.a, m0, mn, k0, k, ke)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::kPerThreadB; ++i) {
+          const int q = lt + i * kLoaderThreads;
+          int mn, k;
+          chunk_coords<B_MN, Cfg::kRowsB>(q, mn, k);
+          rb[i] = q < Cfg::kChunksB ? load_chunk<B_MN>(p.b, n0, mn, k0, k, ke)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      if (nk > 0) load(0);
+      for (int kk = 0; kk < nk; ++kk) {
+        float4 ca[Cfg::kPerThreadA], cb[Cfg::kPerThreadB];
+#pragma unroll
+        for (int i = 0; i < Cfg::kPerThreadA; ++i) ca[i] = ra[i];
+#pragma unroll
+        for (int i = 0; i < Cfg::kPerThreadB; ++i) cb[i] = rb[i];
+        if (kk + 1 < nk) load(kk + 1);  // next stage's loads in flight
+        mbar_wait(&empty[stage], phase ^ 1u);
+        unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
+        unsigned char* a_hi = st;
+        unsigned char* a_lo = st + Cfg::kTileA;
+        unsigned char* b_hi = st + 2 * Cfg::kTileA;
+        unsigned char* b_lo = b_hi + Cfg::kTileB;
+#pragma unroll
+        for (int i = 0; i < Cfg::kPerThreadA; ++i) {
+          const int q = lt + i * kLoaderThreads;
+          if (q < Cfg::kChunksA) {
+            int mn, k;
+            chunk_coords<A_MN, kBM>(q, mn, k);
+            store_chunk<A_MN, kBM>(a_hi, a_lo, mn, k, ca[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::kPerThreadB; ++i) {
+          const int q = lt + i * kLoaderThreads;
+          if (q < Cfg::kChunksB) {
+            int mn, k;
+            chunk_coords<B_MN, Cfg::kRowsB>(q, mn, k);
+            store_chunk<B_MN, Cfg::kRowsB>(b_hi, b_lo, mn, k, cb[i]);
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == STAGES) stage = 0, phase ^= 1u;
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr unsigned idesc = instr_desc(BN, A_MN, B_MN);
+    int stage = 0;
+    unsigned phase = 0;
+    int acc = 0;
+    unsigned acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int mt, nt, sp;
+      tile_coords(t, mt, nt, sp);
+      i64 kb, ke;
+      k_range(sp, kb, ke);
+      const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
+      mbar_wait(&tempty[acc], acc_phase ^ 1u);
+      tc_fence_after();
+      const unsigned d = tmem + static_cast<unsigned>(acc * Cfg::kAccStride);
+      for (int kk = 0; kk < nk; ++kk) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const unsigned base = smem_u32(smem + static_cast<size_t>(stage) * Cfg::kStage);
+          const unsigned a_hi = base, a_lo = base + Cfg::kTileA;
+          const unsigned b_hi = base + 2 * Cfg::kTileA, b_lo = b_hi + Cfg::kTileB;
+#pragma unroll
+          for (int ks = 0; ks < kBK / 8; ++ks) {
+            const u64 dah = OperandTile<A_MN>::desc(a_hi, ks, kBM);
+            const u64 dal = OperandTile<A_MN>::desc(a_lo, ks, kBM);
+            const u64 dbh = OperandTile<B_MN>::desc(b_hi, ks, Cfg::kRowsB);
+            const u64 dbl = OperandTile<B_MN>::desc(b_lo, ks, Cfg::kRowsB);
+            const unsigned first = (kk == 0 && ks == 0) ? 0u : 1u;
+            tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
+            tc_mma_tf32(d, dah, dbl, idesc, 1u);
+            tc_mma_tf32(d, dah, dbh, idesc, 1u);
+          }
+          tc_commit(&empty[stage]);  // frees the smem stage when the MMAs finish
+        }
+        __syncwarp();
+        if (++stage == STAGES) stage = 0, phase ^= 1u;
+      }
+      if (lane == 0) {
+        if (nk == 0) {
+          // empty k range: the epilogue writes zeros without reading TMEM
+          mbar_arrive(&tfull[acc]);
+        } else {
+          tc_commit(&tfull[acc]);
+        }
+      }
+      __syncwarp();
+      if (++acc == 2) acc = 0, acc_phase ^= 1u;
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    int acc = 0;
+    unsigned acc_phase = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      int mt, nt, sp;
+      tile_coords(t, mt, nt, sp);
+      i64 kb, ke;
+      k_range(sp, kb, ke);
+      const bool zero = ke <= kb;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const i64 gm = static_cast<i64>(mt) * kBM + row;
+      const i64 n0 = static_cast<i64>(nt) * BN;
+      float* out = p.c + static_cast<i64>(sp) * p.split_stride;
+      const unsigned taddr =
+          tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * Cfg::kAccStride);
+      const bool vec_out = (p.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 8) {
+        float v[8];
+        if (zero) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = 0.f;
+        } else {
+          tmem_ld8(taddr + static_cast<unsigned>(c0), v);
+        }
+        if (gm < p.m) {
+          float* dst = out + gm * p.ldc + n0 + c0;
+          const i64 left = p.n - (n0 + c0);
+          if (vec_out && left >= 8) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < left) dst[i] = v[i];
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) acc = 0, acc_phase ^= 1u;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(Cfg::kTmemCols));
+  }
+}
+
+// Deterministic split combine: C = partial[0] + partial[1] + ... in order.
+__global__ void tc_split_reduce_kernel(const float* __restrict__ part, int splits, i64 m, i64 n,
+                                       i64 ldp, i64 stride, float* __restrict__ c, i64 ldc) {
+  const i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (idx >= m * n) return;
+  const i64 i = idx / n, j = idx % n;
+  float s = part[i * ldp + j];
+  for (int z = 1; z < splits; ++z) s += part[z * stride + i * ldp + j];
+  c[i * ldc + j] = s;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+void launch_bn(const TcParams& p0, cudaStream_t st) {
+  constexpr int kStageBytes = TcConfig<A_MN, B_MN, BN, 1>::kStage;
+  constexpr int STAGES = std::min(6, std::max(2, (200 * 1024) / kStageBytes));
+  using Cfg = TcConfig<A_MN, B_MN, BN, STAGES>;
+  auto kernel = gemm_tc_kernel<A_MN, B_MN, BN, STAGES>;
+  static thread_local bool attr = false;
+  if (!attr) {
+    PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Cfg::kSmem)));
+    attr = true;
+  }
+  TcParams p = p0;
+  const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles * p.splits;
+  const int grid = static_cast<int>(std::min<i64>(tiles, sm_count()));
+  kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p);
+  PK_LAUNCH("gemm tcgen05 kernel");
+}
+
+template <bool A_MN, bool B_MN>
+void launch_forms(const TcParams& p, int bn, cudaStream_t st) {
+  switch (bn) {
+    case 16: return launch_bn<A_MN, B_MN, 16>(p, st);
+    case 32: return launch_bn<A_MN, B_MN, 32>(p, st);
+    case 48: return launch_bn<A_MN, B_MN, 48>(p, st);
+    case 64: return launch_bn<A_MN, B_MN, 64>(p, st);
+    case 96: return launch_bn<A_MN, B_MN, 96>(p, st);
+    case 128: return launch_bn<A_MN, B_MN, 128>(p, st);
+    case 192: return launch_bn<A_MN, B_MN, 192>(p, st);
+    default: return launch_bn<A_MN, B_MN, 256>(p, st);
+  }
+}
+
+int pick_bn(i64 n) {
+  static const int opts[] = {16, 32, 48, 64, 96, 128, 192, 256};
+  for (int b : opts)
+    if (n <= b) return b;
+  // wide outputs: the fewest 256-column tiles... unless a 192 split is tighter
+  return 256;
+}
+
+bool aligned16(const void* p, i64 ld) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 4 == 0;
+}
+
+}  // namespace
+
+bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
+                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st) {
+  if (ta && tb) return false;  // not used by the layer
+  TcParams p{};
+  p.m = m, p.n = n, p.k = k;
+  // A: NN/NT -> K-major (storage m x k); TN -> MN-major (storage k x m)
+  p.a = OperandSrc{a, lda, m, aligned16(a, lda)};
+  // B: NN -> MN-major (storage k x n); NT -> K-major (storage n x k); TN -> MN-major
+  p.b = OperandSrc{b, ldb, n, aligned16(b, ldb)};
+  const int bn = pick_bn(n);
+  p.m_tiles = static_cast<int>((m + kBM - 1) / kBM);
+  p.n_tiles = static_cast<int>((n + bn - 1) / bn);
+  const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles;
+  // split k when the output alone cannot fill the machine and k is long
+  int splits = 1;
+  const i64 sms = sm_count();
+  if (tiles < sms && k >= 8 * kBK) {
+    splits = static_cast<int>(std::min<i64>((sms + tiles - 1) / tiles * 2, k / (4 * kBK)));
+    splits = std::max(splits, 1);
+  }
+  p.k_chunk = ((k + splits - 1) / splits + kBK - 1) / kBK * kBK;
+  splits = static_cast<int>((k + p.k_chunk - 1) / p.k_chunk);
+  p.splits = splits;
+  static thread_local DevBuf<float> part;
+  if (splits > 1) {
+    const i64 ldp = static_cast<i64>(p.n_tiles) * bn;
+    p.split_stride = m * ldp;
+    part.ensure(static_cast<size_t>(splits) * p.split_stride);
+    p.c = part.p;
+    p.ldc = ldp;
+  } else {
+    p.c = c;
+    p.ldc = ldc;
+    p.split_stride = 0;
+  }
+  if (!ta && !tb)
+    launch_forms<false, true>(p, bn, st);
+  else if (!ta && tb)
+    launch_forms<false, false>(p, bn, st);
+  else
+    launch_forms<true, true>(p, bn, st);
+  if (splits > 1) {
+    tc_split_reduce_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(part.p, splits, m, n, p.ldc,
+                                                                 p.split_stride, c, ldc);
+    PK_LAUNCH("gemm tcgen05 split reduce");
+  }
+  return true;
 }
 
 }  // namespace pk
