@@ -11,20 +11,20 @@
 // Why the loads are register-staged and not TMA: the split has to happen
 // between HBM and the tensor core. Loader warps read fp32 tiles with 16-B
 // coalesced loads (the next k-stage's loads are in flight while the current
-// one is split and stored), write hi and lo into 128-B-swizzled shared
-// memory in the canonical UMMA layouts (K-major or MN-major, whichever the
-// operand's row-major storage gives without a transpose), and arrive on the
-// stage's mbarrier. One elected thread issues the MMAs; epilogue warps drain
+// one is split and stored), write hi and lo into 128-B-swizzled K-major
+// shared-memory tiles (transposing 4x4 register blocks when the operand's
+// row-major storage runs along M/N), and arrive on the stage's mbarrier. One elected thread issues the MMAs; epilogue warps drain
 // the double-buffered TMEM accumulator with tcgen05.ld and store rows.
 //
 // Persistent CTAs walk a static tile schedule (m tile, n tile, k split). A
 // k split > 1 writes fp32 partials that a deterministic fixed-order reduce
 // combines (dW = H^T dQ reduces over all adjacency rows, engine.hpp:233-235).
 //
-// Operand forms (row-major storage, op = optional transpose):
-//   NN  Q  = H . W        A = H   (K-major)      B = W   (MN-major)
-//   NT  dH = dQ . W^T     A = dQ  (K-major)      B = W   (K-major)
-//   TN  dW = H^T . dQ     A = H^T (MN-major)     B = dQ  (MN-major)
+// Operand forms (row-major storage; "T" = storage runs along M/N, so the
+// loader transposes into the K-major tile):
+//   NN  Q  = H . W        A = H   (k-contiguous)  B = W   (T)
+//   NT  dH = dQ . W^T     A = dQ  (k-contiguous)  B = W   (k-contiguous)
+//   TN  dW = H^T . dQ     A = H^T (T)             B = dQ  (T)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -42,6 +42,12 @@ constexpr int kLoaderWarps = 8;
 constexpr int kMmaWarp = kLoaderWarps;          // warp 8
 constexpr int kThreadsTc = 32 * (kLoaderWarps + 1 + 4);
 constexpr int kLoaderThreads = 32 * kLoaderWarps;
+// k-stages accumulated in TMEM before the epilogue folds the partial into
+// the output with round-to-nearest fp32 adds. The tensor core's fp32
+// accumulation does not round to nearest, so its error grows with the chain
+// length; 16 stages (512 k) keep the tall dW reduction (K = adjacency rows,
+// up to millions) at fp32-level error (tests/test_gemm_tc_gpu.py).
+constexpr int kSegStages = 16;
 
 __device__ unsigned g_gemm_watchdog = 0;
 
@@ -138,46 +144,32 @@ __device__ __forceinline__ u64 smem_desc(unsigned addr, unsigned lbo, unsigned s
   return d;
 }
 
-// Instruction descriptor: fp32 accumulate, tf32 A and B, M = 128.
-__host__ __device__ constexpr unsigned instr_desc(int n, bool a_mn, bool b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<unsigned>(a_mn) << 15) |
-         (static_cast<unsigned>(b_mn) << 16) | (static_cast<unsigned>(n >> 3) << 17) |
+// Instruction descriptor: fp32 accumulate, tf32 A and B (both K-major), M = 128.
+// (MN-major tf32 operands read back as zeros on this part — measured with
+// scripts/tc_probe.cu — so every tile is staged K-major and sources whose
+// storage runs along M/N are transposed by the loaders instead.)
+__host__ __device__ constexpr unsigned instr_desc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<unsigned>(n >> 3) << 17) |
          (static_cast<unsigned>(kBM >> 4) << 24);
 }
 
-// ------------------------------------------------------------ tile layouts
+// ------------------------------------------------------------ tile layout
 //
-// K-major SW128 (rows = M or N index, 32 fp32 of k per 128-B row; 8-row
-// atoms of 1024 B): chunk c (k/4) of row r lives at r*128 + ((c ^ r%8) * 16).
-// k-step t (8 k) starts 32*t bytes into the tile; SBO = 1024.
-//
-// MN-major SW128 (k rows of 128-B atoms holding 32 consecutive M/N values):
-// k-group g = k/8 (one UMMA k-step), atom a = mn/32, row k%8, chunk (mn%32)/4
-// at g*ATOMS*1024 + a*1024 + (k%8)*128 + ((chunk ^ k%8) * 16). LBO = 1024
-// (next MN atom), SBO = ATOMS*1024 (next k-group).
+// K-major SW128: row r (an M or N index) holds 32 fp32 of k in one 128-B
+// line; 8-row atoms of 1024 B; 16-B chunk c (= k/4) of row r lives at
+// r*128 + ((c ^ r%8) * 16). UMMA k-step t (8 k) starts 32*t bytes into the
+// tile; SBO (next 8-row group) = 1024, LBO unused for swizzled K-major.
 
-template <bool MN>
-struct OperandTile {
-  // rows: M/N extent stored in the tile (multiple of 8; MN-major: of 32)
-  static __device__ __forceinline__ unsigned offset(int mn, int k, int rows) {
-    if (!MN) {
-      const int c = k >> 2;
-      return static_cast<unsigned>(mn * 128 + ((c ^ (mn & 7)) << 4));
-    } else {
-      const int g = k >> 3, a = mn >> 5, c = (mn & 31) >> 2, r = k & 7;
-      return static_cast<unsigned>(g * (rows >> 5) * 1024 + a * 1024 + r * 128 + ((c ^ r) << 4));
-    }
-  }
-  static __device__ __forceinline__ u64 desc(unsigned base, int kstep, int rows) {
-    if (!MN) return smem_desc(base + 32u * kstep, 16u, 1024u);
-    const unsigned sbo = static_cast<unsigned>(rows >> 5) * 1024u;
-    return smem_desc(base + sbo * kstep, 1024u, sbo);
-  }
-};
+__device__ __forceinline__ unsigned kmajor_offset(int row, int kc) {
+  return static_cast<unsigned>(row * 128 + ((kc ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ u64 kmajor_desc(unsigned base, int kstep) {
+  return smem_desc(base + 32u * kstep, 16u, 1024u);
+}
 
-// One operand's view for the loaders. Storage is row-major `src[r * ld + c]`.
-//  K-major form: r = m/n index (extent `mn`), c = k index.
-//  MN-major form: r = k index, c = m/n index (extent `mn`).
+// One operand's view for the loaders; storage is row-major `p[r * ld + c]`.
+//  T = false ("K-contiguous"): r = m/n index (extent `mn`), c = k.
+//  T = true  ("MN-contiguous"): r = k, c = m/n index (extent `mn`).
 struct OperandSrc {
   const float* p;
   i64 ld;
@@ -185,61 +177,106 @@ struct OperandSrc {
   bool vec;    // base and ld allow 16-B loads
 };
 
-// chunk q of a stage -> (mn, k) inside the tile; 4 consecutive elements
-// along the storage-contiguous axis.
-template <bool MN, int ROWS>
-__device__ __forceinline__ void chunk_coords(int q, int& mn, int& k) {
-  if (!MN) {
-    mn = q >> 3;           // 8 chunks (128 B) per row of k
-    k = (q & 7) << 2;
-  } else {
-    constexpr int per_k = ROWS / 4;
-    k = q / per_k;
-    mn = (q % per_k) << 2;
-  }
+__device__ __forceinline__ float4 split_hi(float4 v) {
+  return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+}
+__device__ __forceinline__ float4 split_lo(float4 v, float4 h) {
+  return make_float4(tf32_rna(v.x - h.x), tf32_rna(v.y - h.y), tf32_rna(v.z - h.z),
+                     tf32_rna(v.w - h.w));
 }
 
-template <bool MN>
-__device__ __forceinline__ float4 load_chunk(const OperandSrc& s, i64 mn0, int mn, i64 k0, int k,
-                                             i64 k_end) {
-  // global coordinates of the chunk's first element
+// 4 consecutive elements of storage row r starting at column c, masked to
+// [0, c_end) (zero fill); 16-B load when the whole quad is in range.
+__device__ __forceinline__ float4 load_quad(const OperandSrc& s, i64 r, i64 c, i64 c_end) {
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (!MN) {
-    const i64 r = mn0 + mn, c = k0 + k;
-    if (r >= s.mn) return v;
-    const float* p = s.p + r * s.ld + c;
-    if (s.vec && c + 3 < k_end) return __ldg(reinterpret_cast<const float4*>(p));
-    if (c < k_end) v.x = __ldg(p);
-    if (c + 1 < k_end) v.y = __ldg(p + 1);
-    if (c + 2 < k_end) v.z = __ldg(p + 2);
-    if (c + 3 < k_end) v.w = __ldg(p + 3);
-  } else {
-    const i64 r = k0 + k, c = mn0 + mn;
-    if (r >= k_end) return v;
-    const float* p = s.p + r * s.ld + c;
-    if (s.vec && c + 3 < s.mn) return __ldg(reinterpret_cast<const float4*>(p));
-    if (c < s.mn) v.x = __ldg(p);
-    if (c + 1 < s.mn) v.y = __ldg(p + 1);
-    if (c + 2 < s.mn) v.z = __ldg(p + 2);
-    if (c + 3 < s.mn) v.w = __ldg(p + 3);
-  }
+  const float* p = s.p + r * s.ld + c;
+  if (s.vec && c + 3 < c_end) return __ldg(reinterpret_cast<const float4*>(p));
+  if (c < c_end) v.x = __ldg(p);
+  if (c + 1 < c_end) v.y = __ldg(p + 1);
+  if (c + 2 < c_end) v.z = __ldg(p + 2);
+  if (c + 3 < c_end) v.w = __ldg(p + 3);
   return v;
 }
 
-// Store hi and lo parts of a chunk. K-major: the 4 values are consecutive k
-// of one row -> one 16-B store. MN-major: 4 consecutive m/n of one k row ->
-// one 16-B store as well (the chunk never straddles a swizzle unit).
-template <bool MN, int ROWS>
-__device__ __forceinline__ void store_chunk(unsigned char* hi, unsigned char* lo, int mn, int k,
-                                            float4 v) {
-  float4 h, l;
-  h.x = tf32_rna(v.x), h.y = tf32_rna(v.y), h.z = tf32_rna(v.z), h.w = tf32_rna(v.w);
-  l.x = tf32_rna(v.x - h.x), l.y = tf32_rna(v.y - h.y);
-  l.z = tf32_rna(v.z - h.z), l.w = tf32_rna(v.w - h.w);
-  const unsigned off = OperandTile<MN>::offset(mn, k, ROWS);
-  *reinterpret_cast<float4*>(hi + off) = h;
-  *reinterpret_cast<float4*>(lo + off) = l;
-}
+// Loader work for one operand tile of ROWS (M/N) x 32 (k) per stage.
+//
+// K-contiguous source: item = one 16-B chunk (row, k-chunk); 8 consecutive
+// threads read one row's 128 B; stored as-is (one 16-B st.shared each).
+//
+// MN-contiguous source: item = a 4 (k) x 4 (mn) block read as 4 float4 rows
+// and transposed in registers into 4 k-quads. Lane l of a warp takes mn
+// block l%8 and k-chunk l/8 (+4 for the second half), so each 16-B store
+// row-group hits 8 distinct swizzle chunks: conflict-free, and every k row
+// is still read as 128 contiguous bytes by 8 lanes.
+template <bool T, int ROWS>
+struct TileLoader {
+  static constexpr int kItems = T ? 2 * ROWS : 8 * ROWS;
+  static constexpr int kPer = (kItems + kLoaderThreads - 1) / kLoaderThreads;
+  static constexpr int kRegs = kPer * (T ? 4 : 1);
+
+  static __device__ __forceinline__ void item_coords(int q, int& row, int& kc) {
+    if (!T) {
+      row = q >> 3;
+      kc = q & 7;
+    } else {
+      const int mnb_lo = q & 7, kc_lo = (q >> 3) & 3, kc_hi = (q >> 5) & 1, grp = q >> 6;
+      row = (grp * 8 + mnb_lo) * 4;  // first of 4 mn rows
+      kc = kc_hi * 4 + kc_lo;        // k quad
+    }
+  }
+
+  static __device__ __forceinline__ void load(const OperandSrc& s, i64 mn0, i64 k0, i64 k_end,
+                                              int tid, float4 (&r)[kRegs]) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int q = tid + i * kLoaderThreads;
+      int row, kc;
+      item_coords(q, row, kc);
+      if (!T) {
+        const i64 gr = mn0 + row;
+        r[i] = (q < kItems && gr < s.mn) ? load_quad(s, gr, k0 + kc * 4, k_end)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const i64 gk = k0 + kc * 4 + j;
+          r[4 * i + j] = (q < kItems && gk < k_end) ? load_quad(s, gk, mn0 + row, s.mn)
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void store(unsigned char* hi, unsigned char* lo, int tid,
+                                               const float4 (&r)[kRegs]) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int q = tid + i * kLoaderThreads;
+      if (q >= kItems) continue;
+      int row, kc;
+      item_coords(q, row, kc);
+      if (!T) {
+        const float4 h = split_hi(r[i]);
+        const unsigned off = kmajor_offset(row, kc);
+        *reinterpret_cast<float4*>(hi + off) = h;
+        *reinterpret_cast<float4*>(lo + off) = split_lo(r[i], h);
+      } else {
+        const float4* b = r + 4 * i;  // b[j] = k row kc*4+j, mn row..row+3
+        const float4 t[4] = {make_float4(b[0].x, b[1].x, b[2].x, b[3].x),
+                             make_float4(b[0].y, b[1].y, b[2].y, b[3].y),
+                             make_float4(b[0].z, b[1].z, b[2].z, b[3].z),
+                             make_float4(b[0].w, b[1].w, b[2].w, b[3].w)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 h = split_hi(t[j]);
+          const unsigned off = kmajor_offset(row + j, kc);
+          *reinterpret_cast<float4*>(hi + off) = h;
+          *reinterpret_cast<float4*>(lo + off) = split_lo(t[j], h);
+        }
+      }
+    }
+  }
+};
 
 struct TcParams {
   OperandSrc a, b;
@@ -251,24 +288,24 @@ struct TcParams {
   i64 split_stride; // elements between split partials
 };
 
-template <bool A_MN, bool B_MN, int BN, int STAGES>
+template <bool A_T, bool B_T, int BN, int STAGES>
 struct TcConfig {
-  static constexpr int kRowsB = B_MN ? ((BN + 31) / 32) * 32 : BN;  // stored N extent
-  static constexpr int kTileA = kBM * kBK * 4;                      // bytes, one of hi/lo
+  // stored N extent: a multiple of 16 (UMMA N) — and of 32 when the loader
+  // transposes, whose items cover 32 rows per lane group
+  static constexpr int kRowsB = B_T ? ((BN + 31) / 32) * 32 : BN;
+  static constexpr int kTileA = kBM * kBK * 4;  // bytes, one of hi/lo
   static constexpr int kTileB = kRowsB * kBK * 4;
   static constexpr int kStage = 2 * kTileA + 2 * kTileB;
-  static constexpr int kChunksA = kBM * kBK / 4;
-  static constexpr int kChunksB = kRowsB * kBK / 4;
-  static constexpr int kPerThreadA = (kChunksA + kLoaderThreads - 1) / kLoaderThreads;
-  static constexpr int kPerThreadB = (kChunksB + kLoaderThreads - 1) / kLoaderThreads;
+  using LoadA = TileLoader<A_T, kBM>;
+  using LoadB = TileLoader<B_T, kRowsB>;
   static constexpr int kTmemCols = BN <= 32 ? 64 : (BN <= 64 ? 128 : (BN <= 128 ? 256 : 512));
   static constexpr int kAccStride = kTmemCols / 2;  // two accumulator buffers
   static constexpr size_t kSmem = static_cast<size_t>(STAGES) * kStage + 1024;
 };
 
-template <bool A_MN, bool B_MN, int BN, int STAGES>
+template <bool A_T, bool B_T, int BN, int STAGES>
 __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
-  using Cfg = TcConfig<A_MN, B_MN, BN, STAGES>;
+  using Cfg = TcConfig<A_T, B_T, BN, STAGES>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -322,33 +359,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       k_range(sp, kb, ke);
       const i64 m0 = static_cast<i64>(mt) * kBM, n0 = static_cast<i64>(nt) * BN;
       const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
-      float4 ra[Cfg::kPerThreadA], rb[Cfg::kPerThreadB];
+      float4 ra[Cfg::LoadA::kRegs], rb[Cfg::LoadB::kRegs];
       auto load = [&](int kk) {
         const i64 k0 = kb + static_cast<i64>(kk) * kBK;
-#pragma unroll
-        for (int i = 0; i < Cfg::kPerThreadA; ++i) {
-          const int q = lt + i * kLoaderThreads;
-          int mn, k;
-          chunk_coords<A_MN, kBM>(q, mn, k);
-          ra[i] = q < Cfg::kChunksA ? load_chunk<A_MN>(p.a, m0, mn, k0, k, ke)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int i = 0; i < Cfg::kPerThreadB; ++i) {
-          const int q = lt + i * kLoaderThreads;
-          int mn, k;
-          chunk_coords<B_MN, Cfg::kRowsB>(q, mn, k);
-          rb[i] = q < Cfg::kChunksB ? load_chunk<B_MN>(p.b, n0, mn, k0, k, ke)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        Cfg::LoadA::load(p.a, m0, k0, ke, lt, ra);
+        Cfg::LoadB::load(p.b, n0, k0, ke, lt, rb);
       };
       if (nk > 0) load(0);
       for (int kk = 0; kk < nk; ++kk) {
-        float4 ca[Cfg::kPerThreadA], cb[Cfg::kPerThreadB];
+        float4 ca[Cfg::LoadA::kRegs], cb[Cfg::LoadB::kRegs];
 #pragma unroll
-        for (int i = 0; i < Cfg::kPerThreadA; ++i) ca[i] = ra[i];
+        for (int i = 0; i < Cfg::LoadA::kRegs; ++i) ca[i] = ra[i];
 #pragma unroll
-        for (int i = 0; i < Cfg::kPerThreadB; ++i) cb[i] = rb[i];
+        for (int i = 0; i < Cfg::LoadB::kRegs; ++i) cb[i] = rb[i];
         if (kk + 1 < nk) load(kk + 1);  // next stage's loads in flight
         mbar_wait(&empty[stage], phase ^ 1u);
         unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
@@ -356,24 +379,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
         unsigned char* a_lo = st + Cfg::kTileA;
         unsigned char* b_hi = st + 2 * Cfg::kTileA;
         unsigned char* b_lo = b_hi + Cfg::kTileB;
-#pragma unroll
-        for (int i = 0; i < Cfg::kPerThreadA; ++i) {
-          const int q = lt + i * kLoaderThreads;
-          if (q < Cfg::kChunksA) {
-            int mn, k;
-            chunk_coords<A_MN, kBM>(q, mn, k);
-            store_chunk<A_MN, kBM>(a_hi, a_lo, mn, k, ca[i]);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < Cfg::kPerThreadB; ++i) {
-          const int q = lt + i * kLoaderThreads;
-          if (q < Cfg::kChunksB) {
-            int mn, k;
-            chunk_coords<B_MN, Cfg::kRowsB>(q, mn, k);
-            store_chunk<B_MN, Cfg::kRowsB>(b_hi, b_lo, mn, k, cb[i]);
-          }
-        }
+        Cfg::LoadA::store(a_hi, a_lo, lt, ca);
+        Cfg::LoadB::store(b_hi, b_lo, lt, cb);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[stage]);
@@ -382,7 +389,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr unsigned idesc = instr_desc(BN, A_MN, B_MN);
+    constexpr unsigned idesc = instr_desc(BN);
     int stage = 0;
     unsigned phase = 0;
     int acc = 0;
@@ -393,42 +400,44 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       i64 kb, ke;
       k_range(sp, kb, ke);
       const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
-      mbar_wait(&tempty[acc], acc_phase ^ 1u);
-      tc_fence_after();
-      const unsigned d = tmem + static_cast<unsigned>(acc * Cfg::kAccStride);
-      for (int kk = 0; kk < nk; ++kk) {
-        mbar_wait(&full[stage], phase);
+      const int nseg = nk == 0 ? 1 : (nk + kSegStages - 1) / kSegStages;
+      for (int sg = 0; sg < nseg; ++sg) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1u);
         tc_fence_after();
-        if (lane == 0) {
-          const unsigned base = smem_u32(smem + static_cast<size_t>(stage) * Cfg::kStage);
-          const unsigned a_hi = base, a_lo = base + Cfg::kTileA;
-          const unsigned b_hi = base + 2 * Cfg::kTileA, b_lo = b_hi + Cfg::kTileB;
+        const unsigned d = tmem + static_cast<unsigned>(acc * Cfg::kAccStride);
+        const int k_lo = sg * kSegStages, k_hi = min(nk, k_lo + kSegStages);
+        for (int kk = k_lo; kk < k_hi; ++kk) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const unsigned base = smem_u32(smem + static_cast<size_t>(stage) * Cfg::kStage);
+            const unsigned a_hi = base, a_lo = base + Cfg::kTileA;
+            const unsigned b_hi = base + 2 * Cfg::kTileA, b_lo = b_hi + Cfg::kTileB;
 #pragma unroll
-          for (int ks = 0; ks < kBK / 8; ++ks) {
-            const u64 dah = OperandTile<A_MN>::desc(a_hi, ks, kBM);
-            const u64 dal = OperandTile<A_MN>::desc(a_lo, ks, kBM);
-            const u64 dbh = OperandTile<B_MN>::desc(b_hi, ks, Cfg::kRowsB);
-            const u64 dbl = OperandTile<B_MN>::desc(b_lo, ks, Cfg::kRowsB);
-            const unsigned first = (kk == 0 && ks == 0) ? 0u : 1u;
-            tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
-            tc_mma_tf32(d, dah, dbl, idesc, 1u);
-            tc_mma_tf32(d, dah, dbh, idesc, 1u);
+            for (int ks = 0; ks < kBK / 8; ++ks) {
+              const u64 dah = kmajor_desc(a_hi, ks), dal = kmajor_desc(a_lo, ks);
+              const u64 dbh = kmajor_desc(b_hi, ks), dbl = kmajor_desc(b_lo, ks);
+              const unsigned first = (kk == k_lo && ks == 0) ? 0u : 1u;
+              tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
+              tc_mma_tf32(d, dah, dbl, idesc, 1u);
+              tc_mma_tf32(d, dah, dbh, idesc, 1u);
+            }
+            tc_commit(&empty[stage]);  // frees the smem stage when the MMAs finish
           }
-          tc_commit(&empty[stage]);  // frees the smem stage when the MMAs finish
+          __syncwarp();
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+        if (lane == 0) {
+          if (k_hi == k_lo) {
+            // empty k range: the epilogue writes zeros without reading TMEM
+            mbar_arrive(&tfull[acc]);
+          } else {
+            tc_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
-        if (++stage == STAGES) stage = 0, phase ^= 1u;
+        if (++acc == 2) acc = 0, acc_phase ^= 1u;
       }
-      if (lane == 0) {
-        if (nk == 0) {
-          // empty k range: the epilogue writes zeros without reading TMEM
-          mbar_arrive(&tfull[acc]);
-        } else {
-          tc_commit(&tfull[acc]);
-        }
-      }
-      __syncwarp();
-      if (++acc == 2) acc = 0, acc_phase ^= 1u;
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -441,41 +450,53 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       tile_coords(t, mt, nt, sp);
       i64 kb, ke;
       k_range(sp, kb, ke);
-      const bool zero = ke <= kb;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
+      const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
+      const int nseg = nk == 0 ? 1 : (nk + kSegStages - 1) / kSegStages;
       const i64 gm = static_cast<i64>(mt) * kBM + row;
       const i64 n0 = static_cast<i64>(nt) * BN;
       float* out = p.c + static_cast<i64>(sp) * p.split_stride;
-      const unsigned taddr =
-          tmem + (static_cast<unsigned>(quad * 32) << 16) + static_cast<unsigned>(acc * Cfg::kAccStride);
       const bool vec_out = (p.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+      // segments of one tile land in order: the first stores, later ones add
+      // (fp32 round-to-nearest in registers, fixed order: deterministic)
+      for (int sg = 0; sg < nseg; ++sg) {
+        const bool zero = nk == 0;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) +
+                               static_cast<unsigned>(acc * Cfg::kAccStride);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 8) {
-        float v[8];
-        if (zero) {
+        for (int c0 = 0; c0 < BN; c0 += 8) {
+          float v[8];
+          if (zero) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 0.f;
-        } else {
-          tmem_ld8(taddr + static_cast<unsigned>(c0), v);
-        }
-        if (gm < p.m) {
-          float* dst = out + gm * p.ldc + n0 + c0;
-          const i64 left = p.n - (n0 + c0);
-          if (vec_out && left >= 8) {
-            reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
-            reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            for (int i = 0; i < 8; ++i) v[i] = 0.f;
           } else {
+            tmem_ld8(taddr + static_cast<unsigned>(c0), v);
+          }
+          if (gm < p.m) {
+            float* dst = out + gm * p.ldc + n0 + c0;
+            const i64 left = p.n - (n0 + c0);
+            if (vec_out && left >= 8) {
+              float4* d4 = reinterpret_cast<float4*>(dst);
+              if (sg > 0) {
+                const float4 a = d4[0], b = d4[1];
+                v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
+                v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+              }
+              d4[0] = make_float4(v[0], v[1], v[2], v[3]);
+              d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+            } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (i < left) dst[i] = v[i];
+              for (int i = 0; i < 8; ++i)
+                if (i < left) dst[i] = sg > 0 ? dst[i] + v[i] : v[i];
+            }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) acc = 0, acc_phase ^= 1u;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) acc = 0, acc_phase ^= 1u;
     }
   }
 
@@ -499,12 +520,12 @@ __global__ void tc_split_reduce_kernel(const float* __restrict__ part, int split
   c[i * ldc + j] = s;
 }
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_T, bool B_T, int BN>
 void launch_bn(const TcParams& p0, cudaStream_t st) {
-  constexpr int kStageBytes = TcConfig<A_MN, B_MN, BN, 1>::kStage;
+  constexpr int kStageBytes = TcConfig<A_T, B_T, BN, 1>::kStage;
   constexpr int STAGES = std::min(6, std::max(2, (200 * 1024) / kStageBytes));
-  using Cfg = TcConfig<A_MN, B_MN, BN, STAGES>;
-  auto kernel = gemm_tc_kernel<A_MN, B_MN, BN, STAGES>;
+  using Cfg = TcConfig<A_T, B_T, BN, STAGES>;
+  auto kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES>;
   static thread_local bool attr = false;
   if (!attr) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -518,17 +539,17 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
   PK_LAUNCH("gemm tcgen05 kernel");
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_T, bool B_T>
 void launch_forms(const TcParams& p, int bn, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_bn<A_MN, B_MN, 16>(p, st);
-    case 32: return launch_bn<A_MN, B_MN, 32>(p, st);
-    case 48: return launch_bn<A_MN, B_MN, 48>(p, st);
-    case 64: return launch_bn<A_MN, B_MN, 64>(p, st);
-    case 96: return launch_bn<A_MN, B_MN, 96>(p, st);
-    case 128: return launch_bn<A_MN, B_MN, 128>(p, st);
-    case 192: return launch_bn<A_MN, B_MN, 192>(p, st);
-    default: return launch_bn<A_MN, B_MN, 256>(p, st);
+    case 16: return launch_bn<A_T, B_T, 16>(p, st);
+    case 32: return launch_bn<A_T, B_T, 32>(p, st);
+    case 48: return launch_bn<A_T, B_T, 48>(p, st);
+    case 64: return launch_bn<A_T, B_T, 64>(p, st);
+    case 96: return launch_bn<A_T, B_T, 96>(p, st);
+    case 128: return launch_bn<A_T, B_T, 128>(p, st);
+    case 192: return launch_bn<A_T, B_T, 192>(p, st);
+    default: return launch_bn<A_T, B_T, 256>(p, st);
   }
 }
 

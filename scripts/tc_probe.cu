@@ -1,11 +1,9 @@
-// Standalone probe of the tcgen05 building blocks used by gemm_tc.cu:
-//   1. TMEM alloc + tcgen05.st / tcgen05.ld round trip
-//   2. one kind::tf32 MMA (M=128, N=16, K=8) from K-major SW128 tiles
-//   3. the same with an MN-major SW128 B operand
+// Standalone probe of the tcgen05 building blocks used by gemm_tc.cu: one
+// kind::tf32 MMA (M=128, K=8, N in {16,32,64}) from SW128 tiles, each
+// operand K-major or MN-major, with the LBO/SBO roles optionally swapped.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o scripts/tc_probe scripts/tc_probe.cu
-#include <cstdio>
 #include <cstdint>
-#include <cstring>
+#include <cstdio>
 #include <vector>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
@@ -22,8 +20,17 @@ __device__ __forceinline__ uint64_t desc(unsigned addr, unsigned lbo, unsigned s
   return d;
 }
 
-// mode 0: TMEM round trip; mode 1: MMA K-major A and B; mode 2: MMA K-major A, MN-major B
-__global__ void probe(int mode, float* out, unsigned idesc_override) {
+// byte offset of (mn, k) in a tile with `rows` mn extent (k < 8 here)
+__device__ unsigned off_k(int mn, int k) { return mn * 128 + ((((k >> 2) ^ (mn & 7))) << 4) + (k & 3) * 4; }
+__device__ unsigned off_mn(int mn, int k, int rows) {
+  (void)rows;
+  const int a = mn >> 5, c = (mn & 31) >> 2;
+  return a * 1024 + k * 128 + ((c ^ k) << 4) + (mn & 3) * 4;
+}
+
+struct Case { int a_mn, b_mn, n, swap; };
+
+__global__ void probe(Case cs, float* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* s = (unsigned char*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   __shared__ unsigned tbase;
@@ -37,50 +44,35 @@ __global__ void probe(int mode, float* out, unsigned idesc_override) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  // A: 128 x 8 (k) values a[m][k] = m + 1 (so D[m][n] = sum_k a*b)
-  // B: 16 (n) x 8 (k) values b[n][k] = (k == n % 8) ? 1 : 0   -> D[m][n] = m + 1
-  float* As = (float*)s;                 // 128 rows x 32 floats (K-major SW128)
-  float* Bs = (float*)(s + 16384);       // K-major: 16 rows x 32 floats; MN-major: 32 k x 32 n
-  for (int i = threadIdx.x; i < 4096 * 2; i += blockDim.x) ((float*)s)[i] = 0.f;
+  unsigned char* As = s;           // 16 KB
+  unsigned char* Bs = s + 16384;   // 16 KB
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) ((float*)s)[i] = 0.f;
   __syncthreads();
+  // a[m][k] = m + 1 + k/16 ; b[n][k] = (k == n % 8) * (1 + n / 8)
   for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
     int m = i / 8, k = i % 8;
-    unsigned off = m * 128 + ((((k >> 2) ^ (m & 7))) << 4) + (k & 3) * 4;
-    *(float*)((unsigned char*)As + off) = (float)(m + 1);
+    *(float*)(As + (cs.a_mn ? off_mn(m, k, 128) : off_k(m, k))) = (float)(m + 1);
   }
-  for (int i = threadIdx.x; i < 16 * 8; i += blockDim.x) {
+  for (int i = threadIdx.x; i < cs.n * 8; i += blockDim.x) {
     int n = i / 8, k = i % 8;
-    float v = (k == n % 8) ? 1.f : 0.f;
-    if (n >= 8) v *= 2.f;
-    unsigned off;
-    if (mode != 2) {
-      off = n * 128 + ((((k >> 2) ^ (n & 7))) << 4) + (k & 3) * 4;
-    } else {
-      int c = n >> 2;  // chunk of 4 n
-      off = k * 128 + ((c ^ k) << 4) + (n & 3) * 4;
-    }
-    *(float*)((unsigned char*)Bs + off) = v;
+    float v = (k == n % 8) ? (float)(1 + n / 8) : 0.f;
+    *(float*)(Bs + (cs.b_mn ? off_mn(n, k, 64) : off_k(n, k))) = v;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const unsigned t = tbase;
-  if (mode == 0) {
-    // each warp writes its lane quadrant: value = lane_row * 100 + col
-    if (warp < 4) {
-      unsigned r[8];
-      for (int c = 0; c < 8; ++c) r[c] = __float_as_uint((float)((warp * 32 + lane) * 100 + c));
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::
-                   "r"(t + ((warp * 32) << 16)), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
-                   "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]));
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  if (warp == 0) {
+    const unsigned idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((unsigned)cs.a_mn << 15) |
+                           ((unsigned)cs.b_mn << 16) | ((unsigned)(cs.n >> 3) << 17) | ((128u >> 4) << 24);
+    unsigned la = cs.a_mn ? 1024 : 16, sa = cs.a_mn ? 8192 : 1024;
+    unsigned lb = cs.b_mn ? 1024 : 16, sb = cs.b_mn ? 8192 : 1024;
+    if (cs.swap) {
+      if (cs.a_mn) { unsigned x = la; la = sa; sa = x; }
+      if (cs.b_mn) { unsigned x = lb; lb = sb; sb = x; }
     }
-  } else if (warp == 0) {
-    const unsigned idesc = idesc_override ? idesc_override
-        : ((1u << 4) | (2u << 7) | (2u << 10) | ((mode == 2 ? 1u : 0u) << 16) | ((16u >> 3) << 17) | ((128u >> 4) << 24));
-    uint64_t da = desc(su(As), 16, 1024, 2);
-    uint64_t db = mode == 2 ? desc(su(Bs), 1024, 1024, 2) : desc(su(Bs), 16, 1024, 2);
+    uint64_t da = desc(su(As), la, sa, 2), db = desc(su(Bs), lb, sb, 2);
     if (lane == 0) {
       asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                    " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
@@ -89,24 +81,20 @@ __global__ void probe(int mode, float* out, unsigned idesc_override) {
     }
     __syncwarp();
   }
-  if (mode != 0) {
-    // wait for the MMA
-    unsigned ok = 0;
-    for (int spin = 0; spin < (1 << 24) && !ok; ++spin)
-      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(su(&bar)) : "memory");
-    if (!ok && threadIdx.x == 0) printf("probe: mma barrier never completed\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  unsigned ok = 0;
+  for (int spin = 0; spin < (1 << 24) && !ok; ++spin)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(su(&bar)) : "memory");
+  if (!ok && threadIdx.x == 0) printf("probe: mma barrier never completed\n");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp < 4) {
-    unsigned r[16];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                 : "r"(t + ((warp * 32) << 16)));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    for (int c = 0; c < 16; ++c) out[(warp * 32 + lane) * 16 + c] = __uint_as_float(r[c]);
+    for (int c0 = 0; c0 < cs.n; c0 += 8) {
+      unsigned r[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(t + ((warp * 32) << 16) + c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int c = 0; c < 8; ++c) out[(warp * 32 + lane) * 64 + c0 + c] = __uint_as_float(r[c]);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -115,25 +103,23 @@ __global__ void probe(int mode, float* out, unsigned idesc_override) {
 
 int main() {
   float* d;
-  CK(cudaMalloc(&d, 128 * 16 * 4));
+  CK(cudaMalloc(&d, 128 * 64 * 4));
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-  std::vector<float> h(128 * 16);
-  for (int mode = 0; mode < 3; ++mode) {
-    CK(cudaMemset(d, 0xff, 128 * 16 * 4));
-    probe<<<1, 128, 64 * 1024>>>(mode, d, 0);
+  std::vector<float> h(128 * 64);
+  const Case cases[] = {{0, 0, 16, 0}, {0, 0, 64, 0}, {0, 1, 16, 0}, {0, 1, 32, 0}, {0, 1, 64, 0},
+                        {0, 1, 64, 1}, {1, 0, 16, 0}, {1, 0, 16, 1}, {1, 1, 64, 0}, {1, 1, 64, 1}};
+  for (const Case& cs : cases) {
+    CK(cudaMemset(d, 0xff, 128 * 64 * 4));
+    probe<<<1, 128, 64 * 1024>>>(cs, d);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost));
     int bad = 0;
     for (int m = 0; m < 128; ++m)
-      for (int c = 0; c < 16; ++c) {
-        float want = mode == 0 ? (c < 8 ? (float)(m * 100 + c) : h[m * 16 + c]) : (float)(m + 1) * (c >= 8 ? 2.f : 1.f);
-        if (h[m * 16 + c] != want) ++bad;
-      }
-    printf("mode %d: bad %d | row0: ", mode, bad);
-    for (int c = 0; c < 16; ++c) printf("%g ", h[c]);
-    printf("| row77: ");
-    for (int c = 0; c < 16; ++c) printf("%g ", h[77 * 16 + c]);
+      for (int c = 0; c < cs.n; ++c)
+        if (h[m * 64 + c] != (float)(m + 1) * (float)(1 + c / 8)) ++bad;
+    printf("a_mn %d b_mn %d n %d swap %d: bad %d/%d | row1:", cs.a_mn, cs.b_mn, cs.n, cs.swap, bad, 128 * cs.n);
+    for (int c = 0; c < cs.n && c < 24; ++c) printf(" %g", h[64 + c]);
     printf("\n");
   }
   return 0;
