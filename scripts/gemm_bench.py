@@ -26,7 +26,12 @@ def timeit(fn, it=5):
         e0.record(); fn(); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     return min(ts)
 
-modes = sys.argv[1:] or ["fast", "cublas"]
+args = [a for a in sys.argv[1:] if not a.startswith("--only=")]
+only = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--only=")]
+modes = args or ["fast", "cublas"]
+if only:  # e.g. --only=NN,2097152,256,256
+    f, m_, n_, k_ = only[0].split(",")
+    shapes = [(f, int(m_), int(n_), int(k_))]
 tot = {m: 0.0 for m in modes}
 for form, m, n, kk in shapes:
     ta, tb = form[0] == "T", form[1] == "T"

@@ -1,0 +1,109 @@
+"""torchrun worker for tests/test_multigpu_gpu.py: one rank per GPU runs one
+forward+backward pass of the device engine on grid --grid and rank 0 checks
+the reassembled logits / dW / dF0 against the reference's own distributed
+pass at the same grid (oracle/_ref, ref_distributed_pass ->
+rank_forward_backward, trainer.hpp:478-527), the way test_engine.cpp:30-84
+reassembles and compares. Also runs --epochs of train_distributed and checks
+the loss curve against the reference's train_distributed on the same grid.
+
+    torchrun --nproc-per-node 2 tests/mp/engine_pass_worker.py --grid 2,1,1
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from paper_2505_04083_b200 import distributed as D, graph, trainer  # noqa: E402
+from paper_2505_04083_b200.layout import GridConfig  # noqa: E402
+
+
+def nrel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    den = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--grid", default="2,1,1")
+    ap.add_argument("--scale", type=int, default=11)
+    ap.add_argument("--edges", type=int, default=20000)
+    ap.add_argument("--feat", type=int, default=12)
+    ap.add_argument("--classes", type=int, default=5)
+    ap.add_argument("--hidden", default="16,16")
+    ap.add_argument("--mode", default="parity")
+    ap.add_argument("--epochs", type=int, default=4)
+    ap.add_argument("--block-count", type=int, default=0)
+    args = ap.parse_args()
+    grid = GridConfig(*[int(g) for g in args.grid.split(",")])
+    hidden = [int(h) for h in args.hidden.split(",")]
+    rank, world, local = D.dist_env()
+    torch.cuda.set_device(local)
+    D.init_control_plane()
+    mode = trainer.PK_MODE_PARITY if args.mode == "parity" else trainer.PK_MODE_FAST
+    opts = trainer.TrainOptions(hidden_dims=hidden, mode=mode, epochs=args.epochs,
+                                hub_threshold=64, block_count=args.block_count)
+    pre = graph.preprocess(graph.synth_rmat(args.scale, args.edges, args.feat, args.classes,
+                                            seed=2), perm_seed=2)
+    # --- one pass, reassembled like test_engine.cpp:30-84
+    eng = trainer.RankEngine(pre.n, pre.feat_dim, pre.num_classes, grid, rank, opts, local)
+    eng.comm_init(D.broadcast_unique_id(trainer.nccl_unique_id), world)
+    eng.load(pre)
+    loss, acc = eng.forward_backward(0)
+    L = len(eng.dims) - 1
+    mine = {"fout": eng.tensor(trainer.PK_T_FOUT).cpu().numpy(),
+            "dw": [eng.tensor(trainer.PK_T_DW, l).cpu().numpy() for l in range(L)],
+            "df0": eng.tensor(trainer.PK_T_DF0).cpu().numpy(), "loss": loss, "acc": acc}
+    dims = list(eng.dims)
+    eng.close()
+    allr = [None] * world
+    dist.all_gather_object(allr, mine)
+    # --- train_distributed over epochs
+    res = D.train_distributed(lambda: pre, grid, opts)
+    report = {"grid": args.grid, "mode": args.mode}
+    ok = True
+    if rank == 0:
+        from oracle import ref
+        rpre = ref.synth_rmat(args.scale, args.edges, args.feat, args.classes, seed=2).preprocess(2)
+        want = rpre.distributed_pass(tuple(grid_t for grid_t in (grid.gx, grid.gy, grid.gz)),
+                                     hidden=hidden, seed=0, block_count=args.block_count)
+        logits, dw, df0 = trainer.gather_rank_pass(allr, grid, pre.n, dims)
+        tol = 1e-5 if args.mode == "parity" else 1e-4
+        # two members per axis: a + b = b + a, so PARITY sums are the
+        # reference's bit for bit; wider axes reduce in NCCL's order
+        two_max = max(grid.gx, grid.gy, grid.gz) <= 2
+        logit_tol = 0.0 if (args.mode == "parity" and two_max) else 1e-5
+        report["loss_rel"] = abs(allr[0]["loss"] - want["loss"]) / abs(want["loss"])
+        report["losses_equal_across_ranks"] = len({round(r["loss"], 12) for r in allr}) == 1
+        report["logits_bitwise"] = bool(np.array_equal(logits.view(np.uint32),
+                                                       want["logits"].view(np.uint32)))
+        report["logits_nrel"] = nrel(logits, want["logits"])
+        report["dw_nrel"] = [nrel(a, b) for a, b in zip(dw, want["dw"])]
+        report["df0_nrel"] = nrel(df0, want["df0"])
+        curve = rpre.train_distributed((grid.gx, grid.gy, grid.gz), hidden=hidden, seed=0,
+                                       epochs=args.epochs, params=True)
+        got = np.array([g["loss"] for g in res.global_metrics])
+        report["curve_rel"] = (np.abs(got - curve["loss"]) / curve["loss"]).tolist()
+        report["w_nrel"] = [nrel(a, b) for a, b in zip(res.weights, curve["weights"])]
+        report["f0_nrel"] = nrel(res.features, curve["features"])
+        ok = (report["loss_rel"] <= 1e-6 and report["losses_equal_across_ranks"]
+              and report["logits_nrel"] <= logit_tol
+              and max(report["dw_nrel"]) <= tol and report["df0_nrel"] <= tol
+              and max(report["curve_rel"]) <= 1e-4 and max(report["w_nrel"]) <= 1e-4
+              and report["f0_nrel"] <= 1e-4)
+        report["ok"] = bool(ok)
+        print("MPRESULT " + json.dumps(report), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

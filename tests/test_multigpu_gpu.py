@@ -1,0 +1,70 @@
+"""Multi-GPU engine parity (one process per GPU, NCCL axis communicators)
+against the reference's distributed pass and train_distributed at the same
+grid. Needs >= 2 GPUs on one box (`gpurun --gpus 2|4`); skipped otherwise."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+WORKER = os.path.join(HERE, "mp", "engine_pass_worker.py")
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run(nproc, *args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           WORKER, *args]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    lines = [l for l in p.stdout.splitlines() if l.startswith("MPRESULT ")]
+    assert lines, p.stdout[-3000:] + p.stderr[-3000:]
+    rep = json.loads(lines[-1][len("MPRESULT "):])
+    assert p.returncode == 0 and rep["ok"], rep
+    return rep
+
+
+def _grids(g):
+    out = []
+    for gx in range(1, g + 1):
+        if g % gx:
+            continue
+        for gy in range(1, g // gx + 1):
+            if (g // gx) % gy == 0:
+                out.append(f"{gx},{gy},{g // gx // gy}")
+    return out
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("grid", _grids(2))
+def test_two_gpu_grids_match_reference(cuda, grid):
+    rep = _run(2, "--grid", grid)
+    assert rep["logits_bitwise"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_gpu_fast_mode_and_blocks(cuda):
+    _run(2, "--grid", "2,1,1", "--mode", "fast", "--block-count", "3")
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("grid", _grids(4))
+def test_four_gpu_grids_match_reference(cuda, grid):
+    _run(4, "--grid", grid)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 8, reason="needs 8 GPUs")
+@pytest.mark.parametrize("grid", ["2,2,2", "8,1,1", "1,1,8", "4,1,2"])
+def test_eight_gpu_grids_match_reference(cuda, grid):
+    _run(8, "--grid", grid)
