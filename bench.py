@@ -46,7 +46,18 @@ CONFIGS = {
                workload="Reddit-shaped flat RMAT s18 (262,144 nodes, 57.3M edges), "
                         "3-layer GCN 602-128-128-41"),
 }
-GRIDS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 1, 2), 8: (2, 2, 2)}
+# One 8-GPU NVSwitch box: every axis is intra-node at the measured NCCL bus
+# bandwidth (B200_PROFILING: 725 GB/s all-reduce busBW at 1 GiB).
+B200_MACHINE = dict(g_node=8, beta_intra=725e9, beta_inter=50e9, bytes_per_scalar=4)
+
+
+def pick_grid(gpus, n, nnz, dims):
+    """The performance model's choice (rank_configs, perf_model.cpp:207-229)
+    for this dataset on this machine."""
+    from paper_2505_04083_b200 import perf_model as pm
+    best = pm.rank_configs(gpus, pm.DatasetStats(n, nnz, list(dims)),
+                           pm.MachineParams(**B200_MACHINE), pm.default_coefficients())[0]
+    return tuple(best.shape)
 
 
 def parse():
@@ -172,8 +183,10 @@ def run_reference(args):
     import torch
     torch.cuda.set_device(local)
     cfg = CONFIGS[args.config]
-    grid = tuple(int(x) for x in args.grid.split(",")) if args.grid else GRIDS[args.gpus]
     pre = build_dataset(cfg, local)
+    dims = [cfg["feat"], *cfg["hidden"], cfg["classes"]]
+    grid = (tuple(int(x) for x in args.grid.split(",")) if args.grid
+            else pick_grid(args.gpus, pre.n, pre.a_even.nnz, dims))
     threads = os.cpu_count() or 1
     vals = []
     for step in range(args.warmup + args.steps):
@@ -213,9 +226,6 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
-    grid = tuple(int(x) for x in args.grid.split(",")) if args.grid else GRIDS[args.gpus]
-    gridc = layout.GridConfig(*grid)
-    assert gridc.size == world
 
     def new_uid():
         if world == 1:
@@ -230,6 +240,11 @@ def run_ours(args):
     pre = build_dataset(cfg, local)
     t_build = time.time() - t_build
     n, nnz = pre.n, pre.a_even.nnz
+    dims = [cfg["feat"], *cfg["hidden"], cfg["classes"]]
+    grid = (tuple(int(x) for x in args.grid.split(",")) if args.grid
+            else pick_grid(world, n, nnz, dims))
+    gridc = layout.GridConfig(*grid)
+    assert gridc.size == world, (grid, world)
 
     eng = trainer.RankEngine(pre.n, pre.feat_dim, pre.num_classes, gridc, rank, opts, local)
     if world > 1:

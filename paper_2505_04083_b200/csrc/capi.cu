@@ -73,21 +73,15 @@ void spmm_common(const pk_csr* a, i64 r0, i64 r1, const float* x, i64 x_rows, i6
                                shape(x_rows, d));
   check(r0 >= 0 && r0 <= r1 && r1 <= a->rows, std::string(who) + ": row range out of bounds");
   check(d >= 0 && ldx >= d && ldy >= d, std::string(who) + ": leading dimension smaller than width");
-  SpmmArgs args;
-  args.rp = a->row_ptr;
-  args.ci = a->col_idx;
-  args.val = a->values;
-  args.x = x;
-  args.ldx = ldx;
-  args.y = y;
-  args.ldy = ldy;
-  args.r0 = r0;
-  args.nrows = r1 - r0;
   if (plan) {
-    args.hub_threshold = plan->threshold;
-    args.hub_rows = spmm_plan_range(*plan, r0, r1, &args.hub_count, st);
+    spmm_run(*plan, *a, r0, r1, x, ldx, d, y, ldy, st);
+  } else {
+    // a one-off call builds a throwaway plan (the engine keeps one per shard)
+    SpmmPlan tmp;
+    spmm_plan_build(tmp, *a, 0, st);
+    spmm_run(tmp, *a, r0, r1, x, ldx, d, y, ldy, st);
+    PK_CUDA(cudaStreamSynchronize(st));
   }
-  spmm_launch(args, d, st);
   if (flops) *flops += 2 * nnz_of_rows(a, r0, r1, st) * static_cast<u64>(d);
 }
 

@@ -300,20 +300,8 @@ void Engine::forward_layer(int l, bool fault) {
   for (int b = 0; b < blocks; ++b) {
     const i64 r0 = chunk_start(sh.a.rows, blocks, b), r1 = chunk_start(sh.a.rows, blocks, b + 1);
     clock_.begin(0, st_);
-    SpmmArgs args;
-    args.rp = sh.a.row_ptr;
-    args.ci = sh.a.col_idx;
-    args.val = sh.a.values;
-    args.x = f;
-    args.ldx = ldf;
-    args.y = h.p() + r0 * h.ld;
-    args.ldy = h.ld;
-    args.r0 = r0;
-    args.nrows = r1 - r0;
-    auto& plan = const_cast<SpmmPlan&>(sh.plan_a);
-    args.hub_threshold = plan.threshold;
-    args.hub_rows = spmm_plan_range(plan, r0, r1, &args.hub_count, st_);
-    spmm_launch(args, s.f_cols, st_);
+    spmm_run(const_cast<SpmmPlan&>(sh.plan_a), view(sh.a), r0, r1, f, ldf, s.f_cols,
+             h.p() + r0 * h.ld, h.ld, st_);
     spmm_flops_ += 2 * sh.block_nnz[b] * static_cast<u64>(s.f_cols);
     spmm_bytes_ += spmm_alg_bytes(r1 - r0, sh.block_nnz[b], s.f_cols);
     clock_.end(st_);
@@ -427,20 +415,8 @@ void Engine::backward_layer(int l) {
   clock_.end(st_);
   clock_.begin(5, st_);
   const i64 lddf = pad4(s.f_cols);
-  SpmmArgs args;
-  args.rp = sh.at.row_ptr;
-  args.ci = sh.at.col_idx;
-  args.val = sh.at.values;
-  args.x = dh_.p();
-  args.ldx = lddh;
-  args.y = df_.p();
-  args.ldy = lddf;
-  args.r0 = 0;
-  args.nrows = sh.at.rows;
-  auto& plan = const_cast<SpmmPlan&>(sh.plan_at);
-  args.hub_threshold = plan.threshold;
-  args.hub_rows = spmm_plan_range(plan, 0, sh.at.rows, &args.hub_count, st_);
-  spmm_launch(args, s.f_cols, st_);
+  spmm_run(const_cast<SpmmPlan&>(sh.plan_at), view(sh.at), 0, sh.at.rows, dh_.p(), lddh, s.f_cols,
+           df_.p(), lddf, st_);
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.f_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.f_cols);
   clock_.end(st_);

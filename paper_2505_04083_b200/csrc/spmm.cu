@@ -8,24 +8,31 @@
 // result is bit-identical to the CPU reference. All parallelism is across
 // rows and columns, never across k.
 //
-// The operation is HBM/gather bound (8 B per nonzero of index +
-// value, plus one gathered feature row per nonzero). Design:
-//   * short rows ("warp path"): a LANES-wide lane group owns a row; lanes
-//     span the feature columns with 16-B (or 8-/4-B) vector loads so each
-//     gathered row is read with full sectors; the (col, val) pairs are
-//     fetched coalesced, LANES at a time, and broadcast with shuffles; the
-//     gathers are unrolled U deep so each lane keeps U*NV loads in flight.
+// The operation is a gather-bound stream (8 B of index + value
+// per nonzero plus one gathered feature row per nonzero). ncu on the first
+// version showed it issue- and latency-bound, not DRAM-bound (~60 warp
+// instructions per nonzero, 37 % DRAM throughput), so the design minimises
+// per-nonzero instructions and keeps many gathers in flight:
+//   * regular rows ("list kernel"): the plan compacts their nonzeros into
+//     one stream of packed 8-B (col, val) pairs plus a bitmap marking row
+//     ends. A lane group (4-32 lanes, sized to the feature width) takes an
+//     nnz-balanced chunk, loads 32 pairs per coalesced 8-B load, broadcasts
+//     each pair with two shuffles, keeps U gathered 16-B feature slices in
+//     flight per lane, and stores a row when its end bit comes up — a bit
+//     test of a uniform mask instead of per-nonzero row bookkeeping.
 //   * hub rows (RMAT degree skew: median 3, max 155,518 nnz per row at the
 //     products shape): a whole CTA serves one (row, 32*VEC-column slice);
-//     seven loader warps stream the gathered row slices into a shared-memory
-//     ring with cp.async so hundreds of gathers are in flight for the single
-//     sequential chain that the consumer warp runs. Hub CTAs are the first
-//     blocks of the same launch, longest row first, so they overlap the
-//     short-row work.
+//     loader warps stream the gathered row slices into a shared-memory ring
+//     with cp.async so hundreds of gathers are in flight for the single
+//     sequential chain the consumer warp runs. Hub CTAs run on a forked
+//     stream so they overlap the list kernel.
+//   * empty rows are zero-filled.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstring>
+#include <tuple>
 #include <vector>
 
 #include "pk_common.cuh"
@@ -80,33 +87,38 @@ constexpr int kThreads = 256;
 __device__ unsigned g_spmm_watchdog = 0;
 
 // ---------------------------------------------------------------------------
-// short-row path: persistent nnz-balanced stream
-//
-// [r0, r1) is cut into chunks of ~equal nonzeros (whole rows, empty rows
-// included). Each lane group grabs chunks from an atomic counter and walks
-// its chunk's nonzeros as one contiguous stream in windows of LANES entries:
-// the (col, val) window is a single coalesced load (the next one prefetched),
-// and U gathers are in flight regardless of where rows begin and end. Row
-// boundaries are tracked from a LANES-wide batch of row_ptr values; a row's
-// accumulator is stored the moment its last entry is consumed, so every
-// output element still sums its own k terms strictly in order.
+// list kernel: regular rows as one nnz stream
 
-__global__ void spmm_partition_kernel(const u64* __restrict__ rp, i64 r0, i64 r1, int nchunks,
+struct ListArgs {
+  const u64* cv = nullptr;      // packed (val << 32 | col) per nonzero
+  const u32* rl = nullptr;      // row id per list entry
+  const u64* rpc = nullptr;     // nonzero offset per list entry (+1)
+  const u32* endbits = nullptr; // bit k set: nonzero k is the last of its row
+  const float* x = nullptr;
+  i64 ldx = 0;
+  float* y = nullptr;
+  i64 ldy = 0;
+  i64 r0 = 0;                   // y holds rows [r0, ...)
+  int nvec = 0;
+};
+
+// chunk bounds over list entries [i0, i1), ~equal nonzeros per chunk
+__global__ void list_partition_kernel(const u64* __restrict__ rpc, i64 i0, i64 i1, int nchunks,
                                       i64* __restrict__ bounds, int* __restrict__ counters,
                                       int nslices) {
   const i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (t < nslices) counters[t] = 0;
   if (t > nchunks) return;
   if (t == 0 || t == nchunks) {
-    bounds[t] = t == 0 ? r0 : r1;
+    bounds[t] = t == 0 ? i0 : i1;
     return;
   }
-  const u64 base = rp[r0], total = rp[r1] - base;
+  const u64 base = rpc[i0], total = rpc[i1] - base;
   const u64 target = base + total / nchunks * t + (total % nchunks) * t / nchunks;
-  i64 lo = r0, hi = r1;  // first row with rp[row] >= target
+  i64 lo = i0, hi = i1;  // first entry with rpc[entry] >= target
   while (lo < hi) {
     const i64 mid = lo + (hi - lo) / 2;
-    if (rp[mid] < target)
+    if (rpc[mid] < target)
       lo = mid + 1;
     else
       hi = mid;
@@ -114,130 +126,18 @@ __global__ void spmm_partition_kernel(const u64* __restrict__ rp, i64 r0, i64 r1
   bounds[t] = lo;
 }
 
-template <int VEC, int LANES, int NV, int U>
-__device__ __forceinline__ void stream_rows(const SpmmArgs& a, i64 rs, i64 re, int lane,
-                                            unsigned gmask, int vbase, const bool (&valid)[NV]) {
-  using V = typename Vec<VEC>::T;
-  const u64 hub_t = a.hub_threshold;
-  // ends[i] = rp[rb + 1 + i]: end of row rb + i
-  i64 rb = rs;
-  u64 ends = __ldg(a.rp + min(rb + 1 + lane, re));
-  u64 s = __ldg(a.rp + rs);
-  u64 e = __shfl_sync(gmask, ends, 0, LANES);
-  const u64 kend = __ldg(a.rp + re);
-  i64 r = rs;
-  V acc[NV];
-#pragma unroll
-  for (int t = 0; t < NV; ++t) acc[t] = Vec<VEC>::zero();
-
-  auto store = [&](i64 row) {
-    float* yrow = a.y + (row - a.r0) * a.ldy;
-#pragma unroll
-    for (int t = 0; t < NV; ++t)
-      if (valid[t]) *reinterpret_cast<V*>(yrow + (vbase + t * LANES + lane) * VEC) = acc[t];
-  };
-  auto next_row = [&]() {
-    ++r;
-    s = e;
-    if (r < re) {
-      if (r - rb >= LANES) {
-        rb = r;
-        ends = __ldg(a.rp + min(rb + 1 + lane, re));
-      }
-      e = __shfl_sync(gmask, ends, static_cast<int>(r - rb), LANES);
-    }
-  };
-  // skip empty rows (store zeros) and hub rows (owned by hub CTAs); returns
-  // true when a hub was skipped, i.e. the nonzero stream jumps forward
-  auto settle = [&]() {
-    bool jumped = false;
-    while (r < re) {
-      if (s == e) {
-        store(r);  // acc is zero here
-        next_row();
-      } else if (e - s >= hub_t) {
-        next_row();
-        jumped = true;
-      } else {
-        break;
-      }
-    }
-    return jumped;
-  };
-
-  settle();
-  u64 kb = s;
-  u32 c = 0;
-  float v = 0.f;
-  if (r < re && kb + lane < kend) {
-    c = __ldcs(a.ci + kb + lane);
-    v = __ldcs(a.val + kb + lane);
-  }
-  // every window either consumes >= 1 entry or jumps forward, so a chunk
-  // takes at most (its nonzeros + its rows) windows
-  u64 guard = (kend - kb) + static_cast<u64>(re - rs) + 2;
-  while (r < re) {
-    if (guard-- == 0) {
-      if (atomicAdd(&g_spmm_watchdog, 1u) == 0)
-        printf("spmm stream watchdog: rows [%lld, %lld) stuck at row %lld kb %llu\n",
-               static_cast<long long>(rs), static_cast<long long>(re),
-               static_cast<long long>(r), static_cast<unsigned long long>(kb));
-      return;
-    }
-    // prefetch the next window
-    u32 cn = 0;
-    float vn = 0.f;
-    if (kb + LANES + lane < kend) {
-      cn = __ldcs(a.ci + kb + LANES + lane);
-      vn = __ldcs(a.val + kb + LANES + lane);
-    }
-    const int cnt = static_cast<int>(min(static_cast<u64>(LANES), kend - kb));
-    bool jumped = false;
-    for (int j = 0; j < cnt && !jumped && r < re; j += U) {
-      V xv[U][NV];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const u32 cj = __shfl_sync(gmask, c, (j + u) % LANES, LANES);
-        const float* xrow = a.x + static_cast<i64>(cj) * a.ldx;
-        const bool in = j + u < cnt;
-#pragma unroll
-        for (int t = 0; t < NV; ++t)
-          xv[u][t] = (valid[t] && in) ? ldg<V>(xrow + (vbase + t * LANES + lane) * VEC)
-                                      : Vec<VEC>::zero();
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float vj = __shfl_sync(gmask, v, (j + u) % LANES, LANES);
-        if (j + u < cnt && !jumped && r < re) {
-#pragma unroll
-          for (int t = 0; t < NV; ++t) madd(acc[t], vj, xv[u][t]);
-          if (kb + j + u + 1 == e) {  // last entry of row r
-            store(r);
-#pragma unroll
-            for (int t = 0; t < NV; ++t) acc[t] = Vec<VEC>::zero();
-            next_row();
-            jumped = settle();
-          }
-        }
-      }
-    }
-    if (r >= re) break;
-    if (jumped) {  // restart the window at the next regular row
-      kb = s;
-      c = kb + lane < kend ? __ldcs(a.ci + kb + lane) : 0u;
-      v = kb + lane < kend ? __ldcs(a.val + kb + lane) : 0.f;
-    } else {
-      kb += cnt;
-      c = cn;
-      v = vn;
-    }
-  }
+// 32 end bits starting at nonzero k
+__device__ __forceinline__ unsigned end_mask(const u32* __restrict__ bits, u64 k) {
+  const u64 w = k >> 5;
+  const unsigned lo = __ldg(bits + w), hi = __ldg(bits + w + 1);
+  return __funnelshift_r(lo, hi, static_cast<unsigned>(k & 31));
 }
 
 template <int VEC, int LANES, int NV, int U>
 __global__ void __launch_bounds__(kThreads)
-spmm_stream_kernel(SpmmArgs args, const i64* __restrict__ bounds, int nchunks,
-                   int* __restrict__ counters) {
+spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
+                 int* __restrict__ counters) {
+  using V = typename Vec<VEC>::T;
   const int lane = threadIdx.x % LANES;
   const unsigned gmask =
       LANES == 32 ? 0xffffffffu
@@ -245,16 +145,90 @@ spmm_stream_kernel(SpmmArgs args, const i64* __restrict__ bounds, int nchunks,
   const int vbase = static_cast<int>(blockIdx.y) * (NV * LANES);
   bool valid[NV];
 #pragma unroll
-  for (int t = 0; t < NV; ++t) valid[t] = vbase + t * LANES + lane < args.nvec;
+  for (int t = 0; t < NV; ++t) valid[t] = vbase + t * LANES + lane < a.nvec;
   int* counter = counters + blockIdx.y;
+  const float* xlane = a.x + (vbase + lane) * VEC;
+
   for (;;) {
     int t = 0;
     if (lane == 0) t = atomicAdd(counter, 1);
     t = __shfl_sync(gmask, t, 0, LANES);
     if (t >= nchunks) break;
-    const i64 rs = bounds[t], re = bounds[t + 1];
-    if (rs < re) stream_rows<VEC, LANES, NV, U>(args, rs, re, lane, gmask, vbase, valid);
+    const i64 is = bounds[t], ie = bounds[t + 1];
+    if (is >= ie) continue;
+    u64 k = __ldg(a.rpc + is);
+    const u64 kend = __ldg(a.rpc + ie);
+    // row ids of the chunk, LANES at a time
+    i64 rb = is;
+    u32 rid = rb + lane < ie ? __ldg(a.rl + rb + lane) : 0u;
+    int rn = 0;
+    V acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = Vec<VEC>::zero();
+    auto row_done = [&]() {
+      const u32 row = __shfl_sync(gmask, rid, rn, LANES);
+      float* yrow = a.y + (static_cast<i64>(row) - a.r0) * a.ldy + (vbase + lane) * VEC;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        if (valid[q]) *reinterpret_cast<V*>(yrow + q * LANES * VEC) = acc[q];
+        acc[q] = Vec<VEC>::zero();
+      }
+      if (++rn == LANES) {
+        rn = 0;
+        rb += LANES;
+        rid = rb + lane < ie ? __ldg(a.rl + rb + lane) : 0u;
+      }
+    };
+    u64 w = k + lane < kend ? __ldcs(a.cv + k + lane) : 0ull;
+    while (k < kend) {
+      const int cnt = static_cast<int>(min(static_cast<u64>(LANES), kend - k));
+      const u64 wn = k + LANES + lane < kend ? __ldcs(a.cv + k + LANES + lane) : 0ull;
+      const unsigned em = end_mask(a.endbits, k);
+      const u32 wc = static_cast<u32>(w), wv = static_cast<u32>(w >> 32);
+      if (cnt == LANES) {
+#pragma unroll
+        for (int j = 0; j < LANES; j += U) {
+          V xv[U][NV];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const u32 c = __shfl_sync(gmask, wc, j + u, LANES);
+            const float* xr = xlane + static_cast<i64>(c) * a.ldx;
+#pragma unroll
+            for (int q = 0; q < NV; ++q)
+              xv[u][q] = valid[q] ? ldg<V>(xr + q * LANES * VEC) : Vec<VEC>::zero();
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const float v = __uint_as_float(__shfl_sync(gmask, wv, j + u, LANES));
+#pragma unroll
+            for (int q = 0; q < NV; ++q) madd(acc[q], v, xv[u][q]);
+            if ((em >> (j + u)) & 1u) row_done();
+          }
+        }
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          const u32 c = __shfl_sync(gmask, wc, j, LANES);
+          const float v = __uint_as_float(__shfl_sync(gmask, wv, j, LANES));
+          const float* xr = xlane + static_cast<i64>(c) * a.ldx;
+#pragma unroll
+          for (int q = 0; q < NV; ++q)
+            if (valid[q]) madd(acc[q], v, ldg<V>(xr + q * LANES * VEC));
+          if ((em >> j) & 1u) row_done();
+        }
+      }
+      k += cnt;
+      w = wn;
+    }
   }
+}
+
+// y rows listed in `rows` (absolute ids) := 0 over d columns
+__global__ void zero_rows_kernel(const u32* __restrict__ rows, i64 n, i64 r0, float* y, i64 ldy,
+                                 i64 d) {
+  const i64 total = n * d;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    y[(static_cast<i64>(rows[i / d]) - r0) * ldy + i % d] = 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -442,30 +416,31 @@ spmm_hub_kernel(SpmmArgs args) {
   }
 }
 
+
 // ---------------------------------------------------------------------------
 // launch selection
 
-struct StreamWorkspace {
+struct ListWorkspace {
   DevBuf<i64> bounds;
   DevBuf<int> counters;
 };
 
 template <int VEC, int LANES, int NV>
-void launch_stream(const SpmmArgs& a, cudaStream_t st) {
-  constexpr int U0 = NV >= 4 ? 2 : (NV == 2 ? 4 : 8);
-  constexpr int U = U0 < LANES ? U0 : LANES;
-  auto kernel = spmm_stream_kernel<VEC, LANES, NV, U>;
+void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
+  constexpr int U = NV >= 4 ? 4 : 8;
+  auto kernel = spmm_list_kernel<VEC, LANES, NV, (U < LANES ? U : LANES)>;
   const int slices = ceil_div(a.nvec, NV * LANES);
   // ~1-2K nonzeros per chunk at the products shape; never more chunks than rows
-  const i64 nchunks64 = std::max<i64>(1, std::min<i64>(a.nrows, static_cast<i64>(sm_count()) * 512));
+  const i64 nchunks64 =
+      std::max<i64>(1, std::min<i64>(i1 - i0, static_cast<i64>(sm_count()) * 512));
   const int nchunks = static_cast<int>(nchunks64);
-  static thread_local StreamWorkspace ws;
+  static thread_local ListWorkspace ws;
   ws.bounds.ensure(nchunks + 1);
   ws.counters.ensure(std::max(slices, 1));
-  spmm_partition_kernel<<<ceil_div(nchunks + 1, 256), 256, 0, st>>>(a.rp, a.r0, a.r0 + a.nrows,
-                                                                    nchunks, ws.bounds.p,
-                                                                    ws.counters.p, slices);
-  PK_LAUNCH("spmm partition");
+  list_partition_kernel<<<ceil_div(nchunks + 1, 256), 256, 0, st>>>(rpc, i0, i1, nchunks,
+                                                                    ws.bounds.p, ws.counters.p,
+                                                                    slices);
+  PK_LAUNCH("spmm list partition");
   static thread_local int occ = 0;
   if (occ == 0) {
     PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0));
@@ -477,7 +452,7 @@ void launch_stream(const SpmmArgs& a, cudaStream_t st) {
                        (nchunks + groups_per_block - 1) / groups_per_block));
   dim3 grid(static_cast<unsigned>(blocks), slices);
   kernel<<<grid, kThreads, 0, st>>>(a, ws.bounds.p, nchunks, ws.counters.p);
-  PK_LAUNCH("spmm stream kernel");
+  PK_LAUNCH("spmm list kernel");
 }
 
 template <int VEC>
@@ -496,31 +471,21 @@ void launch_hub(const SpmmArgs& a, cudaStream_t st) {
 }
 
 template <int VEC>
-void dispatch_vec(const SpmmArgs& a, cudaStream_t st) {
+void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
   const int nv = a.nvec;
-  // Hub CTAs go first on a forked stream so they hold their SMs while the
-  // short-row blocks stream through the rest of the machine.
-  SideStream& side = side_stream();
-  if (a.hub_blocks > 0) {
-    PK_CUDA(cudaEventRecord(side.fork, st));
-    PK_CUDA(cudaStreamWaitEvent(side.stream, side.fork, 0));
-    launch_hub<VEC>(a, side.stream);
-    PK_CUDA(cudaEventRecord(side.join, side.stream));
-  }
   // lane-group width: smallest power of two covering the row's vectors
   if (nv <= 4)
-    launch_stream<VEC, 4, 1>(a, st);
+    launch_list<VEC, 4, 1>(a, i0, i1, rpc, st);
   else if (nv <= 8)
-    launch_stream<VEC, 8, 1>(a, st);
+    launch_list<VEC, 8, 1>(a, i0, i1, rpc, st);
   else if (nv <= 16)
-    launch_stream<VEC, 16, 1>(a, st);
+    launch_list<VEC, 16, 1>(a, i0, i1, rpc, st);
   else if (nv <= 32)
-    launch_stream<VEC, 32, 1>(a, st);
+    launch_list<VEC, 32, 1>(a, i0, i1, rpc, st);
   else if (nv <= 64)
-    launch_stream<VEC, 32, 2>(a, st);
+    launch_list<VEC, 32, 2>(a, i0, i1, rpc, st);
   else
-    launch_stream<VEC, 32, 4>(a, st);  // wider rows split across blockIdx.y
-  if (a.hub_blocks > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
+    launch_list<VEC, 32, 4>(a, i0, i1, rpc, st);  // wider rows split across blockIdx.y
 }
 
 int pick_vec(const float* x, i64 ldx, const float* y, i64 ldy, i64 d) {
@@ -534,95 +499,268 @@ int pick_vec(const float* x, i64 ldx, const float* y, i64 ldy, i64 d) {
   return 1;
 }
 
+// ---------------------------------------------------------------------------
+// plan construction (device side; runs once per shard)
+
+__global__ void classify_rows_kernel(const u64* __restrict__ rp, i64 rows, u64 thr,
+                                     u8* __restrict__ is_reg, u8* __restrict__ is_empty,
+                                     u8* __restrict__ is_hub, u64* __restrict__ reg_len) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < rows;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const u64 len = rp[i + 1] - rp[i];
+    const bool hub = len >= thr, empty = len == 0;
+    is_reg[i] = !hub && !empty;
+    is_empty[i] = empty;
+    is_hub[i] = hub;
+    reg_len[i] = (!hub && !empty) ? len : 0;
+  }
+}
+
+__global__ void iota_rows_kernel(u32* p, i64 n) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    p[i] = static_cast<u32>(i);
+}
+
+// one warp per regular row: copy its (col, val) pairs into the packed
+// stream and mark its last nonzero
+__global__ void compact_rows_kernel(const u64* __restrict__ rp, const u32* __restrict__ ci,
+                                    const float* __restrict__ val, const u32* __restrict__ rl,
+                                    const u64* __restrict__ rpc, i64 regular,
+                                    u64* __restrict__ cv, u32* __restrict__ endbits) {
+  const int lane = threadIdx.x % 32;
+  for (i64 e = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; e < regular;
+       e += static_cast<i64>(gridDim.x) * blockDim.x / 32) {
+    const u32 row = rl[e];
+    const u64 s = rp[row], len = rp[row + 1] - s, dst = rpc[e];
+    for (u64 j = lane; j < len; j += 32)
+      cv[dst + j] = (static_cast<u64>(__float_as_uint(val[s + j])) << 32) | ci[s + j];
+    if (lane == 0) {
+      const u64 last = dst + len - 1;
+      atomicOr(endbits + (last >> 5), 1u << (last & 31));
+    }
+  }
+}
+
+struct NonZero {
+  __device__ bool operator()(u64 v) const { return v != 0; }
+};
+
+__global__ void hub_len_kernel(const u64* __restrict__ rp, const u32* __restrict__ rows, i64 n,
+                               u64* __restrict__ len) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    len[i] = rp[rows[i] + 1] - rp[rows[i]];
+}
+
+unsigned blocks_for(i64 n, int per = 256) {
+  return static_cast<unsigned>(std::max<i64>(1, std::min<i64>((n + per - 1) / per, 1 << 16)));
+}
+
+template <typename F>
+void cub_run(F&& f, cudaStream_t st) {
+  size_t bytes = 0;
+  PK_CUDA(f(nullptr, bytes));
+  DevBuf<unsigned char> tmp(std::max<size_t>(bytes, 1));
+  PK_CUDA(f(tmp.p, bytes));
+  PK_CUDA(cudaStreamSynchronize(st));  // tmp is released at scope exit
+}
+
+// first index in sorted device array [0, n) with value >= key
+template <typename T>
+__global__ void lower_bound_kernel(const T* __restrict__ a, i64 n, i64 key0, i64 key1,
+                                   i64* __restrict__ out) {
+  const int t = threadIdx.x;
+  if (t > 1) return;
+  const i64 key = t == 0 ? key0 : key1;
+  i64 lo = 0, hi = n;
+  while (lo < hi) {
+    const i64 mid = lo + (hi - lo) / 2;
+    if (static_cast<i64>(a[mid]) < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  out[t] = lo;
+}
+
+template <typename T>
+std::pair<i64, i64> range_of(const T* a, i64 n, i64 r0, i64 r1, cudaStream_t st) {
+  if (n == 0) return {0, 0};
+  DevBuf<i64> out(2);
+  lower_bound_kernel<T><<<1, 32, 0, st>>>(a, n, r0, r1, out.p);
+  PK_LAUNCH("spmm plan range");
+  i64 h[2];
+  PK_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PK_CUDA(cudaStreamSynchronize(st));
+  return {h[0], h[1]};
+}
+
+SpmmPlan::Range& plan_range(SpmmPlan& plan, i64 r0, i64 r1, cudaStream_t st) {
+  for (auto& r : plan.ranges)
+    if (r.r0 == r0 && r.r1 == r1) return r;
+  SpmmPlan::Range rg;
+  rg.r0 = r0, rg.r1 = r1;
+  if (r0 == 0 && r1 == plan.rows) {
+    rg.i0 = 0, rg.i1 = plan.regular, rg.e0 = 0, rg.e1 = plan.empty;
+  } else {
+    std::tie(rg.i0, rg.i1) = range_of(plan.rl.p, plan.regular, r0, r1, st);
+    std::tie(rg.e0, rg.e1) = range_of(plan.empty_rows.p, plan.empty, r0, r1, st);
+  }
+  // hub subset keeps the longest-first order
+  if (plan.hub_count) {
+    std::vector<i64> all(plan.hub_count), sel;
+    PK_CUDA(cudaMemcpyAsync(all.data(), plan.hub_rows.p, all.size() * sizeof(i64),
+                            cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    for (i64 r : all)
+      if (r >= r0 && r < r1) sel.push_back(r);
+    rg.hubs = static_cast<int>(sel.size());
+    if (!sel.empty()) {
+      rg.hub_ids.alloc(sel.size());
+      PK_CUDA(cudaMemcpyAsync(rg.hub_ids.p, sel.data(), sel.size() * sizeof(i64),
+                              cudaMemcpyHostToDevice, st));
+      PK_CUDA(cudaStreamSynchronize(st));
+    }
+  }
+  plan.ranges.push_back(std::move(rg));
+  return plan.ranges.back();
+}
+
 }  // namespace
 
-void spmm_launch(SpmmArgs a, i64 d, cudaStream_t st) {
-  if (a.nrows == 0 || d == 0) return;
-  const int vec = pick_vec(a.x, a.ldx, a.y, a.ldy, d);
-  a.nvec = static_cast<int>(d / vec);
-  // hub CTAs serve 32 vectors per slice
-  a.hub_slices = ceil_div(a.nvec, 32);
-  a.hub_blocks = a.hub_count * a.hub_slices;
-  if (vec == 4)
-    dispatch_vec<4>(a, st);
-  else if (vec == 2)
-    dispatch_vec<2>(a, st);
-  else
-    dispatch_vec<1>(a, st);
-}
-
-// ---------------------------------------------------------------------------
-// plan: hub rows (nnz >= threshold) sorted longest first
-
-
 void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_t st) {
+  plan = SpmmPlan();
   plan.rows = a.rows;
-  plan.hub_rows.release();
-  plan.hub_count = 0;
   if (a.rows == 0) return;
-  // Threshold: a row is a hub when a single lane chain over it would outlast
-  // the short-row work spread over the whole GPU several times over.
+  // A row is a hub when one lane chain over it would outlast the rest of the
+  // work spread over the whole GPU; measured on the products shape
+  // (scripts/spmm_probe.py), 2048 nonzeros is the sweet spot.
   const u64 avg = a.nnz / std::max<i64>(1, a.rows);
-  plan.threshold = threshold ? threshold : std::max<u64>(4096, 64 * avg);
-  // host scan of row_ptr is the simplest exact selection; it runs once per
-  // shard at setup (like the reference's precomputed transposes)
-  std::vector<u64> rp(a.rows + 1);
-  PK_CUDA(cudaMemcpyAsync(rp.data(), a.row_ptr, (a.rows + 1) * sizeof(u64),
+  plan.threshold = threshold ? threshold : std::max<u64>(2048, 32 * avg);
+  const i64 n = a.rows;
+  DevBuf<u8> is_reg(n), is_empty(n), is_hub(n);
+  DevBuf<u64> reg_len(n);
+  DevBuf<u32> ids(n);
+  DevBuf<i64> count(1);
+  classify_rows_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, plan.threshold, is_reg.p,
+                                                       is_empty.p, is_hub.p, reg_len.p);
+  PK_LAUNCH("spmm plan classify");
+  iota_rows_kernel<<<blocks_for(n), 256, 0, st>>>(ids.p, n);
+  PK_LAUNCH("spmm plan iota");
+  auto select = [&](const u8* flags, DevBuf<u32>& out) {
+    DevBuf<u32> tmp(n);
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceSelect::Flagged(t, b, ids.p, flags, tmp.p, count.p, n, st);
+    }, st);
+    i64 c = 0;
+    PK_CUDA(cudaMemcpy(&c, count.p, sizeof(i64), cudaMemcpyDeviceToHost));
+    out.alloc(std::max<i64>(c, 1));
+    if (c)
+      PK_CUDA(cudaMemcpyAsync(out.p, tmp.p, c * sizeof(u32), cudaMemcpyDeviceToDevice, st));
+    return c;
+  };
+  plan.regular = select(is_reg.p, plan.rl);
+  plan.empty = select(is_empty.p, plan.empty_rows);
+  DevBuf<u32> hubs32;
+  const i64 nh = select(is_hub.p, hubs32);
+  // regular offsets: exclusive scan of the lengths over the regular list
+  plan.rpc.alloc(plan.regular + 1);
+  {
+    DevBuf<u64> lens(std::max<i64>(plan.regular, 1));
+    DevBuf<u64> tmp(std::max<i64>(plan.regular, 1));
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceSelect::If(t, b, reg_len.p, tmp.p, count.p, n, NonZero(), st);
+    }, st);
+    // lengths in list order == non-zero entries of reg_len in row order
+    PK_CUDA(cudaMemsetAsync(plan.rpc.p, 0, sizeof(u64), st));
+    if (plan.regular)
+      cub_run([&](void* t, size_t& b) {
+        return cub::DeviceScan::InclusiveSum(t, b, tmp.p, plan.rpc.p + 1, plan.regular, st);
+      }, st);
+  }
+  PK_CUDA(cudaMemcpyAsync(&plan.reg_nnz, plan.rpc.p + plan.regular, sizeof(u64),
                           cudaMemcpyDeviceToHost, st));
   PK_CUDA(cudaStreamSynchronize(st));
-  std::vector<std::pair<u64, i64>> hubs;
-  for (i64 i = 0; i < a.rows; ++i) {
-    const u64 len = rp[i + 1] - rp[i];
-    if (len >= plan.threshold) hubs.push_back({len, i});
+  plan.cv.alloc(std::max<u64>(plan.reg_nnz, 1));
+  const size_t words = plan.reg_nnz / 32 + 2;
+  plan.endbits.alloc(words);
+  PK_CUDA(cudaMemsetAsync(plan.endbits.p, 0, words * sizeof(u32), st));
+  if (plan.regular) {
+    compact_rows_kernel<<<blocks_for(plan.regular * 32), 256, 0, st>>>(
+        a.row_ptr, a.col_idx, a.values, plan.rl.p, plan.rpc.p, plan.regular, plan.cv.p,
+        plan.endbits.p);
+    PK_LAUNCH("spmm plan compact");
   }
-  std::stable_sort(hubs.begin(), hubs.end(),
-                   [](const auto& x, const auto& y) { return x.first > y.first; });
-  std::vector<i64> ids(hubs.size());
-  for (size_t i = 0; i < hubs.size(); ++i) ids[i] = hubs[i].second;
-  plan.hub_count = static_cast<int>(ids.size());
-  if (!ids.empty()) {
-    plan.hub_rows.alloc(ids.size());
-    PK_CUDA(cudaMemcpyAsync(plan.hub_rows.p, ids.data(), ids.size() * sizeof(i64),
-                            cudaMemcpyHostToDevice, st));
+  // hub rows longest first (few: host sort)
+  plan.hub_count = static_cast<int>(nh);
+  if (nh) {
+    std::vector<u32> h(nh);
+    std::vector<u64> lens(nh);
+    DevBuf<u64> dlen(nh);
+    hub_len_kernel<<<blocks_for(nh), 256, 0, st>>>(a.row_ptr, hubs32.p, nh, dlen.p);
+    PK_LAUNCH("spmm plan hub lengths");
+    PK_CUDA(cudaMemcpyAsync(h.data(), hubs32.p, nh * sizeof(u32), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaMemcpyAsync(lens.data(), dlen.p, nh * sizeof(u64), cudaMemcpyDeviceToHost, st));
     PK_CUDA(cudaStreamSynchronize(st));
+    std::vector<std::pair<u64, i64>> by_len(nh);
+    for (i64 i = 0; i < nh; ++i) by_len[i] = {lens[i], h[i]};
+    std::stable_sort(by_len.begin(), by_len.end(),
+                     [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<i64> ids64(nh);
+    for (i64 i = 0; i < nh; ++i) ids64[i] = by_len[i].second;
+    plan.hub_rows.alloc(nh);
+    PK_CUDA(cudaMemcpyAsync(plan.hub_rows.p, ids64.data(), nh * sizeof(i64),
+                            cudaMemcpyHostToDevice, st));
   }
+  PK_CUDA(cudaStreamSynchronize(st));
 }
 
-// Hub rows restricted to [r0, r1): the plan's list is global, so a row-range
-// call filters it on the host (cached per range).
-const i64* spmm_plan_range(SpmmPlan& plan, i64 r0, i64 r1, int* count,
-                           cudaStream_t st) {
-  if (plan.hub_count == 0) {
-    *count = 0;
-    return nullptr;
+void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
+              float* y, i64 ldy, cudaStream_t st) {
+  if (r1 <= r0 || d == 0) return;
+  SpmmPlan::Range& rg = plan_range(plan, r0, r1, st);
+  const int vec = pick_vec(x, ldx, y, ldy, d);
+  const int nvec = static_cast<int>(d / vec);
+  // hub CTAs first, on a forked stream, so they hold their SMs while the
+  // list kernel streams through the rest of the machine
+  SideStream& side = side_stream();
+  SpmmArgs h;
+  if (rg.hubs > 0) {
+    h.rp = a.row_ptr, h.ci = a.col_idx, h.val = a.values;
+    h.x = x, h.ldx = ldx, h.y = y, h.ldy = ldy, h.r0 = r0, h.nrows = r1 - r0, h.nvec = nvec;
+    h.hub_rows = rg.hub_ids.p ? rg.hub_ids.p : plan.hub_rows.p;
+    h.hub_count = rg.hubs;
+    h.hub_slices = ceil_div(nvec, 32);
+    h.hub_blocks = h.hub_count * h.hub_slices;
+    PK_CUDA(cudaEventRecord(side.fork, st));
+    PK_CUDA(cudaStreamWaitEvent(side.stream, side.fork, 0));
+    if (vec == 4)
+      launch_hub<4>(h, side.stream);
+    else if (vec == 2)
+      launch_hub<2>(h, side.stream);
+    else
+      launch_hub<1>(h, side.stream);
+    PK_CUDA(cudaEventRecord(side.join, side.stream));
   }
-  if (r0 == 0 && r1 == plan.rows) {
-    *count = plan.hub_count;
-    return plan.hub_rows.p;
+  if (rg.e1 > rg.e0) {
+    const i64 ne = rg.e1 - rg.e0;
+    zero_rows_kernel<<<blocks_for(ne * d), 256, 0, st>>>(plan.empty_rows.p + rg.e0, ne, r0, y,
+                                                         ldy, d);
+    PK_LAUNCH("spmm zero rows");
   }
-  for (auto& c : plan.range_cache)
-    if (c.r0 == r0 && c.r1 == r1) {
-      *count = c.count;
-      return c.rows.p;
-    }
-  std::vector<i64> all(plan.hub_count);
-  PK_CUDA(cudaMemcpyAsync(all.data(), plan.hub_rows.p, all.size() * sizeof(i64),
-                          cudaMemcpyDeviceToHost, st));
-  PK_CUDA(cudaStreamSynchronize(st));
-  std::vector<i64> sel;
-  for (i64 r : all)
-    if (r >= r0 && r < r1) sel.push_back(r);
-  SpmmPlan::Range rg;
-  rg.r0 = r0, rg.r1 = r1, rg.count = static_cast<int>(sel.size());
-  if (!sel.empty()) {
-    rg.rows.alloc(sel.size());
-    PK_CUDA(cudaMemcpyAsync(rg.rows.p, sel.data(), sel.size() * sizeof(i64),
-                            cudaMemcpyHostToDevice, st));
-    PK_CUDA(cudaStreamSynchronize(st));
+  if (rg.i1 > rg.i0) {
+    ListArgs la;
+    la.cv = plan.cv.p, la.rl = plan.rl.p, la.rpc = plan.rpc.p, la.endbits = plan.endbits.p;
+    la.x = x, la.ldx = ldx, la.y = y, la.ldy = ldy, la.r0 = r0, la.nvec = nvec;
+    if (vec == 4)
+      dispatch_list<4>(la, rg.i0, rg.i1, plan.rpc.p, st);
+    else if (vec == 2)
+      dispatch_list<2>(la, rg.i0, rg.i1, plan.rpc.p, st);
+    else
+      dispatch_list<1>(la, rg.i0, rg.i1, plan.rpc.p, st);
   }
-  plan.range_cache.push_back(std::move(rg));
-  *count = plan.range_cache.back().count;
-  return plan.range_cache.back().rows.p;
+  if (rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
 }
 
 }  // namespace pk

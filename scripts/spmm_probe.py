@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--scale", type=int, default=21)
     ap.add_argument("--edges", type=int, default=62_000_000)
     ap.add_argument("--widths", default="50,100,128,256")
+    ap.add_argument("--thresholds", default="0")
     args = ap.parse_args()
     t0 = time.time()
     ds = graph.synth_rmat(args.scale, args.edges, 100, 47, seed=1)
@@ -65,14 +66,14 @@ def main():
         x = torch.rand(a.cols, d, device="cuda")
         y = torch.empty(a.rows, d, device="cuda")
         byts = 8 * a.nnz + 8 * (a.rows + 1) + 4 * a.nnz * d + 4 * a.rows * d
-        plain = timed(lambda: kernels.spmm(a, x, out=y))
-        plan = a.plan()
-        planned = timed(lambda: kernels.spmm(a, x, out=y, plan=plan))
-        hubs, thr = plan.info()
-        res.append(dict(d=d, bytes=byts, plain_ms=plain, plan_ms=planned, hubs=hubs,
-                        hub_threshold=thr, plain_gbs=byts / plain[1] / 1e6,
-                        plan_gbs=byts / planned[1] / 1e6))
-        print(json.dumps(res[-1]), flush=True)
+        for t in [int(v) for v in args.thresholds.split(",")]:
+            plan = a.plan(t)
+            planned = timed(lambda: kernels.spmm(a, x, out=y, plan=plan))
+            hubs, thr = plan.info()
+            res.append(dict(d=d, bytes=byts, plan_ms=planned, hubs=hubs, hub_threshold=thr,
+                            plan_gbs=byts / planned[1] / 1e6))
+            print(json.dumps(res[-1]), flush=True)
+            del plan
     out["spmm"] = res
     print(json.dumps(out))
 
