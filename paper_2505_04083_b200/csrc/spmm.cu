@@ -179,31 +179,61 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
         rid = rb + lane < ie ? __ldg(a.rl + rb + lane) : 0u;
       }
     };
+    // Full windows are software-pipelined: the gathers of group g+1 (U
+    // nonzeros, the next window's first group at a window's end) are issued
+    // before group g is consumed, so every lane always has U*NV 16-B loads in
+    // flight. Partial windows (a chunk's tail) take the simple path.
     u64 w = k + lane < kend ? __ldcs(a.cv + k + lane) : 0ull;
+    V xa[U][NV], xb[U][NV];
+    auto gather = [&](V (&xv)[U][NV], u32 wc, int j) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const u32 c = __shfl_sync(gmask, wc, j + u, LANES);
+        const float* xr = xlane + static_cast<i64>(c) * a.ldx;
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          xv[u][q] = valid[q] ? ldg<V>(xr + q * LANES * VEC) : Vec<VEC>::zero();
+      }
+    };
+    auto consume = [&](const V (&xv)[U][NV], u32 wv, unsigned em, int j) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float v = __uint_as_float(__shfl_sync(gmask, wv, j + u, LANES));
+#pragma unroll
+        for (int q = 0; q < NV; ++q) madd(acc[q], v, xv[u][q]);
+        if ((em >> (j + u)) & 1u) row_done();
+      }
+    };
+    bool primed = false;  // xa holds the gathers of the current window's group 0
     while (k < kend) {
       const int cnt = static_cast<int>(min(static_cast<u64>(LANES), kend - k));
       const u64 wn = k + LANES + lane < kend ? __ldcs(a.cv + k + LANES + lane) : 0ull;
       const unsigned em = end_mask(a.endbits, k);
       const u32 wc = static_cast<u32>(w), wv = static_cast<u32>(w >> 32);
       if (cnt == LANES) {
+        if (!primed) gather(xa, wc, 0);
+        // the next window is full too: its group 0 can be prefetched
+        const bool next_full = k + 2 * LANES <= kend;
 #pragma unroll
-        for (int j = 0; j < LANES; j += U) {
-          V xv[U][NV];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const u32 c = __shfl_sync(gmask, wc, j + u, LANES);
-            const float* xr = xlane + static_cast<i64>(c) * a.ldx;
-#pragma unroll
-            for (int q = 0; q < NV; ++q)
-              xv[u][q] = valid[q] ? ldg<V>(xr + q * LANES * VEC) : Vec<VEC>::zero();
+        for (int j = 0; j < LANES; j += 2 * U) {
+          if (j + U < LANES) gather(xb, wc, j + U);
+          else if (next_full) gather(xb, static_cast<u32>(wn), 0);
+          consume(xa, wv, em, j);
+          if (j + U < LANES) {
+            if (j + 2 * U < LANES) gather(xa, wc, j + 2 * U);
+            else if (next_full) gather(xa, static_cast<u32>(wn), 0);
+            consume(xb, wv, em, j + U);
           }
+        }
+        // with LANES/U even, the prefetched next group 0 sits in xa
+        primed = next_full && ((LANES / U) % 2 == 0);
+        if (next_full && (LANES / U) % 2 == 1) {
+          // odd group count: the prefetch landed in xb; move it (registers)
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const float v = __uint_as_float(__shfl_sync(gmask, wv, j + u, LANES));
+          for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int q = 0; q < NV; ++q) madd(acc[q], v, xv[u][q]);
-            if ((em >> (j + u)) & 1u) row_done();
-          }
+            for (int q = 0; q < NV; ++q) xa[u][q] = xb[u][q];
+          primed = true;
         }
       } else {
         for (int j = 0; j < cnt; ++j) {
@@ -215,6 +245,7 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
             if (valid[q]) madd(acc[q], v, ldg<V>(xr + q * LANES * VEC));
           if ((em >> j) & 1u) row_done();
         }
+        primed = false;
       }
       k += cnt;
       w = wn;
@@ -427,8 +458,9 @@ struct ListWorkspace {
 
 template <int VEC, int LANES, int NV>
 void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
-  constexpr int U = NV >= 4 ? 4 : 8;
-  auto kernel = spmm_list_kernel<VEC, LANES, NV, (U < LANES ? U : LANES)>;
+  constexpr int U0 = NV >= 4 ? 2 : 4;
+  constexpr int U = U0 < LANES ? U0 : LANES / 2;
+  auto kernel = spmm_list_kernel<VEC, LANES, NV, U>;
   const int slices = ceil_div(a.nvec, NV * LANES);
   // ~1-2K nonzeros per chunk at the products shape; never more chunks than rows
   const i64 nchunks64 =
