@@ -47,6 +47,14 @@ unsigned small_grid(i64 n) {
 
 }  // namespace
 
+void copy_block_launch(const float* src, i64 ld_src, i64 rows, i64 cols, float* dst, i64 ld_dst,
+                       cudaStream_t st) {
+  if (rows == 0 || cols == 0) return;
+  copy_block_kernel<<<small_grid(rows * cols), 256, 0, st>>>(src, ld_src, rows, cols, dst,
+                                                             ld_dst);
+  PK_LAUNCH("copy block");
+}
+
 Comms::~Comms() {
   for (auto& c : axes_)
     if (c) ncclCommDestroy(c);

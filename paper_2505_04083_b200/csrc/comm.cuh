@@ -29,6 +29,10 @@ inline void nccl_check(ncclResult_t r, const char* what) {
 }
 #define PK_NCCL(x) ::pk::nccl_check((x), #x)
 
+// dst[r, c] = src[r, c] for a rows x cols block (strided on both sides)
+void copy_block_launch(const float* src, i64 ld_src, i64 rows, i64 cols, float* dst, i64 ld_dst,
+                       cudaStream_t st);
+
 enum CollOp : int { kAllGather = 0, kAllReduce = 1, kReduceScatter = 2 };
 
 struct CommCounters {

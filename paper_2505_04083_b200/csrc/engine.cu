@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -54,6 +57,19 @@ void DMat::alloc(i64 r, i64 c) {
   ld = pad4(c);
   buf.alloc(static_cast<size_t>(std::max<i64>(1, r) * ld));
   PK_CUDA(cudaMemset(buf.p, 0, buf.n * sizeof(float)));
+}
+
+const std::vector<u64>& AdjShard::blocks_nnz(int blocks, cudaStream_t st) {
+  auto it = block_nnz.find(blocks);
+  if (it != block_nnz.end()) return it->second;
+  // block edges only: blocks + 1 row_ptr entries
+  std::vector<u64> edge(blocks + 1), out;
+  for (int b = 0; b <= blocks; ++b)
+    PK_CUDA(cudaMemcpyAsync(&edge[b], a.row_ptr + chunk_start(a.rows, blocks, b), sizeof(u64),
+                            cudaMemcpyDeviceToHost, st));
+  PK_CUDA(cudaStreamSynchronize(st));
+  for (int b = 0; b < blocks; ++b) out.push_back(edge[b + 1] - edge[b]);
+  return block_nnz[blocks] = out;
 }
 
 AdjShard::~AdjShard() {
@@ -146,6 +162,17 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   check(dsin.feat_dim == dims_[0] && static_cast<i64>(dsin.num_classes) == dims_[L_],
         "engine load: dataset dims do not match the model dims");
   const i64 n = cfg_.n;
+  // PK_TIMING=1: host wall time of each setup phase on stderr
+  static const bool timing = std::getenv("PK_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    PK_CUDA(cudaStreamSynchronize(st_));
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pk load r%d] %-28s %8.2f ms\n", rank_, what,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   // host inputs: stage the whole preprocessed dataset in HBM first
   pk_dataset_view ds = dsin;
   DevBuf<u64> erp, orp;
@@ -166,15 +193,20 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     ds.a_odd.col_idx = up(oci, dsin.a_odd.col_idx, dsin.a_odd.nnz);
     ds.a_odd.values = up(ov, dsin.a_odd.values, dsin.a_odd.nnz);
     feat.alloc(static_cast<size_t>(n * dims_[0]));
-    PK_CUDA(cudaMemcpy2DAsync(feat.p, dims_[0] * sizeof(float), dsin.features,
-                              dsin.ld_features * sizeof(float), dims_[0] * sizeof(float), n,
+    if (dsin.ld_features == dims_[0])  // one DMA: a pitched copy moves row by row
+      PK_CUDA(cudaMemcpyAsync(feat.p, dsin.features, n * dims_[0] * sizeof(float),
                               cudaMemcpyHostToDevice, st_));
+    else
+      PK_CUDA(cudaMemcpy2DAsync(feat.p, dims_[0] * sizeof(float), dsin.features,
+                                dsin.ld_features * sizeof(float), dims_[0] * sizeof(float), n,
+                                cudaMemcpyHostToDevice, st_));
     ds.features = feat.p;
     ds.ld_features = dims_[0];
     ds.labels_row = up(lr, dsin.labels_row, n);
     ds.labels_col = up(lc, dsin.labels_col, n);
     ds.mask_row = up(mr, dsin.mask_row, n);
     ds.mask_col = up(mc, dsin.mask_col, n);
+    mark("h2d dataset");
   }
   // adjacency shards (build_adjacency_shards, engine.hpp:96-113)
   for (auto [plane, parity] : needed_adjacency_keys(L_)) {
@@ -182,30 +214,38 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     check(variant.rows == n && variant.cols == n,
           "build_adjacency_shards: adjacency variants must be square and equal");
     const Slice r = adjacency_block_range(grid_, plane, c_, n);
-    auto sh = std::make_unique<AdjShard>();
+    std::shared_ptr<AdjShard> same;
+    for (auto& prev : shards_)
+      if (prev && prev->parity == parity && prev->r0 == r.r0 && prev->r1 == r.r1 &&
+          prev->c0 == r.c0 && prev->c1 == r.c1)
+        same = prev;
+    if (same) {
+      shards_[plane * 2 + parity] = same;
+      continue;
+    }
+    auto sh = std::make_shared<AdjShard>();
+    sh->parity = parity, sh->r0 = r.r0, sh->r1 = r.r1, sh->c0 = r.c0, sh->c1 = r.c1;
     csr_block(variant, r.r0, r.r1, r.c0, r.c1, &sh->a, st_);
+    mark("csr_block");
     csr_transpose(view(sh->a), &sh->at, st_);
+    mark("csr_transpose");
     spmm_plan_build(sh->plan_a, view(sh->a), static_cast<u64>(cfg_.hub_threshold), st_);
     spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_);
-    // nnz per forward row block, for the FLOP counters
-    std::vector<u64> rp(sh->a.rows + 1);
-    PK_CUDA(cudaMemcpy(rp.data(), sh->a.row_ptr, rp.size() * sizeof(u64),
-                       cudaMemcpyDeviceToHost));
-    const int blocks = forward_blocks(sh->a.rows, plan_layouts(plane + 1).back());
-    for (int b = 0; b < blocks; ++b)
-      sh->block_nnz.push_back(rp[chunk_start(sh->a.rows, blocks, b + 1)] -
-                              rp[chunk_start(sh->a.rows, blocks, b)]);
+    mark("spmm plans");
     sh->nnz_t = sh->at.nnz;
     shards_[plane * 2 + parity] = std::move(sh);
   }
   // trainable features F0 (feature_slice, model.hpp:53-67) + Adam state
   const Slice fs = feature_slice(grid_, c_, n, dims_[0]);
   f0_.alloc(fs.r1 - fs.r0, fs.c1 - fs.c0);
-  if (f0_.rows && f0_.cols)
-    PK_CUDA(cudaMemcpy2DAsync(f0_.p(), f0_.ld * sizeof(float),
-                              ds.features + fs.r0 * ds.ld_features + fs.c0,
-                              ds.ld_features * sizeof(float), f0_.cols * sizeof(float), f0_.rows,
+  if (f0_.rows && f0_.cols) {
+    const float* src = ds.features + fs.r0 * ds.ld_features + fs.c0;
+    if (f0_.ld == f0_.cols && ds.ld_features == f0_.cols)
+      PK_CUDA(cudaMemcpyAsync(f0_.p(), src, f0_.rows * f0_.cols * sizeof(float),
                               cudaMemcpyDeviceToDevice, st_));
+    else
+      copy_block_launch(src, ds.ld_features, f0_.rows, f0_.cols, f0_.p(), f0_.ld, st_);
+  }
   f0_m_.alloc(f0_.rows, f0_.cols);
   f0_v_.alloc(f0_.rows, f0_.cols);
   df0_.alloc(f0_.rows, f0_.cols);
@@ -262,6 +302,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   stage_.alloc(sl.a_rows, dims_[L_]);
   // DMat::alloc zeroes on the legacy stream: drain everything before use
   PK_CUDA(cudaDeviceSynchronize());
+  mark("params, activations");
   loaded_ = true;
 }
 
@@ -277,7 +318,7 @@ int Engine::forward_blocks(i64 rows, const Layout& lay) const {
 void Engine::forward_layer(int l, bool fault) {
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
-  const AdjShard& sh = shard(lay);
+  AdjShard& sh = const_cast<AdjShard&>(shard(lay));
   const float* f;
   i64 ldf;
   if (l == 0) {
@@ -296,14 +337,15 @@ void Engine::forward_layer(int l, bool fault) {
                                    shape(s.f_rows, s.f_cols));
   DMat& h = h_[l];
   const int blocks = forward_blocks(sh.a.rows, lay);
+  const std::vector<u64>& bnnz = sh.blocks_nnz(blocks, st_);
   // blocked aggregation: SpMM row block, then its all-reduce along inner
   for (int b = 0; b < blocks; ++b) {
     const i64 r0 = chunk_start(sh.a.rows, blocks, b), r1 = chunk_start(sh.a.rows, blocks, b + 1);
     clock_.begin(0, st_);
     spmm_run(const_cast<SpmmPlan&>(sh.plan_a), view(sh.a), r0, r1, f, ldf, s.f_cols,
              h.p() + r0 * h.ld, h.ld, st_);
-    spmm_flops_ += 2 * sh.block_nnz[b] * static_cast<u64>(s.f_cols);
-    spmm_bytes_ += spmm_alg_bytes(r1 - r0, sh.block_nnz[b], s.f_cols);
+    spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
+    spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
     clock_.end(st_);
     if (!fault) {
       clock_.begin(4, st_);

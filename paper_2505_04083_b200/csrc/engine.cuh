@@ -3,6 +3,7 @@
 // Engine; collectives go through Comms (NCCL per-axis communicators).
 #pragma once
 
+#include <map>
 #include <memory>
 #include <vector>
 
@@ -26,9 +27,13 @@ struct DMat {
 };
 
 struct AdjShard {
+  int parity = 0;
+  i64 r0 = 0, r1 = 0, c0 = 0, c1 = 0;
   pk_csr_owned a{}, at{};
   SpmmPlan plan_a, plan_at;
-  std::vector<u64> block_nnz;  // nnz of each forward row block
+  // nnz of each forward row block, per block count (filled on first use)
+  std::map<int, std::vector<u64>> block_nnz;
+  const std::vector<u64>& blocks_nnz(int blocks, cudaStream_t st);
   u64 nnz_t = 0;
   ~AdjShard();
 };
@@ -87,7 +92,9 @@ class Engine {
   std::vector<Shapes> shapes_;
   cudaStream_t st_ = nullptr;
   Comms comms_;
-  std::unique_ptr<AdjShard> shards_[6];
+  // one per (plane, parity) key; keys whose block is the same range of the
+  // same variant share one shard (at 1x1x1 planes 0 and 2 are both A_even)
+  std::shared_ptr<AdjShard> shards_[6];
   const AdjShard& shard(const Layout& l) const;
 
   // parameters and optimizer state

@@ -90,6 +90,23 @@ __device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
   }
 }
 
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine, no tensor map), completing
+// `bytes` of transaction count on `bar`.
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsigned bytes,
+                                              u64* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -280,6 +297,9 @@ struct TileLoader {
 
 struct TcParams {
   OperandSrc a, b;
+  // NN / NT: B (the weight) pre-split into per-k-stage [hi | lo] K-major
+  // swizzled tile images, bulk-copied straight into shared memory
+  const unsigned char* b_image;
   i64 m, n, k;
   i64 k_chunk;      // k per split (multiple of kBK)
   int m_tiles, n_tiles, splits;
@@ -288,11 +308,11 @@ struct TcParams {
   i64 split_stride; // elements between split partials
 };
 
-template <bool A_T, bool B_T, int BN, int STAGES>
+template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE>
 struct TcConfig {
   // stored N extent: a multiple of 16 (UMMA N) — and of 32 when the loader
   // transposes, whose items cover 32 rows per lane group
-  static constexpr int kRowsB = B_T ? ((BN + 31) / 32) * 32 : BN;
+  static constexpr int kRowsB = (B_T && !B_PRE) ? ((BN + 31) / 32) * 32 : BN;
   static constexpr int kTileA = kBM * kBK * 4;  // bytes, one of hi/lo
   static constexpr int kTileB = kRowsB * kBK * 4;
   static constexpr int kStage = 2 * kTileA + 2 * kTileB;
@@ -303,9 +323,9 @@ struct TcConfig {
   static constexpr size_t kSmem = static_cast<size_t>(STAGES) * kStage + 1024;
 };
 
-template <bool A_T, bool B_T, int BN, int STAGES>
+template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE>
 __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
-  using Cfg = TcConfig<A_T, B_T, BN, STAGES>;
+  using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -347,7 +367,70 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     ke = min(p.k, kb + p.k_chunk);
   };
 
-  if (warp < kLoaderWarps) {
+  if (warp < kLoaderWarps && B_PRE) {
+    // ------------------------------------------------------------ loaders (B image)
+    // A streams through registers two k-stages ahead, across tile
+    // boundaries; B arrives by one bulk copy per stage.
+    const int lt = threadIdx.x;
+    int stage = 0;
+    unsigned phase = 0;
+    struct Pos {
+      int t, kk, nk;
+      i64 kb, ke, m0;
+    };
+    auto start = [&](Pos& q, int t) {
+      q.t = t;
+      q.kk = 0;
+      q.nk = 0;
+      while (q.t < total_tiles) {
+        int mt, nt, sp;
+        tile_coords(q.t, mt, nt, sp);
+        k_range(sp, q.kb, q.ke);
+        q.m0 = static_cast<i64>(mt) * kBM;
+        q.nk = static_cast<int>((q.ke - q.kb + kBK - 1) / kBK);
+        if (q.nk > 0) return;
+        q.t += gridDim.x;  // empty k range: the MMA warp signals it without stages
+      }
+    };
+    auto advance = [&](Pos& q) {
+      if (++q.kk == q.nk) start(q, q.t + gridDim.x);
+    };
+    auto valid = [&](const Pos& q) { return q.t < total_tiles; };
+    float4 r0[Cfg::LoadA::kRegs], r1[Cfg::LoadA::kRegs];
+    auto load = [&](float4 (&r)[Cfg::LoadA::kRegs], const Pos& q) {
+      if (valid(q)) Cfg::LoadA::load(p.a, q.m0, q.kb + static_cast<i64>(q.kk) * kBK, q.ke, lt, r);
+    };
+    Pos cur, pre;
+    start(cur, blockIdx.x);
+    pre = cur;
+    load(r0, pre);
+    if (valid(pre)) advance(pre);
+    load(r1, pre);
+    if (valid(pre)) advance(pre);
+    auto step = [&](float4 (&r)[Cfg::LoadA::kRegs]) {
+      mbar_wait(&empty[stage], phase ^ 1u);
+      unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
+      if (threadIdx.x == 0) {
+        const i64 g = (cur.kb + static_cast<i64>(cur.kk) * kBK) / kBK;
+        mbar_expect_tx(&full[stage], 2u * Cfg::kTileB);
+        bulk_copy_g2s(st + 2 * Cfg::kTileA, p.b_image + g * 2 * Cfg::kTileB, 2u * Cfg::kTileB,
+                      &full[stage]);
+      }
+      Cfg::LoadA::store(st, st + Cfg::kTileA, lt, r);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[stage]);
+      if (++stage == STAGES) stage = 0, phase ^= 1u;
+      advance(cur);
+      load(r, pre);  // two stages ahead
+      if (valid(pre)) advance(pre);
+    };
+    while (valid(cur)) {
+      step(r0);
+      if (!valid(cur)) break;
+      step(r1);
+    }
+  } else if (warp < kLoaderWarps) {
     // ------------------------------------------------------------ loaders
     const int lt = threadIdx.x;  // 0..255
     int stage = 0;
@@ -509,6 +592,33 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
   }
 }
 
+// B image for NN (W stored k x n) / NT (W stored n x k): per 32-k stage g,
+// [hi tile | lo tile], each `rows` x 128 B, K-major 128-B swizzled, zero
+// padded past n and k. One thread per (g, row, 16-B chunk).
+__global__ void b_image_kernel(const float* __restrict__ w, i64 ldw, bool w_is_kxn, i64 n, i64 k,
+                               int rows, i64 stages, unsigned char* __restrict__ img) {
+  const i64 total = stages * rows * 8;
+  const unsigned tile = static_cast<unsigned>(rows) * 128u;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(i % 8);
+    const int r = static_cast<int>((i / 8) % rows);
+    const i64 g = i / (8 * rows);
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const i64 kk = g * kBK + c * 4 + j;
+      v[j] = (r < n && kk < k) ? (w_is_kxn ? w[kk * ldw + r] : w[r * ldw + kk]) : 0.f;
+    }
+    const float4 x = make_float4(v[0], v[1], v[2], v[3]);
+    const float4 h = split_hi(x);
+    unsigned char* base = img + g * 2 * tile;
+    const unsigned off = kmajor_offset(r, c);
+    *reinterpret_cast<float4*>(base + off) = h;
+    *reinterpret_cast<float4*>(base + tile + off) = split_lo(x, h);
+  }
+}
+
 // Deterministic split combine: C = partial[0] + partial[1] + ... in order.
 __global__ void tc_split_reduce_kernel(const float* __restrict__ part, int splits, i64 m, i64 n,
                                        i64 ldp, i64 stride, float* __restrict__ c, i64 ldc) {
@@ -520,12 +630,12 @@ __global__ void tc_split_reduce_kernel(const float* __restrict__ part, int split
   c[i * ldc + j] = s;
 }
 
-template <bool A_T, bool B_T, int BN>
+template <bool A_T, bool B_T, int BN, bool B_PRE>
 void launch_bn(const TcParams& p0, cudaStream_t st) {
-  constexpr int kStageBytes = TcConfig<A_T, B_T, BN, 1>::kStage;
+  constexpr int kStageBytes = TcConfig<A_T, B_T, BN, 1, B_PRE>::kStage;
   constexpr int STAGES = std::min(6, std::max(2, (200 * 1024) / kStageBytes));
-  using Cfg = TcConfig<A_T, B_T, BN, STAGES>;
-  auto kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES>;
+  using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
+  auto kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE>;
   static thread_local bool attr = false;
   if (!attr) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -533,23 +643,34 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     attr = true;
   }
   TcParams p = p0;
+  if (B_PRE) {
+    // split the weight once per call into its per-stage tile images
+    const i64 stages = (p.k + kBK - 1) / kBK;
+    static thread_local DevBuf<unsigned char> img;
+    img.ensure(static_cast<size_t>(stages) * 2 * Cfg::kTileB);
+    const i64 items = stages * Cfg::kRowsB * 8;
+    b_image_kernel<<<ceil_div(items, 256), 256, 0, st>>>(p.b.p, p.b.ld, B_T, p.n, p.k,
+                                                         Cfg::kRowsB, stages, img.p);
+    PK_LAUNCH("gemm tcgen05 b image");
+    p.b_image = img.p;
+  }
   const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles * p.splits;
   const int grid = static_cast<int>(std::min<i64>(tiles, sm_count()));
   kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p);
   PK_LAUNCH("gemm tcgen05 kernel");
 }
 
-template <bool A_T, bool B_T>
+template <bool A_T, bool B_T, bool B_PRE>
 void launch_forms(const TcParams& p, int bn, cudaStream_t st) {
   switch (bn) {
-    case 16: return launch_bn<A_T, B_T, 16>(p, st);
-    case 32: return launch_bn<A_T, B_T, 32>(p, st);
-    case 48: return launch_bn<A_T, B_T, 48>(p, st);
-    case 64: return launch_bn<A_T, B_T, 64>(p, st);
-    case 96: return launch_bn<A_T, B_T, 96>(p, st);
-    case 128: return launch_bn<A_T, B_T, 128>(p, st);
-    case 192: return launch_bn<A_T, B_T, 192>(p, st);
-    default: return launch_bn<A_T, B_T, 256>(p, st);
+    case 16: return launch_bn<A_T, B_T, 16, B_PRE>(p, st);
+    case 32: return launch_bn<A_T, B_T, 32, B_PRE>(p, st);
+    case 48: return launch_bn<A_T, B_T, 48, B_PRE>(p, st);
+    case 64: return launch_bn<A_T, B_T, 64, B_PRE>(p, st);
+    case 96: return launch_bn<A_T, B_T, 96, B_PRE>(p, st);
+    case 128: return launch_bn<A_T, B_T, 128, B_PRE>(p, st);
+    case 192: return launch_bn<A_T, B_T, 192, B_PRE>(p, st);
+    default: return launch_bn<A_T, B_T, 256, B_PRE>(p, st);
   }
 }
 
@@ -557,7 +678,6 @@ int pick_bn(i64 n) {
   static const int opts[] = {16, 32, 48, 64, 96, 128, 192, 256};
   for (int b : opts)
     if (n <= b) return b;
-  // wide outputs: the fewest 256-column tiles... unless a 192 split is tighter
   return 256;
 }
 
@@ -603,11 +723,11 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
     p.split_stride = 0;
   }
   if (!ta && !tb)
-    launch_forms<false, true>(p, bn, st);
+    launch_forms<false, true, true>(p, bn, st);
   else if (!ta && tb)
-    launch_forms<false, false>(p, bn, st);
+    launch_forms<false, false, true>(p, bn, st);
   else
-    launch_forms<true, true>(p, bn, st);
+    launch_forms<true, true, false>(p, bn, st);
   if (splits > 1) {
     tc_split_reduce_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(part.p, splits, m, n, p.ldc,
                                                                  p.split_stride, c, ldc);

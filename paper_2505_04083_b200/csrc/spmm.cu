@@ -667,9 +667,9 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
   if (a.rows == 0) return;
   // A row is a hub when one lane chain over it would outlast the rest of the
   // work spread over the whole GPU; measured on the products shape
-  // (scripts/spmm_probe.py), 2048 nonzeros is the sweet spot.
+  // (scripts/spmm_probe.py), 4096 nonzeros is the sweet spot (2048-8192 within 3 %).
   const u64 avg = a.nnz / std::max<i64>(1, a.rows);
-  plan.threshold = threshold ? threshold : std::max<u64>(2048, 32 * avg);
+  plan.threshold = threshold ? threshold : std::max<u64>(4096, 64 * avg);
   const i64 n = a.rows;
   DevBuf<u8> is_reg(n), is_empty(n), is_hub(n);
   DevBuf<u64> reg_len(n);
