@@ -13,26 +13,50 @@ namespace pk {
 
 namespace {
 
+// ReLU kernels. Contiguous operands (ld == cols, 16-B aligned) stream as
+// flat float4 arrays; strided views go row by row (a warp per row, lanes over
+// columns), never dividing per element.
+__device__ __forceinline__ float relu1(float v) { return v > 0.f ? v : 0.f; }
+
+__global__ void relu_fwd_flat_kernel(const float4* __restrict__ q, i64 n4,
+                                     float4* __restrict__ out) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const float4 v = __ldcs(q + i);
+    __stcs(out + i, make_float4(relu1(v.x), relu1(v.y), relu1(v.z), relu1(v.w)));
+  }
+}
+
+__global__ void relu_bwd_flat_kernel(const float4* __restrict__ q, const float4* __restrict__ df,
+                                     i64 n4, float4* __restrict__ out) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const float4 a = __ldcs(q + i), d = __ldcs(df + i);
+    __stcs(out + i, make_float4(a.x > 0.f ? d.x : 0.f, a.y > 0.f ? d.y : 0.f,
+                                a.z > 0.f ? d.z : 0.f, a.w > 0.f ? d.w : 0.f));
+  }
+}
+
 __global__ void relu_fwd_kernel(const float* __restrict__ q, i64 ldq, i64 rows, i64 cols,
                                 float* __restrict__ out, i64 ldo) {
-  const i64 n = rows * cols;
-  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 r = i / cols, c = i % cols;
-    const float v = q[r * ldq + c];
-    out[r * ldo + c] = v > 0.f ? v : 0.f;
-  }
+  const int lane = threadIdx.x % 32;
+  const i64 nw = static_cast<i64>(gridDim.x) * (blockDim.x / 32);
+  for (i64 r = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; r < rows; r += nw)
+    for (i64 c = lane; c < cols; c += 32) out[r * ldo + c] = relu1(q[r * ldq + c]);
 }
 
 __global__ void relu_bwd_kernel(const float* __restrict__ q, i64 ldq,
                                 const float* __restrict__ df, i64 lddf, i64 rows, i64 cols,
                                 float* __restrict__ out, i64 ldo) {
-  const i64 n = rows * cols;
-  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 r = i / cols, c = i % cols;
-    out[r * ldo + c] = q[r * ldq + c] > 0.f ? df[r * lddf + c] : 0.f;
-  }
+  const int lane = threadIdx.x % 32;
+  const i64 nw = static_cast<i64>(gridDim.x) * (blockDim.x / 32);
+  for (i64 r = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; r < rows; r += nw)
+    for (i64 c = lane; c < cols; c += 32)
+      out[r * ldo + c] = q[r * ldq + c] > 0.f ? df[r * lddf + c] : 0.f;
+}
+
+bool flat4(const void* p, i64 ld, i64 cols) {
+  return ld == cols && cols % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 
 unsigned stream_grid(i64 n) {
@@ -173,15 +197,28 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
 void relu_forward_launch(const float* q, i64 ldq, i64 rows, i64 cols, float* out, i64 ldo,
                          cudaStream_t st) {
   if (rows * cols == 0) return;
-  relu_fwd_kernel<<<stream_grid(rows * cols), 256, 0, st>>>(q, ldq, rows, cols, out, ldo);
+  if (flat4(q, ldq, cols) && flat4(out, ldo, cols)) {
+    const i64 n4 = rows * cols / 4;
+    relu_fwd_flat_kernel<<<stream_grid(n4), 256, 0, st>>>(reinterpret_cast<const float4*>(q), n4,
+                                                          reinterpret_cast<float4*>(out));
+  } else {
+    relu_fwd_kernel<<<stream_grid(rows * 32), 256, 0, st>>>(q, ldq, rows, cols, out, ldo);
+  }
   PK_LAUNCH("relu forward");
 }
 
 void relu_backward_launch(const float* q, i64 ldq, const float* df, i64 lddf, i64 rows,
                           i64 cols, float* out, i64 ldo, cudaStream_t st) {
   if (rows * cols == 0) return;
-  relu_bwd_kernel<<<stream_grid(rows * cols), 256, 0, st>>>(q, ldq, df, lddf, rows, cols, out,
+  if (flat4(q, ldq, cols) && flat4(df, lddf, cols) && flat4(out, ldo, cols)) {
+    const i64 n4 = rows * cols / 4;
+    relu_bwd_flat_kernel<<<stream_grid(n4), 256, 0, st>>>(reinterpret_cast<const float4*>(q),
+                                                          reinterpret_cast<const float4*>(df), n4,
+                                                          reinterpret_cast<float4*>(out));
+  } else {
+    relu_bwd_kernel<<<stream_grid(rows * 32), 256, 0, st>>>(q, ldq, df, lddf, rows, cols, out,
                                                             ldo);
+  }
   PK_LAUNCH("relu backward");
 }
 

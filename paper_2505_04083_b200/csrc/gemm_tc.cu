@@ -8,26 +8,29 @@
 //     C = A_lo.B_hi + A_hi.B_lo + A_hi.B_hi
 // accumulated in TMEM (error ~2^-22 relative per product, i.e. fp32-level).
 //
-// Why the loads are register-staged and not TMA: the split has to happen
-// between HBM and the tensor core. Loader warps read fp32 tiles with 16-B
-// coalesced loads (the next k-stage's loads are in flight while the current
-// one is split and stored), write hi and lo into 128-B-swizzled K-major
-// shared-memory tiles (transposing 4x4 register blocks when the operand's
-// row-major storage runs along M/N), and arrive on the stage's mbarrier. One elected thread issues the MMAs; epilogue warps drain
-// the double-buffered TMEM accumulator with tcgen05.ld and store rows.
+// Why the big operands are register-staged and not TMA: the split has to
+// happen between HBM and the tensor core. Loader warps read fp32 tiles with
+// 16-B coalesced loads two k-stages ahead (across tile boundaries), write hi
+// and lo into swizzled shared-memory tiles — K-major (128-B swizzle) when the
+// source is k-contiguous, MN-major (the 32-B-atom swizzle tf32 needs) when it
+// runs along M/N — and arrive on the stage's mbarrier. The small weight
+// operand of NN / NT is split once per call into per-stage tile images that
+// one thread bulk-copies (cp.async.bulk, TMA engine) into each stage. One
+// elected thread issues the MMAs; epilogue warps drain the double-buffered
+// TMEM accumulator with tcgen05.ld and store rows.
 //
 // Persistent CTAs walk a static tile schedule (m tile, n tile, k split). A
 // k split > 1 writes fp32 partials that a deterministic fixed-order reduce
 // combines (dW = H^T dQ reduces over all adjacency rows, engine.hpp:233-235).
 //
-// Operand forms (row-major storage; "T" = storage runs along M/N, so the
-// loader transposes into the K-major tile):
-//   NN  Q  = H . W        A = H   (k-contiguous)  B = W   (T)
-//   NT  dH = dQ . W^T     A = dQ  (k-contiguous)  B = W   (k-contiguous)
-//   TN  dW = H^T . dQ     A = H^T (T)             B = dQ  (T)
+// Operand forms (row-major storage; "T" = storage runs along M/N):
+//   NN  Q  = H . W        A = H   (K-major tile)  B = W   (pre-split image)
+//   NT  dH = dQ . W^T     A = dQ  (K-major tile)  B = W   (pre-split image)
+//   TN  dW = H^T . dQ     A = H^T (MN-major tile) B = dQ  (MN-major tile)
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "pk_common.cuh"
@@ -161,12 +164,11 @@ __device__ __forceinline__ u64 smem_desc(unsigned addr, unsigned lbo, unsigned s
   return d;
 }
 
-// Instruction descriptor: fp32 accumulate, tf32 A and B (both K-major), M = 128.
-// (MN-major tf32 operands read back as zeros on this part — measured with
-// scripts/tc_probe.cu — so every tile is staged K-major and sources whose
-// storage runs along M/N are transposed by the loaders instead.)
-__host__ __device__ constexpr unsigned instr_desc(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<unsigned>(n >> 3) << 17) |
+// Instruction descriptor: fp32 accumulate, tf32 A and B, M = 128; bits 15/16
+// mark an MN-major operand (staged in the 32-B-atom swizzle, see below).
+__host__ __device__ constexpr unsigned instr_desc(int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<unsigned>(a_mn) << 15) |
+         (static_cast<unsigned>(b_mn) << 16) | (static_cast<unsigned>(n >> 3) << 17) |
          (static_cast<unsigned>(kBM >> 4) << 24);
 }
 
@@ -225,20 +227,47 @@ __device__ __forceinline__ float4 load_quad(const OperandSrc& s, i64 r, i64 c, i
 // block l%8 and k-chunk l/8 (+4 for the second half), so each 16-B store
 // row-group hits 8 distinct swizzle chunks: conflict-free, and every k row
 // is still read as 128 contiguous bytes by 8 lanes.
+// MN-major "128-B swizzle, 32-B atom" tile (layout type 1, the tf32 MN-major
+// form; the plain 128-B swizzle reads back zeros for tf32 MN-major operands,
+// measured with scripts/tc_probe.cu): atoms of 4 k-rows x 128 B (32 M/N
+// values); the 32-B chunk (mn%32)/8 of row k is XOR-ed with k%4; MN atoms
+// are 512 B apart (LBO), 4-row k groups are SBO = (ROWS/32)*512 apart. A
+// UMMA k-step (8 k) spans two k groups.
+template <int ROWS>
+__device__ __forceinline__ unsigned mnmajor_offset(int mn, int k) {
+  constexpr unsigned kSbo = (ROWS / 32) * 512;
+  const int a = mn >> 5, c = (mn & 31) >> 3, half = (mn >> 2) & 1, r = k & 3, g = k >> 2;
+  return static_cast<unsigned>(g * kSbo + a * 512 + r * 128 + ((c ^ r) << 5) + half * 16);
+}
+template <int ROWS>
+__device__ __forceinline__ u64 mnmajor_desc(unsigned base, int kstep) {
+  constexpr unsigned kSbo = (ROWS / 32) * 512;
+  u64 d = smem_desc(base + 2u * kSbo * kstep, 512u, kSbo);
+  d &= ~(7ull << 61);
+  return d | (1ull << 61);  // SWIZZLE_128B_BASE32B
+}
+
+// Loader work for one operand tile of ROWS (M/N) x 32 (k) per stage. Each
+// item is one 16-B chunk of the row-major source, stored (split into hi/lo)
+// without any transposition:
+//  T = false, K-contiguous source: chunk (row, k quad) -> K-major tile; 8
+//    consecutive threads read one row's 128 B.
+//  T = true, MN-contiguous source: chunk (k row, 4 mn) -> MN-major tile;
+//    consecutive threads read one k row's consecutive 16-B pieces.
 template <bool T, int ROWS>
 struct TileLoader {
-  static constexpr int kItems = T ? 2 * ROWS : 8 * ROWS;
+  static constexpr int kItems = 8 * ROWS;
   static constexpr int kPer = (kItems + kLoaderThreads - 1) / kLoaderThreads;
-  static constexpr int kRegs = kPer * (T ? 4 : 1);
+  static constexpr int kRegs = kPer;
 
-  static __device__ __forceinline__ void item_coords(int q, int& row, int& kc) {
+  static __device__ __forceinline__ void item_coords(int q, int& mn, int& k) {
     if (!T) {
-      row = q >> 3;
-      kc = q & 7;
+      mn = q >> 3;
+      k = (q & 7) << 2;
     } else {
-      const int mnb_lo = q & 7, kc_lo = (q >> 3) & 3, kc_hi = (q >> 5) & 1, grp = q >> 6;
-      row = (grp * 8 + mnb_lo) * 4;  // first of 4 mn rows
-      kc = kc_hi * 4 + kc_lo;        // k quad
+      constexpr int per_k = ROWS / 4;
+      k = q / per_k;
+      mn = (q % per_k) << 2;
     }
   }
 
@@ -247,19 +276,15 @@ struct TileLoader {
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
       const int q = tid + i * kLoaderThreads;
-      int row, kc;
-      item_coords(q, row, kc);
+      int mn, k;
+      item_coords(q, mn, k);
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
       if (!T) {
-        const i64 gr = mn0 + row;
-        r[i] = (q < kItems && gr < s.mn) ? load_quad(s, gr, k0 + kc * 4, k_end)
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        const i64 gr = mn0 + mn;
+        r[i] = (q < kItems && gr < s.mn) ? load_quad(s, gr, k0 + k, k_end) : z;
       } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const i64 gk = k0 + kc * 4 + j;
-          r[4 * i + j] = (q < kItems && gk < k_end) ? load_quad(s, gk, mn0 + row, s.mn)
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        const i64 gk = k0 + k;
+        r[i] = (q < kItems && gk < k_end) ? load_quad(s, gk, mn0 + mn, s.mn) : z;
       }
     }
   }
@@ -270,28 +295,18 @@ struct TileLoader {
     for (int i = 0; i < kPer; ++i) {
       const int q = tid + i * kLoaderThreads;
       if (q >= kItems) continue;
-      int row, kc;
-      item_coords(q, row, kc);
-      if (!T) {
-        const float4 h = split_hi(r[i]);
-        const unsigned off = kmajor_offset(row, kc);
-        *reinterpret_cast<float4*>(hi + off) = h;
-        *reinterpret_cast<float4*>(lo + off) = split_lo(r[i], h);
-      } else {
-        const float4* b = r + 4 * i;  // b[j] = k row kc*4+j, mn row..row+3
-        const float4 t[4] = {make_float4(b[0].x, b[1].x, b[2].x, b[3].x),
-                             make_float4(b[0].y, b[1].y, b[2].y, b[3].y),
-                             make_float4(b[0].z, b[1].z, b[2].z, b[3].z),
-                             make_float4(b[0].w, b[1].w, b[2].w, b[3].w)};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 h = split_hi(t[j]);
-          const unsigned off = kmajor_offset(row + j, kc);
-          *reinterpret_cast<float4*>(hi + off) = h;
-          *reinterpret_cast<float4*>(lo + off) = split_lo(t[j], h);
-        }
-      }
+      int mn, k;
+      item_coords(q, mn, k);
+      const unsigned off = T ? mnmajor_offset<ROWS>(mn, k) : kmajor_offset(mn, k >> 2);
+      const float4 h = split_hi(r[i]);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(lo + off) = split_lo(r[i], h);
     }
+  }
+
+  static __device__ __forceinline__ u64 desc(unsigned base, int kstep) {
+    if constexpr (T) return mnmajor_desc<ROWS>(base, kstep);
+    return kmajor_desc(base, kstep);
   }
 };
 
@@ -300,6 +315,7 @@ struct TcParams {
   // NN / NT: B (the weight) pre-split into per-k-stage [hi | lo] K-major
   // swizzled tile images, bulk-copied straight into shared memory
   const unsigned char* b_image;
+  i64 b_stages;     // k stages per n tile in b_image
   i64 m, n, k;
   i64 k_chunk;      // k per split (multiple of kBK)
   int m_tiles, n_tiles, splits;
@@ -367,16 +383,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     ke = min(p.k, kb + p.k_chunk);
   };
 
-  if (warp < kLoaderWarps && B_PRE) {
-    // ------------------------------------------------------------ loaders (B image)
-    // A streams through registers two k-stages ahead, across tile
-    // boundaries; B arrives by one bulk copy per stage.
+  if (warp < kLoaderWarps) {
+    // ------------------------------------------------------------ loaders
+    // A (and B when it streams) go through registers two k-stages ahead,
+    // across tile boundaries, in two alternating register sets; a pre-split
+    // B arrives by one bulk copy per stage.
     const int lt = threadIdx.x;
     int stage = 0;
     unsigned phase = 0;
     struct Pos {
-      int t, kk, nk;
-      i64 kb, ke, m0;
+      int t, kk, nk, nt;
+      i64 kb, ke, m0, n0;
     };
     auto start = [&](Pos& q, int t) {
       q.t = t;
@@ -387,6 +404,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
         tile_coords(q.t, mt, nt, sp);
         k_range(sp, q.kb, q.ke);
         q.m0 = static_cast<i64>(mt) * kBM;
+        q.nt = nt;
+        q.n0 = static_cast<i64>(nt) * BN;
         q.nk = static_cast<int>((q.ke - q.kb + kBK - 1) / kBK);
         if (q.nk > 0) return;
         q.t += gridDim.x;  // empty k range: the MMA warp signals it without stages
@@ -396,9 +415,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       if (++q.kk == q.nk) start(q, q.t + gridDim.x);
     };
     auto valid = [&](const Pos& q) { return q.t < total_tiles; };
-    float4 r0[Cfg::LoadA::kRegs], r1[Cfg::LoadA::kRegs];
-    auto load = [&](float4 (&r)[Cfg::LoadA::kRegs], const Pos& q) {
-      if (valid(q)) Cfg::LoadA::load(p.a, q.m0, q.kb + static_cast<i64>(q.kk) * kBK, q.ke, lt, r);
+    constexpr int kRB = B_PRE ? 1 : Cfg::LoadB::kRegs;
+    struct Regs {
+      float4 a[Cfg::LoadA::kRegs];
+      float4 b[kRB];
+    };
+    Regs r0, r1;
+    auto load = [&](Regs& r, const Pos& q) {
+      if (!valid(q)) return;
+      const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
+      Cfg::LoadA::load(p.a, q.m0, k0, q.ke, lt, r.a);
+      if constexpr (!B_PRE) Cfg::LoadB::load(p.b, q.n0, k0, q.ke, lt, r.b);
     };
     Pos cur, pre;
     start(cur, blockIdx.x);
@@ -407,16 +434,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     if (valid(pre)) advance(pre);
     load(r1, pre);
     if (valid(pre)) advance(pre);
-    auto step = [&](float4 (&r)[Cfg::LoadA::kRegs]) {
+    auto step = [&](Regs& r) {
       mbar_wait(&empty[stage], phase ^ 1u);
       unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
-      if (threadIdx.x == 0) {
-        const i64 g = (cur.kb + static_cast<i64>(cur.kk) * kBK) / kBK;
-        mbar_expect_tx(&full[stage], 2u * Cfg::kTileB);
-        bulk_copy_g2s(st + 2 * Cfg::kTileA, p.b_image + g * 2 * Cfg::kTileB, 2u * Cfg::kTileB,
-                      &full[stage]);
+      if constexpr (B_PRE) {
+        if (threadIdx.x == 0) {
+          const i64 g = cur.nt * p.b_stages + (cur.kb + static_cast<i64>(cur.kk) * kBK) / kBK;
+          mbar_expect_tx(&full[stage], 2u * Cfg::kTileB);
+          bulk_copy_g2s(st + 2 * Cfg::kTileA, p.b_image + g * 2 * Cfg::kTileB,
+                        2u * Cfg::kTileB, &full[stage]);
+        }
       }
-      Cfg::LoadA::store(st, st + Cfg::kTileA, lt, r);
+      Cfg::LoadA::store(st, st + Cfg::kTileA, lt, r.a);
+      if constexpr (!B_PRE)
+        Cfg::LoadB::store(st + 2 * Cfg::kTileA, st + 2 * Cfg::kTileA + Cfg::kTileB, lt, r.b);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[stage]);
@@ -430,49 +461,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       if (!valid(cur)) break;
       step(r1);
     }
-  } else if (warp < kLoaderWarps) {
-    // ------------------------------------------------------------ loaders
-    const int lt = threadIdx.x;  // 0..255
-    int stage = 0;
-    unsigned phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      int mt, nt, sp;
-      tile_coords(t, mt, nt, sp);
-      i64 kb, ke;
-      k_range(sp, kb, ke);
-      const i64 m0 = static_cast<i64>(mt) * kBM, n0 = static_cast<i64>(nt) * BN;
-      const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
-      float4 ra[Cfg::LoadA::kRegs], rb[Cfg::LoadB::kRegs];
-      auto load = [&](int kk) {
-        const i64 k0 = kb + static_cast<i64>(kk) * kBK;
-        Cfg::LoadA::load(p.a, m0, k0, ke, lt, ra);
-        Cfg::LoadB::load(p.b, n0, k0, ke, lt, rb);
-      };
-      if (nk > 0) load(0);
-      for (int kk = 0; kk < nk; ++kk) {
-        float4 ca[Cfg::LoadA::kRegs], cb[Cfg::LoadB::kRegs];
-#pragma unroll
-        for (int i = 0; i < Cfg::LoadA::kRegs; ++i) ca[i] = ra[i];
-#pragma unroll
-        for (int i = 0; i < Cfg::LoadB::kRegs; ++i) cb[i] = rb[i];
-        if (kk + 1 < nk) load(kk + 1);  // next stage's loads in flight
-        mbar_wait(&empty[stage], phase ^ 1u);
-        unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
-        unsigned char* a_hi = st;
-        unsigned char* a_lo = st + Cfg::kTileA;
-        unsigned char* b_hi = st + 2 * Cfg::kTileA;
-        unsigned char* b_lo = b_hi + Cfg::kTileB;
-        Cfg::LoadA::store(a_hi, a_lo, lt, ca);
-        Cfg::LoadB::store(b_hi, b_lo, lt, cb);
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[stage]);
-        if (++stage == STAGES) stage = 0, phase ^= 1u;
-      }
-    }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr unsigned idesc = instr_desc(BN);
+    constexpr unsigned idesc = instr_desc(BN, A_T, B_T && !B_PRE);
     int stage = 0;
     unsigned phase = 0;
     int acc = 0;
@@ -498,8 +489,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
             const unsigned b_hi = base + 2 * Cfg::kTileA, b_lo = b_hi + Cfg::kTileB;
 #pragma unroll
             for (int ks = 0; ks < kBK / 8; ++ks) {
-              const u64 dah = kmajor_desc(a_hi, ks), dal = kmajor_desc(a_lo, ks);
-              const u64 dbh = kmajor_desc(b_hi, ks), dbl = kmajor_desc(b_lo, ks);
+              const u64 dah = Cfg::LoadA::desc(a_hi, ks), dal = Cfg::LoadA::desc(a_lo, ks);
+              u64 dbh, dbl;
+              if constexpr (B_PRE) {
+                dbh = kmajor_desc(b_hi, ks), dbl = kmajor_desc(b_lo, ks);
+              } else {
+                dbh = Cfg::LoadB::desc(b_hi, ks), dbl = Cfg::LoadB::desc(b_lo, ks);
+              }
               const unsigned first = (kk == k_lo && ks == 0) ? 0u : 1u;
               tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
               tc_mma_tf32(d, dah, dbl, idesc, 1u);
@@ -596,23 +592,26 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
 // [hi tile | lo tile], each `rows` x 128 B, K-major 128-B swizzled, zero
 // padded past n and k. One thread per (g, row, 16-B chunk).
 __global__ void b_image_kernel(const float* __restrict__ w, i64 ldw, bool w_is_kxn, i64 n, i64 k,
-                               int rows, i64 stages, unsigned char* __restrict__ img) {
-  const i64 total = stages * rows * 8;
+                               int rows, i64 stages, int n_tiles, unsigned char* __restrict__ img) {
+  // layout [n tile][stage][hi | lo]; n tile t covers rows [t*rows, (t+1)*rows)
+  const i64 total = static_cast<i64>(n_tiles) * stages * rows * 8;
   const unsigned tile = static_cast<unsigned>(rows) * 128u;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     const int c = static_cast<int>(i % 8);
     const int r = static_cast<int>((i / 8) % rows);
-    const i64 g = i / (8 * rows);
+    const i64 g = (i / (8 * rows)) % stages;
+    const i64 t = i / (8 * rows * stages);
+    const i64 gr = t * rows + r;
     float v[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const i64 kk = g * kBK + c * 4 + j;
-      v[j] = (r < n && kk < k) ? (w_is_kxn ? w[kk * ldw + r] : w[r * ldw + kk]) : 0.f;
+      v[j] = (gr < n && kk < k) ? (w_is_kxn ? w[kk * ldw + gr] : w[gr * ldw + kk]) : 0.f;
     }
     const float4 x = make_float4(v[0], v[1], v[2], v[3]);
     const float4 h = split_hi(x);
-    unsigned char* base = img + g * 2 * tile;
+    unsigned char* base = img + (t * stages + g) * 2 * tile;
     const unsigned off = kmajor_offset(r, c);
     *reinterpret_cast<float4*>(base + off) = h;
     *reinterpret_cast<float4*>(base + tile + off) = split_lo(x, h);
@@ -647,10 +646,11 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     // split the weight once per call into its per-stage tile images
     const i64 stages = (p.k + kBK - 1) / kBK;
     static thread_local DevBuf<unsigned char> img;
-    img.ensure(static_cast<size_t>(stages) * 2 * Cfg::kTileB);
-    const i64 items = stages * Cfg::kRowsB * 8;
+    img.ensure(static_cast<size_t>(p.n_tiles) * stages * 2 * Cfg::kTileB);
+    const i64 items = static_cast<i64>(p.n_tiles) * stages * Cfg::kRowsB * 8;
     b_image_kernel<<<ceil_div(items, 256), 256, 0, st>>>(p.b.p, p.b.ld, B_T, p.n, p.k,
-                                                         Cfg::kRowsB, stages, img.p);
+                                                         Cfg::kRowsB, stages, p.n_tiles, img.p);
+    p.b_stages = stages;
     PK_LAUNCH("gemm tcgen05 b image");
     p.b_image = img.p;
   }
@@ -696,7 +696,14 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
   p.a = OperandSrc{a, lda, m, aligned16(a, lda)};
   // B: NN -> MN-major (storage k x n); NT -> K-major (storage n x k); TN -> MN-major
   p.b = OperandSrc{b, ldb, n, aligned16(b, ldb)};
-  const int bn = pick_bn(n);
+  // TN tile width (both operands stream through registers): PK_TN_BN caps it
+  // for experiments; default 128 (measured faster than 256: two register
+  // sets of 128-wide tiles fit without spills)
+  static const int tn_cap = [] {
+    const char* e = std::getenv("PK_TN_BN");
+    return e ? std::atoi(e) : 128;
+  }();
+  const int bn = (ta && !tb) ? pick_bn(std::min<i64>(n, tn_cap)) : pick_bn(n);
   p.m_tiles = static_cast<int>((m + kBM - 1) / kBM);
   p.n_tiles = static_cast<int>((n + bn - 1) / bn);
   const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles;

@@ -28,7 +28,14 @@ __device__ unsigned off_mn(int mn, int k, int rows) {
   return a * 1024 + k * 128 + ((c ^ k) << 4) + (mn & 3) * 4;
 }
 
-struct Case { int a_mn, b_mn, n, swap; };
+struct Case { int a_mn, b_mn, n, swap; int b32 = 0; };
+
+// SWIZZLE_128B_BASE32B MN-major (layout type 1): atoms of 4 k-rows x 128 B
+// (32 MN values); 32-B chunk (mn%32)/8 XOR (k%4); k-groups of 4 at SBO.
+__device__ unsigned off_mn32(int mn, int k, unsigned sbo) {
+  const int a = mn >> 5, c = (mn & 31) >> 3, r = k & 3, g = k >> 2;
+  return g * sbo + a * 512 + r * 128 + ((c ^ r) << 5) + (mn & 7) * 4;
+}
 
 __global__ void probe(Case cs, float* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -51,12 +58,12 @@ __global__ void probe(Case cs, float* out) {
   // a[m][k] = m + 1 + k/16 ; b[n][k] = (k == n % 8) * (1 + n / 8)
   for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x) {
     int m = i / 8, k = i % 8;
-    *(float*)(As + (cs.a_mn ? off_mn(m, k, 128) : off_k(m, k))) = (float)(m + 1);
+    *(float*)(As + (cs.a_mn ? (cs.b32 ? off_mn32(m, k, 2048) : off_mn(m, k, 128)) : off_k(m, k))) = (float)(m + 1);
   }
   for (int i = threadIdx.x; i < cs.n * 8; i += blockDim.x) {
     int n = i / 8, k = i % 8;
     float v = (k == n % 8) ? (float)(1 + n / 8) : 0.f;
-    *(float*)(Bs + (cs.b_mn ? off_mn(n, k, 64) : off_k(n, k))) = v;
+    *(float*)(Bs + (cs.b_mn ? (cs.b32 ? off_mn32(n, k, 1024) : off_mn(n, k, 64)) : off_k(n, k))) = v;
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -72,7 +79,16 @@ __global__ void probe(Case cs, float* out) {
       if (cs.a_mn) { unsigned x = la; la = sa; sa = x; }
       if (cs.b_mn) { unsigned x = lb; lb = sb; sb = x; }
     }
-    uint64_t da = desc(su(As), la, sa, 2), db = desc(su(Bs), lb, sb, 2);
+    if (cs.b32) {  // atoms of 512 B along MN; k-groups of 4 rows
+      if (cs.a_mn) { la = 512; sa = 2048; }
+      if (cs.b_mn) { lb = 512; sb = 1024; }
+      if (cs.swap) {
+        if (cs.a_mn) { unsigned x = la; la = sa; sa = x; }
+        if (cs.b_mn) { unsigned x = lb; lb = sb; sb = x; }
+      }
+    }
+    uint64_t da = desc(su(As), la, sa, cs.a_mn && cs.b32 ? 1 : 2),
+             db = desc(su(Bs), lb, sb, cs.b_mn && cs.b32 ? 1 : 2);
     if (lane == 0) {
       asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                    " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
@@ -106,8 +122,9 @@ int main() {
   CK(cudaMalloc(&d, 128 * 64 * 4));
   CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
   std::vector<float> h(128 * 64);
-  const Case cases[] = {{0, 0, 16, 0}, {0, 0, 64, 0}, {0, 1, 16, 0}, {0, 1, 32, 0}, {0, 1, 64, 0},
-                        {0, 1, 64, 1}, {1, 0, 16, 0}, {1, 0, 16, 1}, {1, 1, 64, 0}, {1, 1, 64, 1}};
+  const Case cases[] = {{0, 0, 16, 0}, {0, 0, 64, 0}, {0, 1, 64, 0, 1}, {0, 1, 64, 1, 1},
+                        {1, 0, 16, 0, 1}, {1, 0, 16, 1, 1}, {1, 1, 64, 0, 1}, {1, 1, 64, 1, 1},
+                        {0, 1, 32, 0, 1}, {0, 1, 16, 0, 1}};
   for (const Case& cs : cases) {
     CK(cudaMemset(d, 0xff, 128 * 64 * 4));
     probe<<<1, 128, 64 * 1024>>>(cs, d);
@@ -118,7 +135,7 @@ int main() {
     for (int m = 0; m < 128; ++m)
       for (int c = 0; c < cs.n; ++c)
         if (h[m * 64 + c] != (float)(m + 1) * (float)(1 + c / 8)) ++bad;
-    printf("a_mn %d b_mn %d n %d swap %d: bad %d/%d | row1:", cs.a_mn, cs.b_mn, cs.n, cs.swap, bad, 128 * cs.n);
+    printf("b32 %d a_mn %d b_mn %d n %d swap %d: bad %d/%d | row1:", cs.b32, cs.a_mn, cs.b_mn, cs.n, cs.swap, bad, 128 * cs.n);
     for (int c = 0; c < cs.n && c < 24; ++c) printf(" %g", h[64 + c]);
     printf("\n");
   }
