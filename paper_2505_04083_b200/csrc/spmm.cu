@@ -133,8 +133,13 @@ __device__ __forceinline__ unsigned end_mask(const u32* __restrict__ bits, u64 k
   return __funnelshift_r(lo, hi, static_cast<unsigned>(k & 31));
 }
 
+// PK_LIST_MINB (compile-time experiment knob): minimum resident blocks per
+// SM the register allocation must allow.
+#ifndef PK_LIST_MINB
+#define PK_LIST_MINB 2
+#endif
 template <int VEC, int LANES, int NV, int U>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, PK_LIST_MINB)
 spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
                  int* __restrict__ counters) {
   using V = typename Vec<VEC>::T;
