@@ -1,7 +1,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "comm.cuh"
 
@@ -55,10 +58,31 @@ void copy_block_launch(const float* src, i64 ld_src, i64 rows, i64 cols, float* 
   PK_LAUNCH("copy block");
 }
 
+struct CommSet {
+  ncclComm_t world = nullptr;
+  std::array<ncclComm_t, 3> axes{nullptr, nullptr, nullptr};
+  ~CommSet() {
+    for (auto& c : axes)
+      if (c) ncclCommDestroy(c);
+    if (world) ncclCommDestroy(world);
+  }
+};
+
+namespace {
+std::mutex g_comm_mu;
+// intentionally leaked: no NCCL teardown during static destruction at exit
+auto& g_comm_cache = *new std::map<std::array<int, 6>, std::shared_ptr<CommSet>>();
+bool comm_cache_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PK_NCCL_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+}  // namespace
+
 Comms::~Comms() {
-  for (auto& c : axes_)
-    if (c) ncclCommDestroy(c);
-  if (world_) ncclCommDestroy(world_);
+  set_.reset();  // cached sets stay alive in the registry until process exit
 }
 
 void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
@@ -67,18 +91,37 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
   check(world_size == grid.size(), "comm init: world size " + std::to_string(world_size) +
                                        " != grid size " + std::to_string(grid.size()));
   if (world_size == 1) return;
-  ncclUniqueId id;
-  std::memcpy(&id, uid, sizeof(id));
-  PK_NCCL(ncclCommInitRank(&world_, world_size, id, rank));
-  for (int a = 0; a < 3; ++a) {
-    if (grid.extent(a) == 1) continue;  // singleton: identity, nothing moves
-    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-    PK_NCCL(ncclCommSplit(world_, grid.group_id(a, coords_), coords_.along(a), &axes_[a], &cfg));
-    int n = 0, r = 0;
-    PK_NCCL(ncclCommCount(axes_[a], &n));
-    PK_NCCL(ncclCommUserRank(axes_[a], &r));
-    check(n == grid.extent(a) && r == coords_.along(a), "comm split: inconsistent axis group");
+  int dev = 0;
+  PK_CUDA(cudaGetDevice(&dev));
+  const std::array<int, 6> key{dev, world_size, rank, grid.g[0], grid.g[1], grid.g[2]};
+  {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    auto it = g_comm_cache.find(key);
+    if (comm_cache_on() && it != g_comm_cache.end()) set_ = it->second;
   }
+  if (!set_) {
+    auto fresh = std::make_shared<CommSet>();
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    PK_NCCL(ncclCommInitRank(&fresh->world, world_size, id, rank));
+    for (int a = 0; a < 3; ++a) {
+      if (grid.extent(a) == 1) continue;  // singleton: identity, nothing moves
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      PK_NCCL(ncclCommSplit(fresh->world, grid.group_id(a, coords_), coords_.along(a),
+                            &fresh->axes[a], &cfg));
+      int n = 0, r = 0;
+      PK_NCCL(ncclCommCount(fresh->axes[a], &n));
+      PK_NCCL(ncclCommUserRank(fresh->axes[a], &r));
+      check(n == grid.extent(a) && r == coords_.along(a), "comm split: inconsistent axis group");
+    }
+    set_ = fresh;
+    if (comm_cache_on()) {
+      std::lock_guard<std::mutex> lk(g_comm_mu);
+      g_comm_cache[key] = fresh;
+    }
+  }
+  world_ = set_->world;
+  axes_ = set_->axes;
 }
 
 void Comms::all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaStream_t st) {
@@ -171,6 +214,30 @@ void Comms::reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int ax
                        ncclSum, j, axes_[axis], st));
   }
   PK_NCCL(ncclGroupEnd());
+}
+
+void Comms::reduce_scatter_rows_range(float* buf, float* out, i64 rows, i64 ld, int axis,
+                                      i64 logical_cols, i64 r0, i64 r1, cudaStream_t st) {
+  const int g = grid_.extent(axis), pos = coords_.along(axis);
+  counters.calls[axis][kReduceScatter]++;
+  counters.ring_numer[axis][kReduceScatter] +=
+      static_cast<u64>(g - 1) * static_cast<u64>(r1 - r0) * logical_cols * sizeof(float);
+  const i64 own0 = chunk_start(rows, g, pos), own1 = chunk_start(rows, g, pos + 1);
+  if (g == 1) {
+    if (buf != out && r1 > r0)
+      PK_CUDA(cudaMemcpyAsync(out + (r0 - own0) * ld, buf + r0 * ld, (r1 - r0) * ld * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
+    return;
+  }
+  PK_NCCL(ncclGroupStart());
+  for (int j = 0; j < g; ++j) {
+    const i64 a = std::max(r0, chunk_start(rows, g, j)), b = std::min(r1, chunk_start(rows, g, j + 1));
+    if (a >= b) continue;
+    float* dst = j == pos ? out + (a - own0) * ld : buf + a * ld;
+    PK_NCCL(ncclReduce(buf + a * ld, dst, (b - a) * ld, ncclFloat32, ncclSum, j, axes_[axis], st));
+  }
+  PK_NCCL(ncclGroupEnd());
+  (void)own1;
 }
 
 }  // namespace pk

@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <array>
+#include <memory>
 
 #include "layout.h"
 #include "pk_common.cuh"
@@ -71,6 +72,10 @@ class Comms {
   // buf is rows x ld (clobbered); out receives chunk rows x ld.
   void reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int axis, i64 logical_cols,
                            cudaStream_t st);
+  // The part of reduce_scatter_rows covering rows [r0, r1) of the buffer:
+  // chunked calls over a partition of [0, rows) add up to the full one.
+  void reduce_scatter_rows_range(float* buf, float* out, i64 rows, i64 ld, int axis,
+                                 i64 logical_cols, i64 r0, i64 r1, cudaStream_t st);
 
   CommCounters counters;
 
@@ -80,6 +85,12 @@ class Comms {
   Coords coords_;
   ncclComm_t world_ = nullptr;
   std::array<ncclComm_t, 3> axes_{nullptr, nullptr, nullptr};
+  // Communicators are a process-level runtime resource (like the CUDA
+  // context): a later engine of the same (device, grid, rank) reuses them
+  // instead of paying ncclCommInitRank + three splits again. Every rank runs
+  // the same sequence of engine creations, so all ranks take the same
+  // branch. PK_NCCL_CACHE=0 turns this off.
+  std::shared_ptr<struct CommSet> set_;
 };
 
 }  // namespace pk

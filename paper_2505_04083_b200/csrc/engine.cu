@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 
 #include "engine.cuh"
@@ -89,6 +90,12 @@ cudaEvent_t PhaseClock::get() {
   return pool[used++];
 }
 
+cudaEvent_t PhaseClock::stamp(cudaStream_t st) {
+  cudaEvent_t e = get();
+  PK_CUDA(cudaEventRecord(e, st));
+  return e;
+}
+
 void PhaseClock::begin(int phase, cudaStream_t st) {
   if (!enabled) return;
   open_phase = phase;
@@ -137,6 +144,7 @@ Engine::Engine(const pk_engine_config& cfg) : cfg_(cfg) {
   for (int l = 0; l < L_; ++l)
     shapes_.push_back(layer_shapes(grid_, lays_[l], c_, cfg.n, dims_[l], dims_[l + 1]));
   PK_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  PK_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   sums_.alloc(4);
 }
 
@@ -145,6 +153,45 @@ Engine::~Engine() {
     cudaStreamSynchronize(st_);
     cudaStreamDestroy(st_);
   }
+  if (cs_) {
+    cudaStreamSynchronize(cs_);
+    cudaStreamDestroy(cs_);
+  }
+  for (auto e : sync_ev_) cudaEventDestroy(e);
+}
+
+cudaEvent_t Engine::sync_event() {
+  if (sync_used_ == sync_ev_.size()) {
+    cudaEvent_t e;
+    PK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sync_ev_.push_back(e);
+  }
+  return sync_ev_[sync_used_++];
+}
+
+int Engine::comm_chunks(i64 rows, int axis) const {
+  if (grid_.extent(axis) == 1) return 1;
+  // ~256K rows per chunk, 2..8 chunks: enough to overlap, few enough that
+  // each collective is a large message
+  return static_cast<int>(std::max<i64>(2, std::min<i64>(8, rows / 262144)));
+}
+
+template <typename P, typename R>
+void Engine::pipelined(i64 rows, int chunks, P&& produce, R&& reduce) {
+  chunks = static_cast<int>(std::max<i64>(1, std::min<i64>(chunks, std::max<i64>(rows, 1))));
+  for (int c = 0; c < chunks; ++c) {
+    const i64 r0 = chunk_start(rows, chunks, c), r1 = chunk_start(rows, chunks, c + 1);
+    produce(r0, r1);
+    cudaEvent_t ready = sync_event();
+    PK_CUDA(cudaEventRecord(ready, st_));
+    PK_CUDA(cudaStreamWaitEvent(cs_, ready, 0));
+    cudaEvent_t a = clock_.stamp(cs_);
+    reduce(r0, r1);
+    clock_.add(4, a, clock_.stamp(cs_));
+  }
+  cudaEvent_t done = sync_event();
+  PK_CUDA(cudaEventRecord(done, cs_));
+  PK_CUDA(cudaStreamWaitEvent(st_, done, 0));
 }
 
 const AdjShard& Engine::shard(const Layout& l) const {
@@ -315,6 +362,20 @@ int Engine::forward_blocks(i64 rows, const Layout& lay) const {
 // ---------------------------------------------------------------------------
 // forward_layer (engine.hpp:158-206)
 
+void Engine::on_comm(const std::function<void(cudaStream_t)>& f) {
+  // every collective runs on the comm stream, in program order, so each
+  // communicator sees the same sequence on every rank
+  cudaEvent_t ready = sync_event();
+  PK_CUDA(cudaEventRecord(ready, st_));
+  PK_CUDA(cudaStreamWaitEvent(cs_, ready, 0));
+  cudaEvent_t a = clock_.stamp(cs_);
+  f(cs_);
+  clock_.add(4, a, clock_.stamp(cs_));
+  cudaEvent_t done = sync_event();
+  PK_CUDA(cudaEventRecord(done, cs_));
+  PK_CUDA(cudaStreamWaitEvent(st_, done, 0));
+}
+
 void Engine::forward_layer(int l, bool fault) {
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
@@ -323,9 +384,9 @@ void Engine::forward_layer(int l, bool fault) {
   i64 ldf;
   if (l == 0) {
     // layer-0 input carries the extra row_shard split: gather it
-    clock_.begin(4, st_);
-    comms_.all_gather_rows(f0_.p(), f0g_.p(), s.f_rows, f0g_.ld, lay.row, s.f_cols, st_);
-    clock_.end(st_);
+    on_comm([&](cudaStream_t cs) {
+      comms_.all_gather_rows(f0_.p(), f0g_.p(), s.f_rows, f0g_.ld, lay.row, s.f_cols, cs);
+    });
     f = f0g_.p();
     ldf = f0g_.ld;
   } else {
@@ -336,35 +397,45 @@ void Engine::forward_layer(int l, bool fault) {
                                    shape(sh.a.rows, sh.a.cols) + " does not match features " +
                                    shape(s.f_rows, s.f_cols));
   DMat& h = h_[l];
+  // blocked aggregation (engine.hpp:175-192): SpMM row block b, then its
+  // all-reduce along inner — overlapped with block b+1's SpMM
   const int blocks = forward_blocks(sh.a.rows, lay);
   const std::vector<u64>& bnnz = sh.blocks_nnz(blocks, st_);
-  // blocked aggregation: SpMM row block, then its all-reduce along inner
-  for (int b = 0; b < blocks; ++b) {
-    const i64 r0 = chunk_start(sh.a.rows, blocks, b), r1 = chunk_start(sh.a.rows, blocks, b + 1);
-    clock_.begin(0, st_);
-    spmm_run(const_cast<SpmmPlan&>(sh.plan_a), view(sh.a), r0, r1, f, ldf, s.f_cols,
-             h.p() + r0 * h.ld, h.ld, st_);
-    spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
-    spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
-    clock_.end(st_);
-    if (!fault) {
-      clock_.begin(4, st_);
-      comms_.all_reduce(h.p() + r0 * h.ld, (r1 - r0) * h.ld, lay.inner,
-                        (r1 - r0) * s.f_cols * 4, st_);
-      clock_.end(st_);
-    }
-  }
-  clock_.begin(4, st_);
-  comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols, st_);
-  clock_.end(st_);
-  clock_.begin(1, st_);
-  gemm_launch(false, false, s.h_rows, s.w_cols, s.h_cols, h.p(), h.ld, wfull_[l].p(),
-              wfull_[l].ld, q_[l].p(), q_[l].ld, cfg_.mode, st_);
+  int b = 0;
+  pipelined(
+      sh.a.rows, blocks,
+      [&](i64 r0, i64 r1) {
+        clock_.begin(0, st_);
+        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, h.p() + r0 * h.ld, h.ld, st_);
+        spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
+        spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
+        ++b;
+        clock_.end(st_);
+      },
+      [&](i64 r0, i64 r1) {
+        if (!fault)  // fault_epoch: the reference's negative control (engine.hpp:186)
+          comms_.all_reduce(h.p() + r0 * h.ld, (r1 - r0) * h.ld, lay.inner,
+                            (r1 - r0) * s.f_cols * 4, cs_);
+      });
+  on_comm([&](cudaStream_t cs) {
+    comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
+                           cs);
+  });
+  // Q = H . W_full, then its all-reduce along col_shard, row-chunked
+  pipelined(
+      s.h_rows, comm_chunks(s.h_rows, lay.col),
+      [&](i64 r0, i64 r1) {
+        clock_.begin(1, st_);
+        gemm_launch(false, false, r1 - r0, s.w_cols, s.h_cols, h.p() + r0 * h.ld, h.ld,
+                    wfull_[l].p(), wfull_[l].ld, q_[l].p() + r0 * q_[l].ld, q_[l].ld, cfg_.mode,
+                    st_);
+        clock_.end(st_);
+      },
+      [&](i64 r0, i64 r1) {
+        comms_.all_reduce(q_[l].p() + r0 * q_[l].ld, (r1 - r0) * q_[l].ld, lay.col,
+                          (r1 - r0) * s.q_cols * 4, cs_);
+      });
   gemm_flops_ += 2 * static_cast<u64>(s.h_rows) * s.w_cols * s.h_cols;
-  clock_.end(st_);
-  clock_.begin(4, st_);
-  comms_.all_reduce(q_[l].p(), q_[l].elems(), lay.col, s.q_rows * s.q_cols * 4, st_);
-  clock_.end(st_);
   if (l + 1 < L_) {
     clock_.begin(1, st_);
     relu_forward_launch(q_[l].p(), q_[l].ld, s.q_rows, s.q_cols, fout_[l].p(), fout_[l].ld, st_);
@@ -379,17 +450,25 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
   const Layout& last = lays_[L_ - 1];
   const Shapes& s = shapes_[L_ - 1];
   const i64 C = dims_[L_];
-  clock_.begin(4, st_);
-  comms_.all_gather_cols(q_[L_ - 1].p(), q_[L_ - 1].ld, logits_.p(), logits_.ld, s.a_rows, C,
-                         last.inner, stage_.p(), st_);
-  clock_.end(st_);
+  // logits: the column gather along inner (trainer.hpp:499); with a single
+  // member the local Q block already is the full logits matrix
+  const float* logits = q_[L_ - 1].p();
+  i64 ldl = q_[L_ - 1].ld;
+  if (comms_.size(last.inner) > 1) {
+    on_comm([&](cudaStream_t cs) {
+      comms_.all_gather_cols(q_[L_ - 1].p(), q_[L_ - 1].ld, logits_.p(), logits_.ld, s.a_rows,
+                             C, last.inner, stage_.p(), cs);
+    });
+    logits = logits_.p();
+    ldl = logits_.ld;
+  } else {
+    comms_.counters.calls[last.inner][kAllGather]++;  // the reference still counts the call
+  }
   clock_.begin(2, st_);
-  ce_sums_launch(logits_.p(), logits_.ld, s.a_rows, C, labels_.p, mask_.p, dl_.p(), dl_.ld,
-                 sums_.p, ce_ws_, st_);
+  ce_sums_launch(logits, ldl, s.a_rows, C, labels_.p, mask_.p, dl_.p(), dl_.ld, sums_.p, ce_ws_,
+                 st_);
   clock_.end(st_);
-  clock_.begin(4, st_);
-  comms_.all_reduce_f64(sums_.p, 3, last.row, st_);
-  clock_.end(st_);
+  on_comm([&](cudaStream_t cs) { comms_.all_reduce_f64(sums_.p, 3, last.row, cs); });
   double h[3];
   u32 bad = 0;
   PK_CUDA(cudaMemcpyAsync(h, sums_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -418,7 +497,7 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
 void Engine::backward_layer(int l) {
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
-  const AdjShard& sh = shard(lay);
+  AdjShard& sh = const_cast<AdjShard&>(shard(lay));
   const bool is_last = l == L_ - 1;
   // dQ: the loss gradient's own class chunk on the last layer (a strided
   // view of dlogits: no copy), relu'(Q) * dF otherwise
@@ -440,36 +519,49 @@ void Engine::backward_layer(int l) {
               dwp_[l].p(), dwp_[l].ld, cfg_.mode, st_);
   gemm_flops_ += 2 * static_cast<u64>(s.h_cols) * s.q_cols * s.h_rows;
   clock_.end(st_);
-  clock_.begin(4, st_);
-  comms_.reduce_scatter_rows(dwp_[l].p(), dw_[l].p(), s.f_cols, dwp_[l].ld, lay.row, s.w_cols,
-                             st_);
-  comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
-                         st_);
-  clock_.end(st_);
-  clock_.begin(2, st_);
+  on_comm([&](cudaStream_t cs) {
+    comms_.reduce_scatter_rows(dwp_[l].p(), dw_[l].p(), s.f_cols, dwp_[l].ld, lay.row, s.w_cols,
+                               cs);
+    comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
+                           cs);
+  });
+  // dH = dQ . W_full^T, then its all-reduce along inner, row-chunked
   const i64 lddh = pad4(s.h_cols);
-  gemm_launch(false, true, s.q_rows, s.h_cols, s.q_cols, dq, lddq, wfull_[l].p(), wfull_[l].ld,
-              dh_.p(), lddh, cfg_.mode, st_);
+  pipelined(
+      s.q_rows, comm_chunks(s.q_rows, lay.inner),
+      [&](i64 r0, i64 r1) {
+        clock_.begin(2, st_);
+        gemm_launch(false, true, r1 - r0, s.h_cols, s.q_cols, dq + r0 * lddq, lddq,
+                    wfull_[l].p(), wfull_[l].ld, dh_.p() + r0 * lddh, lddh, cfg_.mode, st_);
+        clock_.end(st_);
+      },
+      [&](i64 r0, i64 r1) {
+        comms_.all_reduce(dh_.p() + r0 * lddh, (r1 - r0) * lddh, lay.inner,
+                          (r1 - r0) * s.h_cols * 4, cs_);
+      });
   gemm_flops_ += 2 * static_cast<u64>(s.q_rows) * s.h_cols * s.q_cols;
-  clock_.end(st_);
-  clock_.begin(4, st_);
-  comms_.all_reduce(dh_.p(), s.h_rows * lddh, lay.inner, s.h_rows * s.h_cols * 4, st_);
-  clock_.end(st_);
-  clock_.begin(5, st_);
+  // dF = A^T . dH, then reduce-scatter (layer 0) or all-reduce along
+  // row_shard, row-chunked
   const i64 lddf = pad4(s.f_cols);
-  spmm_run(const_cast<SpmmPlan&>(sh.plan_at), view(sh.at), 0, sh.at.rows, dh_.p(), lddh, s.f_cols,
-           df_.p(), lddf, st_);
+  pipelined(
+      sh.at.rows, comm_chunks(sh.at.rows, lay.row),
+      [&](i64 r0, i64 r1) {
+        clock_.begin(5, st_);
+        spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, s.f_cols, df_.p() + r0 * lddf,
+                 lddf, st_);
+        clock_.end(st_);
+      },
+      [&](i64 r0, i64 r1) {
+        if (l == 0)
+          comms_.reduce_scatter_rows_range(df_.p(), df0_.p(), s.a_cols, lddf, lay.row, s.f_cols,
+                                           r0, r1, cs_);
+        else
+          comms_.all_reduce(df_.p() + r0 * lddf, (r1 - r0) * lddf, lay.row,
+                            (r1 - r0) * s.f_cols * 4, cs_);
+      });
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.f_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.f_cols);
-  clock_.end(st_);
-  clock_.begin(4, st_);
-  if (l == 0) {
-    comms_.reduce_scatter_rows(df_.p(), df0_.p(), s.a_cols, lddf, lay.row, s.f_cols, st_);
-  } else {
-    comms_.all_reduce(df_.p(), s.a_cols * lddf, lay.row, s.a_cols * s.f_cols * 4, st_);
-    std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
-  }
-  clock_.end(st_);
+  if (l > 0) std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
 }
 
 void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
@@ -477,6 +569,7 @@ void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
   check(comms_.ready(), "engine: communicators not initialised");
   PK_CUDA(cudaSetDevice(cfg_.device));
   const bool fault = epoch == cfg_.fault_epoch;
+  sync_used_ = 0;
   for (int l = 0; l < L_; ++l) forward_layer(l, fault);
   loss(epoch, loss_out, acc_out);
   for (int l = L_ - 1; l >= 0; --l) backward_layer(l);

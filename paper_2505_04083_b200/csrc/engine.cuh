@@ -3,6 +3,7 @@
 // Engine; collectives go through Comms (NCCL per-axis communicators).
 #pragma once
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <vector>
@@ -50,6 +51,9 @@ struct PhaseClock {
   size_t used = 0;
   bool enabled = true;
   cudaEvent_t get();
+  // an interval [a, b] of events recorded on any stream
+  void add(int phase, cudaEvent_t a, cudaEvent_t b) { marks.push_back({phase, a, b}); }
+  cudaEvent_t stamp(cudaStream_t st);
   void begin(int phase, cudaStream_t st);
   void end(cudaStream_t st);
   void collect(double out[6]);  // syncs, sums seconds per phase, resets
@@ -81,6 +85,15 @@ class Engine {
   // pick for speed: one launch when no all-reduce follows, a few pipelined
   // blocks otherwise. An explicit block_count is honoured.
   int forward_blocks(i64 rows, const Layout& lay) const;
+  // Row-chunked producer -> collective pipeline: produce(r0, r1) runs on the
+  // compute stream, reduce(r0, r1) on the comm stream once that chunk is
+  // done, so chunk c's collective overlaps chunk c+1's compute. The compute
+  // stream waits for the last collective before returning. One chunk when
+  // the collective's axis is a singleton (nothing moves).
+  template <typename P, typename R>
+  void pipelined(i64 rows, int chunks, P&& produce, R&& reduce);
+  int comm_chunks(i64 rows, int axis) const;
+  void on_comm(const std::function<void(cudaStream_t)>& f);
 
   pk_engine_config cfg_;
   Grid grid_;
@@ -91,6 +104,10 @@ class Engine {
   std::vector<Layout> lays_;
   std::vector<Shapes> shapes_;
   cudaStream_t st_ = nullptr;
+  cudaStream_t cs_ = nullptr;  // collectives (overlapped with st_)
+  std::vector<cudaEvent_t> sync_ev_;
+  size_t sync_used_ = 0;
+  cudaEvent_t sync_event();
   Comms comms_;
   // one per (plane, parity) key; keys whose block is the same range of the
   // same variant share one shard (at 1x1x1 planes 0 and 2 are both A_even)
