@@ -133,13 +133,16 @@ __device__ __forceinline__ unsigned end_mask(const u32* __restrict__ bits, u64 k
   return __funnelshift_r(lo, hi, static_cast<unsigned>(k & 31));
 }
 
-// PK_LIST_MINB (compile-time experiment knob): minimum resident blocks per
-// SM the register allocation must allow.
-#ifndef PK_LIST_MINB
-#define PK_LIST_MINB 2
-#endif
+// Minimum resident blocks per SM for the register allocation: three for
+// the 2-vector (D <= 256) form, where the extra warps' gathers outweigh the
+// registers (measured, scripts/spmm_minb_sweep.sh: -4 % at D=256; the 1-vector
+// form is already register-light and gets slower when squeezed).
+template <int NV>
+constexpr int list_min_blocks() {
+  return NV == 2 ? 3 : 2;
+}
 template <int VEC, int LANES, int NV, int U>
-__global__ void __launch_bounds__(kThreads, PK_LIST_MINB)
+__global__ void __launch_bounds__(kThreads, list_min_blocks<NV>())
 spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
                  int* __restrict__ counters) {
   using V = typename Vec<VEC>::T;
