@@ -103,10 +103,17 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
     auto fresh = std::make_shared<CommSet>();
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
-    PK_NCCL(ncclCommInitRank(&fresh->world, world_size, id, rank));
+    // NCCL's CTAs share the SMs with the SpMM / GEMM they overlap: cap them
+    // (NVLink 5 needs few CTAs per collective). PK_NCCL_MAX_CTAS overrides.
+    const char* mc = std::getenv("PK_NCCL_MAX_CTAS");
+    const int max_ctas = mc ? std::atoi(mc) : 16;
+    ncclConfig_t wcfg = NCCL_CONFIG_INITIALIZER;
+    if (max_ctas > 0) wcfg.maxCTAs = max_ctas;
+    PK_NCCL(ncclCommInitRankConfig(&fresh->world, world_size, id, rank, &wcfg));
     for (int a = 0; a < 3; ++a) {
       if (grid.extent(a) == 1) continue;  // singleton: identity, nothing moves
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      if (max_ctas > 0) cfg.maxCTAs = max_ctas;
       PK_NCCL(ncclCommSplit(fresh->world, grid.group_id(a, coords_), coords_.along(a),
                             &fresh->axes[a], &cfg));
       int n = 0, r = 0;

@@ -75,32 +75,56 @@ __global__ void __launch_bounds__(kCeWarps * 32)
 ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
           const u32* __restrict__ labels, const u8* __restrict__ mask,
           float* __restrict__ dl, i64 ldd, double* __restrict__ partial,
-          u32* __restrict__ bad_label) {
+          u32* __restrict__ bad_label, u64 scale_count) {
+  // (T)1 / (T)global_count (trainer.hpp:84), applied as the reference's
+  // separate multiply, fl(d * s)
+  const float s = scale_count ? __fdiv_rn(1.f, static_cast<float>(scale_count)) : 1.f;
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const i64 gw = static_cast<i64>(blockIdx.x) * kCeWarps + w;
   const i64 nw = static_cast<i64>(gridDim.x) * kCeWarps;
   double loss = 0, count = 0, correct = 0;
-  for (i64 r = gw; r < rows; r += nw) {
+  // the next row's mask, label and logits are loaded before the current row
+  // is processed: one memory latency per row instead of three serial ones
+  const int nt = (classes + 31) / 32;
+  auto fetch = [&](i64 r, u8& m, u32& lab, float (&x)[kCeMaxPerLane]) {
+    m = 0, lab = 0;
+    if (r >= rows) return;
+    m = mask[r];
+    lab = labels[r];
     const float* row = logits + r * ldl;
+#pragma unroll
+    for (int t = 0; t < kCeMaxPerLane; ++t) {
+      const int j = lane + 32 * t;
+      x[t] = (t < nt && j < classes) ? row[j] : -INFINITY;
+    }
+  };
+  u8 m_next;
+  u32 lab_next;
+  float x_next[kCeMaxPerLane];
+  fetch(gw, m_next, lab_next, x_next);
+  for (i64 r = gw; r < rows; r += nw) {
+    const u8 m = m_next;
+    const u32 lab = lab_next;
+    float xv[kCeMaxPerLane];
+#pragma unroll
+    for (int t = 0; t < kCeMaxPerLane; ++t) xv[t] = x_next[t];
+    fetch(r + nw, m_next, lab_next, x_next);
     float* drow = dl + r * ldd;
-    if (!mask[r]) {
+    if (!m) {
       for (int j = lane; j < classes; j += 32) drow[j] = 0.f;
       continue;
     }
-    const u32 lab = labels[r];
     if (lab >= static_cast<u32>(classes)) {
       if (lane == 0) atomicExch(bad_label, 1u);
       for (int j = lane; j < classes; j += 32) drow[j] = 0.f;
       continue;
     }
-    float xv[kCeMaxPerLane];
     // first max, lowest index on ties (kernels.hpp:142-145)
     float mx = -INFINITY;
     int am = 0x7fffffff;
 #pragma unroll
     for (int t = 0; t < kCeMaxPerLane; ++t) {
       const int j = lane + 32 * t;
-      xv[t] = j < classes ? row[j] : -INFINITY;
       if (j < classes && (xv[t] > mx || am == 0x7fffffff)) mx = xv[t], am = j;
     }
 #pragma unroll
@@ -137,7 +161,7 @@ ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
       if (j < classes) {
         float d = __fdiv_rn(ev[t], denom);
         if (j == static_cast<int>(lab)) d = __fsub_rn(d, 1.f);
-        drow[j] = d;
+        drow[j] = scale_count ? __fmul_rn(d, s) : d;
       }
     }
   }
@@ -224,7 +248,7 @@ void relu_backward_launch(const float* q, i64 ldq, const float* df, i64 lddf, i6
 
 void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
                     const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
-                    cudaStream_t st) {
+                    cudaStream_t st, u64 scale_count) {
   check(classes <= 32 * kCeMaxPerLane,
         "cross entropy: at most " + std::to_string(32 * kCeMaxPerLane) + " classes supported");
   const int blocks = std::max(1, std::min<int>(sm_count() * 4, ceil_div(rows, kCeWarps)));
@@ -233,7 +257,8 @@ void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u
   PK_CUDA(cudaMemsetAsync(ws.bad.p, 0, sizeof(u32), st));
   if (rows > 0 && classes > 0) {
     ce_kernel<<<blocks, kCeWarps * 32, 0, st>>>(logits, ldl, rows, static_cast<int>(classes),
-                                               labels, mask, dl, ldd, ws.partial.p, ws.bad.p);
+                                               labels, mask, dl, ldd, ws.partial.p, ws.bad.p,
+                                               scale_count);
     PK_LAUNCH("cross entropy");
     ce_finish_kernel<<<1, 32, 0, st>>>(ws.partial.p, blocks, sums);
   } else {

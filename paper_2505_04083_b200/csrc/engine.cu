@@ -344,6 +344,17 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     PK_CUDA(cudaMemcpyAsync(mask_.p, (parity ? ds.mask_col : ds.mask_row) + lr_rng.first, lrows,
                             cudaMemcpyDeviceToDevice, st_));
   }
+  // global CE count = masked nodes over all row chunks (the label ranges of
+  // the last layer's row group partition [0, n)); constant across epochs, so
+  // the gradient scaling can ride in the CE kernel
+  {
+    std::vector<u8> hm(n);
+    PK_CUDA(cudaMemcpyAsync(hm.data(), parity ? ds.mask_col : ds.mask_row, n,
+                            cudaMemcpyDeviceToHost, st_));
+    PK_CUDA(cudaStreamSynchronize(st_));
+    mask_count_ = 0;
+    for (u8 m : hm) mask_count_ += m != 0;
+  }
   logits_.alloc(sl.a_rows, dims_[L_]);
   dl_.alloc(sl.a_rows, dims_[L_]);
   stage_.alloc(sl.a_rows, dims_[L_]);
@@ -466,7 +477,7 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
   }
   clock_.begin(2, st_);
   ce_sums_launch(logits, ldl, s.a_rows, C, labels_.p, mask_.p, dl_.p(), dl_.ld, sums_.p, ce_ws_,
-                 st_);
+                 st_, mask_count_);
   clock_.end(st_);
   on_comm([&](cudaStream_t cs) { comms_.all_reduce_f64(sums_.p, 3, last.row, cs); });
   double h[3];
@@ -486,9 +497,8 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
                                      std::to_string(loss) + ")");
   *loss_out = loss;
   *acc_out = static_cast<double>(correct) / static_cast<double>(count);
-  clock_.begin(2, st_);
-  scale_by_count_launch(dl_.p(), dl_.ld, s.a_rows, C, sums_.p, st_);
-  clock_.end(st_);
+  check(count == mask_count_, "cross entropy: counted " + std::to_string(count) +
+                                  " masked rows, expected " + std::to_string(mask_count_));
 }
 
 // ---------------------------------------------------------------------------

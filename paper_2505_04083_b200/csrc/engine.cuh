@@ -127,6 +127,7 @@ class Engine {
   DMat logits_, dl_, stage_;
   DevBuf<u32> labels_;
   DevBuf<u8> mask_;
+  u64 mask_count_ = 0;  // global number of masked nodes (the CE count)
   DevBuf<double> sums_;
   CeWorkspace ce_ws_;
   PhaseClock clock_;
