@@ -97,6 +97,11 @@ typedef struct pk_spmm_plan pk_spmm_plan;
  * 0 = automatic (max(4096, 64 x mean row length)). */
 int pk_spmm_plan_create(const pk_csr* a, int64_t hub_threshold, void* stream,
                         pk_spmm_plan** out);
+/* The same with a numeric mode: PK_MODE_PARITY is the call above
+ * (bit-identical); PK_MODE_FAST cuts hub rows into fixed segments whose sums
+ * are combined in a fixed order (deterministic, fp32-level difference). */
+int pk_spmm_plan_create_mode(const pk_csr* a, int64_t hub_threshold, int mode,
+                             void* stream, pk_spmm_plan** out);
 int pk_spmm_plan_destroy(pk_spmm_plan* plan);
 int pk_spmm_plan_rows_f32(const pk_spmm_plan* plan, const pk_csr* a, int64_t r0,
                           int64_t r1, const float* x, int64_t x_rows,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "pk_spmm_rows_f32": (INT, [C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64, U64P, P]),
     "pk_spmm_f32": (INT, [C.POINTER(pk_csr), P, I64, I64, I64, P, I64, U64P, P]),
     "pk_spmm_plan_create": (INT, [C.POINTER(pk_csr), I64, P, C.POINTER(P)]),
+    "pk_spmm_plan_create_mode": (INT, [C.POINTER(pk_csr), I64, INT, P, C.POINTER(P)]),
     "pk_spmm_plan_destroy": (INT, [P]),
     "pk_spmm_plan_rows_f32": (INT, [P, C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64,
                                     U64P, P]),

@@ -141,6 +141,23 @@ int pk_spmm_plan_create(const pk_csr* a, int64_t hub_threshold, void* stream,
   });
 }
 
+int pk_spmm_plan_create_mode(const pk_csr* a, int64_t hub_threshold, int mode, void* stream,
+                             pk_spmm_plan** out) {
+  return guard([&] {
+    check_csr(a, "spmm plan");
+    check(mode == PK_MODE_PARITY || mode == PK_MODE_FAST, "spmm plan: unknown mode");
+    auto* p = new pk_spmm_plan;
+    try {
+      spmm_plan_build(p->plan, *a, static_cast<u64>(hub_threshold), as_stream(stream),
+                      mode == PK_MODE_FAST ? spmm_fast_segment() : 0);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
 int pk_spmm_plan_destroy(pk_spmm_plan* plan) {
   return guard([&] { delete plan; });
 }

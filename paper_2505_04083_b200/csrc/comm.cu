@@ -103,10 +103,11 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
     auto fresh = std::make_shared<CommSet>();
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
-    // NCCL's CTAs share the SMs with the SpMM / GEMM they overlap: cap them
-    // (NVLink 5 needs few CTAs per collective). PK_NCCL_MAX_CTAS overrides.
+    // NCCL's CTAs share the SMs with the SpMM / GEMM they overlap.
+    // PK_NCCL_MAX_CTAS caps them; the default (NCCL's own choice) measured
+    // best: a 16-CTA cap slowed the 2-GPU epoch from 52.9 to 56.6 ms.
     const char* mc = std::getenv("PK_NCCL_MAX_CTAS");
-    const int max_ctas = mc ? std::atoi(mc) : 16;
+    const int max_ctas = mc ? std::atoi(mc) : 0;
     ncclConfig_t wcfg = NCCL_CONFIG_INITIALIZER;
     if (max_ctas > 0) wcfg.maxCTAs = max_ctas;
     PK_NCCL(ncclCommInitRankConfig(&fresh->world, world_size, id, rank, &wcfg));

@@ -276,8 +276,11 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     mark("csr_block");
     csr_transpose(view(sh->a), &sh->at, st_);
     mark("csr_transpose");
-    spmm_plan_build(sh->plan_a, view(sh->a), static_cast<u64>(cfg_.hub_threshold), st_);
-    spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_);
+    // FAST mode cuts hub rows into segments summed in a fixed order
+    // (tolerance-level difference); PARITY keeps every row one exact chain
+    const u64 seg = cfg_.mode == PK_MODE_FAST ? spmm_fast_segment() : 0;
+    spmm_plan_build(sh->plan_a, view(sh->a), static_cast<u64>(cfg_.hub_threshold), st_, seg);
+    spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_, seg);
     mark("spmm plans");
     sh->nnz_t = sh->at.nnz;
     shards_[plane * 2 + parity] = std::move(sh);

@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <tuple>
 #include <vector>
@@ -99,6 +100,8 @@ struct ListArgs {
   float* y = nullptr;
   i64 ldy = 0;
   i64 r0 = 0;                   // y holds rows [r0, ...)
+  float* part = nullptr;        // FAST plan: segment sums (target bit 31 set)
+  i64 ldp = 0;
   int nvec = 0;
 };
 
@@ -175,7 +178,10 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
     for (int q = 0; q < NV; ++q) acc[q] = Vec<VEC>::zero();
     auto row_done = [&]() {
       const u32 row = __shfl_sync(gmask, rid, rn, LANES);
-      float* yrow = a.y + (static_cast<i64>(row) - a.r0) * a.ldy + (vbase + lane) * VEC;
+      float* yrow = (row & 0x80000000u)
+                        ? a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp
+                        : a.y + (static_cast<i64>(row) - a.r0) * a.ldy;
+      yrow += (vbase + lane) * VEC;
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
         if (valid[q]) *reinterpret_cast<V*>(yrow + q * LANES * VEC) = acc[q];
@@ -258,6 +264,22 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
       k += cnt;
       w = wn;
     }
+  }
+}
+
+// FAST plan: y[hub row] = fold of its segment sums in segment order
+__global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* __restrict__ seg0,
+                                        const u32* __restrict__ nseg, i64 nh, i64 r0,
+                                        const float* __restrict__ part, i64 ldp, float* y,
+                                        i64 ldy, i64 d) {
+  const i64 total = nh * d;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 h = i / d, c = i % d;
+    const u64 s0 = seg0[h];
+    float acc = part[s0 * ldp + c];
+    for (u32 k = 1; k < nseg[h]; ++k) acc = __fadd_rn(acc, part[(s0 + k) * ldp + c]);
+    y[(static_cast<i64>(hub[h]) - r0) * ldy + c] = acc;
   }
 }
 
@@ -542,17 +564,20 @@ int pick_vec(const float* x, i64 ldx, const float* y, i64 ldy, i64 d) {
 // ---------------------------------------------------------------------------
 // plan construction (device side; runs once per shard)
 
-__global__ void classify_rows_kernel(const u64* __restrict__ rp, i64 rows, u64 thr,
-                                     u8* __restrict__ is_reg, u8* __restrict__ is_empty,
-                                     u8* __restrict__ is_hub, u64* __restrict__ reg_len) {
+// entries per row: 0 (empty, or hub on the exact plan), 1 (regular), or
+// ceil(len / segment) (hub on the FAST plan)
+__global__ void classify_rows_kernel(const u64* __restrict__ rp, i64 rows, u64 thr, u64 segment,
+                                     u64* __restrict__ ents, u64* __restrict__ hsegs,
+                                     u8* __restrict__ is_empty, u8* __restrict__ is_hub) {
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < rows;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
     const u64 len = rp[i + 1] - rp[i];
     const bool hub = len >= thr, empty = len == 0;
-    is_reg[i] = !hub && !empty;
+    const u64 nseg = (hub && segment) ? (len + segment - 1) / segment : 0;
+    ents[i] = empty ? 0 : (hub ? nseg : 1);
+    hsegs[i] = nseg;
     is_empty[i] = empty;
     is_hub[i] = hub;
-    reg_len[i] = (!hub && !empty) ? len : 0;
   }
 }
 
@@ -562,21 +587,48 @@ __global__ void iota_rows_kernel(u32* p, i64 n) {
     p[i] = static_cast<u32>(i);
 }
 
-// one warp per regular row: copy its (col, val) pairs into the packed
-// stream and mark its last nonzero
+// per row: its entries' row key, store target and length
+__global__ void fill_entries_kernel(const u64* __restrict__ rp, i64 rows, u64 segment,
+                                    const u64* __restrict__ ents, const u64* __restrict__ ent_off,
+                                    const u64* __restrict__ hsegs,
+                                    const u64* __restrict__ hseg_off, u32* __restrict__ rowkey,
+                                    u32* __restrict__ target, u64* __restrict__ elen) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < rows;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const u64 ne = ents[i];
+    if (ne == 0) continue;
+    const u64 len = rp[i + 1] - rp[i], e0 = ent_off[i];
+    if (hsegs[i] == 0) {  // a regular row: one entry, stored to its own row
+      rowkey[e0] = static_cast<u32>(i);
+      target[e0] = static_cast<u32>(i);
+      elen[e0] = len;
+      continue;
+    }
+    for (u64 s = 0; s < ne; ++s) {
+      rowkey[e0 + s] = static_cast<u32>(i);
+      target[e0 + s] = 0x80000000u | static_cast<u32>(hseg_off[i] + s);
+      elen[e0 + s] = min(segment, len - s * segment);
+    }
+  }
+}
+
+// one warp per row: copy its (col, val) pairs into the packed stream and
+// mark the last nonzero of each of its entries
 __global__ void compact_rows_kernel(const u64* __restrict__ rp, const u32* __restrict__ ci,
-                                    const float* __restrict__ val, const u32* __restrict__ rl,
-                                    const u64* __restrict__ rpc, i64 regular,
+                                    const float* __restrict__ val, i64 rows,
+                                    const u64* __restrict__ ents,
+                                    const u64* __restrict__ ent_off, const u64* __restrict__ rpc,
                                     u64* __restrict__ cv, u32* __restrict__ endbits) {
   const int lane = threadIdx.x % 32;
-  for (i64 e = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; e < regular;
-       e += static_cast<i64>(gridDim.x) * blockDim.x / 32) {
-    const u32 row = rl[e];
-    const u64 s = rp[row], len = rp[row + 1] - s, dst = rpc[e];
+  for (i64 i = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; i < rows;
+       i += static_cast<i64>(gridDim.x) * blockDim.x / 32) {
+    const u64 ne = ents[i];
+    if (ne == 0) continue;
+    const u64 s = rp[i], len = rp[i + 1] - s, e0 = ent_off[i], dst = rpc[e0];
     for (u64 j = lane; j < len; j += 32)
       cv[dst + j] = (static_cast<u64>(__float_as_uint(val[s + j])) << 32) | ci[s + j];
-    if (lane == 0) {
-      const u64 last = dst + len - 1;
+    for (u64 e = lane; e < ne; e += 32) {
+      const u64 last = rpc[e0 + e + 1] - 1;
       atomicOr(endbits + (last >> 5), 1u << (last & 31));
     }
   }
@@ -591,6 +643,15 @@ __global__ void hub_len_kernel(const u64* __restrict__ rp, const u32* __restrict
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
     len[i] = rp[rows[i] + 1] - rp[rows[i]];
+}
+
+__global__ void seg_meta_kernel(const u64* __restrict__ hsegs, const u64* __restrict__ hseg_off,
+                                i64 n, u32* __restrict__ lo, u32* __restrict__ cnt) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    lo[i] = static_cast<u32>(hseg_off[i]);
+    cnt[i] = static_cast<u32>(hsegs[i]);
+  }
 }
 
 unsigned blocks_for(i64 n, int per = 256) {
@@ -642,13 +703,15 @@ SpmmPlan::Range& plan_range(SpmmPlan& plan, i64 r0, i64 r1, cudaStream_t st) {
   SpmmPlan::Range rg;
   rg.r0 = r0, rg.r1 = r1;
   if (r0 == 0 && r1 == plan.rows) {
-    rg.i0 = 0, rg.i1 = plan.regular, rg.e0 = 0, rg.e1 = plan.empty;
+    rg.i0 = 0, rg.i1 = plan.entries, rg.e0 = 0, rg.e1 = plan.empty;
+    rg.h0 = 0, rg.h1 = plan.segment ? plan.hub_count : 0;
   } else {
-    std::tie(rg.i0, rg.i1) = range_of(plan.rl.p, plan.regular, r0, r1, st);
+    std::tie(rg.i0, rg.i1) = range_of(plan.rowkey.p, plan.entries, r0, r1, st);
     std::tie(rg.e0, rg.e1) = range_of(plan.empty_rows.p, plan.empty, r0, r1, st);
+    if (plan.segment) std::tie(rg.h0, rg.h1) = range_of(plan.hub_asc.p, plan.hub_count, r0, r1, st);
   }
-  // hub subset keeps the longest-first order
-  if (plan.hub_count) {
+  // exact plan: the hub subset keeps the longest-first order
+  if (!plan.segment && plan.hub_count) {
     std::vector<i64> all(plan.hub_count), sel;
     PK_CUDA(cudaMemcpyAsync(all.data(), plan.hub_rows.p, all.size() * sizeof(i64),
                             cudaMemcpyDeviceToHost, st));
@@ -669,9 +732,19 @@ SpmmPlan::Range& plan_range(SpmmPlan& plan, i64 r0, i64 r1, cudaStream_t st) {
 
 }  // namespace
 
-void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_t st) {
+u64 spmm_fast_segment() {
+  static const u64 seg = [] {
+    const char* e = std::getenv("PK_SPMM_SEGMENT");
+    return e ? static_cast<u64>(std::atoll(e)) : u64{2048};
+  }();
+  return seg;
+}
+
+void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_t st,
+                     u64 segment) {
   plan = SpmmPlan();
   plan.rows = a.rows;
+  plan.segment = segment;
   if (a.rows == 0) return;
   // A row is a hub when one lane chain over it would outlast the rest of the
   // work spread over the whole GPU; measured on the products shape
@@ -679,19 +752,29 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
   const u64 avg = a.nnz / std::max<i64>(1, a.rows);
   plan.threshold = threshold ? threshold : std::max<u64>(4096, 64 * avg);
   const i64 n = a.rows;
-  DevBuf<u8> is_reg(n), is_empty(n), is_hub(n);
-  DevBuf<u64> reg_len(n);
+  DevBuf<u64> ents(n), hsegs(n), ent_off(n + 1), hseg_off(n + 1);
+  DevBuf<u8> is_empty(n), is_hub(n);
   DevBuf<u32> ids(n);
   DevBuf<i64> count(1);
-  classify_rows_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, plan.threshold, is_reg.p,
-                                                       is_empty.p, is_hub.p, reg_len.p);
+  classify_rows_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, plan.threshold, segment,
+                                                       ents.p, hsegs.p, is_empty.p, is_hub.p);
   PK_LAUNCH("spmm plan classify");
   iota_rows_kernel<<<blocks_for(n), 256, 0, st>>>(ids.p, n);
   PK_LAUNCH("spmm plan iota");
-  auto select = [&](const u8* flags, DevBuf<u32>& out) {
+  auto exclusive_scan = [&](const u64* in, u64* out) {  // out[0..n], out[n] = total
+    PK_CUDA(cudaMemsetAsync(out, 0, sizeof(u64), st));
+    cub_run([&](void* t, size_t& b) {
+      return cub::DeviceScan::InclusiveSum(t, b, in, out + 1, n, st);
+    }, st);
+    u64 total = 0;
+    PK_CUDA(cudaMemcpyAsync(&total, out + n, sizeof(u64), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    return total;
+  };
+  auto select = [&](const u32* src, const u8* flags, DevBuf<u32>& out) {
     DevBuf<u32> tmp(n);
     cub_run([&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, ids.p, flags, tmp.p, count.p, n, st);
+      return cub::DeviceSelect::Flagged(t, b, src, flags, tmp.p, count.p, n, st);
     }, st);
     i64 c = 0;
     PK_CUDA(cudaMemcpy(&c, count.p, sizeof(i64), cudaMemcpyDeviceToHost));
@@ -700,41 +783,52 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
       PK_CUDA(cudaMemcpyAsync(out.p, tmp.p, c * sizeof(u32), cudaMemcpyDeviceToDevice, st));
     return c;
   };
-  plan.regular = select(is_reg.p, plan.rl);
-  plan.empty = select(is_empty.p, plan.empty_rows);
+  plan.entries = static_cast<i64>(exclusive_scan(ents.p, ent_off.p));
+  plan.segments = exclusive_scan(hsegs.p, hseg_off.p);
+  plan.empty = select(ids.p, is_empty.p, plan.empty_rows);
   DevBuf<u32> hubs32;
-  const i64 nh = select(is_hub.p, hubs32);
-  // regular offsets: exclusive scan of the lengths over the regular list
-  plan.rpc.alloc(plan.regular + 1);
+  const i64 nh = select(ids.p, is_hub.p, hubs32);
+  plan.hub_count = static_cast<int>(nh);
+  // entries: row key, store target, length -> offsets
+  const i64 E = std::max<i64>(plan.entries, 1);
+  plan.rowkey.alloc(E);
+  plan.rl.alloc(E);
+  plan.rpc.alloc(plan.entries + 1);
   {
-    DevBuf<u64> lens(std::max<i64>(plan.regular, 1));
-    DevBuf<u64> tmp(std::max<i64>(plan.regular, 1));
-    cub_run([&](void* t, size_t& b) {
-      return cub::DeviceSelect::If(t, b, reg_len.p, tmp.p, count.p, n, NonZero(), st);
-    }, st);
-    // lengths in list order == non-zero entries of reg_len in row order
+    DevBuf<u64> elen(E);
+    fill_entries_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, segment, ents.p, ent_off.p,
+                                                       hsegs.p, hseg_off.p, plan.rowkey.p,
+                                                       plan.rl.p, elen.p);
+    PK_LAUNCH("spmm plan entries");
     PK_CUDA(cudaMemsetAsync(plan.rpc.p, 0, sizeof(u64), st));
-    if (plan.regular)
+    if (plan.entries)
       cub_run([&](void* t, size_t& b) {
-        return cub::DeviceScan::InclusiveSum(t, b, tmp.p, plan.rpc.p + 1, plan.regular, st);
+        return cub::DeviceScan::InclusiveSum(t, b, elen.p, plan.rpc.p + 1, plan.entries, st);
       }, st);
   }
-  PK_CUDA(cudaMemcpyAsync(&plan.reg_nnz, plan.rpc.p + plan.regular, sizeof(u64),
+  PK_CUDA(cudaMemcpyAsync(&plan.list_nnz, plan.rpc.p + plan.entries, sizeof(u64),
                           cudaMemcpyDeviceToHost, st));
   PK_CUDA(cudaStreamSynchronize(st));
-  plan.cv.alloc(std::max<u64>(plan.reg_nnz, 1));
-  const size_t words = plan.reg_nnz / 32 + 2;
+  plan.cv.alloc(std::max<u64>(plan.list_nnz, 1));
+  const size_t words = plan.list_nnz / 32 + 2;
   plan.endbits.alloc(words);
   PK_CUDA(cudaMemsetAsync(plan.endbits.p, 0, words * sizeof(u32), st));
-  if (plan.regular) {
-    compact_rows_kernel<<<blocks_for(plan.regular * 32), 256, 0, st>>>(
-        a.row_ptr, a.col_idx, a.values, plan.rl.p, plan.rpc.p, plan.regular, plan.cv.p,
-        plan.endbits.p);
+  if (plan.entries) {
+    compact_rows_kernel<<<blocks_for(n * 32), 256, 0, st>>>(a.row_ptr, a.col_idx, a.values, n,
+                                                             ents.p, ent_off.p, plan.rpc.p,
+                                                             plan.cv.p, plan.endbits.p);
     PK_LAUNCH("spmm plan compact");
   }
-  // hub rows longest first (few: host sort)
-  plan.hub_count = static_cast<int>(nh);
-  if (nh) {
+  if (nh && segment) {
+    // FAST plan: hub rows ascending with their segment ranges
+    plan.hub_asc = std::move(hubs32);
+    DevBuf<u32> lo(n), cnt(n);
+    seg_meta_kernel<<<blocks_for(n), 256, 0, st>>>(hsegs.p, hseg_off.p, n, lo.p, cnt.p);
+    PK_LAUNCH("spmm plan segments");
+    select(lo.p, is_hub.p, plan.hub_seg0);
+    select(cnt.p, is_hub.p, plan.hub_nseg);
+  } else if (nh) {
+    // exact plan: hub rows longest first (few: host sort)
     std::vector<u32> h(nh);
     std::vector<u64> lens(nh);
     DevBuf<u64> dlen(nh);
@@ -766,7 +860,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   // list kernel streams through the rest of the machine
   SideStream& side = side_stream();
   SpmmArgs h;
-  if (rg.hubs > 0) {
+  if (!plan.segment && rg.hubs > 0) {
     h.rp = a.row_ptr, h.ci = a.col_idx, h.val = a.values;
     h.x = x, h.ldx = ldx, h.y = y, h.ldy = ldy, h.r0 = r0, h.nrows = r1 - r0, h.nvec = nvec;
     h.hub_rows = rg.hub_ids.p ? rg.hub_ids.p : plan.hub_rows.p;
@@ -793,6 +887,11 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     ListArgs la;
     la.cv = plan.cv.p, la.rl = plan.rl.p, la.rpc = plan.rpc.p, la.endbits = plan.endbits.p;
     la.x = x, la.ldx = ldx, la.y = y, la.ldy = ldy, la.r0 = r0, la.nvec = nvec;
+    if (plan.segment && plan.segments) {
+      la.ldp = (d + 3) / 4 * 4;
+      plan.partial.ensure(plan.segments * la.ldp);
+      la.part = plan.partial.p;
+    }
     if (vec == 4)
       dispatch_list<4>(la, rg.i0, rg.i1, plan.rpc.p, st);
     else if (vec == 2)
@@ -800,7 +899,14 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     else
       dispatch_list<1>(la, rg.i0, rg.i1, plan.rpc.p, st);
   }
-  if (rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
+  if (plan.segment && rg.h1 > rg.h0) {
+    const i64 nh = rg.h1 - rg.h0;
+    combine_segments_kernel<<<blocks_for(nh * d), 256, 0, st>>>(
+        plan.hub_asc.p + rg.h0, plan.hub_seg0.p + rg.h0, plan.hub_nseg.p + rg.h0, nh, r0,
+        plan.partial.p, (d + 3) / 4 * 4, y, ldy, d);
+    PK_LAUNCH("spmm combine segments");
+  }
+  if (!plan.segment && rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
 }
 
 }  // namespace pk

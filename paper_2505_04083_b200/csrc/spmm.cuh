@@ -35,27 +35,46 @@ struct SpmmArgs {
 struct SpmmPlan {
   i64 rows = 0;
   u64 threshold = ~0ull;
+  // 0: exact plan — hub rows run on the hub kernel (bit-identical chains).
+  // > 0: FAST plan — hub rows are cut into segments of this many nonzeros
+  // that the list kernel sums as virtual rows; a fixed-order combine adds a
+  // row's segment sums (deterministic, fp32-level difference from the
+  // reference's single chain).
+  u64 segment = 0;
   int hub_count = 0;
-  DevBuf<i64> hub_rows;   // sorted by length, descending
-  i64 regular = 0;        // number of regular (non-empty, non-hub) rows
-  u64 reg_nnz = 0;
-  DevBuf<u32> rl;         // regular row ids, ascending
-  DevBuf<u64> rpc;        // offsets into cv, regular + 1
-  DevBuf<u64> cv;         // (val bits << 32) | col, per regular nonzero
-  DevBuf<u32> endbits;    // bit k: nonzero k ends its row
+  DevBuf<i64> hub_rows;   // exact plan: sorted by length, descending
+  DevBuf<u32> hub_asc;    // FAST plan: hub rows ascending ...
+  DevBuf<u32> hub_seg0;   // ... their first segment ...
+  DevBuf<u32> hub_nseg;   // ... and segment count
+  u64 segments = 0;
+  DevBuf<float> partial;  // segments x ld_partial (FAST plan workspace)
+  i64 entries = 0;        // list entries: regular rows (+ hub segments)
+  u64 list_nnz = 0;
+  DevBuf<u32> rowkey;     // row id of every entry, ascending
+  DevBuf<u32> rl;         // store target: row id, or 0x80000000 | segment
+  DevBuf<u64> rpc;        // nonzero offset of every entry (+1)
+  DevBuf<u64> cv;         // (val bits << 32) | col, per list nonzero
+  DevBuf<u32> endbits;    // bit k: nonzero k ends its entry
   i64 empty = 0;
   DevBuf<u32> empty_rows; // ascending
   struct Range {
     i64 r0 = 0, r1 = 0;
-    i64 i0 = 0, i1 = 0;   // regular list range
+    i64 i0 = 0, i1 = 0;   // list entry range
     i64 e0 = 0, e1 = 0;   // empty list range
-    int hubs = 0;
-    DevBuf<i64> hub_ids;  // subset, longest first
+    i64 h0 = 0, h1 = 0;   // FAST plan: hub_asc range
+    int hubs = 0;         // exact plan: hub rows in range ...
+    DevBuf<i64> hub_ids;  // ... longest first
   };
   std::vector<Range> ranges;
 };
 
-void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_t st);
+// Segment length of FAST plans: 2048 nonzeros, PK_SPMM_SEGMENT overrides
+// (0 = exact plans in FAST mode too).
+u64 spmm_fast_segment();
+
+// segment = 0: exact plan; > 0: FAST plan with hub rows cut into segments.
+void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_t st,
+                     u64 segment = 0);
 
 // y[0:r1-r0, 0:d] = A[r0:r1, :] . x, bit-identical to the reference's loop
 // (kernels.hpp:39-62). Launches on `st` (hub CTAs on a forked stream joined

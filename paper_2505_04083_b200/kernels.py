@@ -86,9 +86,12 @@ class DeviceCsr:
         return (self.row_ptr.cpu().numpy().view(np.uint64), self.col_idx.cpu().numpy().view(
             np.uint32), self.values.cpu().numpy())
 
-    def plan(self, hub_threshold=0):
-        if self._plan is None or hub_threshold:
-            self._plan = SpmmPlan(self, hub_threshold)
+    def plan(self, hub_threshold=0, mode=PK_MODE_PARITY):
+        """The cached exact plan, or a new plan for a given threshold / mode."""
+        if hub_threshold or mode != PK_MODE_PARITY:
+            return SpmmPlan(self, hub_threshold, mode=mode)
+        if self._plan is None:
+            self._plan = SpmmPlan(self)
         return self._plan
 
 
@@ -119,12 +122,15 @@ def _wrap_device(ptr, count, dtype, keepalive):
 
 
 class SpmmPlan:
-    """pk_spmm_plan: hub rows split off, longest first (one per matrix)."""
+    """pk_spmm_plan: hub rows split off (one per matrix). mode PARITY keeps
+    every row one exact chain (bit-identical); FAST cuts hub rows into
+    segments combined in a fixed order (fp32-level difference)."""
 
-    def __init__(self, a: DeviceCsr, hub_threshold=0, stream=None):
+    def __init__(self, a: DeviceCsr, hub_threshold=0, stream=None, mode=PK_MODE_PARITY):
         self.a = a
         h = C.c_void_p()
-        call("pk_spmm_plan_create", a.view(), hub_threshold, _stream(stream), C.byref(h))
+        call("pk_spmm_plan_create_mode", a.view(), hub_threshold, mode, _stream(stream),
+             C.byref(h))
         self.h = h
 
     def info(self):

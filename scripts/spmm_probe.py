@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--edges", type=int, default=62_000_000)
     ap.add_argument("--widths", default="50,100,128,256")
     ap.add_argument("--thresholds", default="0")
+    ap.add_argument("--fast", action="store_true", help="FAST plans (segmented hub rows)")
     args = ap.parse_args()
     t0 = time.time()
     ds = graph.synth_rmat(args.scale, args.edges, 100, 47, seed=1)
@@ -67,7 +68,8 @@ def main():
         y = torch.empty(a.rows, d, device="cuda")
         byts = 8 * a.nnz + 8 * (a.rows + 1) + 4 * a.nnz * d + 4 * a.rows * d
         for t in [int(v) for v in args.thresholds.split(",")]:
-            plan = a.plan(t)
+            plan = (kernels.SpmmPlan(a, t, mode=kernels.PK_MODE_FAST) if args.fast
+                    else a.plan(t))
             planned = timed(lambda: kernels.spmm(a, x, out=y, plan=plan))
             hubs, thr = plan.info()
             res.append(dict(d=d, bytes=byts, plan_ms=planned, hubs=hubs, hub_threshold=thr,

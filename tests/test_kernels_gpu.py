@@ -292,3 +292,36 @@ def test_adam_bitwise(cuda):
         assert_bitwise(pt.cpu().numpy(), p)
         assert_bitwise(st.m.cpu().numpy(), m)
         assert_bitwise(st.v.cpu().numpy(), v)
+
+
+# ---------------------------------------------------------------------------
+# FAST SpMM plans: hub rows cut into segments, fixed-order combine
+
+@pytest.mark.parametrize("d", [1, 7, 64, 100, 256])
+def test_spmm_fast_plan_segments_tolerance(cuda, d):
+    """Hub rows (>= threshold) are summed as 2048-nonzero segments combined
+    in a fixed order: within fp32 rounding of the reference's single chain,
+    identical run to run, and non-hub rows stay bit-identical."""
+    k = _k()
+    rng = np.random.default_rng(d)
+    n_rows, n_cols = 300, 20000
+    lens = rng.integers(0, 40, size=n_rows)
+    lens[[3, 77, 150]] = [4500, 9000, 5001]          # hub rows, several segments
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    ci = np.concatenate([np.sort(rng.choice(n_cols, size=l, replace=False)) for l in lens])
+    vals = rng.uniform(-1, 1, size=ci.size).astype(np.float32)
+    a = k.DeviceCsr.from_host(n_rows, n_cols, rp, ci.astype(np.uint32), vals)
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(n_cols, d)).astype(np.float32)).to(cuda)
+    want = restate.spmm_rows(rp, ci.astype(np.uint32), vals, x.cpu().numpy(), 0, n_rows)
+    plan = k.SpmmPlan(a, hub_threshold=4096, mode=k.PK_MODE_FAST)
+    got = k.spmm(a, x, plan=plan).cpu().numpy()
+    again = k.spmm(a, x, plan=plan).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), again.view(np.uint32))
+    hub = lens >= 4096
+    assert np.array_equal(got[~hub].view(np.uint32), want[~hub].view(np.uint32))
+    err = np.abs(got[hub].astype(np.float64) - want[hub])
+    scale = np.abs(vals).max() * np.sqrt(lens.max()) * 4
+    assert err.max() <= 1e-5 * scale, err.max()
+    # row ranges through the same plan (blocked aggregation)
+    part = k.spmm_rows(a, x, 50, 160, plan=plan).cpu().numpy()
+    assert np.array_equal(part.view(np.uint32), got[50:160].view(np.uint32))
