@@ -277,12 +277,14 @@ def run_ours(args):
     spmm_launch_share = spmm_s / (ms_step * 1e-3)
     peak, peak_kind = hbm_peak()
     achieved = spmm_bytes / spmm_s / 1e9 if spmm_s > 0 else None
+    # DRAM bytes of the same SpMM launches of one epoch, from the committed
+    # ncu launch list (scripts/ncu_round.sh -> scripts/spmm_traffic.py)
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_spmm_{args.config}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                traffic = json.load(f).get("dram_bytes_per_epoch")
         except Exception:
             traffic = None
     phases = {k: float(np.mean([m[k] for m in metrics])) * 1e3 for k in
@@ -358,7 +360,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "spmm (all launches of the epoch)",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak if achieved else None,
-                         "traffic": traffic, "alg_bytes_per_epoch": spmm_bytes,
+                         "traffic": traffic, "traffic_unit": "DRAM bytes per epoch (ncu)",
+                         "alg_bytes_per_epoch": spmm_bytes,
                          "spmm_ms_per_epoch": spmm_s * 1e3,
                          "spmm_share_of_step": spmm_launch_share},
             "phases_ms": phases,

@@ -10,7 +10,7 @@
 //
 // Why the big operands are register-staged and not TMA: the split has to
 // happen between HBM and the tensor core. Loader warps read fp32 tiles with
-// 16-B coalesced loads two k-stages ahead (across tile boundaries), write hi
+// 16-B coalesced loads two or three k-stages ahead (across tile boundaries), write hi
 // and lo into swizzled shared-memory tiles — K-major (128-B swizzle) when the
 // source is k-contiguous, MN-major (the 32-B-atom swizzle tf32 needs) when it
 // runs along M/N — and arrive on the stage's mbarrier. The small weight
@@ -420,7 +420,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       float4 a[Cfg::LoadA::kRegs];
       float4 b[kRB];
     };
-    Regs r0, r1;
+    // prefetch depth: three register sets when only A streams (NN / NT), two
+    // when A and B both do (TN)
+    constexpr int kDepth = B_PRE ? 3 : 2;
+    Regs rs[kDepth];
     auto load = [&](Regs& r, const Pos& q) {
       if (!valid(q)) return;
       const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
@@ -430,10 +433,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     Pos cur, pre;
     start(cur, blockIdx.x);
     pre = cur;
-    load(r0, pre);
-    if (valid(pre)) advance(pre);
-    load(r1, pre);
-    if (valid(pre)) advance(pre);
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      load(rs[d], pre);
+      if (valid(pre)) advance(pre);
+    }
     auto step = [&](Regs& r) {
       mbar_wait(&empty[stage], phase ^ 1u);
       unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
@@ -453,13 +457,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       if (lane == 0) mbar_arrive(&full[stage]);
       if (++stage == STAGES) stage = 0, phase ^= 1u;
       advance(cur);
-      load(r, pre);  // two stages ahead
+      load(r, pre);  // kDepth stages ahead
       if (valid(pre)) advance(pre);
     };
     while (valid(cur)) {
-      step(r0);
-      if (!valid(cur)) break;
-      step(r1);
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        if (!valid(cur)) break;
+        step(rs[d]);
+      }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
