@@ -136,6 +136,19 @@ __device__ __forceinline__ unsigned end_mask(const u32* __restrict__ bits, u64 k
   return __funnelshift_r(lo, hi, static_cast<unsigned>(k & 31));
 }
 
+// Gathers in flight per lane and unrolling of the window loop (tuned with
+// scripts/spmm_tune_sweep.sh).
+#ifndef PK_LIST_U1
+#define PK_LIST_U1 4
+#endif
+#ifndef PK_LIST_U2
+#define PK_LIST_U2 4
+#endif
+#ifndef PK_LIST_UNROLL
+#define PK_LIST_UNROLL 16
+#endif
+constexpr int kListUnroll = PK_LIST_UNROLL;
+
 // Minimum resident blocks per SM for the register allocation: three for
 // the 2-vector (D <= 256) form, where the extra warps' gathers outweigh the
 // registers (measured, scripts/spmm_minb_sweep.sh: -4 % at D=256; the 1-vector
@@ -228,7 +241,7 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
         if (!primed) gather(xa, wc, 0);
         // the next window is full too: its group 0 can be prefetched
         const bool next_full = k + 2 * LANES <= kend;
-#pragma unroll
+#pragma unroll (kListUnroll)
         for (int j = 0; j < LANES; j += 2 * U) {
           if (j + U < LANES) gather(xb, wc, j + U);
           else if (next_full) gather(xb, static_cast<u32>(wn), 0);
@@ -488,7 +501,7 @@ struct ListWorkspace {
 
 template <int VEC, int LANES, int NV>
 void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
-  constexpr int U0 = NV >= 4 ? 2 : 4;
+  constexpr int U0 = NV >= 4 ? 2 : (NV == 2 ? PK_LIST_U2 : PK_LIST_U1);
   constexpr int U = U0 < LANES ? U0 : LANES / 2;
   auto kernel = spmm_list_kernel<VEC, LANES, NV, U>;
   const int slices = ceil_div(a.nvec, NV * LANES);
