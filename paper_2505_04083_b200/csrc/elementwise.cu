@@ -155,11 +155,15 @@ ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
       count += 1;
       if (am == static_cast<int>(lab)) correct += 1;
     }
+    // one reciprocal per row instead of a divide per class: within 1 ulp of
+    // the reference's exp/denom (CE is tolerance-checked anyway: expf/logf
+    // differ from glibc in the last ulp)
+    const float rden = __frcp_rn(denom);
 #pragma unroll
     for (int t = 0; t < kCeMaxPerLane; ++t) {
       const int j = lane + 32 * t;
       if (j < classes) {
-        float d = __fdiv_rn(ev[t], denom);
+        float d = __fmul_rn(ev[t], rden);
         if (j == static_cast<int>(lab)) d = __fsub_rn(d, 1.f);
         drow[j] = scale_count ? __fmul_rn(d, s) : d;
       }

@@ -60,6 +60,18 @@ struct Vec<4> {
   using T = float4;
   static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 };
+// 32-B lane slices: one 256-bit load per lane per gathered row slice
+// (LDG.256 on sm_100a) halves the gather instructions of wide rows
+struct alignas(32) float8 {
+  float4 a, b;
+};
+template <>
+struct Vec<8> {
+  using T = float8;
+  static __device__ __forceinline__ T zero() {
+    return float8{make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  }
+};
 
 // acc = fl(acc + fl(v * x)), element-wise, never contracted to FMA.
 __device__ __forceinline__ void madd(float& a, float v, float x) {
@@ -76,9 +88,57 @@ __device__ __forceinline__ void madd(float4& a, float v, float4 x) {
   madd(a.w, v, x.w);
 }
 
+__device__ __forceinline__ void madd(float8& a, float v, const float8& x) {
+  madd(a.a, v, x.a);
+  madd(a.b, v, x.b);
+}
+
 template <typename T>
 __device__ __forceinline__ T ldg(const float* p) {
   return __ldg(reinterpret_cast<const T*>(p));
+}
+template <>
+__device__ __forceinline__ float8 ldg<float8>(const float* p) {
+  float8 r;
+  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+                 "=f"(r.b.z), "=f"(r.b.w)
+               : "l"(p));
+  return r;
+}
+
+// Gather with an L2 eviction hint from the plan's hot-column bit (bit 31 of
+// the packed column): rows of high-degree columns are kept (evict_last),
+// single-use rows of cold columns are streamed (evict_first, no L1
+// allocation), so cold gathers do not push hot rows out of L2. Only the
+// 256-bit load carries the hint on sm_100a; narrower slices load plainly.
+#ifndef PK_LIST_HINTS
+#define PK_LIST_HINTS 1
+#endif
+template <typename T>
+__device__ __forceinline__ T ldg_hint(const float* p, bool hot) {
+  (void)hot;
+  return ldg<T>(p);
+}
+template <>
+__device__ __forceinline__ float8 ldg_hint<float8>(const float* p, bool hot) {
+#if PK_LIST_HINTS
+  float8 r;
+  if (hot)
+    asm volatile("ld.global.nc.L1::evict_last.L2::evict_last.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+                   "=f"(r.b.z), "=f"(r.b.w)
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y),
+                   "=f"(r.b.z), "=f"(r.b.w)
+                 : "l"(p));
+  return r;
+#else
+  (void)hot;
+  return ldg<float8>(p);
+#endif
 }
 
 constexpr int kThreads = 256;
@@ -148,6 +208,9 @@ __device__ __forceinline__ unsigned end_mask(const u32* __restrict__ bits, u64 k
 #define PK_LIST_UNROLL 16
 #endif
 constexpr int kListUnroll = PK_LIST_UNROLL;
+#ifndef PK_LIST_HALF32
+#define PK_LIST_HALF32 0
+#endif
 
 // Minimum resident blocks per SM for the register allocation: three for
 // the 2-vector (D <= 256) form, where the extra warps' gathers outweigh the
@@ -216,10 +279,11 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const u32 c = __shfl_sync(gmask, wc, j + u, LANES);
-        const float* xr = xlane + static_cast<i64>(c) * a.ldx;
+        const float* xr = xlane + static_cast<i64>(c & 0x7fffffffu) * a.ldx;
+        const bool hot = (c >> 31) != 0;
 #pragma unroll
         for (int q = 0; q < NV; ++q)
-          xv[u][q] = valid[q] ? ldg<V>(xr + q * LANES * VEC) : Vec<VEC>::zero();
+          xv[u][q] = valid[q] ? ldg_hint<V>(xr + q * LANES * VEC, hot) : Vec<VEC>::zero();
       }
     };
     auto consume = [&](const V (&xv)[U][NV], u32 wv, unsigned em, int j) {
@@ -266,10 +330,11 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
         for (int j = 0; j < cnt; ++j) {
           const u32 c = __shfl_sync(gmask, wc, j, LANES);
           const float v = __uint_as_float(__shfl_sync(gmask, wv, j, LANES));
-          const float* xr = xlane + static_cast<i64>(c) * a.ldx;
+          const float* xr = xlane + static_cast<i64>(c & 0x7fffffffu) * a.ldx;
+          const bool hot = (c >> 31) != 0;
 #pragma unroll
           for (int q = 0; q < NV; ++q)
-            if (valid[q]) madd(acc[q], v, ldg<V>(xr + q * LANES * VEC));
+            if (valid[q]) madd(acc[q], v, ldg_hint<V>(xr + q * LANES * VEC, hot));
           if ((em >> j) & 1u) row_done();
         }
         primed = false;
@@ -555,6 +620,8 @@ void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream
     launch_list<VEC, 8, 1>(a, i0, i1, rpc, st);
   else if (nv <= 16)
     launch_list<VEC, 16, 1>(a, i0, i1, rpc, st);
+  else if (nv <= 32 && PK_LIST_HALF32)
+    launch_list<VEC, 16, 2>(a, i0, i1, rpc, st);  // two rows per warp instruction
   else if (nv <= 32)
     launch_list<VEC, 32, 1>(a, i0, i1, rpc, st);
   else if (nv <= 64)
@@ -563,10 +630,15 @@ void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream
     launch_list<VEC, 32, 4>(a, i0, i1, rpc, st);  // wider rows split across blockIdx.y
 }
 
-int pick_vec(const float* x, i64 ldx, const float* y, i64 ldy, i64 d) {
+int pick_vec(const float* x, i64 ldx, const float* y, i64 ldy, i64 d, bool allow8) {
   auto aligned = [](const void* p, int bytes) {
     return (reinterpret_cast<uintptr_t>(p) % bytes) == 0;
   };
+  // 32-B slices only when they still fill a 32-lane group (narrower rows
+  // would split warps into diverging sub-groups: measured slower at D=128)
+  if (allow8 && d % 8 == 0 && d >= 256 && ldx % 8 == 0 && ldy % 8 == 0 && aligned(x, 32) &&
+      aligned(y, 32))
+    return 8;
   if (d % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned(x, 16) && aligned(y, 16))
     return 4;
   if (d % 2 == 0 && ldx % 2 == 0 && ldy % 2 == 0 && aligned(x, 8) && aligned(y, 8))
@@ -592,6 +664,12 @@ __global__ void classify_rows_kernel(const u64* __restrict__ rp, i64 rows, u64 t
     is_empty[i] = empty;
     is_hub[i] = hub;
   }
+}
+
+__global__ void col_degree_kernel(const u32* __restrict__ ci, u64 nnz, u32* __restrict__ deg) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < nnz;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    atomicAdd(deg + ci[i], 1u);
 }
 
 __global__ void iota_rows_kernel(u32* p, i64 n) {
@@ -631,6 +709,7 @@ __global__ void compact_rows_kernel(const u64* __restrict__ rp, const u32* __res
                                     const float* __restrict__ val, i64 rows,
                                     const u64* __restrict__ ents,
                                     const u64* __restrict__ ent_off, const u64* __restrict__ rpc,
+                                    const u32* __restrict__ col_deg, u32 hot_deg,
                                     u64* __restrict__ cv, u32* __restrict__ endbits) {
   const int lane = threadIdx.x % 32;
   for (i64 i = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; i < rows;
@@ -638,8 +717,11 @@ __global__ void compact_rows_kernel(const u64* __restrict__ rp, const u32* __res
     const u64 ne = ents[i];
     if (ne == 0) continue;
     const u64 s = rp[i], len = rp[i + 1] - s, e0 = ent_off[i], dst = rpc[e0];
-    for (u64 j = lane; j < len; j += 32)
-      cv[dst + j] = (static_cast<u64>(__float_as_uint(val[s + j])) << 32) | ci[s + j];
+    for (u64 j = lane; j < len; j += 32) {
+      const u32 c = ci[s + j];
+      const u32 hot = col_deg[c] >= hot_deg ? 0x80000000u : 0u;
+      cv[dst + j] = (static_cast<u64>(__float_as_uint(val[s + j])) << 32) | c | hot;
+    }
     for (u64 e = lane; e < ne; e += 32) {
       const u64 last = rpc[e0 + e + 1] - 1;
       atomicOr(endbits + (last >> 5), 1u << (last & 31));
@@ -827,9 +909,25 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
   plan.endbits.alloc(words);
   PK_CUDA(cudaMemsetAsync(plan.endbits.p, 0, words * sizeof(u32), st));
   if (plan.entries) {
+    // hot columns: degree >= PK_HOT_FACTOR (default 2) x the mean
+    check(a.cols < (i64{1} << 31), "spmm plan: more than 2^31 columns");
+    DevBuf<u32> deg(std::max<i64>(a.cols, 1));
+    PK_CUDA(cudaMemsetAsync(deg.p, 0, deg.n * sizeof(u32), st));
+    if (a.nnz) {
+      col_degree_kernel<<<blocks_for(static_cast<i64>(a.nnz)), 256, 0, st>>>(a.col_idx, a.nnz,
+                                                                             deg.p);
+      PK_LAUNCH("spmm plan column degrees");
+    }
+    static const double hot_factor = [] {
+      const char* e = std::getenv("PK_HOT_FACTOR");
+      return e ? std::atof(e) : 2.0;
+    }();
+    const double mean = static_cast<double>(a.nnz) / std::max<i64>(a.cols, 1);
+    const u32 hot_deg = static_cast<u32>(std::max(1.0, std::ceil(hot_factor * mean)));
     compact_rows_kernel<<<blocks_for(n * 32), 256, 0, st>>>(a.row_ptr, a.col_idx, a.values, n,
                                                              ents.p, ent_off.p, plan.rpc.p,
-                                                             plan.cv.p, plan.endbits.p);
+                                                             deg.p, hot_deg, plan.cv.p,
+                                                             plan.endbits.p);
     PK_LAUNCH("spmm plan compact");
   }
   if (nh && segment) {
@@ -867,7 +965,9 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
               float* y, i64 ldy, cudaStream_t st) {
   if (r1 <= r0 || d == 0) return;
   SpmmPlan::Range& rg = plan_range(plan, r0, r1, st);
-  const int vec = pick_vec(x, ldx, y, ldy, d);
+  // 32-B slices for the list kernel; the exact plan's hub kernel stages
+  // 16-B cp.async pieces, so a plan with hub CTAs stays at 16 B
+  const int vec = pick_vec(x, ldx, y, ldy, d, plan.segment || rg.hubs == 0);
   const int nvec = static_cast<int>(d / vec);
   // hub CTAs first, on a forked stream, so they hold their SMs while the
   // list kernel streams through the rest of the machine
@@ -901,11 +1001,13 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     la.cv = plan.cv.p, la.rl = plan.rl.p, la.rpc = plan.rpc.p, la.endbits = plan.endbits.p;
     la.x = x, la.ldx = ldx, la.y = y, la.ldy = ldy, la.r0 = r0, la.nvec = nvec;
     if (plan.segment && plan.segments) {
-      la.ldp = (d + 3) / 4 * 4;
+      la.ldp = (d + 7) / 8 * 8;  // 32-B aligned rows for the widest slices
       plan.partial.ensure(plan.segments * la.ldp);
       la.part = plan.partial.p;
     }
-    if (vec == 4)
+    if (vec == 8)
+      dispatch_list<8>(la, rg.i0, rg.i1, plan.rpc.p, st);
+    else if (vec == 4)
       dispatch_list<4>(la, rg.i0, rg.i1, plan.rpc.p, st);
     else if (vec == 2)
       dispatch_list<2>(la, rg.i0, rg.i1, plan.rpc.p, st);
@@ -916,7 +1018,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     const i64 nh = rg.h1 - rg.h0;
     combine_segments_kernel<<<blocks_for(nh * d), 256, 0, st>>>(
         plan.hub_asc.p + rg.h0, plan.hub_seg0.p + rg.h0, plan.hub_nseg.p + rg.h0, nh, r0,
-        plan.partial.p, (d + 3) / 4 * 4, y, ldy, d);
+        plan.partial.p, (d + 7) / 8 * 8, y, ldy, d);
     PK_LAUNCH("spmm combine segments");
   }
   if (!plan.segment && rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
