@@ -112,8 +112,11 @@ __device__ __forceinline__ float8 ldg<float8>(const float* p) {
 // single-use rows of cold columns are streamed (evict_first, no L1
 // allocation), so cold gathers do not push hot rows out of L2. Only the
 // 256-bit load carries the hint on sm_100a; narrower slices load plainly.
+// Measured (scripts/spmm_hint_sweep.sh, products D=256): 10.57 ms with hints
+// at the best hot-factor vs 10.23 ms without — the hardware's own policy
+// wins, so the hints are compiled out by default.
 #ifndef PK_LIST_HINTS
-#define PK_LIST_HINTS 1
+#define PK_LIST_HINTS 0
 #endif
 template <typename T>
 __device__ __forceinline__ T ldg_hint(const float* p, bool hot) {
