@@ -1,6 +1,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -61,6 +62,11 @@ void copy_block_launch(const float* src, i64 ld_src, i64 rows, i64 cols, float* 
 struct CommSet {
   ncclComm_t world = nullptr;
   std::array<ncclComm_t, 3> axes{nullptr, nullptr, nullptr};
+  // symmetric scratch per axis (grows; re-registered when a larger one is
+  // needed) — lives as long as the communicators
+  std::array<std::unique_ptr<LsaGroup>, 3> lsa;
+  std::array<size_t, 3> lsa_elems{0, 0, 0};
+  std::array<bool, 3> lsa_failed{false, false, false};
   ~CommSet() {
     for (auto& c : axes)
       if (c) ncclCommDestroy(c);
@@ -130,6 +136,41 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
   }
   world_ = set_->world;
   axes_ = set_->axes;
+}
+
+LsaGroup* Comms::lsa(int axis, size_t elems) {
+  const int g = grid_.extent(axis);
+  if (g == 1 || !set_) return nullptr;
+  static const bool on = [] {
+    const char* e = std::getenv("PK_LSA");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || set_->lsa_failed[axis]) return nullptr;
+  if (set_->lsa[axis] && set_->lsa_elems[axis] >= elems) return set_->lsa[axis].get();
+  // (re)create: collective over the axis communicator, same order on all
+  // members (engine load), sizes identical across the group
+  auto grp = std::make_unique<LsaGroup>();
+  if (!grp->init(axes_[axis], g, coords_.along(axis), elems)) {
+    set_->lsa_failed[axis] = true;
+    std::fprintf(stderr, "[pk] axis %d: NVLink peer-memory reductions unavailable, using NCCL\n",
+                 axis);
+    return nullptr;
+  }
+  set_->lsa[axis] = std::move(grp);
+  set_->lsa_elems[axis] = elems;
+  return set_->lsa[axis].get();
+}
+
+LsaGroup* Comms::lsa(int axis) const {
+  if (!set_ || grid_.extent(axis) == 1) return nullptr;
+  return set_->lsa[axis] && set_->lsa[axis]->ready() ? set_->lsa[axis].get() : nullptr;
+}
+
+void Comms::count(int op, int axis, i64 logical_bytes) {
+  const int g = grid_.extent(axis);
+  counters.calls[axis][op]++;
+  counters.ring_numer[axis][op] += (op == kAllReduce ? 2 : 1) * static_cast<u64>(g - 1) *
+                                   static_cast<u64>(logical_bytes);
 }
 
 void Comms::all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaStream_t st) {

@@ -20,6 +20,7 @@
 #include <memory>
 
 #include "layout.h"
+#include "lsa.cuh"
 #include "pk_common.cuh"
 
 namespace pk {
@@ -76,6 +77,16 @@ class Comms {
   // chunked calls over a partition of [0, rows) add up to the full one.
   void reduce_scatter_rows_range(float* buf, float* out, i64 rows, i64 ld, int axis,
                                  i64 logical_cols, i64 r0, i64 r1, cudaStream_t st);
+
+  // Deterministic ordered reductions over NVLink peer memory (lsa.cu) for
+  // one axis: collective setup with the largest partial this axis reduces.
+  // Returns the group, or nullptr when the axis is a singleton or peer
+  // load/store access is unavailable (callers then use NCCL).
+  LsaGroup* lsa(int axis, size_t scratch_elems);
+  LsaGroup* lsa(int axis) const;
+  // ring-model byte accounting of an all-reduce / reduce-scatter done
+  // outside NCCL (cluster.hpp:298-333)
+  void count(int op, int axis, i64 logical_bytes);
 
   CommCounters counters;
 

@@ -416,38 +416,55 @@ void Engine::forward_layer(int l, bool fault) {
   const int blocks = forward_blocks(sh.a.rows, lay);
   const std::vector<u64>& bnnz = sh.blocks_nnz(blocks, st_);
   int b = 0;
+  // partials go to the axis' symmetric scratch when the ordered peer-memory
+  // reduction is available (fault_epoch skips the reduction altogether: the
+  // reference's negative control, engine.hpp:186)
+  LsaGroup* lsa_h = fault ? nullptr : comms_.lsa(lay.inner);
+  float* hpart = lsa_h ? lsa_h->scratch() : h.p();
   pipelined(
       sh.a.rows, blocks,
       [&](i64 r0, i64 r1) {
         clock_.begin(0, st_);
-        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, h.p() + r0 * h.ld, h.ld, st_);
+        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, hpart + r0 * h.ld, h.ld, st_);
         spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
         spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
         ++b;
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        if (!fault)  // fault_epoch: the reference's negative control (engine.hpp:186)
+        if (fault) return;
+        if (lsa_h) {
+          lsa_h->reduce(r0, r1, s.f_cols, h.ld, h.p(), r0, h.ld, cs_);
+          comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.f_cols * 4);
+        } else {
           comms_.all_reduce(h.p() + r0 * h.ld, (r1 - r0) * h.ld, lay.inner,
                             (r1 - r0) * s.f_cols * 4, cs_);
+        }
       });
   on_comm([&](cudaStream_t cs) {
     comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
                            cs);
   });
   // Q = H . W_full, then its all-reduce along col_shard, row-chunked
+  LsaGroup* lsa_q = comms_.lsa(lay.col);
+  float* qpart = lsa_q ? lsa_q->scratch() : q_[l].p();
   pipelined(
       s.h_rows, comm_chunks(s.h_rows, lay.col),
       [&](i64 r0, i64 r1) {
         clock_.begin(1, st_);
         gemm_launch(false, false, r1 - r0, s.w_cols, s.h_cols, h.p() + r0 * h.ld, h.ld,
-                    wfull_[l].p(), wfull_[l].ld, q_[l].p() + r0 * q_[l].ld, q_[l].ld, cfg_.mode,
+                    wfull_[l].p(), wfull_[l].ld, qpart + r0 * q_[l].ld, q_[l].ld, cfg_.mode,
                     st_);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        comms_.all_reduce(q_[l].p() + r0 * q_[l].ld, (r1 - r0) * q_[l].ld, lay.col,
-                          (r1 - r0) * s.q_cols * 4, cs_);
+        if (lsa_q) {
+          lsa_q->reduce(r0, r1, s.q_cols, q_[l].ld, q_[l].p(), r0, q_[l].ld, cs_);
+          comms_.count(kAllReduce, lay.col, (r1 - r0) * s.q_cols * 4);
+        } else {
+          comms_.all_reduce(q_[l].p() + r0 * q_[l].ld, (r1 - r0) * q_[l].ld, lay.col,
+                            (r1 - r0) * s.q_cols * 4, cs_);
+        }
       });
   gemm_flops_ += 2 * static_cast<u64>(s.h_rows) * s.w_cols * s.h_cols;
   if (l + 1 < L_) {
@@ -540,41 +557,83 @@ void Engine::backward_layer(int l) {
   });
   // dH = dQ . W_full^T, then its all-reduce along inner, row-chunked
   const i64 lddh = pad4(s.h_cols);
+  LsaGroup* lsa_dh = comms_.lsa(lay.inner);
+  float* dhpart = lsa_dh ? lsa_dh->scratch() : dh_.p();
   pipelined(
       s.q_rows, comm_chunks(s.q_rows, lay.inner),
       [&](i64 r0, i64 r1) {
         clock_.begin(2, st_);
         gemm_launch(false, true, r1 - r0, s.h_cols, s.q_cols, dq + r0 * lddq, lddq,
-                    wfull_[l].p(), wfull_[l].ld, dh_.p() + r0 * lddh, lddh, cfg_.mode, st_);
+                    wfull_[l].p(), wfull_[l].ld, dhpart + r0 * lddh, lddh, cfg_.mode, st_);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        comms_.all_reduce(dh_.p() + r0 * lddh, (r1 - r0) * lddh, lay.inner,
-                          (r1 - r0) * s.h_cols * 4, cs_);
+        if (lsa_dh) {
+          lsa_dh->reduce(r0, r1, s.h_cols, lddh, dh_.p(), r0, lddh, cs_);
+          comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
+        } else {
+          comms_.all_reduce(dh_.p() + r0 * lddh, (r1 - r0) * lddh, lay.inner,
+                            (r1 - r0) * s.h_cols * 4, cs_);
+        }
       });
   gemm_flops_ += 2 * static_cast<u64>(s.q_rows) * s.h_cols * s.q_cols;
   // dF = A^T . dH, then reduce-scatter (layer 0) or all-reduce along
   // row_shard, row-chunked
   const i64 lddf = pad4(s.f_cols);
+  LsaGroup* lsa_df = comms_.lsa(lay.row);
+  float* dfpart = lsa_df ? lsa_df->scratch() : df_.p();
+  const int gr = grid_.extent(lay.row), pr = c_.along(lay.row);
+  const i64 own0 = chunk_start(s.a_cols, gr, pr), own1 = chunk_start(s.a_cols, gr, pr + 1);
   pipelined(
       sh.at.rows, comm_chunks(sh.at.rows, lay.row),
       [&](i64 r0, i64 r1) {
         clock_.begin(5, st_);
-        spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, s.f_cols, df_.p() + r0 * lddf,
+        spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, s.f_cols, dfpart + r0 * lddf,
                  lddf, st_);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        if (l == 0)
+        if (lsa_df) {
+          if (l == 0) {  // reduce-scatter: this member sums only its own rows
+            const i64 a = std::max(r0, own0), b = std::min(r1, own1);
+            lsa_df->reduce(a, std::max(a, b), s.f_cols, lddf, df0_.p(), a - own0, df0_.ld, cs_);
+            comms_.count(kReduceScatter, lay.row, (r1 - r0) * s.f_cols * 4);
+          } else {
+            lsa_df->reduce(r0, r1, s.f_cols, lddf, df_.p(), r0, lddf, cs_);
+            comms_.count(kAllReduce, lay.row, (r1 - r0) * s.f_cols * 4);
+          }
+        } else if (l == 0) {
           comms_.reduce_scatter_rows_range(df_.p(), df0_.p(), s.a_cols, lddf, lay.row, s.f_cols,
                                            r0, r1, cs_);
-        else
+        } else {
           comms_.all_reduce(df_.p() + r0 * lddf, (r1 - r0) * lddf, lay.row,
                             (r1 - r0) * s.f_cols * 4, cs_);
+        }
       });
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.f_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.f_cols);
   if (l > 0) std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
+}
+
+// Symmetric scratch for the ordered peer-memory reductions: per axis the
+// largest partial it reduces (H and dH along inner, Q along col_shard, dF
+// along row_shard). Collective; every member of a group computes the same
+// sizes (the reduced dimensions do not depend on the member's coordinate
+// along that axis).
+void Engine::setup_lsa() {
+  size_t need[3] = {0, 0, 0};
+  for (int l = 0; l < L_; ++l) {
+    const Layout& lay = lays_[l];
+    const Shapes& s = shapes_[l];
+    auto grow = [&](int axis, size_t e) { need[axis] = std::max(need[axis], e); };
+    grow(lay.inner, static_cast<size_t>(s.a_rows) * h_[l].ld);
+    grow(lay.inner, static_cast<size_t>(s.q_rows) * pad4(s.h_cols));
+    grow(lay.col, static_cast<size_t>(s.h_rows) * q_[l].ld);
+    grow(lay.row, static_cast<size_t>(s.a_cols) * pad4(s.f_cols));
+  }
+  for (int a = 0; a < 3; ++a)
+    if (need[a] && grid_.extent(a) > 1) comms_.lsa(a, need[a]);
+  lsa_ready_ = true;
 }
 
 void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
@@ -583,6 +642,7 @@ void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
   PK_CUDA(cudaSetDevice(cfg_.device));
   const bool fault = epoch == cfg_.fault_epoch;
   sync_used_ = 0;
+  if (!lsa_ready_) setup_lsa();
   for (int l = 0; l < L_; ++l) forward_layer(l, fault);
   loss(epoch, loss_out, acc_out);
   for (int l = L_ - 1; l >= 0; --l) backward_layer(l);

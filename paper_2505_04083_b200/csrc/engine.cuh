@@ -94,6 +94,8 @@ class Engine {
   void pipelined(i64 rows, int chunks, P&& produce, R&& reduce);
   int comm_chunks(i64 rows, int axis) const;
   void on_comm(const std::function<void(cudaStream_t)>& f);
+  void setup_lsa();
+  bool lsa_ready_ = false;
 
   pk_engine_config cfg_;
   Grid grid_;

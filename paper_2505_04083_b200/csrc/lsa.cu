@@ -1,0 +1,172 @@
+// Deterministic all-reduce / reduce-scatter over NVLink peer memory.
+//
+// The reference combines partial sums in ascending coordinate order:
+// acc = s[0]; acc += s[1]; ... (cluster.hpp:345-373). NCCL's ring / tree /
+// NVLS orders differ for groups of three or more, so the engine's large
+// reductions run here instead: every member of an axis group writes its
+// partial into a symmetric buffer (ncclMemAlloc + ncclCommWindowRegister,
+// NCCL_WIN_COLL_SYMMETRIC), and one kernel per member reads all members'
+// partials straight out of their HBM through NVLink (load/store-accessible
+// peer mappings) and sums them in coordinate order. The result is the
+// reference's, bit for bit, for any group size — and no NCCL kernel shares
+// the SMs with the overlapped SpMM / GEMM.
+//
+// Synchronisation: per-CTA flag barriers in a small symmetric flag buffer.
+// CTA b of every member arrives by storing the call's epoch into slot
+// [me][b] of every peer's flags (release, system scope) and waits until all
+// peers' slots [p][b] in its own flags reach the epoch (acquire). One
+// barrier before the reads (all partials complete), one after (nobody reads
+// a buffer its owner is about to overwrite). Waits are bounded: a protocol
+// failure sets an error flag that the host checks, never a hung GPU.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <nccl_device.h>
+
+#include <cstring>
+
+#include "lsa.cuh"
+
+namespace pk {
+
+namespace {
+
+__device__ unsigned g_lsa_timeout = 0;
+
+__device__ __forceinline__ void flag_store(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned flag_load(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// flags of member m: [g][kLsaBlocks] u32; slot [src][b] is written by src
+__device__ void barrier(const LsaPeers& P, int b, unsigned epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < P.g; ++p)
+      if (p != P.me) flag_store(P.flags[p] + P.me * kLsaBlocks + b, epoch);
+    for (int p = 0; p < P.g; ++p) {
+      if (p == P.me) continue;
+      const unsigned* f = P.flags[P.me] + p * kLsaBlocks + b;
+      unsigned spins = 0;
+      while (static_cast<int>(flag_load(f) - epoch) < 0) {
+        if (++spins > (1u << 22)) {  // ~seconds with the backoff below
+          atomicExch(&g_lsa_timeout, 1u);
+          break;
+        }
+        __nanosleep(spins < 64 ? 32 : 256);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// out[r, c] = sum_j part_j[r, c] in ascending j, rows [r0, r1) of the
+// partial buffers (ld_p) -> out rows starting at out_r0 (ld_o)
+template <int VEC>
+__global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64 r1, i64 cols,
+                                                         i64 ld_p, float* __restrict__ out,
+                                                         i64 out_r0, i64 ld_o, unsigned epoch) {
+  barrier(P, blockIdx.x, epoch);
+  const i64 cv = cols / VEC;
+  const i64 total = (r1 - r0) * cv;
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 r = r0 + i / cv, c = (i % cv) * VEC;
+    const i64 off = r * ld_p + c;
+    if constexpr (VEC == 4) {
+      float4 acc = __ldcg(reinterpret_cast<const float4*>(P.data[0] + off));
+      for (int j = 1; j < P.g; ++j) {
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(P.data[j] + off));
+        acc.x = __fadd_rn(acc.x, x.x), acc.y = __fadd_rn(acc.y, x.y);
+        acc.z = __fadd_rn(acc.z, x.z), acc.w = __fadd_rn(acc.w, x.w);
+      }
+      *reinterpret_cast<float4*>(out + (r - r0 + out_r0) * ld_o + c) = acc;
+    } else {
+      float acc = __ldcg(P.data[0] + off);
+      for (int j = 1; j < P.g; ++j) acc = __fadd_rn(acc, __ldcg(P.data[j] + off));
+      out[(r - r0 + out_r0) * ld_o + c] = acc;
+    }
+  }
+  barrier(P, blockIdx.x, epoch + 1);
+}
+
+__global__ void lsa_peer_ptrs_kernel(ncclWindow_t win, int g, void** out) {
+  const int j = threadIdx.x;
+  if (j < g) out[j] = ncclGetLsaPointer(win, 0, j);
+}
+
+void peer_pointers(ncclWindow_t win, int g, void** host_out) {
+  void** d = nullptr;
+  PK_CUDA(cudaMalloc(&d, sizeof(void*) * g));
+  lsa_peer_ptrs_kernel<<<1, 32>>>(win, g, d);
+  PK_LAUNCH("lsa peer pointers");
+  PK_CUDA(cudaMemcpy(host_out, d, sizeof(void*) * g, cudaMemcpyDeviceToHost));
+  PK_CUDA(cudaFree(d));
+}
+
+}  // namespace
+
+LsaGroup::~LsaGroup() {
+  // windows and ncclMemAlloc buffers are released with the communicator
+  // (process lifetime, see Comms); nothing to do per engine
+}
+
+bool LsaGroup::init(ncclComm_t comm, int g, int me, size_t scratch_elems) {
+  g_ = g, me_ = me;
+  if (g < 2 || g > kLsaMaxMembers) return false;
+  ncclTeam_t lsa = ncclTeamLsa(comm);
+  if (lsa.nRanks != g || lsa.rank != me) return false;  // not one node-local group
+  scratch_bytes_ = ((scratch_elems * sizeof(float)) + 4095) / 4096 * 4096;
+  const size_t flag_bytes = ((g * kLsaBlocks * sizeof(unsigned)) + 4095) / 4096 * 4096;
+  if (ncclMemAlloc(&scratch_, scratch_bytes_) != ncclSuccess) return false;
+  if (ncclMemAlloc(reinterpret_cast<void**>(&flags_), flag_bytes) != ncclSuccess) return false;
+  PK_CUDA(cudaMemset(flags_, 0, flag_bytes));
+  PK_CUDA(cudaDeviceSynchronize());
+  if (ncclCommWindowRegister(comm, scratch_, scratch_bytes_, &data_win_,
+                             NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess)
+    return false;
+  if (ncclCommWindowRegister(comm, flags_, flag_bytes, &flag_win_, NCCL_WIN_COLL_SYMMETRIC) !=
+      ncclSuccess)
+    return false;
+  void* dp[kLsaMaxMembers] = {};
+  void* fp[kLsaMaxMembers] = {};
+  peer_pointers(data_win_, g, dp);
+  peer_pointers(flag_win_, g, fp);
+  peers_.g = g, peers_.me = me;
+  for (int j = 0; j < g; ++j) {
+    peers_.data[j] = static_cast<const float*>(dp[j]);
+    peers_.flags[j] = static_cast<unsigned*>(fp[j]);
+  }
+  ready_ = true;
+  return true;
+}
+
+void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
+                      cudaStream_t st) {
+  check(ready_, "lsa reduce: group not initialised");
+  check((r1 > 0 ? r1 : 0) * ld_p * sizeof(float) <= scratch_bytes_,
+        "lsa reduce: partial exceeds the symmetric scratch");
+  const unsigned epoch = epoch_;
+  epoch_ += 2;
+  const bool v4 = cols % 4 == 0 && ld_p % 4 == 0 && ld_o % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (v4)
+    lsa_reduce_kernel<4><<<kLsaBlocks, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
+                                                     epoch);
+  else
+    lsa_reduce_kernel<1><<<kLsaBlocks, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
+                                                     epoch);
+  PK_LAUNCH("lsa ordered reduce");
+}
+
+bool lsa_timed_out() {
+  unsigned v = 0;
+  PK_CUDA(cudaMemcpyFromSymbol(&v, g_lsa_timeout, sizeof(v)));
+  return v != 0;
+}
+
+}  // namespace pk

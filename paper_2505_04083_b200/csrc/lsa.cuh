@@ -1,0 +1,51 @@
+// Deterministic ordered reductions over NVLink peer memory (lsa.cu).
+#pragma once
+
+#include <nccl.h>
+
+#include "pk_common.cuh"
+
+namespace pk {
+
+constexpr int kLsaMaxMembers = 8;
+constexpr int kLsaBlocks = 148 * 2;  // CTAs of every reduce (same on all members)
+
+struct LsaPeers {
+  const float* data[kLsaMaxMembers];  // each member's symmetric scratch
+  unsigned* flags[kLsaMaxMembers];    // each member's barrier flags
+  int g = 0, me = 0;
+};
+
+// One axis group's symmetric scratch + barrier flags.
+class LsaGroup {
+ public:
+  ~LsaGroup();
+  // Collective over `comm` (every member calls it in the same order).
+  // Returns false when the group cannot use load/store peer access (then
+  // the caller keeps NCCL for this axis).
+  bool init(ncclComm_t comm, int g, int me, size_t scratch_elems);
+  bool ready() const { return ready_; }
+  // This member's partial goes here (row-major, the caller's ld).
+  float* scratch() const { return static_cast<float*>(scratch_); }
+  size_t scratch_elems() const { return scratch_bytes_ / sizeof(float); }
+  // out rows [out_r0, out_r0 + r1 - r0) = sum over members, in coordinate
+  // order, of their scratch rows [r0, r1). Collective (same call sequence on
+  // every member); runs on `st`.
+  void reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
+              cudaStream_t st);
+
+ private:
+  int g_ = 0, me_ = 0;
+  bool ready_ = false;
+  void* scratch_ = nullptr;
+  size_t scratch_bytes_ = 0;
+  unsigned* flags_ = nullptr;
+  ncclWindow_t data_win_ = nullptr, flag_win_ = nullptr;
+  LsaPeers peers_;
+  unsigned epoch_ = 1;
+};
+
+// true when a barrier wait gave up (a protocol error; results are invalid)
+bool lsa_timed_out();
+
+}  // namespace pk
