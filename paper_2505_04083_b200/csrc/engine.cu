@@ -545,13 +545,22 @@ void Engine::backward_layer(int l) {
     dq = dq_.p();
   }
   // dW = (dQ^T H)^T computed as H^T dQ: same products, same k order
-  gemm_launch(true, false, s.h_cols, s.q_cols, s.h_rows, h_[l].p(), h_[l].ld, dq, lddq,
-              dwp_[l].p(), dwp_[l].ld, cfg_.mode, st_);
+  LsaGroup* lsa_dw = comms_.lsa(lay.row);
+  float* dwpart = lsa_dw ? lsa_dw->scratch() : dwp_[l].p();
+  gemm_launch(true, false, s.h_cols, s.q_cols, s.h_rows, h_[l].p(), h_[l].ld, dq, lddq, dwpart,
+              dwp_[l].ld, cfg_.mode, st_);
   gemm_flops_ += 2 * static_cast<u64>(s.h_cols) * s.q_cols * s.h_rows;
   clock_.end(st_);
   on_comm([&](cudaStream_t cs) {
-    comms_.reduce_scatter_rows(dwp_[l].p(), dw_[l].p(), s.f_cols, dwp_[l].ld, lay.row, s.w_cols,
-                               cs);
+    if (lsa_dw) {  // reduce-scatter (engine.hpp:237): this member sums its own rows
+      const int g = grid_.extent(lay.row), pos = c_.along(lay.row);
+      const i64 o0 = chunk_start(s.f_cols, g, pos), o1 = chunk_start(s.f_cols, g, pos + 1);
+      lsa_dw->reduce(o0, o1, s.w_cols, dwp_[l].ld, dw_[l].p(), 0, dw_[l].ld, cs);
+      comms_.count(kReduceScatter, lay.row, s.f_cols * s.w_cols * 4);
+    } else {
+      comms_.reduce_scatter_rows(dwp_[l].p(), dw_[l].p(), s.f_cols, dwp_[l].ld, lay.row,
+                                 s.w_cols, cs);
+    }
     comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
                            cs);
   });
@@ -630,6 +639,7 @@ void Engine::setup_lsa() {
     grow(lay.inner, static_cast<size_t>(s.q_rows) * pad4(s.h_cols));
     grow(lay.col, static_cast<size_t>(s.h_rows) * q_[l].ld);
     grow(lay.row, static_cast<size_t>(s.a_cols) * pad4(s.f_cols));
+    grow(lay.row, static_cast<size_t>(s.f_cols) * dwp_[l].ld);
   }
   for (int a = 0; a < 3; ++a)
     if (need[a] && grid_.extent(a) > 1) comms_.lsa(a, need[a]);

@@ -23,11 +23,12 @@ def _port():
         return s.getsockname()[1]
 
 
-def _run(nproc, *args):
+def _run(nproc, *args, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            WORKER, *args]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, **(env or {})})
     lines = [l for l in p.stdout.splitlines() if l.startswith("MPRESULT ")]
     assert lines, p.stdout[-3000:] + p.stderr[-3000:]
     rep = json.loads(lines[-1][len("MPRESULT "):])
@@ -58,10 +59,19 @@ def test_two_gpu_fast_mode_and_blocks(cuda):
     _run(2, "--grid", "2,1,1", "--mode", "fast", "--block-count", "3")
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_gpu_nccl_reductions(cuda):
+    """The NCCL path the engine falls back to without peer-memory access."""
+    _run(2, "--grid", "1,2,1", env={"PK_LSA": "0"})
+
+
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
 @pytest.mark.parametrize("grid", _grids(4))
 def test_four_gpu_grids_match_reference(cuda, grid):
-    _run(4, "--grid", grid)
+    """Four-member axes included: the ordered peer-memory reductions keep the
+    logits bit-identical to the reference's coordinate-order combine."""
+    rep = _run(4, "--grid", grid)
+    assert rep["logits_bitwise"]
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 8, reason="needs 8 GPUs")
