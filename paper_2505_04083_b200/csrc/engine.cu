@@ -506,6 +506,8 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
   PK_CUDA(cudaMemcpyAsync(&bad, ce_ws_.bad.p, sizeof(u32), cudaMemcpyDeviceToHost, st_));
   PK_CUDA(cudaStreamSynchronize(st_));
   check(!bad, "cross entropy: label out of range for " + std::to_string(C) + " classes");
+  if (lsa_ready_ && grid_.size() > 1 && lsa_timed_out())
+    throw Error(PK_ERR_NCCL, "peer-memory reduction: a barrier wait timed out (peer stalled)");
   // finalize_loss (trainer.hpp:71-89)
   const u64 count = static_cast<u64>(h[1]), correct = static_cast<u64>(h[2]);
   if (count == 0)

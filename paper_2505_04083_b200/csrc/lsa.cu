@@ -22,6 +22,8 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "lsa.cuh"
@@ -154,12 +156,20 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   epoch_ += 2;
   const bool v4 = cols % 4 == 0 && ld_p % 4 == 0 && ld_o % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  // CTAs per reduce: every member must launch the same count (the barrier
+  // slots are per CTA). PK_LSA_CTAS trades NVLink/HBM parallelism against
+  // the SMs the overlapped SpMM / GEMM keep.
+  static const int ctas = [] {
+    const char* e = std::getenv("PK_LSA_CTAS");
+    const int v = e ? std::atoi(e) : kLsaBlocks;
+    return std::max(1, std::min(v, kLsaBlocks));
+  }();
   if (v4)
-    lsa_reduce_kernel<4><<<kLsaBlocks, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
-                                                     epoch);
+    lsa_reduce_kernel<4><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
+                                               epoch);
   else
-    lsa_reduce_kernel<1><<<kLsaBlocks, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
-                                                     epoch);
+    lsa_reduce_kernel<1><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
+                                               epoch);
   PK_LAUNCH("lsa ordered reduce");
 }
 
