@@ -23,6 +23,7 @@
 #include <nccl_device.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -68,29 +69,49 @@ __device__ void barrier(const LsaPeers& P, int b, unsigned epoch) {
 
 // out[r, c] = sum_j part_j[r, c] in ascending j, rows [r0, r1) of the
 // partial buffers (ld_p) -> out rows starting at out_r0 (ld_o)
-template <int VEC>
+template <int VEC, int G>
 __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64 r1, i64 cols,
                                                          i64 ld_p, float* __restrict__ out,
                                                          i64 out_r0, i64 ld_o, unsigned epoch) {
   barrier(P, blockIdx.x, epoch);
   const i64 cv = cols / VEC;
   const i64 total = (r1 - r0) * cv;
-  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const i64 r = r0 + i / cv, c = (i % cv) * VEC;
-    const i64 off = r * ld_p + c;
-    if constexpr (VEC == 4) {
-      float4 acc = __ldcg(reinterpret_cast<const float4*>(P.data[0] + off));
-      for (int j = 1; j < P.g; ++j) {
-        const float4 x = __ldcg(reinterpret_cast<const float4*>(P.data[j] + off));
-        acc.x = __fadd_rn(acc.x, x.x), acc.y = __fadd_rn(acc.y, x.y);
-        acc.z = __fadd_rn(acc.z, x.z), acc.w = __fadd_rn(acc.w, x.w);
+  const i64 stride = static_cast<i64>(gridDim.x) * blockDim.x;
+  using V = typename std::conditional<VEC == 4, float4, float>::type;
+  // kUnroll grid-stride elements per pass, all members' loads issued before
+  // the ordered adds: remote NVLink loads are latency-bound, so each thread
+  // keeps kUnroll x g of them in flight
+  constexpr int kUnroll = 4;
+  for (i64 base = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; base < total;
+       base += stride * kUnroll) {
+    V x[kUnroll][G];
+    i64 off[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const i64 i = base + u * stride;
+      const i64 r = r0 + i / cv, c = (i % cv) * VEC;
+      off[u] = i < total ? r * ld_p + c : -1;
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (j < P.g && off[u] >= 0) x[u][j] = __ldcg(reinterpret_cast<const V*>(P.data[j] + off[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (off[u] < 0) continue;
+      const i64 i = base + u * stride;
+      const i64 r = r0 + i / cv, c = (i % cv) * VEC;
+      V acc = x[u][0];
+#pragma unroll
+      for (int j = 1; j < G; ++j) {
+        if (j >= P.g) break;
+        if constexpr (VEC == 4) {
+          acc.x = __fadd_rn(acc.x, x[u][j].x), acc.y = __fadd_rn(acc.y, x[u][j].y);
+          acc.z = __fadd_rn(acc.z, x[u][j].z), acc.w = __fadd_rn(acc.w, x[u][j].w);
+        } else {
+          acc = __fadd_rn(acc, x[u][j]);
+        }
       }
-      *reinterpret_cast<float4*>(out + (r - r0 + out_r0) * ld_o + c) = acc;
-    } else {
-      float acc = __ldcg(P.data[0] + off);
-      for (int j = 1; j < P.g; ++j) acc = __fadd_rn(acc, __ldcg(P.data[j] + off));
-      out[(r - r0 + out_r0) * ld_o + c] = acc;
+      *reinterpret_cast<V*>(out + (r - r0 + out_r0) * ld_o + c) = acc;
     }
   }
   barrier(P, blockIdx.x, epoch + 1);
@@ -161,15 +182,26 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   // the SMs the overlapped SpMM / GEMM keep.
   static const int ctas = [] {
     const char* e = std::getenv("PK_LSA_CTAS");
-    const int v = e ? std::atoi(e) : kLsaBlocks;
+    const int v = e ? std::atoi(e) : kLsaBlocks / 2;  // measured: 148 = NCCL speed, fewer SMs
     return std::max(1, std::min(v, kLsaBlocks));
   }();
-  if (v4)
-    lsa_reduce_kernel<4><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
-                                               epoch);
-  else
-    lsa_reduce_kernel<1><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
-                                               epoch);
+  auto launch = [&](auto vec_tag, auto g_tag) {
+    constexpr int V = decltype(vec_tag)::value, Gm = decltype(g_tag)::value;
+    lsa_reduce_kernel<V, Gm><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
+                                                  epoch);
+  };
+  using V4 = std::integral_constant<int, 4>;
+  using V1 = std::integral_constant<int, 1>;
+  if (g_ <= 2) {
+    if (v4) launch(V4{}, std::integral_constant<int, 2>{});
+    else launch(V1{}, std::integral_constant<int, 2>{});
+  } else if (g_ <= 4) {
+    if (v4) launch(V4{}, std::integral_constant<int, 4>{});
+    else launch(V1{}, std::integral_constant<int, 4>{});
+  } else {
+    if (v4) launch(V4{}, std::integral_constant<int, 8>{});
+    else launch(V1{}, std::integral_constant<int, 8>{});
+  }
   PK_LAUNCH("lsa ordered reduce");
 }
 
