@@ -68,16 +68,6 @@ inline std::string shape(i64 r, i64 c) {
   return std::to_string(r) + "x" + std::to_string(c);
 }
 
-// Device allocations come from the device's stream-ordered memory pool with
-// an unbounded release threshold: an engine that is torn down and rebuilt
-// (the e2e load, re-sharding) reuses the pool's mappings instead of paying
-// cudaMalloc/cudaFree page-table work again. Allocation and free keep
-// cudaMalloc/cudaFree's synchronous semantics (the free waits for the
-// device, like cudaFree does). PK_POOL=0 selects plain cudaMalloc.
-bool pool_enabled();
-void* dev_alloc(size_t bytes);
-void dev_free(void* p);
-
 // Device buffer owned by RAII; used for workspaces.
 template <typename T>
 struct DevBuf {
@@ -98,13 +88,13 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
+    if (count) PK_CUDA(cudaMalloc(&p, count * sizeof(T)));
   }
   void ensure(size_t count) {
     if (count > n) alloc(count);
   }
   void release() {
-    if (p) dev_free(p);
+    if (p) cudaFree(p);
     p = nullptr;
     n = 0;
   }
