@@ -123,6 +123,15 @@ int pk_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k,
                 float* c, int64_t ldc, int mode, uint64_t* flops_host,
                 void* stream);
 
+/* gemm followed by relu_forward in one pass (the forward of a hidden layer:
+ * C = relu(op(A) . op(B))); FAST applies it in the tensor-core epilogue,
+ * PARITY as an in-place pass. Same results as pk_gemm_f32 then
+ * pk_relu_forward_f32. */
+int pk_gemm_relu_f32(int ta, int tb, int64_t m, int64_t n, int64_t k,
+                     const float* a, int64_t lda, const float* b, int64_t ldb,
+                     float* c, int64_t ldc, int mode, uint64_t* flops_host,
+                     void* stream);
+
 /* ------------------------------------------------------------------ */
 /* Fused elementwise                                                   */
 
@@ -269,7 +278,11 @@ enum {
   PK_T_DF0 = 3,    /* its gradient                                       */
   PK_T_FOUT = 4,   /* last layer's raw logits shard (RankPass.f_out)     */
   PK_T_H = 5,      /* cached H of layer l (valid after forward)          */
-  PK_T_Q = 6       /* cached Q of layer l                                */
+  PK_T_Q = 6,      /* cached Q of layer l: the last layer's, or a hidden
+                      layer's when the engine materialised it (NCCL
+                      fallback on a split col_shard); else an error     */
+  PK_T_ACT = 7     /* relu(Q) of hidden layer l (next layer's input; the
+                      backward's ReLU mask, relu(Q) > 0 <=> Q > 0)      */
 };
 
 /* 128-byte ncclUniqueId for rank 0 to broadcast (any bootstrap works). */

@@ -73,6 +73,7 @@ SIGNATURES = {
                                     U64P, P]),
     "pk_spmm_plan_info": (INT, [P, I64P, I64P]),
     "pk_gemm_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),
+    "pk_gemm_relu_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),
     "pk_relu_forward_f32": (INT, [P, I64, I64, I64, P, I64, P]),
     "pk_relu_backward_f32": (INT, [P, I64, P, I64, I64, I64, P, I64, P]),
     "pk_softmax_ce_sums_f32": (INT, [P, I64, I64, I64, P, P, P, I64, P, P]),

@@ -181,17 +181,33 @@ int pk_spmm_plan_info(const pk_spmm_plan* plan, int64_t* hub_rows, int64_t* hub_
   });
 }
 
-int pk_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
-                const float* b, int64_t ldb, float* c, int64_t ldc, int mode,
-                uint64_t* flops_host, void* stream) {
+namespace {
+int gemm_entry(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
+               const float* b, int64_t ldb, float* c, int64_t ldc, int mode,
+               uint64_t* flops_host, void* stream, bool relu) {
   return guard([&] {
     check(m >= 0 && n >= 0 && k >= 0, "gemm: negative dimension");
     check(mode == PK_MODE_PARITY || mode == PK_MODE_FAST, "gemm: unknown mode");
     check(lda >= (ta ? m : k) && ldb >= (tb ? k : n) && ldc >= n,
           "gemm: leading dimension smaller than the stored width");
-    gemm_launch(ta != 0, tb != 0, m, n, k, a, lda, b, ldb, c, ldc, mode, as_stream(stream));
+    gemm_launch(ta != 0, tb != 0, m, n, k, a, lda, b, ldb, c, ldc, mode, as_stream(stream),
+                relu);
     if (flops_host) *flops_host += 2 * static_cast<u64>(m) * n * k;
   });
+}
+
+}  // namespace
+
+int pk_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* a, int64_t lda,
+                const float* b, int64_t ldb, float* c, int64_t ldc, int mode,
+                uint64_t* flops_host, void* stream) {
+  return gemm_entry(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, mode, flops_host, stream, false);
+}
+
+int pk_gemm_relu_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* a,
+                     int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, int mode,
+                     uint64_t* flops_host, void* stream) {
+  return gemm_entry(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, mode, flops_host, stream, true);
 }
 
 int pk_relu_forward_f32(const float* q, int64_t ldq, int64_t rows, int64_t cols, float* out,

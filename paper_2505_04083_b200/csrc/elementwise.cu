@@ -4,6 +4,7 @@
 // (model.hpp:88-111). All are HBM-streaming; ReLU and Adam are bit-exact.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "elementwise.cuh"
@@ -65,120 +66,98 @@ unsigned stream_grid(i64 n) {
 }
 
 // ---------------------------------------------------------------------------
-// cross entropy: one warp per row (grid-stride, fixed grid so the double
-// partial sums reduce in a fixed order -> run-to-run deterministic).
+// cross entropy: a CTA stages a tile of kCeRows logits rows in shared memory
+// with coalesced loads (row stride padded to an odd word count: the per-row
+// passes below are bank-conflict free), then each thread owns one row and
+// walks it in ascending class order exactly like the reference loop; the
+// dlogits tile goes back out through the same buffer with coalesced stores.
+// Fixed grid, per-thread double partials reduced in a fixed tree ->
+// run-to-run deterministic.
 
-constexpr int kCeWarps = 8;
-constexpr int kCeMaxPerLane = 8;  // up to 256 classes per row in registers
+constexpr int kCeRows = 128;  // rows per tile = threads per CTA
+constexpr int kCeMaxClasses = 384;  // tile <= 193 KB of shared memory
 
-__global__ void __launch_bounds__(kCeWarps * 32)
+__host__ __device__ inline int ce_stride(int classes) { return classes | 1; }
+
+__global__ void __launch_bounds__(kCeRows)
 ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
           const u32* __restrict__ labels, const u8* __restrict__ mask,
           float* __restrict__ dl, i64 ldd, double* __restrict__ partial,
           u32* __restrict__ bad_label, u64 scale_count) {
+  extern __shared__ float tile[];  // [kCeRows][ce_stride(classes)]
   // (T)1 / (T)global_count (trainer.hpp:84), applied as the reference's
   // separate multiply, fl(d * s)
   const float s = scale_count ? __fdiv_rn(1.f, static_cast<float>(scale_count)) : 1.f;
-  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
-  const i64 gw = static_cast<i64>(blockIdx.x) * kCeWarps + w;
-  const i64 nw = static_cast<i64>(gridDim.x) * kCeWarps;
+  const int t = threadIdx.x;
+  const int stride = ce_stride(classes);
   double loss = 0, count = 0, correct = 0;
-  // the next row's mask, label and logits are loaded before the current row
-  // is processed: one memory latency per row instead of three serial ones
-  const int nt = (classes + 31) / 32;
-  auto fetch = [&](i64 r, u8& m, u32& lab, float (&x)[kCeMaxPerLane]) {
-    m = 0, lab = 0;
-    if (r >= rows) return;
-    m = mask[r];
-    lab = labels[r];
-    const float* row = logits + r * ldl;
-#pragma unroll
-    for (int t = 0; t < kCeMaxPerLane; ++t) {
-      const int j = lane + 32 * t;
-      x[t] = (t < nt && j < classes) ? row[j] : -INFINITY;
+  for (i64 r0 = static_cast<i64>(blockIdx.x) * kCeRows; r0 < rows;
+       r0 += static_cast<i64>(gridDim.x) * kCeRows) {
+    const int nr = static_cast<int>(rows - r0 < kCeRows ? rows - r0 : kCeRows);
+    const int elems = nr * classes;
+    // coalesced stage-in: flat element e of the tile -> (row, class)
+    for (int e = t; e < elems; e += kCeRows) {
+      const int rr = e / classes, c = e - rr * classes;
+      tile[rr * stride + c] = __ldcs(logits + (r0 + rr) * ldl + c);
     }
-  };
-  u8 m_next;
-  u32 lab_next;
-  float x_next[kCeMaxPerLane];
-  fetch(gw, m_next, lab_next, x_next);
-  for (i64 r = gw; r < rows; r += nw) {
-    const u8 m = m_next;
-    const u32 lab = lab_next;
-    float xv[kCeMaxPerLane];
-#pragma unroll
-    for (int t = 0; t < kCeMaxPerLane; ++t) xv[t] = x_next[t];
-    fetch(r + nw, m_next, lab_next, x_next);
-    float* drow = dl + r * ldd;
-    if (!m) {
-      for (int j = lane; j < classes; j += 32) drow[j] = 0.f;
-      continue;
-    }
-    if (lab >= static_cast<u32>(classes)) {
-      if (lane == 0) atomicExch(bad_label, 1u);
-      for (int j = lane; j < classes; j += 32) drow[j] = 0.f;
-      continue;
-    }
-    // first max, lowest index on ties (kernels.hpp:142-145)
-    float mx = -INFINITY;
-    int am = 0x7fffffff;
-#pragma unroll
-    for (int t = 0; t < kCeMaxPerLane; ++t) {
-      const int j = lane + 32 * t;
-      if (j < classes && (xv[t] > mx || am == 0x7fffffff)) mx = xv[t], am = j;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, mx, off);
-      const int oa = __shfl_xor_sync(0xffffffffu, am, off);
-      if (om > mx || (om == mx && oa < am)) mx = om, am = oa;
-    }
-    // denominator summed in ascending class order like the reference loop
-    float ev[kCeMaxPerLane];
-#pragma unroll
-    for (int t = 0; t < kCeMaxPerLane; ++t) {
-      const int j = lane + 32 * t;
-      ev[t] = j < classes ? expf(xv[t] - mx) : 0.f;
-    }
-    float denom = 0.f;
-#pragma unroll
-    for (int t = 0; t < kCeMaxPerLane; ++t) {
-      if (32 * t >= classes) break;
-      for (int src = 0; src < 32; ++src) {
-        const float e = __shfl_sync(0xffffffffu, ev[t], src);
-        if (32 * t + src < classes) denom = __fadd_rn(denom, e);
+    const i64 r = r0 + t;
+    const bool live = t < nr;
+    const u8 m = live ? mask[r] : 0;
+    const u32 lab = live ? labels[r] : 0;
+    __syncthreads();
+    float* x = tile + t * stride;
+    if (live) {
+      if (!m || lab >= static_cast<u32>(classes)) {
+        if (m) atomicExch(bad_label, 1u);
+        for (int j = 0; j < classes; ++j) x[j] = 0.f;
+      } else {
+        // first max, lowest index on ties (kernels.hpp:142-145)
+        float mx = x[0];
+        int am = 0;
+        for (int j = 1; j < classes; ++j)
+          if (x[j] > mx) mx = x[j], am = j;
+        const float xl = x[lab];
+        // denominator summed in ascending class order like the reference
+        float denom = 0.f;
+        for (int j = 0; j < classes; ++j) {
+          const float e = expf(x[j] - mx);
+          x[j] = e;
+          denom = __fadd_rn(denom, e);
+        }
+        loss += static_cast<double>(__fsub_rn(logf(denom), __fsub_rn(xl, mx)));
+        count += 1;
+        if (am == static_cast<int>(lab)) correct += 1;
+        // one reciprocal per row instead of a divide per class: within 1 ulp
+        // of the reference's exp/denom (CE is tolerance-checked anyway:
+        // expf/logf differ from glibc in the last ulp)
+        const float rden = __frcp_rn(denom);
+        for (int j = 0; j < classes; ++j) {
+          float d = __fmul_rn(x[j], rden);
+          if (j == static_cast<int>(lab)) d = __fsub_rn(d, 1.f);
+          x[j] = scale_count ? __fmul_rn(d, s) : d;
+        }
       }
     }
-    const float xl = __shfl_sync(0xffffffffu, xv[lab / 32], lab % 32);
-    if (lane == 0) {
-      loss += static_cast<double>(__fsub_rn(logf(denom), __fsub_rn(xl, mx)));
-      count += 1;
-      if (am == static_cast<int>(lab)) correct += 1;
+    __syncthreads();
+    for (int e = t; e < elems; e += kCeRows) {
+      const int rr = e / classes, c = e - rr * classes;
+      __stcs(dl + (r0 + rr) * ldd + c, tile[rr * stride + c]);
     }
-    // one reciprocal per row instead of a divide per class: within 1 ulp of
-    // the reference's exp/denom (CE is tolerance-checked anyway: expf/logf
-    // differ from glibc in the last ulp)
-    const float rden = __frcp_rn(denom);
-#pragma unroll
-    for (int t = 0; t < kCeMaxPerLane; ++t) {
-      const int j = lane + 32 * t;
-      if (j < classes) {
-        float d = __fmul_rn(ev[t], rden);
-        if (j == static_cast<int>(lab)) d = __fsub_rn(d, 1.f);
-        drow[j] = scale_count ? __fmul_rn(d, s) : d;
-      }
-    }
+    __syncthreads();
   }
-  // block partials in warp order
-  __shared__ double sh[kCeWarps][3];
-  if (lane == 0) sh[w][0] = loss, sh[w][1] = count, sh[w][2] = correct;
+  // fixed-order tree over the CTA's threads
+  __shared__ double sh[kCeRows][3];
+  sh[t][0] = loss, sh[t][1] = count, sh[t][2] = correct;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0, b = 0, c = 0;
-    for (int i = 0; i < kCeWarps; ++i) a += sh[i][0], b += sh[i][1], c += sh[i][2];
-    partial[3 * blockIdx.x] = a;
-    partial[3 * blockIdx.x + 1] = b;
-    partial[3 * blockIdx.x + 2] = c;
+  for (int h = kCeRows / 2; h > 0; h >>= 1) {
+    if (t < h)
+      for (int k = 0; k < 3; ++k) sh[t][k] += sh[t + h][k];
+    __syncthreads();
+  }
+  if (t == 0) {
+    partial[3 * blockIdx.x] = sh[0][0];
+    partial[3 * blockIdx.x + 1] = sh[0][1];
+    partial[3 * blockIdx.x + 2] = sh[0][2];
   }
 }
 
@@ -203,21 +182,46 @@ __global__ void scale_kernel(float* __restrict__ d, i64 ldd, i64 rows, i64 cols,
   }
 }
 
+__device__ __forceinline__ void adam1(float& p, float g, float& m, float& v,
+                                      const AdamScalars& s) {
+  // m = b1*m + (1-b1)*g ; v = b2*v + ((1-b2)*g)*g   (model.hpp:97-98)
+  m = __fadd_rn(__fmul_rn(s.b1, m), __fmul_rn(s.omb1, g));
+  v = __fadd_rn(__fmul_rn(s.b2, v), __fmul_rn(__fmul_rn(s.omb2, g), g));
+  const float mh = __fdiv_rn(m, s.bias1);
+  const float vh = __fdiv_rn(v, s.bias2);
+  // p -= (lr*m_hat) / (sqrt(v_hat) + eps)   (model.hpp:101)
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(s.lr, mh), __fadd_rn(__fsqrt_rn(vh), s.eps)));
+}
+
+// float4 body over [0, n4) plus a scalar tail [4*n4, n); four streams in,
+// three out, all in-place
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                             float* __restrict__ m, float* __restrict__ v, i64 n, AdamScalars s) {
-  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<i64>(gridDim.x) * blockDim.x) {
-    const float gi = g[i];
-    // m = b1*m + (1-b1)*g ; v = b2*v + ((1-b2)*g)*g   (model.hpp:97-98)
-    const float mi = __fadd_rn(__fmul_rn(s.b1, m[i]), __fmul_rn(s.omb1, gi));
-    const float vi = __fadd_rn(__fmul_rn(s.b2, v[i]), __fmul_rn(__fmul_rn(s.omb2, gi), gi));
-    m[i] = mi;
-    v[i] = vi;
-    const float mh = __fdiv_rn(mi, s.bias1);
-    const float vh = __fdiv_rn(vi, s.bias2);
-    // p -= (lr*m_hat) / (sqrt(v_hat) + eps)   (model.hpp:101)
-    p[i] = __fsub_rn(p[i], __fdiv_rn(__fmul_rn(s.lr, mh), __fadd_rn(__fsqrt_rn(vh), s.eps)));
+  const i64 n4 = n / 4;
+  const i64 step = static_cast<i64>(gridDim.x) * blockDim.x;
+  const i64 t0 = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  float4* p4 = reinterpret_cast<float4*>(p);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* m4 = reinterpret_cast<float4*>(m);
+  float4* v4 = reinterpret_cast<float4*>(v);
+  for (i64 i = t0; i < n4; i += step) {
+    float4 pi = p4[i], mi = m4[i], vi = v4[i];
+    const float4 gi = __ldcs(g4 + i);
+    adam1(pi.x, gi.x, mi.x, vi.x, s);
+    adam1(pi.y, gi.y, mi.y, vi.y, s);
+    adam1(pi.z, gi.z, mi.z, vi.z, s);
+    adam1(pi.w, gi.w, mi.w, vi.w, s);
+    p4[i] = pi, m4[i] = mi, v4[i] = vi;
   }
+  for (i64 i = 4 * n4 + t0; i < n; i += step) adam1(p[i], g[i], m[i], v[i], s);
+}
+
+__global__ void adam_scalar_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                   float* __restrict__ m, float* __restrict__ v, i64 n,
+                                   AdamScalars s) {
+  for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<i64>(gridDim.x) * blockDim.x)
+    adam1(p[i], g[i], m[i], v[i], s);
 }
 
 }  // namespace
@@ -253,16 +257,26 @@ void relu_backward_launch(const float* q, i64 ldq, const float* df, i64 lddf, i6
 void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
                     const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
                     cudaStream_t st, u64 scale_count) {
-  check(classes <= 32 * kCeMaxPerLane,
-        "cross entropy: at most " + std::to_string(32 * kCeMaxPerLane) + " classes supported");
-  const int blocks = std::max(1, std::min<int>(sm_count() * 4, ceil_div(rows, kCeWarps)));
+  const size_t smem = sizeof(float) * kCeRows * ce_stride(static_cast<int>(classes));
+  check(classes <= kCeMaxClasses, "cross entropy: at most " + std::to_string(kCeMaxClasses) +
+                                      " classes supported");
+  static const bool attr = [] {
+    PK_CUDA(cudaFuncSetAttribute(ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(float) * kCeRows *
+                                                  ce_stride(kCeMaxClasses))));
+    return true;
+  }();
+  (void)attr;
+  // CTAs resident per SM by shared memory (<= 8), times the SM count
+  const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / smem)));
+  const int blocks =
+      std::max(1, std::min<int>(sm_count() * per_sm, ceil_div(rows, kCeRows)));
   ws.partial.ensure(3 * static_cast<size_t>(blocks));
   ws.bad.ensure(1);
   PK_CUDA(cudaMemsetAsync(ws.bad.p, 0, sizeof(u32), st));
   if (rows > 0 && classes > 0) {
-    ce_kernel<<<blocks, kCeWarps * 32, 0, st>>>(logits, ldl, rows, static_cast<int>(classes),
-                                               labels, mask, dl, ldd, ws.partial.p, ws.bad.p,
-                                               scale_count);
+    ce_kernel<<<blocks, kCeRows, smem, st>>>(logits, ldl, rows, static_cast<int>(classes), labels,
+                                             mask, dl, ldd, ws.partial.p, ws.bad.p, scale_count);
     PK_LAUNCH("cross entropy");
     ce_finish_kernel<<<1, 32, 0, st>>>(ws.partial.p, blocks, sums);
   } else {
@@ -295,7 +309,12 @@ AdamScalars adam_scalars(u64 step, double lr, double beta1, double beta2, double
 void adam_launch(float* p, const float* g, float* m, float* v, i64 n, const AdamScalars& s,
                  cudaStream_t st) {
   if (n == 0) return;
-  adam_kernel<<<stream_grid(n), 256, 0, st>>>(p, g, m, v, n, s);
+  const bool a16 = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                     reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  if (a16)
+    adam_kernel<<<stream_grid((n + 3) / 4), 256, 0, st>>>(p, g, m, v, n, s);
+  else
+    adam_scalar_kernel<<<stream_grid(n), 256, 0, st>>>(p, g, m, v, n, s);
   PK_LAUNCH("adam");
 }
 

@@ -445,29 +445,40 @@ void Engine::forward_layer(int l, bool fault) {
     comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
                            cs);
   });
-  // Q = H . W_full, then its all-reduce along col_shard, row-chunked
+  // Q = H . W_full, then its all-reduce along col_shard, row-chunked. Hidden
+  // layers store only relu(Q) (the next layer's input and, since
+  // relu(Q) > 0 <=> Q > 0, the backward's ReLU mask): the activation is
+  // fused into the GEMM epilogue when col_shard is a single rank, else into
+  // the ordered peer reduction; only the NCCL fallback materialises Q.
+  const bool hidden = l + 1 < L_;
+  const bool col_single = comms_.size(lay.col) == 1;
   LsaGroup* lsa_q = comms_.lsa(lay.col);
-  float* qpart = lsa_q ? lsa_q->scratch() : q_[l].p();
+  DMat& qout = hidden && (col_single || lsa_q) ? fout_[l] : q_[l];
+  float* qpart = lsa_q ? lsa_q->scratch() : qout.p();
   pipelined(
       s.h_rows, comm_chunks(s.h_rows, lay.col),
       [&](i64 r0, i64 r1) {
         clock_.begin(1, st_);
         gemm_launch(false, false, r1 - r0, s.w_cols, s.h_cols, h.p() + r0 * h.ld, h.ld,
-                    wfull_[l].p(), wfull_[l].ld, qpart + r0 * q_[l].ld, q_[l].ld, cfg_.mode,
-                    st_);
+                    wfull_[l].p(), wfull_[l].ld, qpart + r0 * qout.ld, qout.ld, cfg_.mode, st_,
+                    hidden && col_single);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
         if (lsa_q) {
-          lsa_q->reduce(r0, r1, s.q_cols, q_[l].ld, q_[l].p(), r0, q_[l].ld, cs_);
+          lsa_q->reduce(r0, r1, s.q_cols, qout.ld, qout.p(), r0, qout.ld, cs_, hidden);
           comms_.count(kAllReduce, lay.col, (r1 - r0) * s.q_cols * 4);
         } else {
-          comms_.all_reduce(q_[l].p() + r0 * q_[l].ld, (r1 - r0) * q_[l].ld, lay.col,
+          comms_.all_reduce(qout.p() + r0 * qout.ld, (r1 - r0) * qout.ld, lay.col,
                             (r1 - r0) * s.q_cols * 4, cs_);
         }
       });
   gemm_flops_ += 2 * static_cast<u64>(s.h_rows) * s.w_cols * s.h_cols;
-  if (l + 1 < L_) {
+  if (hidden) {
+    if (q_kept_.size() < static_cast<size_t>(L_)) q_kept_.assign(L_, 0);
+    q_kept_[l] = &qout == &q_[l];
+  }
+  if (hidden && &qout == &q_[l]) {
     clock_.begin(1, st_);
     relu_forward_launch(q_[l].p(), q_[l].ld, s.q_rows, s.q_cols, fout_[l].p(), fout_[l].ld, st_);
     clock_.end(st_);
@@ -542,8 +553,9 @@ void Engine::backward_layer(int l) {
     lddq = dl_.ld;
   } else {
     lddq = pad4(s.q_cols);
-    relu_backward_launch(q_[l].p(), q_[l].ld, df_prev_.p(), pad4(s.q_cols), s.q_rows, s.q_cols,
-                         dq_.p(), lddq, st_);
+    // relu'(Q) from the stored activation: relu(Q) > 0 exactly where Q > 0
+    relu_backward_launch(fout_[l].p(), fout_[l].ld, df_prev_.p(), pad4(s.q_cols), s.q_rows,
+                         s.q_cols, dq_.p(), lddq, st_);
     dq = dq_.p();
   }
   // dW = (dQ^T H)^T computed as H^T dQ: same products, same k order
@@ -731,7 +743,11 @@ bool Engine::tensor(int which, int layer, pk_tensor_view* out) {
     case PK_T_DF0: return fill(df0_, df0_.cols);
     case PK_T_FOUT: return fill(q_[L_ - 1], q_[L_ - 1].cols);
     case PK_T_H: return lay_ok && fill(h_[layer], h_[layer].cols);
-    case PK_T_Q: return lay_ok && fill(q_[layer], q_[layer].cols);
+    case PK_T_Q:
+      return lay_ok && (layer == L_ - 1 || (layer < static_cast<int>(q_kept_.size()) &&
+                                            q_kept_[layer])) &&
+             fill(q_[layer], q_[layer].cols);
+    case PK_T_ACT: return lay_ok && layer + 1 < L_ && fill(fout_[layer], fout_[layer].cols);
     default: return false;
   }
 }

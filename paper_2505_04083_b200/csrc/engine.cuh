@@ -124,6 +124,7 @@ class Engine {
   // activations and workspaces
   DMat f0g_;                           // layer-0 gathered features
   std::vector<DMat> h_, q_, fout_;     // cached H, Q and relu(Q) per layer
+  std::vector<char> q_kept_;           // hidden layer's Q materialised last forward
   std::vector<DMat> wfull_, dwp_;      // gathered W and dW partial per layer
   DMat dq_, dh_, df_, df_prev_;        // backward workspaces (max shapes)
   DMat logits_, dl_, stage_;

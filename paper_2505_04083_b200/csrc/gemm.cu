@@ -15,6 +15,7 @@
 // deterministic split-K for tall reductions.
 #include <cuda_runtime.h>
 
+#include "elementwise.cuh"
 #include "gemm.cuh"
 #include "pk_common.cuh"
 
@@ -212,14 +213,14 @@ void gemm_simt_dispatch(i64 m, i64 n, i64 k, const float* a, i64 lda, const floa
 }  // namespace
 
 void gemm_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda, const float* b,
-                 i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st) {
+                 i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st, bool relu) {
   if (m == 0 || n == 0) return;
-  if (k == 0) {  // reference writes acc = 0 (kernels.hpp:84-89)
+  if (k == 0) {  // reference writes acc = 0 (kernels.hpp:84-89); relu(0) = 0
     zero_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(c, m, n, ldc);
     PK_LAUNCH("gemm zero fill");
     return;
   }
-  if (mode == PK_MODE_FAST && gemm_tc_launch(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, st))
+  if (mode == PK_MODE_FAST && gemm_tc_launch(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, st, relu))
     return;
   if (!ta && !tb)
     gemm_simt_dispatch<false, false>(m, n, k, a, lda, b, ldb, c, ldc, mode, st);
@@ -229,6 +230,7 @@ void gemm_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
     gemm_simt_dispatch<false, true>(m, n, k, a, lda, b, ldb, c, ldc, mode, st);
   else
     gemm_simt_dispatch<true, true>(m, n, k, a, lda, b, ldb, c, ldc, mode, st);
+  if (relu) relu_forward_launch(c, ldc, m, n, c, ldc, st);
 }
 
 }  // namespace pk

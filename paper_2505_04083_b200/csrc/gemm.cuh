@@ -7,12 +7,16 @@ namespace pk {
 
 // C(m x n, ldc) = op(A) . op(B); A stored (ta ? k x m : m x k), B stored
 // (tb ? n x k : k x n). mode: PK_MODE_PARITY (bit-exact) or PK_MODE_FAST.
+// relu: store relu(C) instead (relu_forward, kernels.hpp:94-101), fused into
+// the tensor-core epilogue, else a separate in-place pass.
 void gemm_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
-                 const float* b, i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st);
+                 const float* b, i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st,
+                 bool relu = false);
 
 // Tensor-core (tcgen05, 3xTF32) path; returns false when the shape or
 // alignment is not covered and the caller should fall back.
 bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
-                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st);
+                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st,
+                    bool relu = false);
 
 }  // namespace pk

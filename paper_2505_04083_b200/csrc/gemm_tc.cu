@@ -322,6 +322,7 @@ struct TcParams {
   float* c;         // output (splits == 1) or partials [split][m][ldc]
   i64 ldc;
   i64 split_stride; // elements between split partials
+  int relu;         // 1: the final value is stored as relu(v) (v > 0 ? v : 0)
 };
 
 template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE>
@@ -542,9 +543,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
       float* out = p.c + static_cast<i64>(sp) * p.split_stride;
       const bool vec_out = (p.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
       // segments of one tile land in order: the first stores, later ones add
-      // (fp32 round-to-nearest in registers, fixed order: deterministic)
+      // (fp32 round-to-nearest in registers, fixed order: deterministic); the
+      // fused ReLU applies to the last segment's sum (never to split partials)
       for (int sg = 0; sg < nseg; ++sg) {
         const bool zero = nk == 0;
+        const bool relu = p.relu && p.splits == 1 && sg == nseg - 1;
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) +
@@ -568,12 +571,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
                 v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
                 v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
               }
+              if (relu) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+              }
               d4[0] = make_float4(v[0], v[1], v[2], v[3]);
               d4[1] = make_float4(v[4], v[5], v[6], v[7]);
             } else {
 #pragma unroll
               for (int i = 0; i < 8; ++i)
-                if (i < left) dst[i] = sg > 0 ? dst[i] + v[i] : v[i];
+                if (i < left) {
+                  const float x = sg > 0 ? dst[i] + v[i] : v[i];
+                  dst[i] = relu ? (x > 0.f ? x : 0.f) : x;
+                }
             }
           }
         }
@@ -626,13 +636,14 @@ __global__ void b_image_kernel(const float* __restrict__ w, i64 ldw, bool w_is_k
 
 // Deterministic split combine: C = partial[0] + partial[1] + ... in order.
 __global__ void tc_split_reduce_kernel(const float* __restrict__ part, int splits, i64 m, i64 n,
-                                       i64 ldp, i64 stride, float* __restrict__ c, i64 ldc) {
+                                       i64 ldp, i64 stride, float* __restrict__ c, i64 ldc,
+                                       int relu) {
   const i64 idx = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (idx >= m * n) return;
   const i64 i = idx / n, j = idx % n;
   float s = part[i * ldp + j];
   for (int z = 1; z < splits; ++z) s += part[z * stride + i * ldp + j];
-  c[i * ldc + j] = s;
+  c[i * ldc + j] = relu ? (s > 0.f ? s : 0.f) : s;
 }
 
 template <bool A_T, bool B_T, int BN, bool B_PRE>
@@ -694,10 +705,11 @@ bool aligned16(const void* p, i64 ld) {
 }  // namespace
 
 bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
-                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st) {
+                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st, bool relu) {
   if (ta && tb) return false;  // not used by the layer
   TcParams p{};
   p.m = m, p.n = n, p.k = k;
+  p.relu = relu ? 1 : 0;
   // A: NN/NT -> K-major (storage m x k); TN -> MN-major (storage k x m)
   p.a = OperandSrc{a, lda, m, aligned16(a, lda)};
   // B: NN -> MN-major (storage k x n); NT -> K-major (storage n x k); TN -> MN-major
@@ -743,7 +755,7 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
     launch_forms<true, true, false>(p, bn, st);
   if (splits > 1) {
     tc_split_reduce_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(part.p, splits, m, n, p.ldc,
-                                                                 p.split_stride, c, ldc);
+                                                                 p.split_stride, c, ldc, p.relu);
     PK_LAUNCH("gemm tcgen05 split reduce");
   }
   return true;

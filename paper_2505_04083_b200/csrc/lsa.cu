@@ -72,7 +72,8 @@ __device__ void barrier(const LsaPeers& P, int b, unsigned epoch) {
 template <int VEC, int G>
 __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64 r1, i64 cols,
                                                          i64 ld_p, float* __restrict__ out,
-                                                         i64 out_r0, i64 ld_o, unsigned epoch) {
+                                                         i64 out_r0, i64 ld_o, int relu,
+                                                         unsigned epoch) {
   barrier(P, blockIdx.x, epoch);
   const i64 cv = cols / VEC;
   const i64 total = (r1 - r0) * cv;
@@ -109,6 +110,14 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
           acc.z = __fadd_rn(acc.z, x[u][j].z), acc.w = __fadd_rn(acc.w, x[u][j].w);
         } else {
           acc = __fadd_rn(acc, x[u][j]);
+        }
+      }
+      if (relu) {  // fused relu_forward of the reduced Q (kernels.hpp:94-101)
+        if constexpr (VEC == 4) {
+          acc.x = acc.x > 0.f ? acc.x : 0.f, acc.y = acc.y > 0.f ? acc.y : 0.f;
+          acc.z = acc.z > 0.f ? acc.z : 0.f, acc.w = acc.w > 0.f ? acc.w : 0.f;
+        } else {
+          acc = acc > 0.f ? acc : 0.f;
         }
       }
       *reinterpret_cast<V*>(out + (r - r0 + out_r0) * ld_o + c) = acc;
@@ -169,7 +178,7 @@ bool LsaGroup::init(ncclComm_t comm, int g, int me, size_t scratch_elems) {
 }
 
 void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool relu) {
   check(ready_, "lsa reduce: group not initialised");
   check((r1 > 0 ? r1 : 0) * ld_p * sizeof(float) <= scratch_bytes_,
         "lsa reduce: partial exceeds the symmetric scratch");
@@ -188,7 +197,7 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   auto launch = [&](auto vec_tag, auto g_tag) {
     constexpr int V = decltype(vec_tag)::value, Gm = decltype(g_tag)::value;
     lsa_reduce_kernel<V, Gm><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
-                                                  epoch);
+                                                  relu ? 1 : 0, epoch);
   };
   using V4 = std::integral_constant<int, 4>;
   using V1 = std::integral_constant<int, 1>;

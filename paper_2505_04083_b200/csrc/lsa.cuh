@@ -30,9 +30,10 @@ class LsaGroup {
   size_t scratch_elems() const { return scratch_bytes_ / sizeof(float); }
   // out rows [out_r0, out_r0 + r1 - r0) = sum over members, in coordinate
   // order, of their scratch rows [r0, r1). Collective (same call sequence on
-  // every member); runs on `st`.
+  // every member); runs on `st`. relu: store relu(sum) (the forward's
+  // activation fused into the Q reduction).
   void reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
-              cudaStream_t st);
+              cudaStream_t st, bool relu = false);
 
  private:
   int g_ = 0, me_ = 0;

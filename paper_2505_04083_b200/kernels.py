@@ -178,9 +178,10 @@ def spmm(a: DeviceCsr, x: torch.Tensor, flops=None, out=None, plan=None, stream=
 
 
 def gemm(a, b, transpose_a=False, transpose_b=False, flops=None, mode=PK_MODE_PARITY, out=None,
-         stream=None):
+         stream=None, relu=False):
     """gemm (kernels.hpp:64-92): op(A) . op(B). PARITY is bit-exact with the
-    reference loop; FAST is the tensor-core path."""
+    reference loop; FAST is the tensor-core path. relu=True returns
+    relu_forward(op(A) . op(B)) from one fused call (pk_gemm_relu_f32)."""
     m = a.shape[1] if transpose_a else a.shape[0]
     ka = a.shape[0] if transpose_a else a.shape[1]
     kb = b.shape[1] if transpose_b else b.shape[0]
@@ -193,7 +194,8 @@ def gemm(a, b, transpose_a=False, transpose_b=False, flops=None, mode=PK_MODE_PA
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=a.device)
     fl = _flops_out(flops)
-    call("pk_gemm_f32", int(transpose_a), int(transpose_b), m, n, ka, _ptr(a), _ld(a), _ptr(b),
+    call("pk_gemm_relu_f32" if relu else "pk_gemm_f32", int(transpose_a), int(transpose_b), m, n,
+         ka, _ptr(a), _ld(a), _ptr(b),
          _ld(b), _ptr(out), _ld(out), mode, C.byref(fl) if fl is not None else None,
          _stream(stream))
     if flops is not None:

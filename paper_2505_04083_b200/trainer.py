@@ -22,7 +22,7 @@ from .layout import GridConfig, feature_slice, label_row_range, model_dims, plan
     weight_slice
 
 PK_MAX_LAYERS = 15
-PK_T_W, PK_T_DW, PK_T_F0, PK_T_DF0, PK_T_FOUT, PK_T_H, PK_T_Q = range(7)
+PK_T_W, PK_T_DW, PK_T_F0, PK_T_DF0, PK_T_FOUT, PK_T_H, PK_T_Q, PK_T_ACT = range(8)
 
 
 class pk_engine_config(C.Structure):

@@ -111,3 +111,22 @@ def test_tc_gemm_large_products_shape(cuda):
     rel = (torch.linalg.norm(q[idx].double() - want) / torch.linalg.norm(want)).item()
     assert rel <= TOL, rel
     assert torch.isfinite(q).all()
+
+
+@pytest.mark.parametrize("m,n,kk", [(5000, 256, 256), (300, 47, 100), (4096, 128, 1100),
+                                    (64, 48, 40000), (3, 5, 2)])
+@pytest.mark.parametrize("mode", ["fast", "parity"])
+def test_gemm_relu_fused_equals_gemm_then_relu(cuda, m, n, kk, mode):
+    """pk_gemm_relu_f32 (the hidden layer's GEMM with relu_forward in its
+    epilogue) == relu_forward(gemm) bit for bit: plain tiles, segmented long
+    k (1100 > 16 stages), split-K (k = 40000) and the SIMT parity path."""
+    k = _k()
+    md = k.PK_MODE_FAST if mode == "fast" else k.PK_MODE_PARITY
+    rng = np.random.default_rng(m + n + kk)
+    a = torch.from_numpy(rng.standard_normal(size=(m, kk)).astype(np.float32)).to(cuda)
+    b = torch.from_numpy(rng.standard_normal(size=(kk, n)).astype(np.float32)).to(cuda)
+    plain = k.gemm(a, b, mode=md)
+    fused = k.gemm(a, b, mode=md, relu=True)
+    want = k.relu_forward(plain)
+    assert torch.equal(fused.view(torch.int32), want.view(torch.int32))
+    assert (fused >= 0).all() and (fused == 0).any()

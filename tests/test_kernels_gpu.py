@@ -256,8 +256,11 @@ def test_cross_entropy_known_answer(cuda):
                                 torch.zeros(2, dtype=torch.uint8, device=cuda))
 
 
-@pytest.mark.parametrize("c", [3, 16, 47, 172])
-def test_cross_entropy_vs_oracle(cuda, c):
+@pytest.mark.parametrize("c,pad", [(3, 0), (16, 0), (47, 0), (47, 5), (172, 0), (256, 3),
+                                   (384, 0)])
+def test_cross_entropy_vs_oracle(cuda, c, pad):
+    """Tile-staged CE: odd/even class counts, padded logits rows (ld > C),
+    a partial last tile (4099 rows)."""
     k = _k()
     rng = np.random.default_rng(c)
     rows = 4099
@@ -266,7 +269,9 @@ def test_cross_entropy_vs_oracle(cuda, c):
     labels = rng.integers(0, c, size=rows).astype(np.uint32)
     mask = (rng.random(rows) < 0.8).astype(np.uint8)
     ls, cnt, cor, d = restate.ce_sums(logits, labels, mask)
-    s = k.softmax_cross_entropy_sums(torch.from_numpy(logits).to(cuda),
+    wide = torch.zeros(rows, c + pad, device=cuda)
+    wide[:, :c] = torch.from_numpy(logits).to(cuda)
+    s = k.softmax_cross_entropy_sums(wide[:, :c],
                                      torch.from_numpy(labels.view(np.int32)).to(cuda),
                                      torch.from_numpy(mask).to(cuda))
     assert s.count == cnt and s.correct == cor
