@@ -219,12 +219,21 @@ constexpr int kListUnroll = PK_LIST_UNROLL;
 // the 2-vector (D <= 256) form, where the extra warps' gathers outweigh the
 // registers (measured, scripts/spmm_minb_sweep.sh: -4 % at D=256; the 1-vector
 // form is already register-light and gets slower when squeezed).
-template <int NV>
+#ifndef PK_LIST_MINB1
+#define PK_LIST_MINB1 4
+#endif
+#ifndef PK_LIST_U8
+#define PK_LIST_U8 2
+#endif
+#ifndef PK_LIST_MINB8
+#define PK_LIST_MINB8 4
+#endif
+template <int VEC, int NV>
 constexpr int list_min_blocks() {
-  return NV == 2 ? 3 : 2;
+  return NV == 2 ? 3 : (VEC == 8 ? PK_LIST_MINB8 : PK_LIST_MINB1);
 }
 template <int VEC, int LANES, int NV, int U>
-__global__ void __launch_bounds__(kThreads, list_min_blocks<NV>())
+__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, NV>())
 spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
                  int* __restrict__ counters) {
   using V = typename Vec<VEC>::T;
@@ -569,7 +578,8 @@ struct ListWorkspace {
 
 template <int VEC, int LANES, int NV>
 void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
-  constexpr int U0 = NV >= 4 ? 2 : (NV == 2 ? PK_LIST_U2 : PK_LIST_U1);
+  constexpr int U0 =
+      NV >= 4 ? 2 : (NV == 2 ? PK_LIST_U2 : (VEC == 8 ? PK_LIST_U8 : PK_LIST_U1));
   constexpr int U = U0 < LANES ? U0 : LANES / 2;
   auto kernel = spmm_list_kernel<VEC, LANES, NV, U>;
   const int slices = ceil_div(a.nvec, NV * LANES);

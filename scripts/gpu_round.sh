@@ -8,4 +8,4 @@ timeout 900 python -m pytest tests -m gpu -q --deselect tests/test_gemm_tc_gpu.p
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
 timeout 900 python bench.py --steps 5 --warmup 3 --mode parity --no-e2e --no-cpu-baseline > gpurun_out/bench_parity.log 2>&1; echo "bench parity rc=$?"
-tail -5 gpurun_out/pytest_tc.log gpurun_out/pytest_gpu.log gpurun_out/smoke.log; tail -c 2500 gpurun_out/bench.log; tail -c 1500 gpurun_out/bench_parity.log
+for f in gpurun_out/pytest_tc.log gpurun_out/pytest_gpu.log gpurun_out/smoke.log; do tail -n 3 $f; done; tail -c 2500 gpurun_out/bench.log; tail -c 1500 gpurun_out/bench_parity.log
