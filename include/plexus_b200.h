@@ -107,6 +107,16 @@ int pk_spmm_plan_rows_f32(const pk_spmm_plan* plan, const pk_csr* a, int64_t r0,
                           int64_t r1, const float* x, int64_t x_rows,
                           int64_t ldx, int64_t d, float* y, int64_t ldy,
                           uint64_t* flops_host, void* stream);
+/* spmm_rows then relu_backward in one pass (the backward's dF of layer l+1
+ * feeding layer l): y = mask > 0 ? (A . X)[r0:r1] : 0, mask (r1 - r0) x d
+ * with leading dimension ldm (the cached relu(Q) of layer l). Bit-identical
+ * to pk_spmm_plan_rows_f32 followed by pk_relu_backward_f32. */
+int pk_spmm_plan_rows_relu_bwd_f32(const pk_spmm_plan* plan, const pk_csr* a,
+                                   int64_t r0, int64_t r1, const float* x,
+                                   int64_t x_rows, int64_t ldx, int64_t d,
+                                   const float* mask, int64_t ldm, float* y,
+                                   int64_t ldy, uint64_t* flops_host,
+                                   void* stream);
 /* number of hub rows and the hub threshold the plan chose */
 int pk_spmm_plan_info(const pk_spmm_plan* plan, int64_t* hub_rows,
                       int64_t* hub_threshold);

@@ -71,6 +71,8 @@ SIGNATURES = {
     "pk_spmm_plan_destroy": (INT, [P]),
     "pk_spmm_plan_rows_f32": (INT, [P, C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64,
                                     U64P, P]),
+    "pk_spmm_plan_rows_relu_bwd_f32": (INT, [P, C.POINTER(pk_csr), I64, I64, P, I64, I64, I64,
+                                             P, I64, P, I64, U64P, P]),
     "pk_spmm_plan_info": (INT, [P, I64P, I64P]),
     "pk_gemm_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),
     "pk_gemm_relu_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),

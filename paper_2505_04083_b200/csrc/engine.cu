@@ -551,6 +551,10 @@ void Engine::backward_layer(int l) {
     const i64 c0 = chunk_start(dims_[L_], comms_.size(lay.inner), c_.along(lay.inner));
     dq = dl_.p() + c0;
     lddq = dl_.ld;
+  } else if (df_masked_) {
+    // relu_backward already applied by the SpMM^T / reduction that made dF
+    lddq = pad4(s.q_cols);
+    dq = df_prev_.p();
   } else {
     lddq = pad4(s.q_cols);
     // relu'(Q) from the stored activation: relu(Q) > 0 exactly where Q > 0
@@ -607,12 +611,19 @@ void Engine::backward_layer(int l) {
   float* dfpart = lsa_df ? lsa_df->scratch() : df_.p();
   const int gr = grid_.extent(lay.row), pr = c_.along(lay.row);
   const i64 own0 = chunk_start(s.a_cols, gr, pr), own1 = chunk_start(s.a_cols, gr, pr + 1);
+  // layer l-1's relu_backward rides on whatever writes the final dF: this
+  // SpMM^T when row_shard is one rank, else the ordered reduction (the NCCL
+  // fallback keeps the separate pass)
+  const DMat* act = l > 0 ? &fout_[l - 1] : nullptr;
+  const bool mask_spmm = act && gr == 1;
+  const bool mask_reduce = act && gr > 1 && lsa_df;
   pipelined(
       sh.at.rows, comm_chunks(sh.at.rows, lay.row),
       [&](i64 r0, i64 r1) {
         clock_.begin(5, st_);
         spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, s.f_cols, dfpart + r0 * lddf,
-                 lddf, st_);
+                 lddf, st_, mask_spmm ? act->p() + r0 * act->ld : nullptr,
+                 mask_spmm ? act->ld : 0);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
@@ -622,7 +633,8 @@ void Engine::backward_layer(int l) {
             lsa_df->reduce(a, std::max(a, b), s.f_cols, lddf, df0_.p(), a - own0, df0_.ld, cs_);
             comms_.count(kReduceScatter, lay.row, (r1 - r0) * s.f_cols * 4);
           } else {
-            lsa_df->reduce(r0, r1, s.f_cols, lddf, df_.p(), r0, lddf, cs_);
+            lsa_df->reduce(r0, r1, s.f_cols, lddf, df_.p(), r0, lddf, cs_, false,
+                           mask_reduce ? act->p() : nullptr, mask_reduce ? act->ld : 0);
             comms_.count(kAllReduce, lay.row, (r1 - r0) * s.f_cols * 4);
           }
         } else if (l == 0) {
@@ -636,6 +648,7 @@ void Engine::backward_layer(int l) {
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.f_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.f_cols);
   if (l > 0) std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
+  df_masked_ = mask_spmm || mask_reduce;
 }
 
 // Symmetric scratch for the ordered peer-memory reductions: per axis the

@@ -125,6 +125,7 @@ class Engine {
   DMat f0g_;                           // layer-0 gathered features
   std::vector<DMat> h_, q_, fout_;     // cached H, Q and relu(Q) per layer
   std::vector<char> q_kept_;           // hidden layer's Q materialised last forward
+  bool df_masked_ = false;             // df_prev_ already carries relu_backward
   std::vector<DMat> wfull_, dwp_;      // gathered W and dW partial per layer
   DMat dq_, dh_, df_, df_prev_;        // backward workspaces (max shapes)
   DMat logits_, dl_, stage_;

@@ -73,7 +73,8 @@ template <int VEC, int G>
 __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64 r1, i64 cols,
                                                          i64 ld_p, float* __restrict__ out,
                                                          i64 out_r0, i64 ld_o, int relu,
-                                                         unsigned epoch) {
+                                                         const float* __restrict__ mask,
+                                                         i64 ldm, unsigned epoch) {
   barrier(P, blockIdx.x, epoch);
   const i64 cv = cols / VEC;
   const i64 total = (r1 - r0) * cv;
@@ -120,7 +121,17 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
           acc = acc > 0.f ? acc : 0.f;
         }
       }
-      *reinterpret_cast<V*>(out + (r - r0 + out_r0) * ld_o + c) = acc;
+      const i64 ro = r - r0 + out_r0;
+      if (mask) {  // fused relu_backward: keep where relu(Q) > 0
+        const V m = *reinterpret_cast<const V*>(mask + ro * ldm + c);
+        if constexpr (VEC == 4) {
+          acc.x = m.x > 0.f ? acc.x : 0.f, acc.y = m.y > 0.f ? acc.y : 0.f;
+          acc.z = m.z > 0.f ? acc.z : 0.f, acc.w = m.w > 0.f ? acc.w : 0.f;
+        } else {
+          acc = m > 0.f ? acc : 0.f;
+        }
+      }
+      *reinterpret_cast<V*>(out + ro * ld_o + c) = acc;
     }
   }
   barrier(P, blockIdx.x, epoch + 1);
@@ -178,14 +189,15 @@ bool LsaGroup::init(ncclComm_t comm, int g, int me, size_t scratch_elems) {
 }
 
 void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
-                      cudaStream_t st, bool relu) {
+                      cudaStream_t st, bool relu, const float* mask, i64 ldm) {
   check(ready_, "lsa reduce: group not initialised");
   check((r1 > 0 ? r1 : 0) * ld_p * sizeof(float) <= scratch_bytes_,
         "lsa reduce: partial exceeds the symmetric scratch");
   const unsigned epoch = epoch_;
   epoch_ += 2;
   const bool v4 = cols % 4 == 0 && ld_p % 4 == 0 && ld_o % 4 == 0 &&
-                  (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                  (!mask || (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0));
   // CTAs per reduce: every member must launch the same count (the barrier
   // slots are per CTA). PK_LSA_CTAS trades NVLink/HBM parallelism against
   // the SMs the overlapped SpMM / GEMM keep.
@@ -197,7 +209,7 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   auto launch = [&](auto vec_tag, auto g_tag) {
     constexpr int V = decltype(vec_tag)::value, Gm = decltype(g_tag)::value;
     lsa_reduce_kernel<V, Gm><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
-                                                  relu ? 1 : 0, epoch);
+                                                  relu ? 1 : 0, mask, ldm, epoch);
   };
   using V4 = std::integral_constant<int, 4>;
   using V1 = std::integral_constant<int, 1>;

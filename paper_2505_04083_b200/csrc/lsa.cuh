@@ -31,9 +31,11 @@ class LsaGroup {
   // out rows [out_r0, out_r0 + r1 - r0) = sum over members, in coordinate
   // order, of their scratch rows [r0, r1). Collective (same call sequence on
   // every member); runs on `st`. relu: store relu(sum) (the forward's
-  // activation fused into the Q reduction).
+  // activation fused into the Q reduction). mask (rows indexed like out,
+  // ld = ldm): store mask > 0 ? sum : 0 (the backward's relu_backward fused
+  // into the dF reduction).
   void reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
-              cudaStream_t st, bool relu = false);
+              cudaStream_t st, bool relu = false, const float* mask = nullptr, i64 ldm = 0);
 
  private:
   int g_ = 0, me_ = 0;

@@ -93,6 +93,21 @@ __device__ __forceinline__ void madd(float8& a, float v, const float8& x) {
   madd(a.b, v, x.b);
 }
 
+// relu_backward select: keep a where the mask (relu(Q)) is positive
+__device__ __forceinline__ float keep(float a, float m) { return m > 0.f ? a : 0.f; }
+__device__ __forceinline__ float keep_v(float a, const float* m) { return keep(a, *m); }
+__device__ __forceinline__ float2 keep_v(float2 a, const float* m) {
+  const float2 q = *reinterpret_cast<const float2*>(m);
+  return make_float2(keep(a.x, q.x), keep(a.y, q.y));
+}
+__device__ __forceinline__ float4 keep_v(float4 a, const float* m) {
+  const float4 q = __ldcs(reinterpret_cast<const float4*>(m));
+  return make_float4(keep(a.x, q.x), keep(a.y, q.y), keep(a.z, q.z), keep(a.w, q.w));
+}
+__device__ __forceinline__ float8 keep_v(const float8& a, const float* m) {
+  return float8{keep_v(a.a, m), keep_v(a.b, m + 4)};
+}
+
 template <typename T>
 __device__ __forceinline__ T ldg(const float* p) {
   return __ldg(reinterpret_cast<const T*>(p));
@@ -166,6 +181,8 @@ struct ListArgs {
   float* part = nullptr;        // FAST plan: segment sums (target bit 31 set)
   i64 ldp = 0;
   int nvec = 0;
+  const float* mask = nullptr;  // optional relu_backward mask, rows like y
+  i64 ldm = 0;
 };
 
 // chunk bounds over list entries [i0, i1), ~equal nonzeros per chunk
@@ -266,13 +283,18 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
     for (int q = 0; q < NV; ++q) acc[q] = Vec<VEC>::zero();
     auto row_done = [&]() {
       const u32 row = __shfl_sync(gmask, rid, rn, LANES);
-      float* yrow = (row & 0x80000000u)
-                        ? a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp
+      const bool seg = (row & 0x80000000u) != 0;
+      float* yrow = seg ? a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp
                         : a.y + (static_cast<i64>(row) - a.r0) * a.ldy;
       yrow += (vbase + lane) * VEC;
+      const float* mrow =
+          (a.mask && !seg) ? a.mask + (static_cast<i64>(row) - a.r0) * a.ldm + (vbase + lane) * VEC
+                           : nullptr;
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        if (valid[q]) *reinterpret_cast<V*>(yrow + q * LANES * VEC) = acc[q];
+        if (valid[q])
+          *reinterpret_cast<V*>(yrow + q * LANES * VEC) =
+              mrow ? keep_v(acc[q], mrow + q * LANES * VEC) : acc[q];
         acc[q] = Vec<VEC>::zero();
       }
       if (++rn == LANES) {
@@ -361,7 +383,8 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
 __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* __restrict__ seg0,
                                         const u32* __restrict__ nseg, i64 nh, i64 r0,
                                         const float* __restrict__ part, i64 ldp, float* y,
-                                        i64 ldy, i64 d) {
+                                        i64 ldy, i64 d, const float* __restrict__ mask,
+                                        i64 ldm) {
   const i64 total = nh * d;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -369,7 +392,8 @@ __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* 
     const u64 s0 = seg0[h];
     float acc = part[s0 * ldp + c];
     for (u32 k = 1; k < nseg[h]; ++k) acc = __fadd_rn(acc, part[(s0 + k) * ldp + c]);
-    y[(static_cast<i64>(hub[h]) - r0) * ldy + c] = acc;
+    const i64 rr = static_cast<i64>(hub[h]) - r0;
+    y[rr * ldy + c] = mask ? keep(acc, mask[rr * ldm + c]) : acc;
   }
 }
 
@@ -562,7 +586,8 @@ spmm_hub_kernel(SpmmArgs args) {
     }
     if (valid) {
       const i64 rr = r - args.r0;
-      *reinterpret_cast<V*>(args.y + rr * args.ldy + vcol * VEC) = acc;
+      *reinterpret_cast<V*>(args.y + rr * args.ldy + vcol * VEC) =
+          args.mask ? keep_v(acc, args.mask + rr * args.ldm + vcol * VEC) : acc;
     }
   }
 }
@@ -975,12 +1000,15 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 }
 
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
-              float* y, i64 ldy, cudaStream_t st) {
+              float* y, i64 ldy, cudaStream_t st, const float* mask, i64 ldm) {
   if (r1 <= r0 || d == 0) return;
   SpmmPlan::Range& rg = plan_range(plan, r0, r1, st);
   // 32-B slices for the list kernel; the exact plan's hub kernel stages
   // 16-B cp.async pieces, so a plan with hub CTAs stays at 16 B
-  const int vec = pick_vec(x, ldx, y, ldy, d, plan.segment || rg.hubs == 0);
+  // the mask is read with y's vector width: it must share y's alignment
+  int vec = pick_vec(x, ldx, y, ldy, d, plan.segment || rg.hubs == 0);
+  if (mask)
+    while (vec > 1 && (ldm % vec || (reinterpret_cast<uintptr_t>(mask) % (vec * 4)))) vec /= 2;
   const int nvec = static_cast<int>(d / vec);
   // hub CTAs first, on a forked stream, so they hold their SMs while the
   // list kernel streams through the rest of the machine
@@ -989,6 +1017,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   if (!plan.segment && rg.hubs > 0) {
     h.rp = a.row_ptr, h.ci = a.col_idx, h.val = a.values;
     h.x = x, h.ldx = ldx, h.y = y, h.ldy = ldy, h.r0 = r0, h.nrows = r1 - r0, h.nvec = nvec;
+    h.mask = mask, h.ldm = ldm;
     h.hub_rows = rg.hub_ids.p ? rg.hub_ids.p : plan.hub_rows.p;
     h.hub_count = rg.hubs;
     h.hub_slices = ceil_div(nvec, 32);
@@ -1013,6 +1042,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     ListArgs la;
     la.cv = plan.cv.p, la.rl = plan.rl.p, la.rpc = plan.rpc.p, la.endbits = plan.endbits.p;
     la.x = x, la.ldx = ldx, la.y = y, la.ldy = ldy, la.r0 = r0, la.nvec = nvec;
+    la.mask = mask, la.ldm = ldm;
     if (plan.segment && plan.segments) {
       la.ldp = (d + 7) / 8 * 8;  // 32-B aligned rows for the widest slices
       plan.partial.ensure(plan.segments * la.ldp);
@@ -1031,7 +1061,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     const i64 nh = rg.h1 - rg.h0;
     combine_segments_kernel<<<blocks_for(nh * d), 256, 0, st>>>(
         plan.hub_asc.p + rg.h0, plan.hub_seg0.p + rg.h0, plan.hub_nseg.p + rg.h0, nh, r0,
-        plan.partial.p, (d + 7) / 8 * 8, y, ldy, d);
+        plan.partial.p, (d + 7) / 8 * 8, y, ldy, d, mask, ldm);
     PK_LAUNCH("spmm combine segments");
   }
   if (!plan.segment && rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));

@@ -19,6 +19,8 @@ struct SpmmArgs {
   i64 r0 = 0;
   i64 nrows = 0;
   int nvec = 0;              // d / VEC
+  const float* mask = nullptr;  // optional: y = mask > 0 ? y : 0 (rows as y)
+  i64 ldm = 0;
   const i64* hub_rows = nullptr;  // absolute ids, longest first
   int hub_count = 0;
   int hub_slices = 0;
@@ -79,8 +81,11 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 // y[0:r1-r0, 0:d] = A[r0:r1, :] . x, bit-identical to the reference's loop
 // (kernels.hpp:39-62). Launches on `st` (hub CTAs on a forked stream joined
 // back into `st`).
+// mask (optional, rows laid out like y, ld = ldm): every stored row value
+// becomes mask > 0 ? value : 0 — relu_backward (kernels.hpp:103-111) of the
+// previous layer fused into this SpMM^T's epilogue.
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
-              float* y, i64 ldy, cudaStream_t st);
+              float* y, i64 ldy, cudaStream_t st, const float* mask = nullptr, i64 ldm = 0);
 
 // Per-thread fork/join stream used to overlap hub CTAs with the list kernel.
 struct SideStream {

@@ -170,6 +170,27 @@ def spmm_rows(a: DeviceCsr, x: torch.Tensor, r0: int, r1: int, flops=None, out=N
     return out
 
 
+def spmm_rows_relu_backward(a: DeviceCsr, x: torch.Tensor, r0: int, r1: int, mask, plan,
+                            flops=None, out=None, stream=None):
+    """relu_backward(mask, spmm_rows(A, X, r0, r1)) in one pass
+    (kernels.hpp:39-62 then 103-111): the backward's dF of a layer, masked by
+    the previous layer's cached relu(Q)."""
+    d = x.shape[1]
+    if a.cols != x.shape[0]:
+        raise ContractError(f"spmm_rows: A is {a.rows}x{a.cols} but X is {x.shape[0]}x{d}")
+    if tuple(mask.shape) != (r1 - r0, d):
+        raise ContractError(f"relu_backward: mask is {tuple(mask.shape)}, want {(r1 - r0, d)}")
+    if out is None:
+        out = torch.empty((r1 - r0, d), dtype=torch.float32, device=x.device)
+    fl = _flops_out(flops)
+    call("pk_spmm_plan_rows_relu_bwd_f32", plan.h, a.view(), r0, r1, _ptr(x), x.shape[0], _ld(x),
+         d, _ptr(mask), _ld(mask), _ptr(out), _ld(out), C.byref(fl) if fl is not None else None,
+         _stream(stream))
+    if flops is not None:
+        flops[0] += fl.value
+    return out
+
+
 def spmm(a: DeviceCsr, x: torch.Tensor, flops=None, out=None, plan=None, stream=None):
     """spmm (kernels.hpp:16-37): A . X, bit-exact."""
     if a.cols != x.shape[0]:

@@ -330,3 +330,33 @@ def test_spmm_fast_plan_segments_tolerance(cuda, d):
     # row ranges through the same plan (blocked aggregation)
     part = k.spmm_rows(a, x, 50, 160, plan=plan).cpu().numpy()
     assert np.array_equal(part.view(np.uint32), got[50:160].view(np.uint32))
+
+
+@pytest.mark.parametrize("d", [1, 7, 64, 100, 256])
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_spmm_relu_backward_fused(cuda, d, mode):
+    """SpMM^T with the previous layer's relu_backward in its epilogue ==
+    relu_backward(mask, spmm_rows) bit for bit: list rows, empty rows, hub
+    rows (exact hub kernel / FAST segment combine), partial row ranges."""
+    k = _k()
+    md = k.PK_MODE_FAST if mode == "fast" else k.PK_MODE_PARITY
+    rng = np.random.default_rng(100 + d)
+    n_rows, n_cols = 300, 20000
+    lens = rng.integers(0, 40, size=n_rows)
+    lens[[3, 77, 150]] = [4500, 9000, 5001]
+    lens[[5, 6, 200]] = 0
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    ci = np.concatenate([np.sort(rng.choice(n_cols, size=l, replace=False)) for l in lens])
+    vals = rng.uniform(-1, 1, size=ci.size).astype(np.float32)
+    a = k.DeviceCsr.from_host(n_rows, n_cols, rp, ci.astype(np.uint32), vals)
+    x = torch.from_numpy(rng.uniform(-1, 1, size=(n_cols, d)).astype(np.float32)).to(cuda)
+    act = rng.uniform(-1, 1, size=(n_rows, d)).astype(np.float32)
+    act[act < 0] = 0  # a relu(Q): zeros and positives
+    act[0, :] = -0.0
+    mask = torch.from_numpy(act).to(cuda)
+    plan = k.SpmmPlan(a, hub_threshold=4096, mode=md)
+    for r0, r1 in [(0, n_rows), (50, 160), (140, 160)]:
+        plain = k.spmm_rows(a, x, r0, r1, plan=plan)
+        want = k.relu_backward(mask[r0:r1], plain)
+        got = k.spmm_rows_relu_backward(a, x, r0, r1, mask[r0:r1], plan)
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (r0, r1)
