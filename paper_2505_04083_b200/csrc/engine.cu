@@ -171,9 +171,18 @@ cudaEvent_t Engine::sync_event() {
 
 int Engine::comm_chunks(i64 rows, int axis) const {
   if (grid_.extent(axis) == 1) return 1;
-  // ~256K rows per chunk, 2..8 chunks: enough to overlap, few enough that
-  // each collective is a large message
-  return static_cast<int>(std::max<i64>(2, std::min<i64>(8, rows / 262144)));
+  // Default: one chunk, i.e. the reduction follows its producer without
+  // row-chunked overlap. Measured on C2 (scripts/chunk_sweep.sh): N=2
+  // 48.4 / 48.4 / 49.4 / 51.6 ms and N=4 33.4 / 34.0 / 35.4 ms for 1 / 2 / 4
+  // / 8 chunks — the producers (SpMM, GEMM) are HBM-bound, and a reduction
+  // running beside them takes HBM bandwidth and SMs, and every extra chunk
+  // adds a drain/refill of the persistent SpMM. PK_COMM_CHUNKS forces a count.
+  static const int forced = [] {
+    const char* e = std::getenv("PK_COMM_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced > 0) return static_cast<int>(std::min<i64>(forced, std::max<i64>(rows, 1)));
+  return 1;
 }
 
 template <typename P, typename R>
