@@ -60,9 +60,22 @@ def test_two_gpu_fast_mode_and_blocks(cuda):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_two_gpu_nccl_reductions(cuda):
-    """The NCCL path the engine falls back to without peer-memory access."""
-    _run(2, "--grid", "1,2,1", env={"PK_LSA": "0"})
+@pytest.mark.parametrize("grid", _grids(2))
+def test_two_gpu_nccl_reductions(cuda, grid):
+    """The NCCL path the engine falls back to without peer-memory access
+    (separate ReLU passes, materialised Q)."""
+    _run(2, "--grid", grid, env={"PK_LSA": "0"})
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("grid", _grids(2))
+@pytest.mark.parametrize("lsa", ["1", "0"])
+def test_two_gpu_row_chunked_reductions(cuda, grid, lsa):
+    """Row-chunked producer/reduction pipelines (PK_COMM_CHUNKS=3, odd
+    chunk edges): the same bit-identical logits as the unchunked default."""
+    rep = _run(2, "--grid", grid, env={"PK_LSA": lsa, "PK_COMM_CHUNKS": "3"})
+    if lsa == "1":
+        assert rep["logits_bitwise"]
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 4, reason="needs 4 GPUs")
