@@ -245,12 +245,17 @@ constexpr int kListUnroll = PK_LIST_UNROLL;
 #ifndef PK_LIST_MINB8
 #define PK_LIST_MINB8 4
 #endif
-template <int VEC, int NV>
+#ifndef PK_LIST_MINB8M
+#define PK_LIST_MINB8M 4
+#endif
+template <int VEC, int NV, bool MASK>
 constexpr int list_min_blocks() {
-  return NV == 2 ? 3 : (VEC == 8 ? PK_LIST_MINB8 : PK_LIST_MINB1);
+  return NV == 2 ? 3 : (VEC == 8 ? (MASK ? PK_LIST_MINB8M : PK_LIST_MINB8) : PK_LIST_MINB1);
 }
-template <int VEC, int LANES, int NV, int U>
-__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, NV>())
+// MASK: the relu_backward epilogue variant (its own instantiation, so the
+// plain kernel's register allocation is untouched)
+template <int VEC, int LANES, int NV, int U, bool MASK>
+__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, NV, MASK>())
 spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
                  int* __restrict__ counters) {
   using V = typename Vec<VEC>::T;
@@ -287,14 +292,17 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
       float* yrow = seg ? a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp
                         : a.y + (static_cast<i64>(row) - a.r0) * a.ldy;
       yrow += (vbase + lane) * VEC;
-      const float* mrow =
-          (a.mask && !seg) ? a.mask + (static_cast<i64>(row) - a.r0) * a.ldm + (vbase + lane) * VEC
-                           : nullptr;
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        if (valid[q])
-          *reinterpret_cast<V*>(yrow + q * LANES * VEC) =
-              mrow ? keep_v(acc[q], mrow + q * LANES * VEC) : acc[q];
+        if (valid[q]) {
+          V out = acc[q];
+          if constexpr (MASK) {
+            if (!seg)
+              out = keep_v(out, a.mask + (static_cast<i64>(row) - a.r0) * a.ldm +
+                                    (vbase + lane) * VEC + q * LANES * VEC);
+          }
+          *reinterpret_cast<V*>(yrow + q * LANES * VEC) = out;
+        }
         acc[q] = Vec<VEC>::zero();
       }
       if (++rn == LANES) {
@@ -606,7 +614,9 @@ void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t
   constexpr int U0 =
       NV >= 4 ? 2 : (NV == 2 ? PK_LIST_U2 : (VEC == 8 ? PK_LIST_U8 : PK_LIST_U1));
   constexpr int U = U0 < LANES ? U0 : LANES / 2;
-  auto kernel = spmm_list_kernel<VEC, LANES, NV, U>;
+  const bool masked = a.mask != nullptr;
+  auto kernel = masked ? spmm_list_kernel<VEC, LANES, NV, U, true>
+                       : spmm_list_kernel<VEC, LANES, NV, U, false>;
   const int slices = ceil_div(a.nvec, NV * LANES);
   // ~1-2K nonzeros per chunk at the products shape; never more chunks than rows
   const i64 nchunks64 =
@@ -619,7 +629,8 @@ void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t
                                                                     ws.bounds.p, ws.counters.p,
                                                                     slices);
   PK_LAUNCH("spmm list partition");
-  static thread_local int occ = 0;
+  static thread_local int occs[2] = {0, 0};
+  int& occ = occs[masked ? 1 : 0];
   if (occ == 0) {
     PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0));
     occ = std::max(occ, 1);
