@@ -623,7 +623,11 @@ void Engine::backward_layer(int l) {
   // layer l-1's relu_backward rides on whatever writes the final dF: this
   // SpMM^T when row_shard is one rank, else the ordered reduction (the NCCL
   // fallback keeps the separate pass)
-  const DMat* act = l > 0 ? &fout_[l - 1] : nullptr;
+  static const bool fuse = [] {  // PK_FUSE_RELU_BWD=0: separate relu_backward pass (A/B)
+    const char* e = std::getenv("PK_FUSE_RELU_BWD");
+    return !(e && e[0] == '0');
+  }();
+  const DMat* act = l > 0 && fuse ? &fout_[l - 1] : nullptr;
   const bool mask_spmm = act && gr == 1;
   const bool mask_reduce = act && gr > 1 && lsa_df;
   pipelined(

@@ -107,6 +107,16 @@ __device__ __forceinline__ float4 keep_v(float4 a, const float* m) {
 __device__ __forceinline__ float8 keep_v(const float8& a, const float* m) {
   return float8{keep_v(a.a, m), keep_v(a.b, m + 4)};
 }
+__device__ __forceinline__ float keep_vv(float a, float m) { return keep(a, m); }
+__device__ __forceinline__ float2 keep_vv(float2 a, float2 m) {
+  return make_float2(keep(a.x, m.x), keep(a.y, m.y));
+}
+__device__ __forceinline__ float4 keep_vv(float4 a, float4 m) {
+  return make_float4(keep(a.x, m.x), keep(a.y, m.y), keep(a.z, m.z), keep(a.w, m.w));
+}
+__device__ __forceinline__ float8 keep_vv(const float8& a, const float8& m) {
+  return float8{keep_vv(a.a, m.a), keep_vv(a.b, m.b)};
+}
 
 template <typename T>
 __device__ __forceinline__ T ldg(const float* p) {
@@ -286,6 +296,23 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
     V acc[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) acc[q] = Vec<VEC>::zero();
+    // MASK: the current row's relu_backward mask is loaded when the row
+    // starts (right after the previous row's store), so its latency hides
+    // behind the row's gathers instead of stalling the store
+    V mk[MASK ? NV : 1];
+    auto load_mask = [&]() {
+      if constexpr (MASK) {
+        const u32 row = __shfl_sync(gmask, rid, rn, LANES);
+        if (rb + rn < ie && !(row & 0x80000000u)) {
+          const float* mr =
+              a.mask + (static_cast<i64>(row) - a.r0) * a.ldm + (vbase + lane) * VEC;
+#pragma unroll
+          for (int q = 0; q < NV; ++q)
+            mk[q] = valid[q] ? ldg<V>(mr + q * LANES * VEC) : Vec<VEC>::zero();
+        }
+      }
+    };
+    load_mask();
     auto row_done = [&]() {
       const u32 row = __shfl_sync(gmask, rid, rn, LANES);
       const bool seg = (row & 0x80000000u) != 0;
@@ -297,9 +324,7 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
         if (valid[q]) {
           V out = acc[q];
           if constexpr (MASK) {
-            if (!seg)
-              out = keep_v(out, a.mask + (static_cast<i64>(row) - a.r0) * a.ldm +
-                                    (vbase + lane) * VEC + q * LANES * VEC);
+            if (!seg) out = keep_vv(out, mk[q]);
           }
           *reinterpret_cast<V*>(yrow + q * LANES * VEC) = out;
         }
@@ -310,6 +335,7 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
         rb += LANES;
         rid = rb + lane < ie ? __ldg(a.rl + rb + lane) : 0u;
       }
+      load_mask();
     };
     // Full windows are software-pipelined: the gathers of group g+1 (U
     // nonzeros, the next window's first group at a window's end) are issued
