@@ -620,15 +620,18 @@ void Engine::backward_layer(int l) {
   float* dfpart = lsa_df ? lsa_df->scratch() : df_.p();
   const int gr = grid_.extent(lay.row), pr = c_.along(lay.row);
   const i64 own0 = chunk_start(s.a_cols, gr, pr), own1 = chunk_start(s.a_cols, gr, pr + 1);
-  // layer l-1's relu_backward rides on whatever writes the final dF: this
-  // SpMM^T when row_shard is one rank, else the ordered reduction (the NCCL
-  // fallback keeps the separate pass)
-  static const bool fuse = [] {  // PK_FUSE_RELU_BWD=0: separate relu_backward pass (A/B)
+  // layer l-1's relu_backward rides on the ordered dF reduction when
+  // row_shard is split (the reduction is NVLink-bound; the mask read is
+  // free there). Inside the SpMM^T epilogue it is measured slower than the
+  // separate streaming pass (C2 1x1x1: 67.3 vs 65.6 ms per epoch — the mask
+  // reads compete with the gathers), so that variant is opt-in.
+  // PK_FUSE_RELU_BWD: 0 = never, 1 = reduction only (default), 2 = also SpMM^T.
+  static const int fuse = [] {
     const char* e = std::getenv("PK_FUSE_RELU_BWD");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 1;
   }();
-  const DMat* act = l > 0 && fuse ? &fout_[l - 1] : nullptr;
-  const bool mask_spmm = act && gr == 1;
+  const DMat* act = l > 0 && fuse > 0 ? &fout_[l - 1] : nullptr;
+  const bool mask_spmm = act && gr == 1 && fuse >= 2;
   const bool mask_reduce = act && gr > 1 && lsa_df;
   pipelined(
       sh.at.rows, comm_chunks(sh.at.rows, lay.row),

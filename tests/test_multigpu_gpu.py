@@ -91,3 +91,12 @@ def test_four_gpu_grids_match_reference(cuda, grid):
 @pytest.mark.parametrize("grid", ["2,2,2", "8,1,1", "1,1,8", "4,1,2"])
 def test_eight_gpu_grids_match_reference(cuda, grid):
     _run(8, "--grid", grid)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("grid", _grids(2))
+def test_two_gpu_relu_backward_in_spmm_epilogue(cuda, grid):
+    """PK_FUSE_RELU_BWD=2: layer l-1's ReLU' applied by the SpMM^T epilogue
+    where row_shard is one rank (opt-in variant), same results."""
+    rep = _run(2, "--grid", grid, env={"PK_FUSE_RELU_BWD": "2"})
+    assert rep["logits_bitwise"]
