@@ -4,20 +4,25 @@
 // The reference multiplies in fp32 with a plain k-ascending loop
 // (kernels.hpp:64-92). TF32 alone (10-bit mantissa) misses the 1e-4
 // normwise budget (~3e-4 per GEMM), so every operand is
-// split x = hi + lo with hi = rna_tf32(x), lo = x - hi, and
+// split x = hi + lo (hi = tf32 part, lo = tf32 of the remainder), and
 //     C = A_lo.B_hi + A_hi.B_lo + A_hi.B_hi
-// accumulated in TMEM (error ~2^-22 relative per product, i.e. fp32-level).
+// accumulated in TMEM (error ~2^-21 relative per product, i.e. fp32-level).
 //
-// Why the big operands are register-staged and not TMA: the split has to
-// happen between HBM and the tensor core. Loader warps read fp32 tiles with
-// 16-B coalesced loads two or three k-stages ahead (across tile boundaries), write hi
-// and lo into swizzled shared-memory tiles — K-major (128-B swizzle) when the
-// source is k-contiguous, MN-major (the 32-B-atom swizzle tf32 needs) when it
-// runs along M/N — and arrive on the stage's mbarrier. The small weight
-// operand of NN / NT is split once per call into per-stage tile images that
-// one thread bulk-copies (cp.async.bulk, TMA engine) into each stage. One
-// elected thread issues the MMAs; epilogue warps drain the double-buffered
-// TMEM accumulator with tcgen05.ld and store rows.
+// Feeding the big operands. The tensor core reads an fp32 operand by
+// truncating it to tf32 (measured, scripts/tf32_round_probe.cu), so a raw
+// fp32 tile already is the "hi" operand of hi = trunc(x), lo = x - hi. TMA
+// (cp.async.bulk.tensor) streams raw tiles straight into swizzled shared
+// memory — K-major with the 128-B swizzle, MN-major in 32-wide atoms with the
+// 128-B/32-B-atom swizzle tf32 needs — and four converter warps derive each
+// stage's lo tile in shared memory (lo = rna_tf32(x - trunc(x))), then fence
+// and release the stage to the MMA. Converters never hold outstanding global
+// loads, so their proxy fence is cheap; the first version staged operands
+// through registers, where every fence waited for the prefetched loads and
+// the pipeline collapsed to ~one stage in flight (kept for unaligned
+// operands, PK_TC_TMA=0). The small weight operand of NN / NT is split once
+// per call into per-stage hi/lo tile images that ride the same TMA barrier
+// (cp.async.bulk). One elected thread issues the MMAs; epilogue warps drain
+// the double-buffered TMEM accumulator with tcgen05.ld and store rows.
 //
 // Persistent CTAs walk a static tile schedule (m tile, n tile, k split). A
 // k split > 1 writes fp32 partials that a deterministic fixed-order reduce
@@ -27,10 +32,12 @@
 //   NN  Q  = H . W        A = H   (K-major tile)  B = W   (pre-split image)
 //   NT  dH = dQ . W^T     A = dQ  (K-major tile)  B = W   (pre-split image)
 //   TN  dW = H^T . dQ     A = H^T (MN-major tile) B = dQ  (MN-major tile)
+#include <cuda.h>  // CUtensorMap (type only; the encoder comes from the runtime's entry point)
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "gemm.cuh"
 #include "pk_common.cuh"
@@ -45,6 +52,7 @@ constexpr int kLoaderWarps = 8;
 constexpr int kMmaWarp = kLoaderWarps;          // warp 8
 constexpr int kThreadsTc = 32 * (kLoaderWarps + 1 + 4);
 constexpr int kLoaderThreads = 32 * kLoaderWarps;
+constexpr int kConvWarps = 4;  // TMA path: warps 4..7 derive the lo tiles
 // k-stages accumulated in TMEM before the epilogue folds the partial into
 // the output with round-to-nearest fp32 adds. The tensor core's fp32
 // accumulation does not round to nearest, so its error grows with the chain
@@ -110,6 +118,16 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, unsign
       : "memory");
 }
 
+// TMA tile loads (tensor maps built on the host per call)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            u64* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<u64>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -145,6 +163,37 @@ __device__ __forceinline__ void tmem_ld8(unsigned taddr, float (&v)[8]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 32 lanes x 32 bit, 16 / 32 consecutive columns per thread, one wait
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, float (&v)[16]) {
+  unsigned r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld32(unsigned taddr, float (&v)[32]) {
+  unsigned r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __device__ __forceinline__ float tf32_rna(float x) {
@@ -247,6 +296,26 @@ __device__ __forceinline__ u64 mnmajor_desc(unsigned base, int kstep) {
   return d | (1ull << 61);  // SWIZZLE_128B_BASE32B
 }
 
+// MN-major tile as TMA writes it: one {32 mn x 32 k} box per 32-wide mn atom,
+// 4 KB each (k row r at r*128, 32-B chunks swizzled in 4-row groups), so
+// mn atoms are 4096 B apart (LBO) and 4-row k groups 512 B (SBO).
+__device__ __forceinline__ u64 mnmajor_tma_desc(unsigned base, int kstep) {
+  u64 d = smem_desc(base + 1024u * kstep, 4096u, 512u);
+  d &= ~(7ull << 61);
+  return d | (1ull << 61);  // SWIZZLE_128B_BASE32B
+}
+
+// lo = x - trunc_tf32(x), rounded to tf32: the tensor core reads an fp32
+// operand by truncating it to tf32 (scripts/tf32_round_probe.cu), so the raw
+// tile itself serves as "hi" and only lo is computed.
+__device__ __forceinline__ float4 lo_of_raw(float4 v) {
+  auto one = [](float x) {
+    const float t = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+    return tf32_rna(x - t);
+  };
+  return make_float4(one(v.x), one(v.y), one(v.z), one(v.w));
+}
+
 // Loader work for one operand tile of ROWS (M/N) x 32 (k) per stage. Each
 // item is one 16-B chunk of the row-major source, stored (split into hi/lo)
 // without any transposition:
@@ -340,21 +409,29 @@ struct TcConfig {
   static constexpr size_t kSmem = static_cast<size_t>(STAGES) * kStage + 1024;
 };
 
-template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE>
-__global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
+// TMA: the big operands arrive by TMA as raw fp32 tiles (the tensor core's
+// own truncation makes them the "hi" operand); four converter warps derive
+// each stage's lo tile from shared memory. Otherwise they are register-staged
+// by eight loader warps (unaligned operands, or PK_TC_TMA=0).
+template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE, bool TMA>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    gemm_tc_kernel(TcParams p, const __grid_constant__ CUtensorMap tma_a,
+                   const __grid_constant__ CUtensorMap tma_b) {
   using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
+  static_assert(!TMA || B_PRE || B_T, "TMA path: a streamed B must be MN-major");
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  __shared__ u64 full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ u64 full[STAGES], empty[STAGES], raw[STAGES], tfull[2], tempty[2];
   __shared__ unsigned tmem_base;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], kLoaderWarps);
+      mbar_init(&full[s], TMA ? kConvWarps : kLoaderWarps);
       mbar_init(&empty[s], 1);
+      mbar_init(&raw[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -374,9 +451,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
   const unsigned tmem = tmem_base;
 
   const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
+  // n tile fastest: the CTAs that share an A row block (several n tiles)
+  // run side by side, so A comes from DRAM once and from L2 after
   auto tile_coords = [&](int t, int& mt, int& nt, int& sp) {
-    mt = t % p.m_tiles;
-    nt = (t / p.m_tiles) % p.n_tiles;
+    nt = t % p.n_tiles;
+    mt = (t / p.n_tiles) % p.m_tiles;
     sp = t / (p.m_tiles * p.n_tiles);
   };
   auto k_range = [&](int sp, i64& kb, i64& ke) {
@@ -384,7 +463,98 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     ke = min(p.k, kb + p.k_chunk);
   };
 
-  if (warp < kLoaderWarps) {
+  // k-stage walk shared by the loaders / producer / converters
+  struct Pos {
+    int t, kk, nk, nt;
+    i64 kb, ke, m0, n0;
+  };
+  auto start = [&](Pos& q, int t) {
+    q.t = t;
+    q.kk = 0;
+    q.nk = 0;
+    while (q.t < total_tiles) {
+      int mt, nt, sp;
+      tile_coords(q.t, mt, nt, sp);
+      k_range(sp, q.kb, q.ke);
+      q.m0 = static_cast<i64>(mt) * kBM;
+      q.nt = nt;
+      q.n0 = static_cast<i64>(nt) * BN;
+      q.nk = static_cast<int>((q.ke - q.kb + kBK - 1) / kBK);
+      if (q.nk > 0) return;
+      q.t += gridDim.x;  // empty k range: the MMA warp signals it without stages
+    }
+  };
+  auto advance = [&](Pos& q) {
+    if (++q.kk == q.nk) start(q, q.t + gridDim.x);
+  };
+  auto valid = [&](const Pos& q) { return q.t < total_tiles; };
+
+  if (TMA && warp < kLoaderWarps) {
+    if constexpr (TMA) {
+      if (warp == 0 && lane == 0) {
+        // ---------------------------------------------------- TMA producer
+        int stage = 0;
+        unsigned phase = 0;
+        Pos q;
+        start(q, blockIdx.x);
+        constexpr unsigned kBytes =
+            Cfg::kTileA + (B_PRE ? 2u * Cfg::kTileB : static_cast<unsigned>(Cfg::kTileB));
+        while (valid(q)) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
+          const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
+          mbar_expect_tx(&raw[stage], kBytes);
+          if constexpr (!A_T) {
+            tma_load_2d(st, &tma_a, static_cast<int>(k0), static_cast<int>(q.m0), &raw[stage]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < kBM / 32; ++a)
+              tma_load_2d(st + a * 4096, &tma_a, static_cast<int>(q.m0 + a * 32),
+                          static_cast<int>(k0), &raw[stage]);
+          }
+          if constexpr (B_PRE) {
+            const i64 g = q.nt * p.b_stages + k0 / kBK;
+            bulk_copy_g2s(st + 2 * Cfg::kTileA, p.b_image + g * 2 * Cfg::kTileB,
+                          2u * Cfg::kTileB, &raw[stage]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < Cfg::kRowsB / 32; ++a)
+              tma_load_2d(st + 2 * Cfg::kTileA + a * 4096, &tma_b,
+                          static_cast<int>(q.n0 + a * 32), static_cast<int>(k0), &raw[stage]);
+          }
+          mbar_arrive(&raw[stage]);
+          advance(q);
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      } else if (warp >= kLoaderWarps - kConvWarps) {
+        // ------------------------------------------------------ converters
+        const int ct = threadIdx.x - 32 * (kLoaderWarps - kConvWarps);
+        int stage = 0;
+        unsigned phase = 0;
+        Pos q;
+        start(q, blockIdx.x);
+        auto convert = [&](unsigned char* src, unsigned char* dst, int bytes) {
+#pragma unroll 4
+          for (int i = ct; i < bytes / 16; i += 32 * kConvWarps) {
+            const float4 v = *reinterpret_cast<const float4*>(src + 16 * i);
+            *reinterpret_cast<float4*>(dst + 16 * i) = lo_of_raw(v);
+          }
+        };
+        while (valid(q)) {
+          mbar_wait(&raw[stage], phase);
+          unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
+          convert(st, st + Cfg::kTileA, Cfg::kTileA);
+          if constexpr (!B_PRE)
+            convert(st + 2 * Cfg::kTileA, st + 2 * Cfg::kTileA + Cfg::kTileB, Cfg::kTileB);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[stage]);
+          advance(q);
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp < kLoaderWarps) {
     // ------------------------------------------------------------ loaders
     // A (and B when it streams) go through registers two k-stages ahead,
     // across tile boundaries, in two alternating register sets; a pre-split
@@ -392,30 +562,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
     const int lt = threadIdx.x;
     int stage = 0;
     unsigned phase = 0;
-    struct Pos {
-      int t, kk, nk, nt;
-      i64 kb, ke, m0, n0;
-    };
-    auto start = [&](Pos& q, int t) {
-      q.t = t;
-      q.kk = 0;
-      q.nk = 0;
-      while (q.t < total_tiles) {
-        int mt, nt, sp;
-        tile_coords(q.t, mt, nt, sp);
-        k_range(sp, q.kb, q.ke);
-        q.m0 = static_cast<i64>(mt) * kBM;
-        q.nt = nt;
-        q.n0 = static_cast<i64>(nt) * BN;
-        q.nk = static_cast<int>((q.ke - q.kb + kBK - 1) / kBK);
-        if (q.nk > 0) return;
-        q.t += gridDim.x;  // empty k range: the MMA warp signals it without stages
-      }
-    };
-    auto advance = [&](Pos& q) {
-      if (++q.kk == q.nk) start(q, q.t + gridDim.x);
-    };
-    auto valid = [&](const Pos& q) { return q.t < total_tiles; };
     constexpr int kRB = B_PRE ? 1 : Cfg::LoadB::kRegs;
     struct Regs {
       float4 a[Cfg::LoadA::kRegs];
@@ -488,6 +634,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
         const unsigned d = tmem + static_cast<unsigned>(acc * Cfg::kAccStride);
         const int k_lo = sg * kSegStages, k_hi = min(nk, k_lo + kSegStages);
         for (int kk = k_lo; kk < k_hi; ++kk) {
+          if constexpr (TMA) mbar_wait(&raw[stage], phase);  // TMA bytes landed
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
@@ -496,10 +643,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
             const unsigned b_hi = base + 2 * Cfg::kTileA, b_lo = b_hi + Cfg::kTileB;
 #pragma unroll
             for (int ks = 0; ks < kBK / 8; ++ks) {
-              const u64 dah = Cfg::LoadA::desc(a_hi, ks), dal = Cfg::LoadA::desc(a_lo, ks);
-              u64 dbh, dbl;
+              u64 dah, dal, dbh, dbl;
+              if constexpr (TMA && A_T) {
+                dah = mnmajor_tma_desc(a_hi, ks), dal = mnmajor_tma_desc(a_lo, ks);
+              } else {
+                dah = Cfg::LoadA::desc(a_hi, ks), dal = Cfg::LoadA::desc(a_lo, ks);
+              }
               if constexpr (B_PRE) {
                 dbh = kmajor_desc(b_hi, ks), dbl = kmajor_desc(b_lo, ks);
+              } else if constexpr (TMA) {
+                dbh = mnmajor_tma_desc(b_hi, ks), dbl = mnmajor_tma_desc(b_lo, ks);
               } else {
                 dbh = Cfg::LoadB::desc(b_hi, ks), dbl = Cfg::LoadB::desc(b_lo, ks);
               }
@@ -552,34 +705,50 @@ __global__ void __launch_bounds__(kThreadsTc, 1) gemm_tc_kernel(TcParams p) {
         tc_fence_after();
         const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) +
                                static_cast<unsigned>(acc * Cfg::kAccStride);
+        // CH columns per step: one TMEM load and, for a later segment, all
+        // CH/4 old-value loads in flight together (RMW latency once per step)
+#ifndef PK_EPI_CH
+#define PK_EPI_CH 8  // measured: 8 beats 32 (11.0 vs 11.7 ms per epoch's GEMMs)
+#endif
+        constexpr int CH = (BN % PK_EPI_CH == 0) ? PK_EPI_CH : (BN % 16 == 0 ? 16 : 8);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 8) {
-          float v[8];
+        for (int c0 = 0; c0 < BN; c0 += CH) {
+          float v[CH];
           if (zero) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[i] = 0.f;
+            for (int i = 0; i < CH; ++i) v[i] = 0.f;
+          } else if constexpr (CH == 32) {
+            tmem_ld32(taddr + static_cast<unsigned>(c0), v);
+          } else if constexpr (CH == 16) {
+            tmem_ld16(taddr + static_cast<unsigned>(c0), v);
           } else {
             tmem_ld8(taddr + static_cast<unsigned>(c0), v);
           }
           if (gm < p.m) {
             float* dst = out + gm * p.ldc + n0 + c0;
             const i64 left = p.n - (n0 + c0);
-            if (vec_out && left >= 8) {
+            if (vec_out && left >= CH) {
               float4* d4 = reinterpret_cast<float4*>(dst);
               if (sg > 0) {
-                const float4 a = d4[0], b = d4[1];
-                v[0] += a.x, v[1] += a.y, v[2] += a.z, v[3] += a.w;
-                v[4] += b.x, v[5] += b.y, v[6] += b.z, v[7] += b.w;
+                float4 o[CH / 4];
+#pragma unroll
+                for (int j = 0; j < CH / 4; ++j) o[j] = d4[j];
+#pragma unroll
+                for (int j = 0; j < CH / 4; ++j) {
+                  v[4 * j] += o[j].x, v[4 * j + 1] += o[j].y;
+                  v[4 * j + 2] += o[j].z, v[4 * j + 3] += o[j].w;
+                }
               }
               if (relu) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+                for (int i = 0; i < CH; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
               }
-              d4[0] = make_float4(v[0], v[1], v[2], v[3]);
-              d4[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+              for (int j = 0; j < CH / 4; ++j)
+                d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             } else {
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
+              for (int i = 0; i < CH; ++i)
                 if (i < left) {
                   const float x = sg > 0 ? dst[i] + v[i] : v[i];
                   dst[i] = relu ? (x > 0.f ? x : 0.f) : x;
@@ -646,17 +815,71 @@ __global__ void tc_split_reduce_kernel(const float* __restrict__ part, int split
   c[i * ldc + j] = relu ? (s > 0.f ? s : 0.f) : s;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link). fp32 row-major operand `rows x cols` (cols contiguous, ld elements),
+// box {32 cols, box_rows}, zero fill out of bounds.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static const EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const float* base, i64 rows, i64 cols, i64 ld, int box_rows,
+              bool mn_major) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+  const cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PK_TC_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <bool A_T, bool B_T, int BN, bool B_PRE>
 void launch_bn(const TcParams& p0, cudaStream_t st) {
   constexpr int kStageBytes = TcConfig<A_T, B_T, BN, 1, B_PRE>::kStage;
   constexpr int STAGES = std::min(6, std::max(2, (200 * 1024) / kStageBytes));
   using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
-  auto kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE>;
-  static thread_local bool attr = false;
-  if (!attr) {
+  // TMA maps: K-major A {k, m} box {32, 128}; MN-major A {m, k} / B {n, k}
+  // box {32, 32} per 32-wide atom. Needs 16-B aligned bases and ld % 4 == 0.
+  CUtensorMap map_a, map_b;
+  std::memset(&map_a, 0, sizeof(map_a));
+  std::memset(&map_b, 0, sizeof(map_b));
+  bool tma = tma_enabled() && p0.a.vec && (B_PRE || p0.b.vec);
+  if (tma)
+    tma = A_T ? make_map(&map_a, p0.a.p, p0.k, p0.a.mn, p0.a.ld, 32, true)
+              : make_map(&map_a, p0.a.p, p0.a.mn, p0.k, p0.a.ld, kBM, false);
+  if (tma && !B_PRE) tma = make_map(&map_b, p0.b.p, p0.k, p0.b.mn, p0.b.ld, 32, true);
+  auto kernel = tma ? gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true>
+                    : gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, false>;
+  static thread_local bool attr[2] = {false, false};
+  if (!attr[tma]) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Cfg::kSmem)));
-    attr = true;
+    attr[tma] = true;
   }
   TcParams p = p0;
   if (B_PRE) {
@@ -673,7 +896,7 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
   }
   const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles * p.splits;
   const int grid = static_cast<int>(std::min<i64>(tiles, sm_count()));
-  kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p);
+  kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p, map_a, map_b);
   PK_LAUNCH("gemm tcgen05 kernel");
 }
 
@@ -717,11 +940,20 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
   // TN tile width (both operands stream through registers): PK_TN_BN caps it
   // for experiments; default 128 (measured faster than 256: two register
   // sets of 128-wide tiles fit without spills)
+  // TMA-fed TN holds no operand registers: 256-wide tiles (each H row block
+  // read once) measured 2.1 vs 2.8 ms for the 256x256 dW
   static const int tn_cap = [] {
     const char* e = std::getenv("PK_TN_BN");
-    return e ? std::atoi(e) : 128;
+    return e ? std::atoi(e) : 0;
   }();
-  const int bn = (ta && !tb) ? pick_bn(std::min<i64>(n, tn_cap)) : pick_bn(n);
+  const bool tn_tma = tma_enabled() && aligned16(a, lda) && aligned16(b, ldb);
+  const int tn_width = tn_cap > 0 ? tn_cap : (tn_tma ? 256 : 128);
+  static const int nn_cap = [] {  // NN / NT tile width cap (experiments)
+    const char* e = std::getenv("PK_NN_BN");
+    return e ? std::atoi(e) : 256;
+  }();
+  const int bn =
+      (ta && !tb) ? pick_bn(std::min<i64>(n, tn_width)) : pick_bn(std::min<i64>(n, nn_cap));
   p.m_tiles = static_cast<int>((m + kBM - 1) / kBM);
   p.n_tiles = static_cast<int>((n + bn - 1) / bn);
   const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles;
