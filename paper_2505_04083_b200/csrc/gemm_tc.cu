@@ -128,6 +128,33 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// bulk copy into the same smem offset of every CTA in `mask`, completing
+// `bytes` on each one's barrier at `bar`'s offset
+__device__ __forceinline__ void bulk_copy_g2s_mc(void* dst, const void* src, unsigned bytes,
+                                                 u64* bar, unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(u64* bar, unsigned short mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -413,12 +440,22 @@ struct TcConfig {
 // own truncation makes them the "hi" operand); four converter warps derive
 // each stage's lo tile from shared memory. Otherwise they are register-staged
 // by eight loader warps (unaligned operands, or PK_TC_TMA=0).
-template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE, bool TMA>
+// CS > 1 (TMA + pre-split B, one n tile, no k split): clusters of CS CTAs
+// on consecutive m tiles share each stage's weight image — every CTA bulk-
+// copies 1/CS of it multicast into all CTAs of the cluster, and a stage is
+// refilled only when every CTA's MMAs are done with it (commit multicast to
+// all `empty` barriers). The weight's L2 -> SM traffic drops CS-fold. A CTA
+// whose own tile runs past the end follows its cluster through a phantom
+// tile (A zero-filled by TMA, nothing stored).
+template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE, bool TMA, int CS>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     gemm_tc_kernel(TcParams p, const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b) {
   using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
   static_assert(!TMA || B_PRE || B_T, "TMA path: a streamed B must be MN-major");
+  static_assert(CS == 1 || (TMA && B_PRE), "clusters need the TMA + weight-image path");
+  constexpr unsigned short kMask = static_cast<unsigned short>((1u << CS) - 1u);
+  const int crank = CS > 1 ? static_cast<int>(cluster_rank()) : 0;
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -430,7 +467,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], TMA ? kConvWarps : kLoaderWarps);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);  // every cluster CTA's MMAs release the stage
       mbar_init(&raw[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -447,13 +484,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const unsigned tmem = tmem_base;
 
   const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
+  // a tile index is live while its cluster leader's is (phantoms beyond)
+  auto live = [&](int t) { return t - crank < total_tiles; };
   // n tile fastest: the CTAs that share an A row block (several n tiles)
   // run side by side, so A comes from DRAM once and from L2 after
   auto tile_coords = [&](int t, int& mt, int& nt, int& sp) {
+    if (CS > 1 && t >= total_tiles) {  // phantom: past the last m tile
+      mt = p.m_tiles, nt = 0, sp = 0;
+      return;
+    }
     nt = t % p.n_tiles;
     mt = (t / p.n_tiles) % p.m_tiles;
     sp = t / (p.m_tiles * p.n_tiles);
@@ -472,7 +516,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     q.t = t;
     q.kk = 0;
     q.nk = 0;
-    while (q.t < total_tiles) {
+    while (live(q.t)) {
       int mt, nt, sp;
       tile_coords(q.t, mt, nt, sp);
       k_range(sp, q.kb, q.ke);
@@ -487,7 +531,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   auto advance = [&](Pos& q) {
     if (++q.kk == q.nk) start(q, q.t + gridDim.x);
   };
-  auto valid = [&](const Pos& q) { return q.t < total_tiles; };
+  auto valid = [&](const Pos& q) { return live(q.t); };
 
   if (TMA && warp < kLoaderWarps) {
     if constexpr (TMA) {
@@ -514,8 +558,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
           if constexpr (B_PRE) {
             const i64 g = q.nt * p.b_stages + k0 / kBK;
-            bulk_copy_g2s(st + 2 * Cfg::kTileA, p.b_image + g * 2 * Cfg::kTileB,
-                          2u * Cfg::kTileB, &raw[stage]);
+            if constexpr (CS > 1) {
+              constexpr unsigned kPiece = 2u * Cfg::kTileB / CS;
+              bulk_copy_g2s_mc(st + 2 * Cfg::kTileA + crank * kPiece,
+                               p.b_image + g * 2 * Cfg::kTileB + crank * kPiece, kPiece,
+                               &raw[stage], kMask);
+            } else {
+              bulk_copy_g2s(st + 2 * Cfg::kTileA, p.b_image + g * 2 * Cfg::kTileB,
+                            2u * Cfg::kTileB, &raw[stage]);
+            }
           } else {
 #pragma unroll
             for (int a = 0; a < Cfg::kRowsB / 32; ++a)
@@ -621,7 +672,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     unsigned phase = 0;
     int acc = 0;
     unsigned acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; live(t); t += gridDim.x) {
       int mt, nt, sp;
       tile_coords(t, mt, nt, sp);
       i64 kb, ke;
@@ -661,7 +712,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               tc_mma_tf32(d, dah, dbl, idesc, 1u);
               tc_mma_tf32(d, dah, dbh, idesc, 1u);
             }
-            tc_commit(&empty[stage]);  // frees the smem stage when the MMAs finish
+            // frees the smem stage (in every cluster CTA) when the MMAs finish
+            if constexpr (CS > 1)
+              tc_commit_mc(&empty[stage], kMask);
+            else
+              tc_commit(&empty[stage]);
           }
           __syncwarp();
           if (++stage == STAGES) stage = 0, phase ^= 1u;
@@ -684,7 +739,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int row = quad * 32 + lane;
     int acc = 0;
     unsigned acc_phase = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; live(t); t += gridDim.x) {
       int mt, nt, sp;
       tile_coords(t, mt, nt, sp);
       i64 kb, ke;
@@ -766,6 +821,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -873,13 +929,35 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     tma = A_T ? make_map(&map_a, p0.a.p, p0.k, p0.a.mn, p0.a.ld, 32, true)
               : make_map(&map_a, p0.a.p, p0.a.mn, p0.k, p0.a.ld, kBM, false);
   if (tma && !B_PRE) tma = make_map(&map_b, p0.b.p, p0.k, p0.b.mn, p0.b.ld, 32, true);
-  auto kernel = tma ? gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true>
-                    : gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, false>;
-  static thread_local bool attr[2] = {false, false};
-  if (!attr[tma]) {
+  // weight-image multicast across a cluster of CS CTAs (PK_TC_CLUSTER)
+  static const int cluster_pref = [] {
+    const char* e = std::getenv("PK_TC_CLUSTER");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 4 ? 4 : (v >= 2 ? 2 : 1);
+  }();
+  int cs = 1;
+  if (B_PRE && tma && p0.n_tiles == 1 && p0.splits == 1)
+    while (cs < cluster_pref && p0.m_tiles >= 4 * cs * 2) cs *= 2;
+  using KernelT = void (*)(TcParams, const CUtensorMap, const CUtensorMap);
+  KernelT kernel;
+  int variant;
+  if (!tma) {
+    kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, false, 1>, variant = 0;
+  } else if constexpr (B_PRE) {
+    if (cs == 4)
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 4>, variant = 3;
+    else if (cs == 2)
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 2>, variant = 2;
+    else
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 1>, variant = 1;
+  } else {
+    kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 1>, variant = 1;
+  }
+  static thread_local bool attr[4] = {false, false, false, false};
+  if (!attr[variant]) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Cfg::kSmem)));
-    attr[tma] = true;
+    attr[variant] = true;
   }
   TcParams p = p0;
   if (B_PRE) {
@@ -895,8 +973,25 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     p.b_image = img.p;
   }
   const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles * p.splits;
-  const int grid = static_cast<int>(std::min<i64>(tiles, sm_count()));
-  kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p, map_a, map_b);
+  int grid = static_cast<int>(std::min<i64>(tiles, sm_count()));
+  if (cs > 1) {
+    grid = std::max(cs, grid / cs * cs);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreadsTc);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = static_cast<unsigned>(cs);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PK_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, map_a, map_b));
+  } else {
+    kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p, map_a, map_b);
+  }
   PK_LAUNCH("gemm tcgen05 kernel");
 }
 

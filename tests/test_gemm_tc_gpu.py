@@ -130,3 +130,31 @@ def test_gemm_relu_fused_equals_gemm_then_relu(cuda, m, n, kk, mode):
     want = k.relu_forward(plain)
     assert torch.equal(fused.view(torch.int32), want.view(torch.int32))
     assert (fused >= 0).all() and (fused == 0).any()
+
+
+def _variant(tmp_path, name, env):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / f"{name}.npz"
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "mp", "gemm_variant_worker.py"),
+                        str(out), root], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    return dict(np.load(out))
+
+
+def test_gemm_cluster_multicast_matches_single_cta(cuda, tmp_path):
+    """Weight-image multicast across 2- and 4-CTA clusters (with phantom
+    tiles: 149 and 37 m tiles) gives the single-CTA results bit for bit; the
+    register-staged fallback (PK_TC_TMA=0) stays within the 3xTF32 bound."""
+    one = _variant(tmp_path, "cs1", {"PK_TC_CLUSTER": "1"})
+    for cs in ("2", "4"):
+        got = _variant(tmp_path, "cs" + cs, {"PK_TC_CLUSTER": cs})
+        for key in one:
+            assert np.array_equal(got[key].view(np.uint32), one[key].view(np.uint32)), (cs, key)
+    reg = _variant(tmp_path, "reg", {"PK_TC_TMA": "0"})
+    for key in one:
+        den = np.linalg.norm(one[key].astype(np.float64)) or 1.0
+        assert np.linalg.norm(reg[key].astype(np.float64) - one[key]) / den <= 2e-6, key
