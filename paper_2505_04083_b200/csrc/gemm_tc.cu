@@ -62,6 +62,23 @@ constexpr int kSegStages = 16;
 
 __device__ unsigned g_gemm_watchdog = 0;
 
+// PK_TC_PROF builds (scripts/tc_prof.sh): cycles each role spends in its
+// barrier waits, summed over threads and CTAs — 0 producer/empty, 1
+// converters/raw (x128 threads), 2 MMA warp/raw, 6 MMA warp/full (x32), 3 MMA
+// warp/tempty (x32), 4 epilogue/tfull (x128); 5 kernel cycles (thread 0 of
+// every CTA); 7 stages issued.
+#ifdef PK_TC_PROF
+__device__ unsigned long long g_tc_prof[8];
+#define TC_PROF_WAIT(slot, call)                                  \
+  do {                                                            \
+    const long long t0_ = clock64();                              \
+    call;                                                         \
+    atomicAdd(&g_tc_prof[slot], (unsigned long long)(clock64() - t0_)); \
+  } while (0)
+#else
+#define TC_PROF_WAIT(slot, call) call
+#endif
+
 // ---------------------------------------------------------------- PTX glue
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -456,6 +473,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   static_assert(CS == 1 || (TMA && B_PRE), "clusters need the TMA + weight-image path");
   constexpr unsigned short kMask = static_cast<unsigned short>((1u << CS) - 1u);
   const int crank = CS > 1 ? static_cast<int>(cluster_rank()) : 0;
+#ifdef PK_TC_PROF
+  const long long t_kernel = clock64();
+#endif
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -544,7 +564,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         constexpr unsigned kBytes =
             Cfg::kTileA + (B_PRE ? 2u * Cfg::kTileB : static_cast<unsigned>(Cfg::kTileB));
         while (valid(q)) {
-          mbar_wait(&empty[stage], phase ^ 1u);
+          TC_PROF_WAIT(0, mbar_wait(&empty[stage], phase ^ 1u));
           unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
           const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
           mbar_expect_tx(&raw[stage], kBytes);
@@ -584,15 +604,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         unsigned phase = 0;
         Pos q;
         start(q, blockIdx.x);
+        // shared-window addresses: explicit ld/st.shared (generic pointers
+        // compiled to generic LD/ST, measured as the converters' stall)
+        // Batches of 4 chunks per thread: four loads in flight, then the
+        // math and four stores.
         auto convert = [&](unsigned char* src, unsigned char* dst, int bytes) {
-#pragma unroll 4
-          for (int i = ct; i < bytes / 16; i += 32 * kConvWarps) {
-            const float4 v = *reinterpret_cast<const float4*>(src + 16 * i);
-            *reinterpret_cast<float4*>(dst + 16 * i) = lo_of_raw(v);
+          const unsigned s0 = smem_u32(src), d0 = smem_u32(dst);
+          constexpr int kStep = 32 * kConvWarps;
+          for (int i0 = ct; i0 < bytes / 16; i0 += 4 * kStep) {
+            float4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = i0 + j * kStep;
+              if (i < bytes / 16)
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
+                             : "r"(s0 + 16u * i));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = i0 + j * kStep;
+              if (i < bytes / 16) {
+                const float4 l = lo_of_raw(v[j]);
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d0 + 16u * i),
+                             "f"(l.x), "f"(l.y), "f"(l.z), "f"(l.w)
+                             : "memory");
+              }
+            }
           }
         };
         while (valid(q)) {
-          mbar_wait(&raw[stage], phase);
+          TC_PROF_WAIT(1, mbar_wait(&raw[stage], phase));
           unsigned char* st = smem + static_cast<size_t>(stage) * Cfg::kStage;
           convert(st, st + Cfg::kTileA, Cfg::kTileA);
           if constexpr (!B_PRE)
@@ -680,13 +722,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const int nk = static_cast<int>((ke - kb + kBK - 1) / kBK);
       const int nseg = nk == 0 ? 1 : (nk + kSegStages - 1) / kSegStages;
       for (int sg = 0; sg < nseg; ++sg) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1u);
+        TC_PROF_WAIT(3, mbar_wait(&tempty[acc], acc_phase ^ 1u));
         tc_fence_after();
         const unsigned d = tmem + static_cast<unsigned>(acc * Cfg::kAccStride);
         const int k_lo = sg * kSegStages, k_hi = min(nk, k_lo + kSegStages);
         for (int kk = k_lo; kk < k_hi; ++kk) {
-          if constexpr (TMA) mbar_wait(&raw[stage], phase);  // TMA bytes landed
-          mbar_wait(&full[stage], phase);
+          if constexpr (TMA) TC_PROF_WAIT(2, mbar_wait(&raw[stage], phase));  // TMA landed
+          TC_PROF_WAIT(6, mbar_wait(&full[stage], phase));
           tc_fence_after();
           if (lane == 0) {
             const unsigned base = smem_u32(smem + static_cast<size_t>(stage) * Cfg::kStage);
@@ -712,6 +754,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               tc_mma_tf32(d, dah, dbl, idesc, 1u);
               tc_mma_tf32(d, dah, dbh, idesc, 1u);
             }
+#ifdef PK_TC_PROF
+            atomicAdd(&g_tc_prof[7], 1ull);
+#endif
             // frees the smem stage (in every cluster CTA) when the MMAs finish
             if constexpr (CS > 1)
               tc_commit_mc(&empty[stage], kMask);
@@ -756,7 +801,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       for (int sg = 0; sg < nseg; ++sg) {
         const bool zero = nk == 0;
         const bool relu = p.relu && p.splits == 1 && sg == nseg - 1;
-        mbar_wait(&tfull[acc], acc_phase);
+        TC_PROF_WAIT(4, mbar_wait(&tfull[acc], acc_phase));
         tc_fence_after();
         const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) +
                                static_cast<unsigned>(acc * Cfg::kAccStride);
@@ -821,6 +866,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 
   tc_fence_before();
   __syncthreads();
+#ifdef PK_TC_PROF
+  if (threadIdx.x == 0) atomicAdd(&g_tc_prof[5], (unsigned long long)(clock64() - t_kernel));
+#endif
   if constexpr (CS > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
   if (warp == kMmaWarp) {
     tc_fence_after();
@@ -1089,3 +1137,14 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
 }
 
 }  // namespace pk
+
+#ifdef PK_TC_PROF
+extern "C" int pk_tc_prof(unsigned long long* out8, int reset) {
+  cudaMemcpyFromSymbol(out8, pk::g_tc_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(pk::g_tc_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
