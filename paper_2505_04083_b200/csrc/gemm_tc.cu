@@ -52,7 +52,13 @@ constexpr int kLoaderWarps = 8;
 constexpr int kMmaWarp = kLoaderWarps;          // warp 8
 constexpr int kThreadsTc = 32 * (kLoaderWarps + 1 + 4);
 constexpr int kLoaderThreads = 32 * kLoaderWarps;
-constexpr int kConvWarps = 4;  // TMA path: warps 4..7 derive the lo tiles
+#ifndef PK_CONV_WARPS
+#define PK_CONV_WARPS 7
+#endif
+// TMA path: warps 8-PK_CONV_WARPS..7 derive the lo tiles (warp 0 lane 0 is
+// the TMA producer)
+constexpr int kConvWarps = PK_CONV_WARPS;
+static_assert(kConvWarps >= 1 && kConvWarps <= kLoaderWarps - 1, "converter warps");
 // k-stages accumulated in TMEM before the epilogue folds the partial into
 // the output with round-to-nearest fp32 adds. The tensor core's fp32
 // accumulation does not round to nearest, so its error grows with the chain
@@ -63,17 +69,16 @@ constexpr int kSegStages = 16;
 __device__ unsigned g_gemm_watchdog = 0;
 
 // PK_TC_PROF builds (scripts/tc_prof.sh): cycles each role spends in its
-// barrier waits, summed over threads and CTAs — 0 producer/empty, 1
-// converters/raw (x128 threads), 2 MMA warp/raw, 6 MMA warp/full (x32), 3 MMA
-// warp/tempty (x32), 4 epilogue/tfull (x128); 5 kernel cycles (thread 0 of
-// every CTA); 7 stages issued.
+// barrier waits, lane 0 of each warp, summed over CTAs — 0 producer/empty,
+// 1 converters/raw (x4 warps), 2 MMA/raw, 6 MMA/full, 3 MMA/tempty, 4
+// epilogue/tfull (x4 warps); 5 kernel cycles (thread 0); 7 stages issued.
 #ifdef PK_TC_PROF
 __device__ unsigned long long g_tc_prof[8];
-#define TC_PROF_WAIT(slot, call)                                  \
-  do {                                                            \
-    const long long t0_ = clock64();                              \
-    call;                                                         \
-    atomicAdd(&g_tc_prof[slot], (unsigned long long)(clock64() - t0_)); \
+#define TC_PROF_WAIT(slot, call)          \
+  do {                                    \
+    const long long t0_ = clock64();      \
+    call;                                 \
+    prof_acc[slot] += clock64() - t0_;    \
   } while (0)
 #else
 #define TC_PROF_WAIT(slot, call) call
@@ -475,6 +480,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int crank = CS > 1 ? static_cast<int>(cluster_rank()) : 0;
 #ifdef PK_TC_PROF
   const long long t_kernel = clock64();
+  long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   extern __shared__ unsigned char smem_raw[];
   // 1024-B alignment for the swizzle atoms
@@ -755,7 +761,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               tc_mma_tf32(d, dah, dbh, idesc, 1u);
             }
 #ifdef PK_TC_PROF
-            atomicAdd(&g_tc_prof[7], 1ull);
+            prof_acc[7] += 1;
 #endif
             // frees the smem stage (in every cluster CTA) when the MMAs finish
             if constexpr (CS > 1)
@@ -867,7 +873,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   tc_fence_before();
   __syncthreads();
 #ifdef PK_TC_PROF
-  if (threadIdx.x == 0) atomicAdd(&g_tc_prof[5], (unsigned long long)(clock64() - t_kernel));
+  if (threadIdx.x == 0) prof_acc[5] = clock64() - t_kernel;
+  if (lane == 0)  // one sample per warp (lane 0 waits like its warp)
+    for (int i = 0; i < 8; ++i)
+      if (prof_acc[i]) atomicAdd(&g_tc_prof[i], static_cast<unsigned long long>(prof_acc[i]));
 #endif
   if constexpr (CS > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
   if (warp == kMmaWarp) {

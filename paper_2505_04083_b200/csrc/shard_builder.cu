@@ -132,6 +132,11 @@ void counts_to_row_ptr(u64* counts, i64 len, u64* row_ptr, cudaStream_t st) {
   }, st);
 }
 
+__global__ void rebase_row_ptr(const u64* rp, i64 count, u64 base, u64* out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < count) out[i] = rp[i] - base;
+}
+
 __global__ void block_flags(const u32* ci, u64 n, u32 c0, u32 c1, u32* flags) {
   for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<u64>(gridDim.x) * blockDim.x)
@@ -241,6 +246,22 @@ void csr_block(const pk_csr& a, i64 r0, i64 r1, i64 c0, i64 c1, pk_csr_owned* ou
   PK_CUDA(cudaMemcpyAsync(&e, a.row_ptr + r1, sizeof(u64), cudaMemcpyDeviceToHost, st));
   PK_CUDA(cudaStreamSynchronize(st));
   const u64 n = e - b;
+  if (c0 == 0 && c1 == a.cols) {
+    // every column kept (the inner axis is one rank): a row range is a plain
+    // copy with the row pointers rebased
+    alloc_owned(out, r1 - r0, c1 - c0, n);
+    rebase_row_ptr<<<grid_for(r1 - r0 + 1), 256, 0, st>>>(a.row_ptr + r0, r1 - r0 + 1, b,
+                                                          out->row_ptr);
+    PK_LAUNCH("block row_ptr rebase");
+    if (n) {
+      PK_CUDA(cudaMemcpyAsync(out->col_idx, a.col_idx + b, n * sizeof(u32),
+                              cudaMemcpyDeviceToDevice, st));
+      PK_CUDA(cudaMemcpyAsync(out->values, a.values + b, n * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
+    }
+    PK_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   DevBuf<u32> flags(n ? n : 1);
   DevBuf<u64> pos(n + 1);
   u64 total = 0;

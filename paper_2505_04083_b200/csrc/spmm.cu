@@ -947,7 +947,8 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
       return cub::DeviceSelect::Flagged(t, b, src, flags, tmp.p, count.p, n, st);
     }, st);
     i64 c = 0;
-    PK_CUDA(cudaMemcpy(&c, count.p, sizeof(i64), cudaMemcpyDeviceToHost));
+    PK_CUDA(cudaMemcpyAsync(&c, count.p, sizeof(i64), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
     out.alloc(std::max<i64>(c, 1));
     if (c)
       PK_CUDA(cudaMemcpyAsync(out.p, tmp.p, c * sizeof(u32), cudaMemcpyDeviceToDevice, st));

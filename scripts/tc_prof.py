@@ -16,8 +16,11 @@ shapes = [("NN", N, 256, 100), ("TN", 100, 256, N), ("NT", N, 100, 256), ("NN", 
           ("TN", 256, 256, N), ("NN", N, 47, 256), ("TN", 256, 47, N), ("NT", N, 256, 47)]
 for form, m, n, kk in shapes:
     ta, tb = form[0] == "T", form[1] == "T"
-    a = torch.rand((kk, m) if ta else (m, kk), device="cuda")
-    b = torch.rand((n, kk) if tb else (kk, n), device="cuda")
+    # padded leading dimensions like the engine's buffers (16-B rows)
+    def mat(r, c):
+        return torch.rand((r, (c + 3) // 4 * 4), device="cuda")[:, :c]
+    a = mat(kk, m) if ta else mat(m, kk)
+    b = mat(n, kk) if tb else mat(kk, n)
     out = torch.empty(m, n, device="cuda")
     k.gemm(a, b, ta, tb, mode=k.PK_MODE_FAST, out=out)
     torch.cuda.synchronize()
@@ -37,6 +40,6 @@ for form, m, n, kk in shapes:
         return f"{100 * x / kern:5.1f}%" if kern else "-"
     print(f"{form} m={m} n={n} k={kk}: {e0.elapsed_time(e1):.3f} ms, stages/CTA {stages:.0f}, "
           f"cyc/stage {kern / max(stages, 1):.0f} | waits per CTA: producer/empty {pct(v[0] / ctas)}"
-          f" conv/raw {pct(v[1] / ctas / 128)} mma/raw {pct(v[2] / ctas / 32)}"
-          f" mma/full {pct(v[6] / ctas / 32)} mma/tempty {pct(v[3] / ctas / 32)}"
-          f" epi/tfull {pct(v[4] / ctas / 128)}", flush=True)
+          f" conv/raw {pct(v[1] / ctas / int(os.environ.get("CONV", "7")))} mma/raw {pct(v[2] / ctas)}"
+          f" mma/full {pct(v[6] / ctas)} mma/tempty {pct(v[3] / ctas)}"
+          f" epi/tfull {pct(v[4] / ctas / 4)}", flush=True)

@@ -93,9 +93,11 @@ def test_csr_transpose_and_block_bitwise(cuda):
     rows, cols, _ = a_ref.info()
     a = _k().DeviceCsr.from_host(rows, cols, *a_ref.arrays())
     assert_csr_equal(_g().csr_transpose(a), a_ref.transpose().arrays())
-    for _ in range(6):
-        r0, r1 = sorted(rng.integers(0, rows + 1, size=2))
-        c0, c1 = sorted(rng.integers(0, cols + 1, size=2))
+    ranges = [tuple(sorted(rng.integers(0, rows + 1, size=2))) +
+              tuple(sorted(rng.integers(0, cols + 1, size=2))) for _ in range(6)]
+    # all columns (the row-range copy path), whole matrix, empty row range
+    ranges += [(0, rows, 0, cols), (17, 700, 0, cols), (5, 5, 0, cols)]
+    for r0, r1, c0, c1 in ranges:
         blk = _g().csr_block(a, int(r0), int(r1), int(c0), int(c1))
         want = a_ref.block(int(r0), int(r1), int(c0), int(c1))
         assert_csr_equal(blk, want.arrays())
