@@ -828,13 +828,50 @@ unsigned blocks_for(i64 n, int per = 256) {
   return static_cast<unsigned>(std::max<i64>(1, std::min<i64>((n + per - 1) / per, 1 << 16)));
 }
 
+// Device scratch for plan construction: one buffer per host thread, grown to
+// the largest plan's need and kept, bump-allocated. Building a plan then
+// allocates only the plan's own arrays — the ~15 cudaMalloc/cudaFree pairs
+// of temporaries per plan were most of the engine's load time.
+class Scratch {
+ public:
+  static Scratch& get() {
+    static thread_local Scratch s;
+    return s;
+  }
+  void reset(size_t reserve) {
+    extra_.clear();
+    if (buf_.n < reserve) buf_.alloc(reserve);
+    off_ = 0;
+  }
+  template <typename T>
+  T* take(size_t count) {
+    const size_t b = (std::max<size_t>(count, 1) * sizeof(T) + 255) / 256 * 256;
+    if (off_ + b > buf_.n) {  // beyond the reservation: a dedicated buffer until reset
+      extra_.emplace_back(b);
+      return reinterpret_cast<T*>(extra_.back().p);
+    }
+    T* p = reinterpret_cast<T*>(buf_.p + off_);
+    off_ += b;
+    return p;
+  }
+  size_t mark() const { return off_; }
+  void release_to(size_t m) { off_ = m; }
+
+ private:
+  DevBuf<unsigned char> buf_;
+  size_t off_ = 0;
+  std::vector<DevBuf<unsigned char>> extra_;
+};
+
 template <typename F>
 void cub_run(F&& f, cudaStream_t st) {
   size_t bytes = 0;
   PK_CUDA(f(nullptr, bytes));
-  DevBuf<unsigned char> tmp(std::max<size_t>(bytes, 1));
-  PK_CUDA(f(tmp.p, bytes));
-  PK_CUDA(cudaStreamSynchronize(st));  // tmp is released at scope exit
+  Scratch& sc = Scratch::get();
+  const size_t m = sc.mark();
+  PK_CUDA(f(sc.take<unsigned char>(bytes), bytes));
+  PK_CUDA(cudaStreamSynchronize(st));
+  sc.release_to(m);
 }
 
 // first index in sorted device array [0, n) with value >= key
@@ -922,14 +959,24 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
   const u64 avg = a.nnz / std::max<i64>(1, a.rows);
   plan.threshold = threshold ? threshold : std::max<u64>(4096, 64 * avg);
   const i64 n = a.rows;
-  DevBuf<u64> ents(n), hsegs(n), ent_off(n + 1), hseg_off(n + 1);
-  DevBuf<u8> is_empty(n), is_hub(n);
-  DevBuf<u32> ids(n);
-  DevBuf<i64> count(1);
+  // temporaries (scratch): per-row tables, flags, ids, select output, entry
+  // lengths (<= rows + segments), column degrees, cub workspaces
+  Scratch& sc = Scratch::get();
+  const u64 seg_bound = segment ? a.nnz / segment + 1 : 0;
+  sc.reset(static_cast<size_t>(n) * 72 + (n + seg_bound) * 8 + static_cast<size_t>(a.cols) * 4 +
+           (64u << 20));
+  u64* ents = sc.take<u64>(n);
+  u64* hsegs = sc.take<u64>(n);
+  u64* ent_off = sc.take<u64>(n + 1);
+  u64* hseg_off = sc.take<u64>(n + 1);
+  u8* is_empty = sc.take<u8>(n);
+  u8* is_hub = sc.take<u8>(n);
+  u32* ids = sc.take<u32>(n);
+  i64* count = sc.take<i64>(1);
   classify_rows_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, plan.threshold, segment,
-                                                       ents.p, hsegs.p, is_empty.p, is_hub.p);
+                                                       ents, hsegs, is_empty, is_hub);
   PK_LAUNCH("spmm plan classify");
-  iota_rows_kernel<<<blocks_for(n), 256, 0, st>>>(ids.p, n);
+  iota_rows_kernel<<<blocks_for(n), 256, 0, st>>>(ids, n);
   PK_LAUNCH("spmm plan iota");
   auto exclusive_scan = [&](const u64* in, u64* out) {  // out[0..n], out[n] = total
     PK_CUDA(cudaMemsetAsync(out, 0, sizeof(u64), st));
@@ -941,24 +988,25 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
     PK_CUDA(cudaStreamSynchronize(st));
     return total;
   };
+  u32* sel_tmp = sc.take<u32>(n);
   auto select = [&](const u32* src, const u8* flags, DevBuf<u32>& out) {
-    DevBuf<u32> tmp(n);
+    u32* tmp = sel_tmp;
     cub_run([&](void* t, size_t& b) {
-      return cub::DeviceSelect::Flagged(t, b, src, flags, tmp.p, count.p, n, st);
+      return cub::DeviceSelect::Flagged(t, b, src, flags, tmp, count, n, st);
     }, st);
     i64 c = 0;
-    PK_CUDA(cudaMemcpyAsync(&c, count.p, sizeof(i64), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaMemcpyAsync(&c, count, sizeof(i64), cudaMemcpyDeviceToHost, st));
     PK_CUDA(cudaStreamSynchronize(st));
     out.alloc(std::max<i64>(c, 1));
     if (c)
-      PK_CUDA(cudaMemcpyAsync(out.p, tmp.p, c * sizeof(u32), cudaMemcpyDeviceToDevice, st));
+      PK_CUDA(cudaMemcpyAsync(out.p, tmp, c * sizeof(u32), cudaMemcpyDeviceToDevice, st));
     return c;
   };
-  plan.entries = static_cast<i64>(exclusive_scan(ents.p, ent_off.p));
-  plan.segments = exclusive_scan(hsegs.p, hseg_off.p);
-  plan.empty = select(ids.p, is_empty.p, plan.empty_rows);
+  plan.entries = static_cast<i64>(exclusive_scan(ents, ent_off));
+  plan.segments = exclusive_scan(hsegs, hseg_off);
+  plan.empty = select(ids, is_empty, plan.empty_rows);
   DevBuf<u32> hubs32;
-  const i64 nh = select(ids.p, is_hub.p, hubs32);
+  const i64 nh = select(ids, is_hub, hubs32);
   plan.hub_count = static_cast<int>(nh);
   // entries: row key, store target, length -> offsets
   const i64 E = std::max<i64>(plan.entries, 1);
@@ -966,15 +1014,15 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
   plan.rl.alloc(E);
   plan.rpc.alloc(plan.entries + 1);
   {
-    DevBuf<u64> elen(E);
-    fill_entries_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, segment, ents.p, ent_off.p,
-                                                       hsegs.p, hseg_off.p, plan.rowkey.p,
-                                                       plan.rl.p, elen.p);
+    u64* elen = sc.take<u64>(E);
+    fill_entries_kernel<<<blocks_for(n), 256, 0, st>>>(a.row_ptr, n, segment, ents, ent_off,
+                                                       hsegs, hseg_off, plan.rowkey.p,
+                                                       plan.rl.p, elen);
     PK_LAUNCH("spmm plan entries");
     PK_CUDA(cudaMemsetAsync(plan.rpc.p, 0, sizeof(u64), st));
     if (plan.entries)
       cub_run([&](void* t, size_t& b) {
-        return cub::DeviceScan::InclusiveSum(t, b, elen.p, plan.rpc.p + 1, plan.entries, st);
+        return cub::DeviceScan::InclusiveSum(t, b, elen, plan.rpc.p + 1, plan.entries, st);
       }, st);
   }
   PK_CUDA(cudaMemcpyAsync(&plan.list_nnz, plan.rpc.p + plan.entries, sizeof(u64),
@@ -987,11 +1035,12 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
   if (plan.entries) {
     // hot columns: degree >= PK_HOT_FACTOR (default 2) x the mean
     check(a.cols < (i64{1} << 31), "spmm plan: more than 2^31 columns");
-    DevBuf<u32> deg(std::max<i64>(a.cols, 1));
-    PK_CUDA(cudaMemsetAsync(deg.p, 0, deg.n * sizeof(u32), st));
+    const size_t ncols = static_cast<size_t>(std::max<i64>(a.cols, 1));
+    u32* deg = sc.take<u32>(ncols);
+    PK_CUDA(cudaMemsetAsync(deg, 0, ncols * sizeof(u32), st));
     if (a.nnz) {
       col_degree_kernel<<<blocks_for(static_cast<i64>(a.nnz)), 256, 0, st>>>(a.col_idx, a.nnz,
-                                                                             deg.p);
+                                                                             deg);
       PK_LAUNCH("spmm plan column degrees");
     }
     static const double hot_factor = [] {
@@ -1001,19 +1050,20 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
     const double mean = static_cast<double>(a.nnz) / std::max<i64>(a.cols, 1);
     const u32 hot_deg = static_cast<u32>(std::max(1.0, std::ceil(hot_factor * mean)));
     compact_rows_kernel<<<blocks_for(n * 32), 256, 0, st>>>(a.row_ptr, a.col_idx, a.values, n,
-                                                             ents.p, ent_off.p, plan.rpc.p,
-                                                             deg.p, hot_deg, plan.cv.p,
+                                                             ents, ent_off, plan.rpc.p,
+                                                             deg, hot_deg, plan.cv.p,
                                                              plan.endbits.p);
     PK_LAUNCH("spmm plan compact");
   }
   if (nh && segment) {
     // FAST plan: hub rows ascending with their segment ranges
     plan.hub_asc = std::move(hubs32);
-    DevBuf<u32> lo(n), cnt(n);
-    seg_meta_kernel<<<blocks_for(n), 256, 0, st>>>(hsegs.p, hseg_off.p, n, lo.p, cnt.p);
+    u32* lo = sc.take<u32>(n);
+    u32* cnt = sc.take<u32>(n);
+    seg_meta_kernel<<<blocks_for(n), 256, 0, st>>>(hsegs, hseg_off, n, lo, cnt);
     PK_LAUNCH("spmm plan segments");
-    select(lo.p, is_hub.p, plan.hub_seg0);
-    select(cnt.p, is_hub.p, plan.hub_nseg);
+    select(lo, is_hub, plan.hub_seg0);
+    select(cnt, is_hub, plan.hub_nseg);
   } else if (nh) {
     // exact plan: hub rows longest first (few: host sort)
     std::vector<u32> h(nh);
