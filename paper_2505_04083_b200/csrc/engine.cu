@@ -281,7 +281,20 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     }
     auto sh = std::make_shared<AdjShard>();
     sh->parity = parity, sh->r0 = r.r0, sh->r1 = r.r1, sh->c0 = r.c0, sh->c1 = r.c1;
-    csr_block(variant, r.r0, r.r1, r.c0, r.c1, &sh->a, st_);
+    const bool whole = r.r0 == 0 && r.r1 == n && r.c0 == 0 && r.c1 == n;
+    if (host && whole) {
+      // the staged upload already is this block: adopt it (one rank on the
+      // row and inner axes; every plane of this parity shares the shard)
+      auto& rp = parity ? orp : erp;
+      auto& ci = parity ? oci : eci;
+      auto& va = parity ? ov : ev;
+      sh->a.rows = n, sh->a.cols = n, sh->a.nnz = variant.nnz;
+      sh->a.row_ptr = rp.release_ownership();
+      sh->a.col_idx = ci.release_ownership();
+      sh->a.values = va.release_ownership();
+    } else {
+      csr_block(variant, r.r0, r.r1, r.c0, r.c1, &sh->a, st_);
+    }
     mark("csr_block");
     csr_transpose(view(sh->a), &sh->at, st_);
     mark("csr_transpose");
