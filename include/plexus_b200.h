@@ -71,6 +71,11 @@ const char* pk_last_error(void);
 int pk_abi_version(void);
 /* total kernels launched by this library in the process (evidence counter) */
 uint64_t pk_kernel_launch_count(void);
+
+/* Device memory the library freed is kept in a per-process cache and reused
+ * by the next allocation of the same size (a rebuilt engine allocates
+ * nothing new). This returns every cached block to the driver. */
+int pk_device_cache_release(void);
 int pk_device_sm_count(int device);
 
 /* ------------------------------------------------------------------ */

@@ -63,6 +63,7 @@ SIGNATURES = {
     "pk_last_error": (C.c_char_p, []),
     "pk_abi_version": (INT, []),
     "pk_kernel_launch_count": (U64, []),
+    "pk_device_cache_release": (INT, []),
     "pk_device_sm_count": (INT, [INT]),
     "pk_spmm_rows_f32": (INT, [C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P, I64, U64P, P]),
     "pk_spmm_f32": (INT, [C.POINTER(pk_csr), P, I64, I64, I64, P, I64, U64P, P]),

@@ -103,6 +103,10 @@ int pk_abi_version(void) { return 1; }
 
 uint64_t pk_kernel_launch_count(void) { return g_launches.load(); }
 
+int pk_device_cache_release(void) {
+  return guard([&] { dev_trim(); });
+}
+
 int pk_device_sm_count(int device) {
   int n = 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;

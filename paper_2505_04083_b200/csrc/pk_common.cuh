@@ -68,6 +68,13 @@ inline std::string shape(i64 r, i64 c) {
   return std::to_string(r) + "x" + std::to_string(c);
 }
 
+// Device memory of the library: a caching allocator over cudaMalloc
+// (memory.cu). dev_free synchronises the device like cudaFree; dev_trim
+// returns every cached block to the driver.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+void dev_trim();
+
 // Device buffer owned by RAII; used for workspaces.
 template <typename T>
 struct DevBuf {
@@ -88,13 +95,13 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) PK_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
   }
   void ensure(size_t count) {
     if (count > n) alloc(count);
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p);
     p = nullptr;
     n = 0;
   }

@@ -116,10 +116,10 @@ void alloc_owned(pk_csr_owned* out, i64 rows, i64 cols, u64 nnz) {
   out->row_ptr = nullptr;
   out->col_idx = nullptr;
   out->values = nullptr;
-  PK_CUDA(cudaMalloc(&out->row_ptr, (rows + 1) * sizeof(u64)));
+  out->row_ptr = static_cast<u64*>(dev_alloc((rows + 1) * sizeof(u64)));
   if (nnz) {
-    PK_CUDA(cudaMalloc(&out->col_idx, nnz * sizeof(u32)));
-    PK_CUDA(cudaMalloc(&out->values, nnz * sizeof(float)));
+    out->col_idx = static_cast<u32*>(dev_alloc(nnz * sizeof(u32)));
+    out->values = static_cast<float*>(dev_alloc(nnz * sizeof(float)));
   }
 }
 
@@ -361,9 +361,9 @@ void permute_csr(const pk_csr& a, const u32* row_perm, const u32* col_perm, pk_c
 
 void csr_free(pk_csr_owned* m) {
   if (!m) return;
-  if (m->row_ptr) cudaFree(m->row_ptr);
-  if (m->col_idx) cudaFree(m->col_idx);
-  if (m->values) cudaFree(m->values);
+  if (m->row_ptr) dev_free(m->row_ptr);
+  if (m->col_idx) dev_free(m->col_idx);
+  if (m->values) dev_free(m->values);
   m->row_ptr = nullptr;
   m->col_idx = nullptr;
   m->values = nullptr;
