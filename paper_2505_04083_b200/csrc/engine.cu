@@ -57,7 +57,10 @@ void DMat::alloc(i64 r, i64 c) {
   cols = c;
   ld = pad4(c);
   buf.alloc(static_cast<size_t>(std::max<i64>(1, r) * ld));
+  // legacy-stream memset, completed before any engine stream touches the
+  // block (the allocator hands back reused, non-zero blocks)
   PK_CUDA(cudaMemset(buf.p, 0, buf.n * sizeof(float)));
+  PK_CUDA(cudaStreamSynchronize(0));
 }
 
 const std::vector<u64>& AdjShard::blocks_nnz(int blocks, cudaStream_t st) {
@@ -355,6 +358,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
+  PK_CUDA(cudaStreamSynchronize(0));
   // labels / mask of this rank's logit rows (trainer.hpp:241-248)
   const Shapes& sl = shapes_[L_ - 1];
   const int parity = (L_ - 1) % 2;

@@ -10,12 +10,14 @@
 // are handed back to the next allocation of that size — a re-built engine of
 // the same shape allocates nothing new. A free still synchronises the device
 // first, like cudaFree, so a block is never reused under a running kernel.
-// The cache is bounded (PK_ALLOC_CACHE_GB, default 32): going over it, or an
-// out-of-memory cudaMalloc, releases every cached block first.
+// The cache is bounded (PK_ALLOC_CACHE_GB, default half the device): going
+// over it releases cached blocks until it fits; an out-of-memory cudaMalloc
+// releases all of them and retries.
 // PK_ALLOC_CACHE=0 selects plain cudaMalloc / cudaFree.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <iterator>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -53,11 +55,15 @@ bool caching() {
   return on;
 }
 
+// default: half of the device's memory (an engine of the bench shape holds
+// tens of GB; a smaller cap would drop it on close and defeat the reuse)
 size_t cache_cap() {
   static const size_t cap = [] {
     const char* e = std::getenv("PK_ALLOC_CACHE_GB");
-    const double gb = e ? std::atof(e) : 32.0;
-    return static_cast<size_t>(gb * (1ull << 30));
+    if (e) return static_cast<size_t>(std::atof(e) * (1ull << 30));
+    size_t free_b = 0, total = 0;
+    if (cudaMemGetInfo(&free_b, &total) != cudaSuccess) total = size_t{64} << 30;
+    return total / 2;
   }();
   return cap;
 }
@@ -67,6 +73,23 @@ size_t round_size(size_t b) {
   if (b < (size_t{1} << 20)) return (b + 511) / 512 * 512;
   const size_t g = size_t{2} << 20;
   return (b + g - 1) / g * g;
+}
+
+// release cached blocks until `keep` bytes or fewer stay cached
+void trim_to_locked(Cache& c, size_t keep) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto it = c.free.begin(); it != c.free.end() && c.cached > keep;) {
+    cudaSetDevice(it->first.first);
+    auto& blocks = it->second;
+    while (!blocks.empty() && c.cached > keep) {
+      cudaFree(blocks.back());
+      blocks.pop_back();
+      c.cached -= it->first.second;
+    }
+    it = blocks.empty() ? c.free.erase(it) : std::next(it);
+  }
+  cudaSetDevice(cur);
 }
 
 void trim_locked(Cache& c) {
@@ -131,7 +154,12 @@ void dev_free(void* p) {
   const bool ok = cudaDeviceSynchronize() == cudaSuccess;
   if (cur != b.dev) cudaSetDevice(cur);
   if (!ok) return;  // a failed context: drop the block rather than reuse it
-  if (c.cached + b.bytes > cache_cap()) trim_locked(c);
+  const size_t cap = cache_cap();
+  if (b.bytes > cap) {  // never cache a block bigger than the whole cache
+    cudaFree(p);
+    return;
+  }
+  if (c.cached + b.bytes > cap) trim_to_locked(c, cap - b.bytes);
   c.free[{b.dev, b.bytes}].push_back(p);
   c.cached += b.bytes;
 }
