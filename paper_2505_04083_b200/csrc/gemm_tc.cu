@@ -59,6 +59,7 @@ constexpr int kLoaderThreads = 32 * kLoaderWarps;
 // the TMA producer)
 constexpr int kConvWarps = PK_CONV_WARPS;
 static_assert(kConvWarps >= 1 && kConvWarps <= kLoaderWarps - 1, "converter warps");
+constexpr int kConvRingWarps = kLoaderWarps - 2;  // ring mode: warps 2..7
 // k-stages accumulated in TMEM before the epilogue folds the partial into
 // the output with round-to-nearest fp32 adds. The tensor core's fp32
 // accumulation does not round to nearest, so its error grows with the chain
@@ -456,6 +457,15 @@ struct TcConfig {
   static constexpr int kTmemCols = BN <= 32 ? 64 : (BN <= 64 ? 128 : (BN <= 128 ? 256 : 512));
   static constexpr int kAccStride = kTmemCols / 2;  // two accumulator buffers
   static constexpr size_t kSmem = static_cast<size_t>(STAGES) * kStage + 1024;
+  // Ring layout (TMA + weight image, single-CTA): the raw A tiles, their lo
+  // tiles and the weight images live in three rings of their own depth, so
+  // the DRAM-fed raw ring can run far ahead of the L2-fed weight ring.
+  static constexpr int kRB = 2;                 // weight images (hi | lo)
+  static constexpr int kRL = 2;                 // converted lo tiles
+  static constexpr int kRingBudget = 224 * 1024;
+  static constexpr int kRA = std::min(8, (kRingBudget - kRB * 2 * kTileB - kRL * kTileA) / kTileA);
+  static constexpr size_t kSmemRing =
+      static_cast<size_t>(kRA + kRL) * kTileA + static_cast<size_t>(kRB) * 2 * kTileB + 1024;
 };
 
 // TMA: the big operands arrive by TMA as raw fp32 tiles (the tensor core's
@@ -478,6 +488,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   static_assert(CS == 1 || (TMA && B_PRE), "clusters need the TMA + weight-image path");
   constexpr unsigned short kMask = static_cast<unsigned short>((1u << CS) - 1u);
   const int crank = CS > 1 ? static_cast<int>(cluster_rank()) : 0;
+  constexpr bool kRing = TMA && B_PRE && CS == 1;
+  constexpr int kRA = Cfg::kRA, kRL = Cfg::kRL, kRB = Cfg::kRB;
+  static_assert(!kRing || kRA >= 2, "ring layout: at least two raw stages");
 #ifdef PK_TC_PROF
   const long long t_kernel = clock64();
   long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -487,6 +500,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   __shared__ u64 full[STAGES], empty[STAGES], raw[STAGES], tfull[2], tempty[2];
+  // ring mode: raw A full/empty, lo full/empty, weight image full/empty
+  __shared__ u64 ra_full[kRing ? kRA : 1], ra_empty[kRing ? kRA : 1];
+  __shared__ u64 rl_full[kRing ? kRL : 1], rl_empty[kRing ? kRL : 1];
+  __shared__ u64 rb_full[kRing ? kRB : 1], rb_empty[kRing ? kRB : 1];
   __shared__ unsigned tmem_base;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -499,6 +516,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);
+    }
+    if constexpr (kRing) {
+      for (int i = 0; i < kRA; ++i) mbar_init(&ra_full[i], 1), mbar_init(&ra_empty[i], 1);
+      for (int i = 0; i < kRL; ++i) mbar_init(&rl_full[i], kConvRingWarps), mbar_init(&rl_empty[i], 1);
+      for (int i = 0; i < kRB; ++i) mbar_init(&rb_full[i], 1), mbar_init(&rb_empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -559,7 +581,87 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   };
   auto valid = [&](const Pos& q) { return live(q.t); };
 
-  if (TMA && warp < kLoaderWarps) {
+  // smem of the rings: [raw A x kRA][lo A x kRL][weight image (hi|lo) x kRB]
+  auto ra_slot = [&](int i) { return smem + static_cast<size_t>(i) * Cfg::kTileA; };
+  auto rl_slot = [&](int i) { return smem + static_cast<size_t>(kRA + i) * Cfg::kTileA; };
+  auto rb_slot = [&](int i) {
+    return smem + static_cast<size_t>(kRA + kRL) * Cfg::kTileA +
+           static_cast<size_t>(i) * 2 * Cfg::kTileB;
+  };
+
+  if (kRing && warp < kLoaderWarps) {
+    if constexpr (kRing) {
+      if (warp == 0 && lane == 0) {
+        // ------------------------------------------- raw A producer (DRAM)
+        Pos q;
+        start(q, blockIdx.x);
+        for (u64 s = 0; valid(q); ++s) {
+          const int i = static_cast<int>(s % kRA);
+          const unsigned ph = static_cast<unsigned>((s / kRA) & 1);
+          TC_PROF_WAIT(0, mbar_wait(&ra_empty[i], ph ^ 1u));
+          const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
+          mbar_expect_tx(&ra_full[i], Cfg::kTileA);
+          tma_load_2d(ra_slot(i), &tma_a, static_cast<int>(k0), static_cast<int>(q.m0),
+                      &ra_full[i]);
+          mbar_arrive(&ra_full[i]);
+          advance(q);
+        }
+      } else if (warp == 1 && lane == 0) {
+        // ------------------------------------- weight image producer (L2)
+        Pos q;
+        start(q, blockIdx.x);
+        for (u64 s = 0; valid(q); ++s) {
+          const int i = static_cast<int>(s % kRB);
+          const unsigned ph = static_cast<unsigned>((s / kRB) & 1);
+          mbar_wait(&rb_empty[i], ph ^ 1u);
+          const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
+          const i64 g = q.nt * p.b_stages + k0 / kBK;
+          mbar_expect_tx(&rb_full[i], 2u * Cfg::kTileB);
+          bulk_copy_g2s(rb_slot(i), p.b_image + g * 2 * Cfg::kTileB, 2u * Cfg::kTileB,
+                        &rb_full[i]);
+          mbar_arrive(&rb_full[i]);
+          advance(q);
+        }
+      } else if (warp >= 2) {
+        // ------------------------------------------------------ converters
+        const int ct = threadIdx.x - 64;
+        constexpr int kStep = 32 * kConvRingWarps;
+        Pos q;
+        start(q, blockIdx.x);
+        for (u64 s = 0; valid(q); ++s) {
+          const int ia = static_cast<int>(s % kRA), il = static_cast<int>(s % kRL);
+          TC_PROF_WAIT(1, mbar_wait(&ra_full[ia], static_cast<unsigned>((s / kRA) & 1)));
+          mbar_wait(&rl_empty[il], static_cast<unsigned>((s / kRL) & 1) ^ 1u);
+          const unsigned s0 = smem_u32(ra_slot(ia)), d0 = smem_u32(rl_slot(il));
+          for (int i0 = ct; i0 < Cfg::kTileA / 16; i0 += 4 * kStep) {
+            float4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = i0 + j * kStep;
+              if (i < Cfg::kTileA / 16)
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[j].x), "=f"(v[j].y), "=f"(v[j].z), "=f"(v[j].w)
+                             : "r"(s0 + 16u * i));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = i0 + j * kStep;
+              if (i < Cfg::kTileA / 16) {
+                const float4 l = lo_of_raw(v[j]);
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(d0 + 16u * i),
+                             "f"(l.x), "f"(l.y), "f"(l.z), "f"(l.w)
+                             : "memory");
+              }
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rl_full[il]);
+          advance(q);
+        }
+      }
+    }
+  } else if (TMA && warp < kLoaderWarps) {
     if constexpr (TMA) {
       if (warp == 0 && lane == 0) {
         // ---------------------------------------------------- TMA producer
@@ -718,6 +820,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     constexpr unsigned idesc = instr_desc(BN, A_T, B_T && !B_PRE);
     int stage = 0;
     unsigned phase = 0;
+    u64 ring_s = 0;  // ring mode: k-stages consumed so far
     int acc = 0;
     unsigned acc_phase = 0;
     for (int t = blockIdx.x; live(t); t += gridDim.x) {
@@ -733,6 +836,36 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const unsigned d = tmem + static_cast<unsigned>(acc * Cfg::kAccStride);
         const int k_lo = sg * kSegStages, k_hi = min(nk, k_lo + kSegStages);
         for (int kk = k_lo; kk < k_hi; ++kk) {
+          if constexpr (kRing) {
+            const int ia = static_cast<int>(ring_s % kRA), il = static_cast<int>(ring_s % kRL),
+                      ib = static_cast<int>(ring_s % kRB);
+            TC_PROF_WAIT(2, mbar_wait(&ra_full[ia], static_cast<unsigned>((ring_s / kRA) & 1)));
+            TC_PROF_WAIT(6, mbar_wait(&rl_full[il], static_cast<unsigned>((ring_s / kRL) & 1)));
+            mbar_wait(&rb_full[ib], static_cast<unsigned>((ring_s / kRB) & 1));
+            tc_fence_after();
+            if (lane == 0) {
+              const unsigned a_hi = smem_u32(ra_slot(ia)), a_lo = smem_u32(rl_slot(il));
+              const unsigned b_hi = smem_u32(rb_slot(ib)), b_lo = b_hi + Cfg::kTileB;
+#pragma unroll
+              for (int ks = 0; ks < kBK / 8; ++ks) {
+                const u64 dah = kmajor_desc(a_hi, ks), dal = kmajor_desc(a_lo, ks);
+                const u64 dbh = kmajor_desc(b_hi, ks), dbl = kmajor_desc(b_lo, ks);
+                const unsigned first = (kk == k_lo && ks == 0) ? 0u : 1u;
+                tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
+                tc_mma_tf32(d, dah, dbl, idesc, 1u);
+                tc_mma_tf32(d, dah, dbh, idesc, 1u);
+              }
+#ifdef PK_TC_PROF
+              prof_acc[7] += 1;
+#endif
+              tc_commit(&ra_empty[ia]);
+              tc_commit(&rl_empty[il]);
+              tc_commit(&rb_empty[ib]);
+            }
+            __syncwarp();
+            ++ring_s;
+            continue;
+          }
           if constexpr (TMA) TC_PROF_WAIT(2, mbar_wait(&raw[stage], phase));  // TMA landed
           TC_PROF_WAIT(6, mbar_wait(&full[stage], phase));
           tc_fence_after();
@@ -989,7 +1122,7 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
   // weight-image multicast across a cluster of CS CTAs (PK_TC_CLUSTER)
   static const int cluster_pref = [] {
     const char* e = std::getenv("PK_TC_CLUSTER");
-    const int v = e ? std::atoi(e) : 2;
+    const int v = e ? std::atoi(e) : 1;  // measured neutral at 2, slower at 4
     return v >= 4 ? 4 : (v >= 2 ? 2 : 1);
   }();
   int cs = 1;
@@ -1010,10 +1143,12 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
   } else {
     kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 1>, variant = 1;
   }
+  // the single-CTA TMA + weight-image kernel runs the ring layout
+  const size_t smem = (B_PRE && variant == 1) ? Cfg::kSmemRing : Cfg::kSmem;
   static thread_local bool attr[4] = {false, false, false, false};
   if (!attr[variant]) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(Cfg::kSmem)));
+                                 static_cast<int>(smem)));
     attr[variant] = true;
   }
   TcParams p = p0;
@@ -1036,7 +1171,7 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(kThreadsTc);
-    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1047,7 +1182,7 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     cfg.numAttrs = 1;
     PK_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, map_a, map_b));
   } else {
-    kernel<<<grid, kThreadsTc, Cfg::kSmem, st>>>(p, map_a, map_b);
+    kernel<<<grid, kThreadsTc, smem, st>>>(p, map_a, map_b);
   }
   PK_LAUNCH("gemm tcgen05 kernel");
 }
