@@ -366,7 +366,17 @@ def run_ours(args):
                          "traffic": traffic, "traffic_unit": "DRAM bytes per epoch (ncu)",
                          "alg_bytes_per_epoch": spmm_bytes,
                          "spmm_ms_per_epoch": spmm_s * 1e3,
-                         "spmm_share_of_step": spmm_launch_share},
+                         "spmm_share_of_step": spmm_launch_share,
+                         # DRAM view of the same launches: ncu bytes over the
+                         # live SpMM time (frac above exceeds 1 because L2
+                         # serves about half of the gathered feature rows)
+                         "dram_achieved": (traffic / spmm_s / 1e9
+                                           if traffic and spmm_s > 0 else None),
+                         "dram_frac": (traffic / spmm_s / 1e9 / peak
+                                       if traffic and spmm_s > 0 else None),
+                         "note": "achieved = SURVEY 8(d) algorithmic bytes "
+                                 "(8nnz + 8(rows+1) + 4nnz*D + 4rows*D per SpMM) / "
+                                 "measured SpMM time"},
             "phases_ms": phases,
             "losses": losses,
             "gpu_launches": int(launches),
