@@ -36,7 +36,14 @@ typedef enum pk_status {
   PK_ERR_CUDA = 2,     /* CUDA runtime / launch failure               */
   PK_ERR_NCCL = 3,     /* NCCL failure                                */
   PK_ERR_MEMORY = 4,   /* MemoryError (common.hpp:22-26), device OOM  */
-  PK_ERR_TRAINING = 5  /* TrainingError (trainer.hpp:26-29)           */
+  PK_ERR_TRAINING = 5, /* TrainingError (trainer.hpp:26-29)           */
+  /* IoError (common.hpp:28-41): 10 + IoErrorCode                        */
+  PK_ERR_IO_MISSING = 10,   /* MissingFile                              */
+  PK_ERR_IO_TRUNCATED = 11, /* TruncatedFile                            */
+  PK_ERR_IO_CHECKSUM = 12,  /* ChecksumMismatch                         */
+  PK_ERR_IO_MANIFEST = 13,  /* ManifestMismatch                         */
+  PK_ERR_IO_FORMAT = 14,    /* BadFormat                                */
+  PK_ERR_IO_WRITE = 15      /* WriteFailed                              */
 } pk_status;
 
 /* Numeric mode of the dense transforms. PARITY reproduces the reference's
@@ -384,6 +391,59 @@ int pk_enumerate_configs(int g, int* gxyz, int cap, int* count);
 int pk_perf_rank_configs(int g, const pk_dataset_stats* stats,
                          const pk_machine* m, const pk_perf_coeffs* c,
                          pk_config_prediction* out, int cap, int* count);
+
+/* ------------------------------------------------------------------ */
+/* PLXS shard files (shard_io.hpp:26-414, trainer.hpp:252-438)         */
+
+/* One CSR block in host memory for the writer; values are `precision`
+ * bytes each (4 = f32, 8 = f64). */
+typedef struct pk_plxs_csr_host {
+  uint64_t rows, cols, nnz;
+  const uint64_t* row_ptr;
+  const uint32_t* col_idx;
+  const void* values;
+} pk_plxs_csr_host;
+
+/* write_shards' per-file body (shard_io.hpp:311-361): header, CSR even,
+ * CSR odd, feature block, labels/masks of the row block; byte-identical to
+ * the reference. checksums_out = the four sections' FNV-1a 64. */
+int pk_plxs_write(const char* path, const uint64_t ranges[6], uint32_t precision,
+                  const pk_plxs_csr_host* even, const pk_plxs_csr_host* odd,
+                  uint64_t f_rows, uint64_t f_cols, const void* features,
+                  uint64_t label_count, const uint32_t* labels_row,
+                  const uint32_t* labels_col, const uint8_t* mask_row,
+                  const uint8_t* mask_col, uint64_t checksums_out[4]);
+
+/* ShardFileReader (shard_io.hpp:90-276). open checks magic, version,
+ * precision (0 = any) and the block ranges against the manifest (NULL =
+ * skip). Reads of a whole section verify its checksum (`expected`);
+ * partial reads cannot, like the reference. `device` = 1 streams col_idx /
+ * values / features into device memory through a pinned double buffer on
+ * `stream`. */
+typedef struct pk_plxs pk_plxs;
+int pk_plxs_open(const char* path, const uint64_t expect_ranges[6], uint32_t precision,
+                 pk_plxs** out);
+int pk_plxs_close(pk_plxs* h);
+int pk_plxs_info(const pk_plxs* h, uint64_t ranges_out[6], uint32_t* precision,
+                 uint64_t* bytes_read);
+int pk_plxs_csr_extent(pk_plxs* h, int section, uint64_t r0, uint64_t r1, uint64_t* rows,
+                       uint64_t* cols, uint64_t* nnz, uint64_t* e0, uint64_t* e1);
+int pk_plxs_read_csr_rows(pk_plxs* h, int section, uint64_t r0, uint64_t r1,
+                          uint64_t expected, uint64_t* row_ptr, uint32_t* col_idx,
+                          void* values, int device, void* stream);
+int pk_plxs_read_feature_rows(pk_plxs* h, uint64_t r0, uint64_t r1, uint64_t expected,
+                              void* dst, int device, void* stream);
+int pk_plxs_read_labels(pk_plxs* h, uint64_t r0, uint64_t r1, uint64_t expected,
+                        uint32_t* labels_row, uint32_t* labels_col, uint8_t* mask_row,
+                        uint8_t* mask_col);
+
+/* load_rank_shards' row merge (trainer.hpp:276-309) on the device: pieces
+ * k = 0..count-1 hold the same rows (row_ptr on the device, rebased), with
+ * column origin col0[k] in the global numbering; out = for each row, the
+ * pieces' entries in piece order whose global column lies in [c0, c1),
+ * renumbered from c0. Allocates out (free with pk_csr_free). */
+int pk_csr_hconcat(const pk_csr* pieces, const uint64_t* col0, int count, uint64_t c0,
+                   uint64_t c1, pk_csr_owned* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -502,3 +502,66 @@ def fit_regression(features, seconds):
     out = np.empty(5)
     _check(lib().ref_fit_regression(_p(f), _p(s), C.c_int(len(s)), _p(out)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# shard files (shard_io.hpp, trainer.hpp:252-438)
+
+def _io_check(rc):
+    """IoError codes come back as 10 + IoErrorCode (common.hpp:28-35)."""
+    if rc != 0:
+        raise RuntimeError(f"rc={rc}: " + lib().ref_last_error().decode())
+
+
+def write_shards(pre, p, q, directory, name="dataset"):
+    """shard_io::write_shards (shard_io.hpp:278-414)."""
+    _io_check(lib().ref_write_shards(pre.h, C.c_int(p), C.c_int(q),
+                                     str(directory).encode(), name.encode()))
+
+
+def load_preprocessed(directory):
+    """load_manifest + load_preprocessed (shard_io.hpp:416-486, trainer.hpp:386-438)."""
+    lib().ref_load_preprocessed.restype = C.c_void_p
+    lib().ref_load_preprocessed.argtypes = [C.c_char_p]
+    h = lib().ref_load_preprocessed(str(directory).encode())
+    if not h:
+        raise RuntimeError(lib().ref_last_error().decode())
+    # precision from the manifest
+    import json
+    with open(os.path.join(str(directory), "manifest.json")) as f:
+        f64 = json.load(f)["precision"] == "f64"
+    return Pre(h, f64)
+
+
+class RankShards(_Handle):
+    """load_rank_shards (trainer.hpp:256-384) for one rank."""
+    _free = "ref_rank_free"
+
+    @classmethod
+    def load(cls, directory, grid, coords, layers, f64=False):
+        lib().ref_load_rank_shards.restype = C.c_void_p
+        lib().ref_load_rank_shards.argtypes = [C.c_char_p] + [C.c_int] * 7
+        lib().ref_rank_adj.restype = C.c_void_p
+        lib().ref_rank_adj.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        lib().ref_rank_free.argtypes = [C.c_void_p]
+        h = lib().ref_load_rank_shards(str(directory).encode(), *grid, *coords, layers)
+        return cls(h, f64)
+
+    def adj(self, plane, parity, transposed=False):
+        return Csr(lib().ref_rank_adj(self.h, plane, parity, int(transposed)), self.f64)
+
+    def info(self):
+        fr, fc, nl = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        files, nbytes = C.c_int(), C.c_uint64()
+        lib().ref_rank_info(self.h, C.byref(fr), C.byref(fc), C.byref(nl), C.byref(files),
+                            C.byref(nbytes))
+        return dict(f0_rows=fr.value, f0_cols=fc.value, labels=nl.value, files_read=files.value,
+                    bytes_read=nbytes.value)
+
+    def arrays(self):
+        i = self.info()
+        f0 = np.empty((i["f0_rows"], i["f0_cols"]), _dt(self.f64))
+        lab = np.empty(i["labels"], np.uint32)
+        mask = np.empty(i["labels"], np.uint8)
+        lib().ref_rank_copy(self.h, _p(f0), _p(lab), _p(mask))
+        return f0, lab, mask

@@ -39,6 +39,9 @@ int guarded(F&& f) {
   } catch (const MemoryError& e) {
     g_err = std::string("MemoryError: ") + e.what();
     return 4;
+  } catch (const IoError& e) {  // 10 + IoErrorCode (common.hpp:28-35)
+    g_err = std::string("IoError: ") + e.what();
+    return 10 + static_cast<int>(e.code());
   } catch (const std::exception& e) {
     g_err = std::string("Error: ") + e.what();
     return 9;
@@ -1011,5 +1014,116 @@ int ref_epoch_sample(void* pre, const u64* hidden, int nh, u64 rows, int threads
     out[1] = wall;
   });
 }
+
+// ---------------------------------------------------------------------------
+// shard files (shard_io.hpp:278-536, trainer.hpp:252-438): the reference's
+// writer and readers, for byte-level parity of the PLXS files and the
+// per-rank loader
+
+int ref_write_shards(void* pre, int p, int q, const char* dir, const char* name) {
+  auto* h = static_cast<Pre*>(pre);
+  return guarded([&] {
+    if (h->f64)
+      shard_io::write_shards(h->d, p, q, dir, name);
+    else
+      shard_io::write_shards(h->f, p, q, dir, name);
+  });
+}
+
+void* ref_load_preprocessed(const char* dir) {
+  auto* out = new Pre;
+  int rc = guarded([&] {
+    auto m = shard_io::load_manifest(dir);
+    out->f64 = m.precision == 8;
+    if (out->f64)
+      out->d = load_preprocessed<double>(m);
+    else
+      out->f = load_preprocessed<float>(m);
+  });
+  if (rc) {
+    delete out;
+    return nullptr;
+  }
+  return out;
+}
+
+struct RankHolder {
+  int f64 = 0;
+  RankTensors<float> f;
+  RankTensors<double> d;
+};
+
+void* ref_load_rank_shards(const char* dir, int gx, int gy, int gz, int x, int y, int z,
+                           int layers) {
+  auto* out = new RankHolder;
+  int rc = guarded([&] {
+    auto m = shard_io::load_manifest(dir);
+    out->f64 = m.precision == 8;
+    if (out->f64)
+      out->d = load_rank_shards<double>(m, GridConfig(gx, gy, gz), Coords{x, y, z}, layers);
+    else
+      out->f = load_rank_shards<float>(m, GridConfig(gx, gy, gz), Coords{x, y, z}, layers);
+  });
+  if (rc) {
+    delete out;
+    return nullptr;
+  }
+  return out;
+}
+
+// the (plane, parity) adjacency block (0) or its transpose (1) as a Csr handle
+void* ref_rank_adj(void* h, int plane, int parity, int transposed) {
+  auto* r = static_cast<RankHolder*>(h);
+  auto* c = new Csr;
+  c->f64 = r->f64;
+  LayerLayout lay;  // get() keys by (layer % 3, layer % 2)
+  for (int l = 0; l < 6; ++l)
+    if (l % 3 == plane && l % 2 == parity) lay.layer = l;
+  int rc = guarded([&] {
+    if (r->f64) {
+      const auto& s = r->d.adj.get(lay);
+      c->d = transposed ? s.at : s.a;
+    } else {
+      const auto& s = r->f.adj.get(lay);
+      c->f = transposed ? s.at : s.a;
+    }
+  });
+  if (rc) {
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+void ref_rank_info(void* h, u64* f0_rows, u64* f0_cols, u64* labels, int* files_read,
+                   u64* bytes_read) {
+  auto* r = static_cast<RankHolder*>(h);
+  auto info = [&](auto& t) {
+    *f0_rows = t.f0.rows();
+    *f0_cols = t.f0.cols();
+    *labels = t.labels.size();
+    *files_read = t.files_read;
+    *bytes_read = t.bytes_read;
+  };
+  if (r->f64)
+    info(r->d);
+  else
+    info(r->f);
+}
+
+void ref_rank_copy(void* h, void* f0, u32* labels, u8* mask) {
+  auto* r = static_cast<RankHolder*>(h);
+  auto copy = [&](auto& t) {
+    dense_out(t.f0, f0);
+    if (!t.labels.empty()) std::memcpy(labels, t.labels.data(), t.labels.size() * 4);
+    if (!t.mask.empty()) std::memcpy(mask, t.mask.data(), t.mask.size());
+  };
+  if (r->f64)
+    copy(r->d);
+  else
+    copy(r->f);
+}
+
+void ref_rank_free(void* h) { delete static_cast<RankHolder*>(h); }
 
 }  // extern "C"

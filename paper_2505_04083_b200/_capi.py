@@ -35,12 +35,32 @@ class NcclError(RuntimeError):
     pass
 
 
+class IoError(RuntimeError):
+    """plexuskit::IoError (common.hpp:28-41); `code` is the IoErrorCode name."""
+    CODES = {10: "MissingFile", 11: "TruncatedFile", 12: "ChecksumMismatch",
+             13: "ManifestMismatch", 14: "BadFormat", 15: "WriteFailed"}
+
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def _io_error(rc):
+    return lambda msg: IoError(IoError.CODES[rc], msg)
+
+
 _ERRORS = {PK_ERR_CONTRACT: ContractError, PK_ERR_CUDA: CudaError, PK_ERR_NCCL: NcclError,
            PK_ERR_MEMORY: MemoryError_, PK_ERR_TRAINING: TrainingError}
+_ERRORS.update({rc: _io_error(rc) for rc in IoError.CODES})
 
 
 class pk_csr(C.Structure):
     _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_uint64),
+                ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+class pk_plxs_csr_host(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("nnz", C.c_uint64),
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
 
 
@@ -87,6 +107,16 @@ SIGNATURES = {
     "pk_normalize_adjacency": (INT, [I64, P, U64, INT, C.POINTER(pk_csr_owned), P]),
     "pk_permute_csr": (INT, [C.POINTER(pk_csr), P, P, C.POINTER(pk_csr_owned), P]),
     "pk_csr_free": (None, [C.POINTER(pk_csr_owned)]),
+    "pk_csr_hconcat": (INT, [C.POINTER(pk_csr), P, INT, U64, U64, C.POINTER(pk_csr_owned), P]),
+    "pk_plxs_write": (INT, [C.c_char_p, P, C.c_uint32, C.POINTER(pk_plxs_csr_host),
+                            C.POINTER(pk_plxs_csr_host), U64, U64, P, U64, P, P, P, P, P]),
+    "pk_plxs_open": (INT, [C.c_char_p, P, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "pk_plxs_close": (INT, [P]),
+    "pk_plxs_info": (INT, [P, P, P, P]),
+    "pk_plxs_csr_extent": (INT, [P, INT, U64, U64, P, P, P, P, P]),
+    "pk_plxs_read_csr_rows": (INT, [P, INT, U64, U64, U64, P, P, P, INT, P]),
+    "pk_plxs_read_feature_rows": (INT, [P, U64, U64, U64, P, INT, P]),
+    "pk_plxs_read_labels": (INT, [P, U64, U64, U64, P, P, P, P]),
     "pk_permutation_pair_host": (INT, [U64, U64, P, P]),
     "pk_philox_permutation_host": (INT, [U64, U64, U64, P]),
     "pk_rmat_edges": (INT, [INT, U64, DBL, DBL, DBL, U64, P, U64P, P]),

@@ -295,6 +295,15 @@ int pk_csr_block(const pk_csr* a, int64_t r0, int64_t r1, int64_t c0, int64_t c1
   });
 }
 
+int pk_csr_hconcat(const pk_csr* pieces, const uint64_t* col0, int count, uint64_t c0,
+                   uint64_t c1, pk_csr_owned* out, void* stream) {
+  return guard([&] {
+    check(pieces && col0 && out, "csr hconcat: null argument");
+    for (int k = 0; k < count; ++k) check_csr(&pieces[k], "csr hconcat");
+    csr_hconcat(pieces, col0, count, c0, c1, out, as_stream(stream));
+  });
+}
+
 int pk_normalize_adjacency(int64_t n, const uint32_t* edges_uv, uint64_t num_edges,
                            int undirected, pk_csr_owned* out, void* stream) {
   return guard([&] {

@@ -359,6 +359,113 @@ void permute_csr(const pk_csr& a, const u32* row_perm, const u32* col_perm, pk_c
   PK_CUDA(cudaStreamSynchronize(st));
 }
 
+// ---------------------------------------------------------------------------
+// row merge of column pieces (load_rank_shards' assemble_csr,
+// trainer.hpp:276-309): columns within a piece row ascend, so the entries
+// that fall in [c0, c1) are one contiguous run found by two binary searches
+
+constexpr int kMaxPieces = 64;
+
+struct Pieces {
+  const u64* rp[kMaxPieces];
+  const u32* ci[kMaxPieces];
+  const float* v[kMaxPieces];
+  u64 col0[kMaxPieces];
+  int count;
+};
+
+__device__ u64 lower_bound_col(const u32* ci, u64 lo, u64 hi, u64 key) {
+  while (lo < hi) {
+    const u64 mid = lo + (hi - lo) / 2;
+    if (ci[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// the run of piece k's row r whose global column is in [c0, c1)
+__device__ void piece_run(const Pieces& P, int k, i64 r, u64 c0, u64 c1, u64& lo, u64& hi) {
+  const u64 b = P.rp[k][r], e = P.rp[k][r + 1];
+  const u64 o = P.col0[k];
+  const u64 klo = c0 > o ? c0 - o : 0, khi = c1 > o ? c1 - o : 0;
+  lo = lower_bound_col(P.ci[k], b, e, klo);
+  hi = lower_bound_col(P.ci[k], lo, e, khi);
+}
+
+__global__ void hconcat_count(Pieces P, i64 rows, u64 c0, u64 c1, u64* counts) {
+  for (i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<i64>(gridDim.x) * blockDim.x) {
+    u64 total = 0;
+    for (int k = 0; k < P.count; ++k) {
+      u64 lo, hi;
+      piece_run(P, k, r, c0, c1, lo, hi);
+      total += hi - lo;
+    }
+    counts[r] = total;
+  }
+}
+
+// one warp per row: runs copied in piece order, lanes over entries
+__global__ void hconcat_fill(Pieces P, i64 rows, u64 c0, u64 c1, const u64* out_rp,
+                             u32* out_ci, float* out_v) {
+  const int lane = threadIdx.x % 32;
+  const i64 warps = static_cast<i64>(gridDim.x) * (blockDim.x / 32);
+  for (i64 r = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) / 32; r < rows;
+       r += warps) {
+    u64 pos = out_rp[r];
+    for (int k = 0; k < P.count; ++k) {
+      u64 lo, hi;
+      piece_run(P, k, r, c0, c1, lo, hi);
+      const u64 shift = P.col0[k] - c0;  // global = col0 + local; out = global - c0
+      for (u64 i = lo + lane; i < hi; i += 32) {
+        out_ci[pos + (i - lo)] = static_cast<u32>(P.ci[k][i] + shift);
+        out_v[pos + (i - lo)] = P.v[k][i];
+      }
+      pos += hi - lo;
+    }
+  }
+}
+
+void csr_hconcat(const pk_csr* pieces, const u64* col0, int count, u64 c0, u64 c1,
+                 pk_csr_owned* out, cudaStream_t st) {
+  check(count >= 1 && count <= kMaxPieces, "csr hconcat: 1.." + std::to_string(kMaxPieces) +
+                                               " pieces");
+  check(c0 <= c1, "csr hconcat: empty column range");
+  const i64 rows = pieces[0].rows;
+  Pieces P{};
+  P.count = count;
+  for (int k = 0; k < count; ++k) {
+    check(pieces[k].rows == rows, "csr hconcat: pieces must hold the same rows");
+    check(col0[k] <= c0 || col0[k] - c0 < (u64{1} << 32), "csr hconcat: column origin");
+    P.rp[k] = pieces[k].row_ptr;
+    P.ci[k] = pieces[k].col_idx;
+    P.v[k] = pieces[k].values;
+    P.col0[k] = col0[k];
+  }
+  DevBuf<u64> counts(rows + 1);
+  PK_CUDA(cudaMemsetAsync(counts.p + rows, 0, sizeof(u64), st));
+  if (rows) {
+    hconcat_count<<<grid_for(rows), 256, 0, st>>>(P, rows, c0, c1, counts.p);
+    PK_LAUNCH("hconcat count");
+  }
+  DevBuf<u64> rp(rows + 1);
+  counts_to_row_ptr(counts.p, rows, rp.p, st);
+  u64 nnz = 0;
+  PK_CUDA(cudaMemcpyAsync(&nnz, rp.p + rows, sizeof(u64), cudaMemcpyDeviceToHost, st));
+  PK_CUDA(cudaStreamSynchronize(st));
+  alloc_owned(out, rows, static_cast<i64>(c1 - c0), nnz);
+  PK_CUDA(cudaMemcpyAsync(out->row_ptr, rp.p, (rows + 1) * sizeof(u64),
+                          cudaMemcpyDeviceToDevice, st));
+  if (rows && nnz) {
+    hconcat_fill<<<grid_for(rows * 32), 256, 0, st>>>(P, rows, c0, c1, out->row_ptr,
+                                                      out->col_idx, out->values);
+    PK_LAUNCH("hconcat fill");
+  }
+  PK_CUDA(cudaStreamSynchronize(st));
+}
+
 void csr_free(pk_csr_owned* m) {
   if (!m) return;
   if (m->row_ptr) dev_free(m->row_ptr);

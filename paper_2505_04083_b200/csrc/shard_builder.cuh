@@ -13,6 +13,9 @@ void normalize_adjacency(i64 n, const u32* uv, u64 m, bool undirected, pk_csr_ow
 void permute_csr(const pk_csr& a, const u32* row_perm, const u32* col_perm, pk_csr_owned* out,
                  cudaStream_t st);
 void csr_free(pk_csr_owned* m);
+// load_rank_shards' row merge of column pieces (trainer.hpp:276-309)
+void csr_hconcat(const pk_csr* pieces, const u64* col0, int count, u64 c0, u64 c1,
+                 pk_csr_owned* out, cudaStream_t st);
 
 u64 rmat_edges(int scale, u64 edges, double a, double b, double c, u64 seed, u32* uv,
                cudaStream_t st);
