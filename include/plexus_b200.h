@@ -273,6 +273,19 @@ typedef struct pk_dataset_view {
   const uint8_t* mask_col;
 } pk_dataset_view;
 
+/* RankTensors (trainer.hpp:217-224) in device memory: what a per-rank
+ * loader (load_rank_shards, the file_handle path) produces. adj[plane * 2 +
+ * parity] holds the block A[rows(row_shard), cols(inner)] of every key
+ * needed_adjacency_keys lists (others: rows = cols = 0). */
+typedef struct pk_rank_view {
+  pk_csr adj[6];
+  const float* f0;            /* feature_slice rows x cols, row-major       */
+  int64_t f0_rows, f0_cols, ld_f0;
+  const uint32_t* labels;     /* final-parity labels of label_row_range     */
+  const uint8_t* mask;
+  int64_t label_rows;
+} pk_rank_view;
+
 /* EpochMetrics (trainer.hpp:40-49); phase seconds are device time of this
  * rank (CUDA events), byte counters use the reference's ring model. */
 typedef struct pk_epoch_metrics {
@@ -314,6 +327,11 @@ int pk_engine_create(const pk_engine_config* cfg, pk_engine** out);
 int pk_engine_comm_init(pk_engine* e, const void* unique_id128, int world_size);
 int pk_engine_load(pk_engine* e, const pk_dataset_view* ds);
 int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds_host);
+/* The file_handle path (trainer.hpp:461-466): this rank's tensors only
+ * (e.g. from load_rank_shards); blocks are copied, the global CE count is
+ * summed over the last layer's row_shard group (comm_init first when the
+ * grid has more than one rank). */
+int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rank_tensors);
 int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss_host,
                                double* accuracy_host);
 int pk_engine_optimizer_step(pk_engine* e);

@@ -213,6 +213,96 @@ const AdjShard& Engine::shard(const Layout& l) const {
   return *s;
 }
 
+// Transpose + SpMM plans of a freshly cut block; stored under its key.
+template <typename Mark>
+void Engine::finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, Mark& mark) {
+  csr_transpose(view(sh->a), &sh->at, st_);
+  mark("csr_transpose");
+  // FAST mode cuts hub rows into segments summed in a fixed order
+  // (tolerance-level difference); PARITY keeps every row one exact chain
+  const u64 seg = cfg_.mode == PK_MODE_FAST ? spmm_fast_segment() : 0;
+  spmm_plan_build(sh->plan_a, view(sh->a), static_cast<u64>(cfg_.hub_threshold), st_, seg);
+  spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_, seg);
+  mark("spmm plans");
+  sh->nnz_t = sh->at.nnz;
+  shards_[plane * 2 + parity] = std::move(sh);
+}
+
+// F0 shard from device rows of width feature_slice's column count (ld given)
+void Engine::set_f0(const float* src, i64 ld) {
+  const Slice fs = feature_slice(grid_, c_, cfg_.n, dims_[0]);
+  f0_.alloc(fs.r1 - fs.r0, fs.c1 - fs.c0);
+  if (f0_.rows && f0_.cols) {
+    if (f0_.ld == f0_.cols && ld == f0_.cols)
+      PK_CUDA(cudaMemcpyAsync(f0_.p(), src, f0_.rows * f0_.cols * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st_));
+    else
+      copy_block_launch(src, ld, f0_.rows, f0_.cols, f0_.p(), f0_.ld, st_);
+  }
+  f0_m_.alloc(f0_.rows, f0_.cols);
+  f0_v_.alloc(f0_.rows, f0_.cols);
+  df0_.alloc(f0_.rows, f0_.cols);
+  f0_step_ = 0;
+}
+
+// Weights (global init, then weight_slice), Adam state, activations and
+// workspaces of every layer.
+void Engine::alloc_params() {
+  w_.resize(L_), w_m_.resize(L_), w_v_.resize(L_), dw_.resize(L_);
+  wfull_.resize(L_), dwp_.resize(L_), h_.resize(L_), q_.resize(L_), fout_.resize(L_);
+  i64 max_dq = 1, max_dh = 1, max_df = 1;
+  for (int l = 0; l < L_; ++l) {
+    const Shapes& s = shapes_[l];
+    const Slice ws = weight_slice(grid_, lays_[l], c_, dims_[l], dims_[l + 1]);
+    w_[l].alloc(ws.r1 - ws.r0, ws.c1 - ws.c0);
+    auto blk = init_weight_block(cfg_.seed, l, dims_[l], dims_[l + 1], ws);
+    upload_block(w_[l], blk.data(), w_[l].cols, st_);
+    PK_CUDA(cudaStreamSynchronize(st_));
+    w_m_[l].alloc(w_[l].rows, w_[l].cols);
+    w_v_[l].alloc(w_[l].rows, w_[l].cols);
+    dw_[l].alloc(w_[l].rows, w_[l].cols);
+    wfull_[l].alloc(s.f_cols, s.w_cols);
+    dwp_[l].alloc(s.f_cols, s.w_cols);
+    h_[l].alloc(s.h_rows, s.h_cols);
+    q_[l].alloc(s.q_rows, s.q_cols);
+    if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols);
+    max_dq = std::max(max_dq, s.q_rows * pad4(s.q_cols));
+    max_dh = std::max(max_dh, s.h_rows * pad4(s.h_cols));
+    max_df = std::max(max_df, s.a_cols * pad4(s.f_cols));
+  }
+  w_step_ = 0;
+  f0g_.alloc(shapes_[0].f_rows, shapes_[0].f_cols);
+  dq_.buf.alloc(max_dq);
+  dh_.buf.alloc(max_dh);
+  df_.buf.alloc(max_df);
+  df_prev_.buf.alloc(max_df);
+  PK_CUDA(cudaMemset(dq_.buf.p, 0, dq_.buf.n * sizeof(float)));
+  PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
+  PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
+  PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
+  PK_CUDA(cudaStreamSynchronize(0));
+}
+
+// This rank's logit-row labels and mask (device pointers, lrows rows) and
+// the global masked-row count the CE scaling divides by.
+void Engine::set_labels(const u32* labels, const u8* mask, i64 lrows, u64 global_count) {
+  const Shapes& sl = shapes_[L_ - 1];
+  check(lrows == sl.a_rows, "engine: label rows disagree with the logits shard");
+  labels_.alloc(std::max<i64>(1, lrows));
+  mask_.alloc(std::max<i64>(1, lrows));
+  if (lrows) {
+    PK_CUDA(cudaMemcpyAsync(labels_.p, labels, lrows * sizeof(u32), cudaMemcpyDeviceToDevice,
+                            st_));
+    PK_CUDA(cudaMemcpyAsync(mask_.p, mask, lrows, cudaMemcpyDeviceToDevice, st_));
+  }
+  mask_count_ = global_count;
+  logits_.alloc(sl.a_rows, dims_[L_]);
+  dl_.alloc(sl.a_rows, dims_[L_]);
+  stage_.alloc(sl.a_rows, dims_[L_]);
+  // DMat::alloc zeroes on the legacy stream: drain everything before use
+  PK_CUDA(cudaDeviceSynchronize());
+}
+
 void Engine::load(const pk_dataset_view& dsin, bool host) {
   PK_CUDA(cudaSetDevice(cfg_.device));
   check(dsin.n == cfg_.n, "engine load: dataset has " + std::to_string(dsin.n) +
@@ -299,97 +389,84 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
       csr_block(variant, r.r0, r.r1, r.c0, r.c1, &sh->a, st_);
     }
     mark("csr_block");
-    csr_transpose(view(sh->a), &sh->at, st_);
-    mark("csr_transpose");
-    // FAST mode cuts hub rows into segments summed in a fixed order
-    // (tolerance-level difference); PARITY keeps every row one exact chain
-    const u64 seg = cfg_.mode == PK_MODE_FAST ? spmm_fast_segment() : 0;
-    spmm_plan_build(sh->plan_a, view(sh->a), static_cast<u64>(cfg_.hub_threshold), st_, seg);
-    spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_, seg);
-    mark("spmm plans");
-    sh->nnz_t = sh->at.nnz;
-    shards_[plane * 2 + parity] = std::move(sh);
+    finish_shard(std::move(sh), plane, parity, mark);
   }
   // trainable features F0 (feature_slice, model.hpp:53-67) + Adam state
   const Slice fs = feature_slice(grid_, c_, n, dims_[0]);
-  f0_.alloc(fs.r1 - fs.r0, fs.c1 - fs.c0);
-  if (f0_.rows && f0_.cols) {
-    const float* src = ds.features + fs.r0 * ds.ld_features + fs.c0;
-    if (f0_.ld == f0_.cols && ds.ld_features == f0_.cols)
-      PK_CUDA(cudaMemcpyAsync(f0_.p(), src, f0_.rows * f0_.cols * sizeof(float),
-                              cudaMemcpyDeviceToDevice, st_));
-    else
-      copy_block_launch(src, ds.ld_features, f0_.rows, f0_.cols, f0_.p(), f0_.ld, st_);
-  }
-  f0_m_.alloc(f0_.rows, f0_.cols);
-  f0_v_.alloc(f0_.rows, f0_.cols);
-  df0_.alloc(f0_.rows, f0_.cols);
-  f0_step_ = 0;
-  // weights (global init, then weight_slice) + Adam state
-  w_.resize(L_), w_m_.resize(L_), w_v_.resize(L_), dw_.resize(L_);
-  wfull_.resize(L_), dwp_.resize(L_), h_.resize(L_), q_.resize(L_), fout_.resize(L_);
-  i64 max_dq = 1, max_dh = 1, max_df = 1;
-  for (int l = 0; l < L_; ++l) {
-    const Shapes& s = shapes_[l];
-    const Slice ws = weight_slice(grid_, lays_[l], c_, dims_[l], dims_[l + 1]);
-    w_[l].alloc(ws.r1 - ws.r0, ws.c1 - ws.c0);
-    auto blk = init_weight_block(cfg_.seed, l, dims_[l], dims_[l + 1], ws);
-    upload_block(w_[l], blk.data(), w_[l].cols, st_);
-    PK_CUDA(cudaStreamSynchronize(st_));
-    w_m_[l].alloc(w_[l].rows, w_[l].cols);
-    w_v_[l].alloc(w_[l].rows, w_[l].cols);
-    dw_[l].alloc(w_[l].rows, w_[l].cols);
-    wfull_[l].alloc(s.f_cols, s.w_cols);
-    dwp_[l].alloc(s.f_cols, s.w_cols);
-    h_[l].alloc(s.h_rows, s.h_cols);
-    q_[l].alloc(s.q_rows, s.q_cols);
-    if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols);
-    max_dq = std::max(max_dq, s.q_rows * pad4(s.q_cols));
-    max_dh = std::max(max_dh, s.h_rows * pad4(s.h_cols));
-    max_df = std::max(max_df, s.a_cols * pad4(s.f_cols));
-  }
-  w_step_ = 0;
-  f0g_.alloc(shapes_[0].f_rows, shapes_[0].f_cols);
-  dq_.buf.alloc(max_dq);
-  dh_.buf.alloc(max_dh);
-  df_.buf.alloc(max_df);
-  df_prev_.buf.alloc(max_df);
-  PK_CUDA(cudaMemset(dq_.buf.p, 0, dq_.buf.n * sizeof(float)));
-  PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
-  PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
-  PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
-  PK_CUDA(cudaStreamSynchronize(0));
+  set_f0(ds.features + fs.r0 * ds.ld_features + fs.c0, ds.ld_features);
+  alloc_params();
   // labels / mask of this rank's logit rows (trainer.hpp:241-248)
-  const Shapes& sl = shapes_[L_ - 1];
   const int parity = (L_ - 1) % 2;
   const auto lr_rng = label_row_range(grid_, c_, n, L_);
-  const i64 lrows = lr_rng.second - lr_rng.first;
-  check(lrows == sl.a_rows, "engine: label rows disagree with the logits shard");
-  labels_.alloc(std::max<i64>(1, lrows));
-  mask_.alloc(std::max<i64>(1, lrows));
-  if (lrows) {
-    PK_CUDA(cudaMemcpyAsync(labels_.p, (parity ? ds.labels_col : ds.labels_row) + lr_rng.first,
-                            lrows * sizeof(u32), cudaMemcpyDeviceToDevice, st_));
-    PK_CUDA(cudaMemcpyAsync(mask_.p, (parity ? ds.mask_col : ds.mask_row) + lr_rng.first, lrows,
-                            cudaMemcpyDeviceToDevice, st_));
-  }
   // global CE count = masked nodes over all row chunks (the label ranges of
   // the last layer's row group partition [0, n)); constant across epochs, so
   // the gradient scaling can ride in the CE kernel
+  u64 count = 0;
   {
     std::vector<u8> hm(n);
     PK_CUDA(cudaMemcpyAsync(hm.data(), parity ? ds.mask_col : ds.mask_row, n,
                             cudaMemcpyDeviceToHost, st_));
     PK_CUDA(cudaStreamSynchronize(st_));
-    mask_count_ = 0;
-    for (u8 m : hm) mask_count_ += m != 0;
+    for (u8 m : hm) count += m != 0;
   }
-  logits_.alloc(sl.a_rows, dims_[L_]);
-  dl_.alloc(sl.a_rows, dims_[L_]);
-  stage_.alloc(sl.a_rows, dims_[L_]);
-  // DMat::alloc zeroes on the legacy stream: drain everything before use
-  PK_CUDA(cudaDeviceSynchronize());
+  set_labels((parity ? ds.labels_col : ds.labels_row) + lr_rng.first,
+             (parity ? ds.mask_col : ds.mask_row) + lr_rng.first,
+             lr_rng.second - lr_rng.first, count);
   mark("params, activations");
+  loaded_ = true;
+}
+
+// The file_handle path (trainer.hpp:461-466): the rank's own tensors.
+void Engine::load_rank(const pk_rank_view& rv) {
+  PK_CUDA(cudaSetDevice(cfg_.device));
+  const i64 n = cfg_.n;
+  auto mark = [](const char*) {};
+  for (auto [plane, parity] : needed_adjacency_keys(L_)) {
+    const pk_csr& b = rv.adj[plane * 2 + parity];
+    const Slice r = adjacency_block_range(grid_, plane, c_, n);
+    check(b.rows == r.r1 - r.r0 && b.cols == r.c1 - r.c0,
+          "engine load_rank: adjacency block (" + std::to_string(plane) + ", " +
+              std::to_string(parity) + ") is " + std::to_string(b.rows) + "x" +
+              std::to_string(b.cols) + ", expected " + std::to_string(r.r1 - r.r0) + "x" +
+              std::to_string(r.c1 - r.c0));
+    std::shared_ptr<AdjShard> same;
+    for (auto& prev : shards_)
+      if (prev && prev->parity == parity && prev->r0 == r.r0 && prev->r1 == r.r1 &&
+          prev->c0 == r.c0 && prev->c1 == r.c1)
+        same = prev;
+    if (same) {
+      shards_[plane * 2 + parity] = same;
+      continue;
+    }
+    auto sh = std::make_shared<AdjShard>();
+    sh->parity = parity, sh->r0 = r.r0, sh->r1 = r.r1, sh->c0 = r.c0, sh->c1 = r.c1;
+    csr_block(b, 0, b.rows, 0, b.cols, &sh->a, st_);  // an all-columns block: a plain copy
+    finish_shard(std::move(sh), plane, parity, mark);
+  }
+  const Slice fs = feature_slice(grid_, c_, n, dims_[0]);
+  check(rv.f0_rows == fs.r1 - fs.r0 && rv.f0_cols == fs.c1 - fs.c0,
+        "engine load_rank: F0 shard shape disagrees with feature_slice");
+  set_f0(rv.f0, rv.ld_f0);
+  alloc_params();
+  // global CE count: this rank's masked label rows summed over the last
+  // layer's row_shard group (its label ranges partition [0, n))
+  const Layout& last = lays_[L_ - 1];
+  double count = 0;
+  if (rv.label_rows) {
+    std::vector<u8> hm(rv.label_rows);
+    PK_CUDA(cudaMemcpyAsync(hm.data(), rv.mask, hm.size(), cudaMemcpyDeviceToHost, st_));
+    PK_CUDA(cudaStreamSynchronize(st_));
+    for (u8 m : hm) count += m != 0;
+  }
+  if (grid_.extent(last.row) > 1) {
+    check(comms_.ready(), "engine load_rank: comm_init before loading a multi-rank grid");
+    DevBuf<double> d(1);
+    PK_CUDA(cudaMemcpyAsync(d.p, &count, sizeof(double), cudaMemcpyHostToDevice, st_));
+    comms_.all_reduce_f64(d.p, 1, last.row, st_);
+    PK_CUDA(cudaMemcpyAsync(&count, d.p, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    PK_CUDA(cudaStreamSynchronize(st_));
+  }
+  set_labels(rv.labels, rv.mask, rv.label_rows, static_cast<u64>(count));
   loaded_ = true;
 }
 
@@ -844,6 +921,13 @@ int pk_engine_load(pk_engine* e, const pk_dataset_view* ds) {
 
 int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds) {
   return guard([&] { e->e->load(*ds, true); });
+}
+
+int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rv) {
+  return guard([&] {
+    check(e && rv, "engine load_rank: null argument");
+    e->e->load_rank(*rv);
+  });
 }
 
 int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss, double* acc) {

@@ -69,6 +69,7 @@ class Engine {
 
   void comm_init(const void* uid, int world_size) { comms_.init(grid_, rank_, uid, world_size); }
   void load(const pk_dataset_view& ds, bool host);
+  void load_rank(const pk_rank_view& rv);
   // rank_forward_backward (trainer.hpp:478-527): returns loss/accuracy
   void forward_backward(int epoch, double* loss, double* acc);
   void optimizer_step();
@@ -138,6 +139,12 @@ class Engine {
   u64 spmm_flops_ = 0, gemm_flops_ = 0;
   double spmm_bytes_ = 0;
   bool loaded_ = false;
+  // load pieces shared by load() and load_rank()
+  template <typename Mark>
+  void finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, Mark& mark);
+  void set_f0(const float* src, i64 ld);
+  void alloc_params();
+  void set_labels(const u32* labels, const u8* mask, i64 lrows, u64 global_count);
 };
 
 }  // namespace pk

@@ -64,6 +64,10 @@ class ShardManifest:
     nnz_odd: int
     files: List[ShardFileInfo]
 
+    @property
+    def num_classes(self):  # DatasetHandle's shape metadata (trainer.hpp:443-450)
+        return self.classes
+
     def file(self, i, j) -> ShardFileInfo:
         if not (0 <= i < self.p and 0 <= j < self.q):
             raise ContractError("manifest: shard index out of range")

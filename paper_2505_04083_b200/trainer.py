@@ -53,6 +53,12 @@ class pk_epoch_metrics(C.Structure):
                 ("reducescatter_bytes", C.c_double)]
 
 
+class pk_rank_view(C.Structure):
+    _fields_ = [("adj", _capi.pk_csr * 6), ("f0", C.c_void_p), ("f0_rows", C.c_int64),
+                ("f0_cols", C.c_int64), ("ld_f0", C.c_int64), ("labels", C.c_void_p),
+                ("mask", C.c_void_p), ("label_rows", C.c_int64)]
+
+
 class pk_tensor_view(C.Structure):
     _fields_ = [("data", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64),
                 ("ld", C.c_int64)]
@@ -64,6 +70,7 @@ _SIGS = {
     "pk_engine_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
     "pk_engine_load": (C.c_int, [C.c_void_p, C.POINTER(pk_dataset_view)]),
     "pk_engine_load_host": (C.c_int, [C.c_void_p, C.POINTER(pk_dataset_view)]),
+    "pk_engine_load_rank": (C.c_int, [C.c_void_p, C.POINTER(pk_rank_view)]),
     "pk_engine_forward_backward": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double),
                                              C.POINTER(C.c_double)]),
     "pk_engine_optimizer_step": (C.c_int, [C.c_void_p]),
@@ -203,6 +210,15 @@ class RankEngine:
         call("pk_engine_comm_init", self.h, C.cast(buf, C.c_void_p), world_size)
 
     def load(self, pre):
+        """A PreprocessedDataset (device), a HostDataset (pinned host), or a
+        shard manifest — the file_handle path (trainer.hpp:461-466): this
+        rank reads only its blocks (shard_io.load_rank_shards)."""
+        from . import shard_io
+        if isinstance(pre, shard_io.ShardManifest):
+            rt = shard_io.load_rank_shards(pre, self.grid, self.grid.coords_of(self.rank),
+                                           len(self.dims) - 1)
+            self.load_rank(rt)
+            return
         if isinstance(pre, HostDataset):
             v = pre.view()
             call("pk_engine_load_host", self.h, C.byref(v))
@@ -210,6 +226,20 @@ class RankEngine:
             v = dataset_view(pre)
             torch.cuda.synchronize()
             call("pk_engine_load", self.h, C.byref(v))
+
+    def load_rank(self, rt):
+        """RankTensors (shard_io.RankTensors) -> pk_engine_load_rank."""
+        v = pk_rank_view()
+        for (plane, parity), (blk, _) in rt.adj.items():
+            v.adj[plane * 2 + parity] = blk._view
+        f0 = rt.f0.contiguous()
+        v.f0 = f0.data_ptr() if f0.numel() else None
+        v.f0_rows, v.f0_cols, v.ld_f0 = f0.shape[0], f0.shape[1], f0.shape[1]
+        v.labels = rt.labels.data_ptr() if rt.labels.numel() else None
+        v.mask = rt.mask.data_ptr() if rt.mask.numel() else None
+        v.label_rows = rt.labels.numel()
+        torch.cuda.synchronize()
+        call("pk_engine_load_rank", self.h, C.byref(v))
 
     def forward_backward(self, epoch=0):
         loss, acc = C.c_double(), C.c_double()

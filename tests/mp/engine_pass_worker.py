@@ -41,6 +41,10 @@ def main():
     ap.add_argument("--mode", default="parity")
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--block-count", type=int, default=0)
+    ap.add_argument("--files", default="",
+                    help="write PLXS shards (p x q) here on rank 0 and load every rank "
+                         "from them (the file_handle path)")
+    ap.add_argument("--shard-grid", default="2,3")
     args = ap.parse_args()
     grid = GridConfig(*[int(g) for g in args.grid.split(",")])
     hidden = [int(h) for h in args.hidden.split(",")]
@@ -52,10 +56,18 @@ def main():
                                 hub_threshold=64, block_count=args.block_count)
     pre = graph.preprocess(graph.synth_rmat(args.scale, args.edges, args.feat, args.classes,
                                             seed=2), perm_seed=2)
+    source = pre
+    if args.files:
+        from paper_2505_04083_b200 import shard_io
+        p, q = (int(x) for x in args.shard_grid.split(","))
+        if rank == 0:
+            shard_io.write_shards(pre, p, q, args.files, "worker")
+        dist.barrier()
+        source = shard_io.load_manifest(args.files)
     # --- one pass, reassembled like test_engine.cpp:30-84
     eng = trainer.RankEngine(pre.n, pre.feat_dim, pre.num_classes, grid, rank, opts, local)
     eng.comm_init(D.broadcast_unique_id(trainer.nccl_unique_id), world)
-    eng.load(pre)
+    eng.load(source)
     loss, acc = eng.forward_backward(0)
     L = len(eng.dims) - 1
     mine = {"fout": eng.tensor(trainer.PK_T_FOUT).cpu().numpy(),
@@ -66,7 +78,7 @@ def main():
     allr = [None] * world
     dist.all_gather_object(allr, mine)
     # --- train_distributed over epochs
-    res = D.train_distributed(lambda: pre, grid, opts)
+    res = D.train_distributed(lambda: source, grid, opts)
     report = {"grid": args.grid, "mode": args.mode}
     ok = True
     if rank == 0:

@@ -100,3 +100,13 @@ def test_two_gpu_relu_backward_in_spmm_epilogue(cuda, grid):
     where row_shard is one rank (opt-in variant), same results."""
     rep = _run(2, "--grid", grid, env={"PK_FUSE_RELU_BWD": "2"})
     assert rep["logits_bitwise"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("grid", _grids(2))
+def test_two_gpu_engines_from_shard_files(cuda, grid, tmp_path):
+    """The file_handle path (trainer.hpp:461-466): rank 0 writes a 2x3 PLXS
+    shard set, every rank loads only its blocks from it; same results as the
+    reference's distributed pass and train_distributed."""
+    rep = _run(2, "--grid", grid, "--files", str(tmp_path / "shards"), "--shard-grid", "2,3")
+    assert rep["logits_bitwise"]

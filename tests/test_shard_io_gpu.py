@@ -102,3 +102,24 @@ def test_device_read_detects_corruption(cuda, datasets, tmp_path):
         r.read_feature_rows(0, rows)
     assert e.value.code == "ChecksumMismatch"
     r.read_feature_rows(2, 9)            # partial reads are not checksummed (reference too)
+
+
+def test_engine_from_shard_files_matches_in_memory_load(cuda, datasets):
+    """The file_handle path: an engine loaded with only this rank's blocks
+    read from the files runs the same pass as one loaded from the in-memory
+    dataset (1x1x1; multi-rank grids go through test_multigpu_gpu.py)."""
+    _, layout, shard_io = _mods()
+    from paper_2505_04083_b200 import trainer as tr
+    pre, _, ours, _ = datasets
+    mani = shard_io.load_manifest(ours)
+    opts = tr.TrainOptions(hidden_dims=[16, 16], mode=tr.PK_MODE_PARITY, hub_threshold=64)
+    outs = []
+    for src in (pre, mani):
+        eng = tr.RankEngine(pre.n, pre.feat_dim, pre.num_classes, layout.GridConfig(1, 1, 1), 0,
+                            opts)
+        eng.load(src)
+        m = [eng.train_epoch(e) for e in range(2)]
+        outs.append(([x["loss"] for x in m], eng.tensor(tr.PK_T_FOUT).cpu().numpy()))
+        eng.close()
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
