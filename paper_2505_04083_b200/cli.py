@@ -1,0 +1,333 @@
+"""Command line front end mirroring the reference's tools/main.cpp
+(preprocess / train / rank-configs) over this package. f32 only: the device
+path computes in fp32 (`--precision f64` is refused, exit code 2).
+
+    python -m paper_2505_04083_b200 preprocess --synth rmat:scale=17,edges=2000000 \\
+        --feat-dim 128 --classes 16 --p 2 --q 2 --seed 1 --precision f32 --out shards/
+    python -m paper_2505_04083_b200 train --manifest shards/ --grid 1,1,1 --epochs 10 \\
+        --layers 128,128 --out run/           # torchrun --nproc-per-node N for N ranks
+    python -m paper_2505_04083_b200 rank-configs --stats n=2097152,nnz=116573894,dims=100-256-256-47 --g 8
+
+Exit codes follow main.cpp:20-24 (0 ok, 1 validation, 2 input, 3 output,
+4 resource)."""
+
+import argparse
+import os
+import struct
+import sys
+
+import numpy as np
+
+EXIT_OK, EXIT_VALIDATION, EXIT_INPUT, EXIT_OUTPUT, EXIT_RESOURCE = range(5)
+
+
+class CliError(Exception):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def parse_synth(spec):
+    """'kind:key=value,...' (main.cpp:44-61)."""
+    kind, _, rest = spec.partition(":")
+    params = {}
+    for kv in filter(None, rest.split(",")):
+        k, eq, v = kv.partition("=")
+        if not eq:
+            raise CliError(EXIT_INPUT, f"bad synth parameter '{kv}' (expected key=value)")
+        try:
+            params[k] = float(v)
+        except ValueError:
+            raise CliError(EXIT_INPUT, f"bad synth parameter value in '{kv}'")
+    return kind, params
+
+
+def _ints(s):
+    return [int(x) for x in s.split(",") if x]
+
+
+def ensure_out_dir(d):
+    try:
+        os.makedirs(d, exist_ok=True)
+        probe = os.path.join(d, ".plexuskit_write_probe")
+        open(probe, "w").close()
+        os.remove(probe)
+    except OSError:
+        raise CliError(EXIT_OUTPUT, f"output directory {d} is not writable")
+
+
+def cmd_preprocess(a):
+    import torch
+
+    from . import graph, shard_io
+    if bool(a.edges) == bool(a.synth):
+        raise CliError(EXIT_INPUT, "preprocess needs exactly one of --edges or --synth")
+    if a.precision != "f32":
+        raise CliError(EXIT_INPUT, "this build writes f32 shards (--precision f32)")
+    if a.synth:
+        kind, p = parse_synth(a.synth)
+        if kind != "rmat":
+            raise CliError(EXIT_INPUT, f"unknown synth kind '{kind}' (this build: rmat)")
+        ds = graph.synth_rmat(int(p.get("scale", 10)), int(p.get("edges", 0)), a.feat_dim,
+                              a.classes, a.seed, p.get("a", 0.57), p.get("b", 0.19),
+                              p.get("c", 0.19), train_fraction=a.train_fraction)
+    else:
+        ds = load_dataset_files(a)
+    ensure_out_dir(a.out)
+    pre = graph.preprocess(ds, a.seed)
+    m = shard_io.write_shards(pre, a.p, a.q, a.out, a.name)
+    torch.cuda.synchronize()
+    print(f"dataset {a.name}: {pre.n} nodes, {pre.a_even.nnz} nonzeros, {pre.feat_dim} "
+          f"features, {pre.num_classes} classes")
+    print(f"balance (max/mean over {a.p}x{a.q} blocks): double permutation "
+          f"{graph.balance_metric(pre.a_even, a.p, a.q)}")
+    print(f"wrote {len(m.files)} shard files + manifest to {a.out}")
+    return EXIT_OK
+
+
+def load_dataset_files(a):
+    """Edge list ('src dst' per line, '#' comments) + optional labels / mask
+    text files (main.cpp:87-159); features from Philox stream 3 like the
+    reference when no feature file is given."""
+    import torch
+
+    from . import _capi, graph
+    try:
+        uv = []
+        with open(a.edges) as f:
+            for lineno, line in enumerate(f, 1):
+                line = line.split("#", 1)[0].split()
+                if not line:
+                    continue
+                if len(line) != 2:
+                    raise CliError(EXIT_INPUT, f"{a.edges}:{lineno}: expected 'src dst' per line")
+                uv.append((int(line[0]), int(line[1])))
+    except OSError:
+        raise CliError(EXIT_INPUT, f"cannot open edge list {a.edges}")
+    e = np.asarray(uv, np.uint64).reshape(-1, 2)
+    n = int(e.max()) + 1 if e.size else 0
+    if a.nodes:
+        if a.nodes < n:
+            raise CliError(EXIT_INPUT, "--nodes is smaller than the largest edge endpoint")
+        n = a.nodes
+    dev = "cuda"
+    edges = torch.from_numpy(e.astype(np.uint32).view(np.int32)).to(dev)
+    feats = torch.empty((n, a.feat_dim), dtype=torch.float32, device=dev)
+    _capi.call("pk_rmat_features", a.seed, n, a.feat_dim, feats.data_ptr(), a.feat_dim, None)
+    if a.labels:
+        lab = np.loadtxt(a.labels, dtype=np.uint64).reshape(-1)
+        if lab.size != n:
+            raise CliError(EXIT_INPUT, "labels file length does not match the node count")
+        classes = max(a.classes, int(lab.max()) + 1)
+        labels = torch.from_numpy(lab.astype(np.uint32).view(np.int32)).to(dev)
+    else:
+        classes = a.classes
+        labels = torch.empty(n, dtype=torch.int32, device=dev)
+        _capi.call("pk_degree_quantile_labels", edges.data_ptr(), edges.shape[0], n, classes,
+                   labels.data_ptr(), None)
+    if a.train_mask:
+        mk = np.loadtxt(a.train_mask, dtype=np.int64).reshape(-1)
+        if mk.size != n:
+            raise CliError(EXIT_INPUT, "mask file length does not match the node count")
+        mask = torch.from_numpy((mk != 0).astype(np.uint8)).to(dev)
+    else:
+        mask = torch.ones(n, dtype=torch.uint8, device=dev)
+    return graph.GraphDataset(n, edges, feats, labels, classes, mask, not a.directed)
+
+
+def write_model_file(weights, features, path):
+    """write_model_file (shard_io.hpp:640-662): PLXM, f32."""
+    with open(path, "wb") as f:
+        f.write(b"PLXM" + struct.pack("<III", 1, 4, len(weights)))
+        for m in list(weights) + [features]:
+            m = np.ascontiguousarray(m, np.float32)
+            f.write(struct.pack("<QQ", m.shape[0], m.shape[1]))
+            f.write(m.tobytes())
+
+
+METRIC_COLS = ("loss", "accuracy", "load_s", "forward_spmm_s", "forward_gemm_s", "backward_s",
+               "optimizer_s", "collectives_s", "spmm_flops", "gemm_flops", "allreduce_bytes",
+               "allgather_bytes", "reducescatter_bytes")
+
+
+def cmd_train(a):
+    import torch
+
+    from . import distributed as D, perf_model as pm, shard_io, trainer
+    from .layout import GridConfig
+    mani = shard_io.load_manifest(a.manifest)
+    if a.precision and a.precision != ("f32" if mani.precision == 4 else "f64"):
+        raise CliError(EXIT_INPUT, f"--precision {a.precision} does not match the manifest")
+    if mani.precision != 4:
+        raise CliError(EXIT_INPUT, "this build trains f32 manifests")
+    hidden = _ints(a.layers)
+    if a.grid == "auto":
+        if not a.machine:
+            raise CliError(EXIT_INPUT, "--grid auto requires --machine")
+        if a.ranks < 1:
+            raise CliError(EXIT_INPUT, "--grid auto requires --ranks")
+        machine = pm.machine_from_json_file(a.machine)
+        coeffs = pm.coefficients_from_json_file(a.coeffs) if a.coeffs \
+            else pm.default_coefficients()
+        stats = pm.DatasetStats(mani.n, mani.nnz_even,
+                                trainer.model_dims(mani.feat_dim, hidden, mani.classes))
+        best = pm.rank_configs(a.ranks, stats, machine, coeffs)[0]
+        shape = best.shape
+        print(f"auto-selected grid {shape[0]}x{shape[1]}x{shape[2]} (predicted "
+              f"{best.total_seconds} s/epoch)")
+    else:
+        shape = tuple(_ints(a.grid))
+        if len(shape) != 3:
+            raise CliError(EXIT_INPUT, "--grid expects X,Y,Z or 'auto'")
+    grid = GridConfig(*shape)
+    rank, world, local = D.dist_env()
+    torch.cuda.set_device(local)
+    opts = trainer.TrainOptions(hidden_dims=hidden, epochs=a.epochs, lr=a.lr, seed=a.seed,
+                                block_count=a.block_count,
+                                mode=trainer.PK_MODE_FAST if a.mode == "fast"
+                                else trainer.PK_MODE_PARITY)
+    res = D.train_distributed(lambda: mani, grid, opts)
+    if rank != 0:
+        return EXIT_OK
+    ensure_out_dir(a.out)
+    with open(os.path.join(a.out, "metrics.csv"), "w") as f:
+        f.write("epoch,rank," + ",".join(METRIC_COLS) + "\n")
+        for e in range(a.epochs):
+            rows = [(str(r), res.per_rank[r][e]) for r in range(grid.size)]
+            rows.append(("global", res.global_metrics[e]))
+            for name, m in rows:
+                f.write(f"{e},{name}," + ",".join(str(m.get(k, 0)) for k in METRIC_COLS) + "\n")
+    g = res.global_metrics
+    first = 2 if len(g) > 2 else 0  # average_window, main.cpp:213-231
+    avg = {k: float(np.mean([m.get(k, 0.0) for m in g[first:]])) for k in METRIC_COLS}
+    with open(os.path.join(a.out, "summary.csv"), "w") as f:
+        f.write("grid,epochs,averaged_from_epoch,loss,accuracy,forward_spmm_s,forward_gemm_s,"
+                "backward_s,optimizer_s,collectives_s\n")
+        f.write(f"{grid.gx}x{grid.gy}x{grid.gz},{a.epochs},{first},{avg['loss']},"
+                f"{avg['accuracy']},{avg['forward_spmm_s']},{avg['forward_gemm_s']},"
+                f"{avg['backward_s']},{avg['optimizer_s']},{avg['collectives_s']}\n")
+    write_model_file(res.weights, res.features, os.path.join(a.out, "model.plxm"))
+    print(f"trained {a.epochs} epochs on grid {grid.gx}x{grid.gy}x{grid.gz}: loss "
+          f"{g[0]['loss']} -> {g[-1]['loss']}, accuracy {g[-1]['accuracy']}")
+    print(f"wrote metrics.csv, summary.csv, model.plxm to {a.out}")
+    return EXIT_OK
+
+
+def cmd_rank_configs(a):
+    from . import perf_model as pm, shard_io, trainer
+    hidden = _ints(a.layers)
+    if a.manifest:
+        m = shard_io.load_manifest(a.manifest)
+        stats = pm.DatasetStats(m.n, m.nnz_even, trainer.model_dims(m.feat_dim, hidden, m.classes))
+    elif a.stats:
+        kv = {}
+        for part in a.stats.split(","):
+            k, eq, v = part.partition("=")
+            if not eq:
+                raise CliError(EXIT_INPUT, f"bad --stats entry '{part}'")
+            kv[k] = v
+        try:
+            stats = pm.DatasetStats(int(kv["n"]), int(kv["nnz"]),
+                                    [int(d) for d in kv["dims"].split("-")])
+        except (KeyError, ValueError):
+            raise CliError(EXIT_INPUT, "--stats expects n=..,nnz=..,dims=D0-H1-...-C")
+    else:
+        raise CliError(EXIT_INPUT, "rank-configs needs --manifest or --stats")
+    machine = pm.machine_from_json_file(a.machine) if a.machine else pm.MachineParams()
+    if a.fit_samples:
+        coeffs = pm.fit_regression(pm.samples_from_csv_file(a.fit_samples))
+        print(f"fitted coefficients: c1={coeffs.c1} c2={coeffs.c2} c3={coeffs.c3} "
+              f"(train R2 {coeffs.train_r2}, RMSE {coeffs.train_rmse})")
+        if a.coeffs_out:
+            pm.coefficients_to_json_file(coeffs, a.coeffs_out)
+    elif a.coeffs:
+        coeffs = pm.coefficients_from_json_file(a.coeffs)
+    else:
+        coeffs = pm.default_coefficients()
+        print("warning: no coefficients supplied, using built-in defaults", file=sys.stderr)
+    ranked = pm.rank_configs(a.g, stats, machine, coeffs)
+    print("gx,gy,gz,spmm_s,comm_s,total_s")
+    for p in ranked:
+        print(f"{p.shape[0]},{p.shape[1]},{p.shape[2]},{p.spmm_seconds},{p.comm_seconds},"
+              f"{p.total_seconds}" + (" (spmm clamped to 0)" if p.clamped else ""))
+    if a.csv:
+        try:
+            with open(a.csv, "w") as f:
+                f.write("gx,gy,gz,spmm_s,comm_s,total_s,clamped\n")
+                for p in ranked:
+                    f.write(f"{p.shape[0]},{p.shape[1]},{p.shape[2]},{p.spmm_seconds},"
+                            f"{p.comm_seconds},{p.total_seconds},{int(p.clamped)}\n")
+        except OSError:
+            raise CliError(EXIT_OUTPUT, f"cannot write {a.csv}")
+    return EXIT_OK
+
+
+def build_parser():
+    ap = argparse.ArgumentParser(prog="paper_2505_04083_b200",
+                                 description="3D tensor-parallel full-graph GCN training on B200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    p = sub.add_parser("preprocess", help="synthesize or ingest a graph, write PLXS shards")
+    p.add_argument("--edges", default="")
+    p.add_argument("--synth", default="")
+    p.add_argument("--labels", default="")
+    p.add_argument("--train-mask", default="")
+    p.add_argument("--nodes", type=int, default=0)
+    p.add_argument("--feat-dim", type=int, default=128)
+    p.add_argument("--classes", type=int, default=32)
+    p.add_argument("--train-fraction", type=float, default=1.0)
+    p.add_argument("--directed", action="store_true")
+    p.add_argument("--p", type=int, default=8)
+    p.add_argument("--q", type=int, default=8)
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--precision", default="f32")
+    p.add_argument("--name", default="dataset")
+    p.add_argument("--out", required=True)
+    t = sub.add_parser("train", help="train from shards (torchrun for several ranks)")
+    t.add_argument("--manifest", required=True)
+    t.add_argument("--grid", default="1,1,1")
+    t.add_argument("--ranks", type=int, default=0)
+    t.add_argument("--epochs", type=int, default=10)
+    t.add_argument("--layers", default="128,128")
+    t.add_argument("--seed", type=int, default=0)
+    t.add_argument("--precision", default="")
+    t.add_argument("--lr", type=float, default=1e-2)
+    t.add_argument("--block-count", type=int, default=0)
+    t.add_argument("--mode", default="fast", choices=["fast", "parity"],
+                   help="fast: tcgen05 3xTF32 GEMMs, segmented hub rows; parity: bit-exact")
+    t.add_argument("--machine", default="")
+    t.add_argument("--coeffs", default="")
+    t.add_argument("--out", default="train_out")
+    r = sub.add_parser("rank-configs", help="rank grid shapes with the performance model")
+    r.add_argument("--manifest", default="")
+    r.add_argument("--stats", default="")
+    r.add_argument("--layers", default="128,128")
+    r.add_argument("--g", type=int, required=True)
+    r.add_argument("--machine", default="")
+    r.add_argument("--coeffs", default="")
+    r.add_argument("--fit-samples", default="")
+    r.add_argument("--coeffs-out", default="")
+    r.add_argument("--csv", default="")
+    return ap
+
+
+def main(argv=None):
+    from ._capi import ContractError, IoError, MemoryError_, TrainingError
+    a = build_parser().parse_args(argv)
+    try:
+        return {"preprocess": cmd_preprocess, "train": cmd_train,
+                "rank-configs": cmd_rank_configs}[a.cmd](a)
+    except CliError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return e.code
+    except IoError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_OUTPUT if e.code == "WriteFailed" else EXIT_INPUT
+    except TrainingError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_VALIDATION
+    except MemoryError_ as e:
+        print(f"error: out of memory: {e}", file=sys.stderr)
+        return EXIT_RESOURCE
+    except ContractError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_INPUT

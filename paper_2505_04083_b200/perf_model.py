@@ -24,12 +24,7 @@ AXES = {"X": 0, "Y": 1, "Z": 2}
 COLL_OPS = {"all_gather": 0, "all_reduce": 1, "reduce_scatter": 2}
 
 
-class IoError(RuntimeError):
-    """plexuskit::IoError (common.hpp:28-45)."""
-
-    def __init__(self, code, msg):
-        super().__init__(msg)
-        self.code = code
+IoError = _capi.IoError  # plexuskit::IoError (common.hpp:28-45); code = IoErrorCode name
 
 
 class pk_dataset_stats(C.Structure):
@@ -256,16 +251,16 @@ def rank_configs(g: int, stats: DatasetStats, machine: MachineParams,
 
 
 # --------------------------------------------------------------- files
-# IoErrorCode (common.hpp:28-37): MissingFile=1, BadFormat=2, WriteFailed=4
+# IoErrorCode (common.hpp:28-37) by name: MissingFile, BadFormat, WriteFailed
 
 def _read_json(path, what):
     try:
         with open(path) as f:
             return json.load(f)
     except FileNotFoundError:
-        raise IoError(1, f"cannot open {what} file {path}")
+        raise IoError("MissingFile", f"cannot open {what} file {path}")
     except (json.JSONDecodeError, UnicodeDecodeError) as exc:
-        raise IoError(2, f"{what} file {path}: {exc}")
+        raise IoError("BadFormat", f"{what} file {path}: {exc}")
 
 
 def machine_from_json_file(path) -> MachineParams:
@@ -286,7 +281,7 @@ def coefficients_from_json_file(path) -> PerfCoefficients:
         return PerfCoefficients(float(j["c1"]), float(j["c2"]), float(j["c3"]),
                                 float(j.get("train_r2", 0.0)), float(j.get("train_rmse", 0.0)))
     except KeyError as exc:
-        raise IoError(2, f"coefficients file {path}: missing {exc}")
+        raise IoError("BadFormat", f"coefficients file {path}: missing {exc}")
 
 
 def coefficients_to_json_file(c: PerfCoefficients, path):
@@ -296,7 +291,7 @@ def coefficients_to_json_file(c: PerfCoefficients, path):
                        "train_rmse": c.train_rmse}, f, indent=2)
             f.write("\n")
     except OSError:
-        raise IoError(4, f"cannot write coefficients file {path}")
+        raise IoError("WriteFailed", f"cannot write coefficients file {path}")
 
 
 def samples_from_csv_file(path) -> List[RegressionSample]:
@@ -305,14 +300,14 @@ def samples_from_csv_file(path) -> List[RegressionSample]:
     try:
         lines = open(path).read().splitlines()
     except FileNotFoundError:
-        raise IoError(1, f"cannot open sample log {path}")
+        raise IoError("MissingFile", f"cannot open sample log {path}")
     head = lines[0].split(",") if lines else []
     if len(head) == 4 and head[0] == "f1":
         raw = False
     elif len(head) == 7 and head[0] == "n":
         raw = True
     else:
-        raise IoError(2, f"sample log {path}: expected header f1,f2,f3,seconds or "
+        raise IoError("BadFormat", f"sample log {path}: expected header f1,f2,f3,seconds or "
                          "n,nnz,dims,gx,gy,gz,seconds")
     out = []
     for line in lines[1:]:
@@ -332,7 +327,7 @@ def samples_from_csv_file(path) -> List[RegressionSample]:
                 out.append(RegressionSample(comp_features(st, (int(f[3]), int(f[4]), int(f[5]))),
                                             float(f[6])))
         except (ValueError, ContractError) as exc:
-            raise IoError(2, f"sample log {path}: bad row '{line}': {exc}")
+            raise IoError("BadFormat", f"sample log {path}: bad row '{line}': {exc}")
     return out
 
 

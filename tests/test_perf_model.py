@@ -166,7 +166,7 @@ def test_files_round_trip(tmp_path):
     assert (m.g_node, m.beta_intra, m.beta_inter) == (8, 7.25e11, 25e9)
     with pytest.raises(pm.IoError) as e:
         pm.machine_from_json_file(tmp_path / "missing.json")
-    assert e.value.code == 1
+    assert e.value.code == "MissingFile"
     csv = tmp_path / "s.csv"
     csv.write_text("n,nnz,dims,gx,gy,gz,seconds\n2449029,126167053,100-256-256-47,2,2,2,0.0123\n")
     s = pm.samples_from_csv_file(csv)
