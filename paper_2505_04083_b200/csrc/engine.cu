@@ -328,33 +328,46 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   DevBuf<u32> eci, oci, lr, lc;
   DevBuf<float> ev, ov, feat;
   DevBuf<u8> mr, mc;
+  // Host inputs are staged in HBM on the (idle) comm stream in the order
+  // they are consumed — even variant, odd variant, features, labels — and
+  // each piece's event gates its consumer on st_, so the shards of one
+  // variant are cut, transposed and planned while the next one uploads.
+  cudaEvent_t staged[4] = {nullptr, nullptr, nullptr, nullptr};  // even, odd, feat, labels
+  auto gate = [&](int i) {
+    if (staged[i]) PK_CUDA(cudaStreamWaitEvent(st_, staged[i], 0));
+  };
   if (host) {
+    for (auto& e : staged) PK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     auto up = [&](auto& buf, const auto* src, size_t count) {
       buf.alloc(count ? count : 1);
       if (count)
-        PK_CUDA(cudaMemcpyAsync(buf.p, src, count * sizeof(*src), cudaMemcpyHostToDevice, st_));
+        PK_CUDA(cudaMemcpyAsync(buf.p, src, count * sizeof(*src), cudaMemcpyHostToDevice, cs_));
       return buf.p;
     };
     ds.a_even.row_ptr = up(erp, dsin.a_even.row_ptr, n + 1);
     ds.a_even.col_idx = up(eci, dsin.a_even.col_idx, dsin.a_even.nnz);
     ds.a_even.values = up(ev, dsin.a_even.values, dsin.a_even.nnz);
+    PK_CUDA(cudaEventRecord(staged[0], cs_));
     ds.a_odd.row_ptr = up(orp, dsin.a_odd.row_ptr, n + 1);
     ds.a_odd.col_idx = up(oci, dsin.a_odd.col_idx, dsin.a_odd.nnz);
     ds.a_odd.values = up(ov, dsin.a_odd.values, dsin.a_odd.nnz);
+    PK_CUDA(cudaEventRecord(staged[1], cs_));
     feat.alloc(static_cast<size_t>(n * dims_[0]));
     if (dsin.ld_features == dims_[0])  // one DMA: a pitched copy moves row by row
       PK_CUDA(cudaMemcpyAsync(feat.p, dsin.features, n * dims_[0] * sizeof(float),
-                              cudaMemcpyHostToDevice, st_));
+                              cudaMemcpyHostToDevice, cs_));
     else
       PK_CUDA(cudaMemcpy2DAsync(feat.p, dims_[0] * sizeof(float), dsin.features,
                                 dsin.ld_features * sizeof(float), dims_[0] * sizeof(float), n,
-                                cudaMemcpyHostToDevice, st_));
+                                cudaMemcpyHostToDevice, cs_));
+    PK_CUDA(cudaEventRecord(staged[2], cs_));
     ds.features = feat.p;
     ds.ld_features = dims_[0];
     ds.labels_row = up(lr, dsin.labels_row, n);
     ds.labels_col = up(lc, dsin.labels_col, n);
     ds.mask_row = up(mr, dsin.mask_row, n);
     ds.mask_col = up(mc, dsin.mask_col, n);
+    PK_CUDA(cudaEventRecord(staged[3], cs_));
     mark("h2d dataset");
   }
   // adjacency shards (build_adjacency_shards, engine.hpp:96-113)
@@ -362,6 +375,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
     const pk_csr& variant = parity ? ds.a_odd : ds.a_even;
     check(variant.rows == n && variant.cols == n,
           "build_adjacency_shards: adjacency variants must be square and equal");
+    gate(parity);
     const Slice r = adjacency_block_range(grid_, plane, c_, n);
     std::shared_ptr<AdjShard> same;
     for (auto& prev : shards_)
@@ -393,6 +407,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   }
   // trainable features F0 (feature_slice, model.hpp:53-67) + Adam state
   const Slice fs = feature_slice(grid_, c_, n, dims_[0]);
+  gate(2);
   set_f0(ds.features + fs.r0 * ds.ld_features + fs.c0, ds.ld_features);
   alloc_params();
   // labels / mask of this rank's logit rows (trainer.hpp:241-248)
@@ -402,6 +417,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   // the last layer's row group partition [0, n)); constant across epochs, so
   // the gradient scaling can ride in the CE kernel
   u64 count = 0;
+  gate(3);
   {
     std::vector<u8> hm(n);
     PK_CUDA(cudaMemcpyAsync(hm.data(), parity ? ds.mask_col : ds.mask_row, n,
@@ -413,6 +429,9 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
              (parity ? ds.mask_col : ds.mask_row) + lr_rng.first,
              lr_rng.second - lr_rng.first, count);
   mark("params, activations");
+  PK_CUDA(cudaStreamSynchronize(cs_));  // the staged uploads are released with this scope
+  for (auto& e : staged)
+    if (e) cudaEventDestroy(e);
   loaded_ = true;
 }
 
