@@ -161,13 +161,25 @@ ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
   }
 }
 
-__global__ void ce_finish_kernel(const double* __restrict__ partial, int blocks,
-                                 double* __restrict__ sums) {
-  if (threadIdx.x != 0) return;
+// one CTA: thread t sums blocks t, t + 256, ... in order, then a fixed tree
+// (deterministic; the per-block partials were summed in a fixed order too)
+constexpr int kCeFinishThreads = 256;
+
+__global__ void __launch_bounds__(kCeFinishThreads)
+ce_finish_kernel(const double* __restrict__ partial, int blocks, double* __restrict__ sums) {
+  __shared__ double sh[kCeFinishThreads][3];
+  const int t = threadIdx.x;
   double a = 0, b = 0, c = 0;
-  for (int i = 0; i < blocks; ++i)
+  for (int i = t; i < blocks; i += kCeFinishThreads)
     a += partial[3 * i], b += partial[3 * i + 1], c += partial[3 * i + 2];
-  sums[0] = a, sums[1] = b, sums[2] = c;
+  sh[t][0] = a, sh[t][1] = b, sh[t][2] = c;
+  __syncthreads();
+  for (int h = kCeFinishThreads / 2; h > 0; h >>= 1) {
+    if (t < h)
+      for (int k = 0; k < 3; ++k) sh[t][k] += sh[t + h][k];
+    __syncthreads();
+  }
+  if (t == 0) sums[0] = sh[0][0], sums[1] = sh[0][1], sums[2] = sh[0][2];
 }
 
 __global__ void scale_kernel(float* __restrict__ d, i64 ldd, i64 rows, i64 cols,
@@ -278,7 +290,7 @@ void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u
     ce_kernel<<<blocks, kCeRows, smem, st>>>(logits, ldl, rows, static_cast<int>(classes), labels,
                                              mask, dl, ldd, ws.partial.p, ws.bad.p, scale_count);
     PK_LAUNCH("cross entropy");
-    ce_finish_kernel<<<1, 32, 0, st>>>(ws.partial.p, blocks, sums);
+    ce_finish_kernel<<<1, kCeFinishThreads, 0, st>>>(ws.partial.p, blocks, sums);
   } else {
     PK_CUDA(cudaMemsetAsync(sums, 0, 3 * sizeof(double), st));
   }
