@@ -178,6 +178,29 @@ __device__ __forceinline__ void tc_commit_mc(u64* bar, unsigned short mask) {
       : "memory");
 }
 
+// arrive on the barrier at the same smem offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_cluster(u64* bar, unsigned rank) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+// CTA-pair commit: arrives on `bar` in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(u64* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(static_cast<unsigned short>(3))
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(unsigned d_tmem, u64 adesc, u64 bdesc,
+                                                 unsigned idesc, unsigned accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -265,10 +288,10 @@ __device__ __forceinline__ u64 smem_desc(unsigned addr, unsigned lbo, unsigned s
 
 // Instruction descriptor: fp32 accumulate, tf32 A and B, M = 128; bits 15/16
 // mark an MN-major operand (staged in the 32-B-atom swizzle, see below).
-__host__ __device__ constexpr unsigned instr_desc(int n, bool a_mn, bool b_mn) {
+__host__ __device__ constexpr unsigned instr_desc(int n, bool a_mn, bool b_mn, int m = kBM) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<unsigned>(a_mn) << 15) |
          (static_cast<unsigned>(b_mn) << 16) | (static_cast<unsigned>(n >> 3) << 17) |
-         (static_cast<unsigned>(kBM >> 4) << 24);
+         (static_cast<unsigned>(m >> 4) << 24);
 }
 
 // ------------------------------------------------------------ tile layout
@@ -466,6 +489,10 @@ struct TcConfig {
   static constexpr int kRA = std::min(8, (kRingBudget - kRB * 2 * kTileB - kRL * kTileA) / kTileA);
   static constexpr size_t kSmemRing =
       static_cast<size_t>(kRA + kRL) * kTileA + static_cast<size_t>(kRB) * 2 * kTileB + 1024;
+  // CTA-pair rings: each CTA keeps half of every weight image (its N/2 rows)
+  static constexpr int kRAPair = std::min(8, (kRingBudget - kRB * kTileB - kRL * kTileA) / kTileA);
+  static constexpr size_t kSmemPair =
+      static_cast<size_t>(kRAPair + kRL) * kTileA + static_cast<size_t>(kRB) * kTileB + 1024;
 };
 
 // TMA: the big operands arrive by TMA as raw fp32 tiles (the tensor core's
@@ -479,17 +506,33 @@ struct TcConfig {
 // all `empty` barriers). The weight's L2 -> SM traffic drops CS-fold. A CTA
 // whose own tile runs past the end follows its cluster through a phantom
 // tile (A zero-filled by TMA, nothing stored).
-template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE, bool TMA, int CS>
+//
+// PAIR (TMA + weight image, one n tile, no k split; launched as 2-CTA
+// clusters): the ring kernel as a CTA pair — tcgen05.mma.cta_group::2 with
+// M = 256, each CTA supplying its 128 A rows and half of the weight image's
+// N rows, so each SM's shared memory feeds a third less operand traffic per
+// MMA. The leader (rank 0) issues the MMAs; both CTAs load, convert and
+// drain their own TMEM half; the peer's converters and epilogue warps
+// arrive on the leader's barriers across the cluster, and the leader's
+// commits release both CTAs' stages.
+template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE, bool TMA, int CS, bool PAIR = false>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     gemm_tc_kernel(TcParams p, const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b) {
   using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
   static_assert(!TMA || B_PRE || B_T, "TMA path: a streamed B must be MN-major");
   static_assert(CS == 1 || (TMA && B_PRE), "clusters need the TMA + weight-image path");
+  static_assert(!PAIR || (TMA && B_PRE && CS == 2 && !A_T && BN % 32 == 0),
+                "CTA pairs: TMA K-major A, weight image, 2-CTA clusters, BN % 32 == 0");
   constexpr unsigned short kMask = static_cast<unsigned short>((1u << CS) - 1u);
   const int crank = CS > 1 ? static_cast<int>(cluster_rank()) : 0;
-  constexpr bool kRing = TMA && B_PRE && CS == 1;
-  constexpr int kRA = Cfg::kRA, kRL = Cfg::kRL, kRB = Cfg::kRB;
+  constexpr bool kRing = TMA && B_PRE && (CS == 1 || PAIR);
+  constexpr int kRA = PAIR ? Cfg::kRAPair : Cfg::kRA, kRL = Cfg::kRL, kRB = Cfg::kRB;
+  constexpr int kBSlot = PAIR ? Cfg::kTileB : 2 * Cfg::kTileB;  // bytes of one weight slot
+  const bool leader = !PAIR || crank == 0;
+  // pair mode walks pair tiles: one index per cluster, CTA rank picks the half
+  const int tile_first = PAIR ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int tile_step = PAIR ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
   static_assert(!kRing || kRA >= 2, "ring layout: at least two raw stages");
 #ifdef PK_TC_PROF
   const long long t_kernel = clock64();
@@ -515,20 +558,28 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], PAIR ? 8 : 4);  // pair: both CTAs' epilogue warps
     }
     if constexpr (kRing) {
       for (int i = 0; i < kRA; ++i) mbar_init(&ra_full[i], 1), mbar_init(&ra_empty[i], 1);
-      for (int i = 0; i < kRL; ++i) mbar_init(&rl_full[i], kConvRingWarps), mbar_init(&rl_empty[i], 1);
+      for (int i = 0; i < kRL; ++i)
+        mbar_init(&rl_full[i], (PAIR ? 2 : 1) * kConvRingWarps), mbar_init(&rl_empty[i], 1);
       for (int i = 0; i < kRB; ++i) mbar_init(&rb_full[i], 1), mbar_init(&rb_empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base)),
-                 "n"(Cfg::kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base)),
+                   "n"(Cfg::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base)),
+                   "n"(Cfg::kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -536,12 +587,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   tc_fence_after();
   const unsigned tmem = tmem_base;
 
-  const int total_tiles = p.m_tiles * p.n_tiles * p.splits;
+  const int total_tiles = PAIR ? (p.m_tiles + 1) / 2 : p.m_tiles * p.n_tiles * p.splits;
   // a tile index is live while its cluster leader's is (phantoms beyond)
-  auto live = [&](int t) { return t - crank < total_tiles; };
+  auto live = [&](int t) { return PAIR ? t < total_tiles : t - crank < total_tiles; };
   // n tile fastest: the CTAs that share an A row block (several n tiles)
   // run side by side, so A comes from DRAM once and from L2 after
   auto tile_coords = [&](int t, int& mt, int& nt, int& sp) {
+    if (PAIR) {  // the pair's 256 rows: this CTA's 128 (zero-filled past m)
+      mt = 2 * t + crank, nt = 0, sp = 0;
+      return;
+    }
     if (CS > 1 && t >= total_tiles) {  // phantom: past the last m tile
       mt = p.m_tiles, nt = 0, sp = 0;
       return;
@@ -573,11 +628,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       q.n0 = static_cast<i64>(nt) * BN;
       q.nk = static_cast<int>((q.ke - q.kb + kBK - 1) / kBK);
       if (q.nk > 0) return;
-      q.t += gridDim.x;  // empty k range: the MMA warp signals it without stages
+      q.t += tile_step;  // empty k range: the MMA warp signals it without stages
     }
   };
   auto advance = [&](Pos& q) {
-    if (++q.kk == q.nk) start(q, q.t + gridDim.x);
+    if (++q.kk == q.nk) start(q, q.t + tile_step);
   };
   auto valid = [&](const Pos& q) { return live(q.t); };
 
@@ -585,8 +640,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   auto ra_slot = [&](int i) { return smem + static_cast<size_t>(i) * Cfg::kTileA; };
   auto rl_slot = [&](int i) { return smem + static_cast<size_t>(kRA + i) * Cfg::kTileA; };
   auto rb_slot = [&](int i) {
-    return smem + static_cast<size_t>(kRA + kRL) * Cfg::kTileA +
-           static_cast<size_t>(i) * 2 * Cfg::kTileB;
+    return smem + static_cast<size_t>(kRA + kRL) * Cfg::kTileA + static_cast<size_t>(i) * kBSlot;
   };
 
   if (kRing && warp < kLoaderWarps) {
@@ -594,7 +648,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       if (warp == 0 && lane == 0) {
         // ------------------------------------------- raw A producer (DRAM)
         Pos q;
-        start(q, blockIdx.x);
+        start(q, tile_first);
         for (u64 s = 0; valid(q); ++s) {
           const int i = static_cast<int>(s % kRA);
           const unsigned ph = static_cast<unsigned>((s / kRA) & 1);
@@ -609,16 +663,26 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       } else if (warp == 1 && lane == 0) {
         // ------------------------------------- weight image producer (L2)
         Pos q;
-        start(q, blockIdx.x);
+        start(q, tile_first);
         for (u64 s = 0; valid(q); ++s) {
           const int i = static_cast<int>(s % kRB);
           const unsigned ph = static_cast<unsigned>((s / kRB) & 1);
           mbar_wait(&rb_empty[i], ph ^ 1u);
           const i64 k0 = q.kb + static_cast<i64>(q.kk) * kBK;
           const i64 g = q.nt * p.b_stages + k0 / kBK;
-          mbar_expect_tx(&rb_full[i], 2u * Cfg::kTileB);
-          bulk_copy_g2s(rb_slot(i), p.b_image + g * 2 * Cfg::kTileB, 2u * Cfg::kTileB,
-                        &rb_full[i]);
+          if constexpr (PAIR) {
+            // this CTA's N/2 rows of the hi and the lo image (K-major rows
+            // are contiguous 128-B lines, so each half is one block)
+            constexpr unsigned kHalf = Cfg::kTileB / 2;
+            const unsigned char* img = p.b_image + g * 2 * Cfg::kTileB + crank * kHalf;
+            mbar_expect_tx(&rb_full[i], 2u * kHalf);
+            bulk_copy_g2s(rb_slot(i), img, kHalf, &rb_full[i]);
+            bulk_copy_g2s(rb_slot(i) + kHalf, img + Cfg::kTileB, kHalf, &rb_full[i]);
+          } else {
+            mbar_expect_tx(&rb_full[i], 2u * Cfg::kTileB);
+            bulk_copy_g2s(rb_slot(i), p.b_image + g * 2 * Cfg::kTileB, 2u * Cfg::kTileB,
+                          &rb_full[i]);
+          }
           mbar_arrive(&rb_full[i]);
           advance(q);
         }
@@ -627,7 +691,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         const int ct = threadIdx.x - 64;
         constexpr int kStep = 32 * kConvRingWarps;
         Pos q;
-        start(q, blockIdx.x);
+        start(q, tile_first);
         for (u64 s = 0; valid(q); ++s) {
           const int ia = static_cast<int>(s % kRA), il = static_cast<int>(s % kRL);
           TC_PROF_WAIT(1, mbar_wait(&ra_full[ia], static_cast<unsigned>((s / kRA) & 1)));
@@ -655,8 +719,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             }
           }
           fence_async_smem();
+          if constexpr (PAIR) {
+            // the leader's MMA reads this CTA's weight half and lo tile too:
+            // signal it once both are in place
+            mbar_wait(&rb_full[static_cast<int>(s % kRB)],
+                      static_cast<unsigned>((s / kRB) & 1));
+          }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&rl_full[il]);
+          if (lane == 0) {
+            if (PAIR && crank != 0)
+              mbar_arrive_cluster(&rl_full[il], 0);
+            else
+              mbar_arrive(&rl_full[il]);
+          }
           advance(q);
         }
       }
@@ -668,7 +743,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         int stage = 0;
         unsigned phase = 0;
         Pos q;
-        start(q, blockIdx.x);
+        start(q, tile_first);
         constexpr unsigned kBytes =
             Cfg::kTileA + (B_PRE ? 2u * Cfg::kTileB : static_cast<unsigned>(Cfg::kTileB));
         while (valid(q)) {
@@ -711,7 +786,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         int stage = 0;
         unsigned phase = 0;
         Pos q;
-        start(q, blockIdx.x);
+        start(q, tile_first);
         // shared-window addresses: explicit ld/st.shared (generic pointers
         // compiled to generic LD/ST, measured as the converters' stall)
         // Batches of 4 chunks per thread: four loads in flight, then the
@@ -779,7 +854,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       if constexpr (!B_PRE) Cfg::LoadB::load(p.b, q.n0, k0, q.ke, lt, r.b);
     };
     Pos cur, pre;
-    start(cur, blockIdx.x);
+    start(cur, tile_first);
     pre = cur;
 #pragma unroll
     for (int d = 0; d < kDepth; ++d) {
@@ -817,13 +892,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr unsigned idesc = instr_desc(BN, A_T, B_T && !B_PRE);
+    if (!leader) goto mma_done;  // the pair's MMAs are the leader's
+    {
+    constexpr unsigned idesc = instr_desc(BN, A_T, B_T && !B_PRE, PAIR ? 2 * kBM : kBM);
     int stage = 0;
     unsigned phase = 0;
     u64 ring_s = 0;  // ring mode: k-stages consumed so far
     int acc = 0;
     unsigned acc_phase = 0;
-    for (int t = blockIdx.x; live(t); t += gridDim.x) {
+    for (int t = tile_first; live(t); t += tile_step) {
       int mt, nt, sp;
       tile_coords(t, mt, nt, sp);
       i64 kb, ke;
@@ -845,22 +922,34 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             tc_fence_after();
             if (lane == 0) {
               const unsigned a_hi = smem_u32(ra_slot(ia)), a_lo = smem_u32(rl_slot(il));
-              const unsigned b_hi = smem_u32(rb_slot(ib)), b_lo = b_hi + Cfg::kTileB;
+              const unsigned b_hi = smem_u32(rb_slot(ib)), b_lo = b_hi + kBSlot / 2;
 #pragma unroll
               for (int ks = 0; ks < kBK / 8; ++ks) {
                 const u64 dah = kmajor_desc(a_hi, ks), dal = kmajor_desc(a_lo, ks);
                 const u64 dbh = kmajor_desc(b_hi, ks), dbl = kmajor_desc(b_lo, ks);
                 const unsigned first = (kk == k_lo && ks == 0) ? 0u : 1u;
-                tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
-                tc_mma_tf32(d, dah, dbl, idesc, 1u);
-                tc_mma_tf32(d, dah, dbh, idesc, 1u);
+                if constexpr (PAIR) {
+                  tc_mma_tf32_pair(d, dal, dbh, idesc, first);
+                  tc_mma_tf32_pair(d, dah, dbl, idesc, 1u);
+                  tc_mma_tf32_pair(d, dah, dbh, idesc, 1u);
+                } else {
+                  tc_mma_tf32(d, dal, dbh, idesc, first);  // small terms first
+                  tc_mma_tf32(d, dah, dbl, idesc, 1u);
+                  tc_mma_tf32(d, dah, dbh, idesc, 1u);
+                }
               }
 #ifdef PK_TC_PROF
               prof_acc[7] += 1;
 #endif
-              tc_commit(&ra_empty[ia]);
-              tc_commit(&rl_empty[il]);
-              tc_commit(&rb_empty[ib]);
+              if constexpr (PAIR) {  // release the stage in both CTAs
+                tc_commit_pair(&ra_empty[ia]);
+                tc_commit_pair(&rl_empty[il]);
+                tc_commit_pair(&rb_empty[ib]);
+              } else {
+                tc_commit(&ra_empty[ia]);
+                tc_commit(&rl_empty[il]);
+                tc_commit(&rb_empty[ib]);
+              }
             }
             __syncwarp();
             ++ring_s;
@@ -909,6 +998,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           if (k_hi == k_lo) {
             // empty k range: the epilogue writes zeros without reading TMEM
             mbar_arrive(&tfull[acc]);
+          } else if constexpr (PAIR) {
+            tc_commit_pair(&tfull[acc]);  // both CTAs' epilogues
           } else {
             tc_commit(&tfull[acc]);
           }
@@ -917,13 +1008,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (++acc == 2) acc = 0, acc_phase ^= 1u;
       }
     }
+    }
+  mma_done:;
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
     int acc = 0;
     unsigned acc_phase = 0;
-    for (int t = blockIdx.x; live(t); t += gridDim.x) {
+    for (int t = tile_first; live(t); t += tile_step) {
       int mt, nt, sp;
       tile_coords(t, mt, nt, sp);
       i64 kb, ke;
@@ -997,7 +1090,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if (PAIR && crank != 0)
+            mbar_arrive_cluster(&tempty[acc], 0);  // the leader reuses the pair's TMEM
+          else
+            mbar_arrive(&tempty[acc]);
+        }
         if (++acc == 2) acc = 0, acc_phase ^= 1u;
       }
     }
@@ -1014,8 +1112,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if constexpr (CS > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "n"(Cfg::kTmemCols));
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "n"(Cfg::kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                   "n"(Cfg::kTmemCols));
   }
 }
 
@@ -1125,14 +1227,34 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     const int v = e ? std::atoi(e) : 1;  // measured neutral at 2, slower at 4
     return v >= 4 ? 4 : (v >= 2 ? 2 : 1);
   }();
+  // CTA pairs (tcgen05 cta_group::2, M = 256) for the weight-image forms:
+  // bit-identical, but measured slower on the epoch's shapes (NN 256x256
+  // 1.77 vs 1.44 ms: the leader waits for the slower CTA's conversion every
+  // stage), so opt-in with PK_TC_PAIR=1
+  static const bool pair_pref = [] {
+    const char* e = std::getenv("PK_TC_PAIR");
+    return e && e[0] == '1';
+  }();
   int cs = 1;
   if (B_PRE && tma && p0.n_tiles == 1 && p0.splits == 1)
     while (cs < cluster_pref && p0.m_tiles >= 4 * cs * 2) cs *= 2;
+  const bool pair = B_PRE && !A_T && BN % 32 == 0 && tma && pair_pref && cs == 1 &&
+                    p0.n_tiles == 1 && p0.splits == 1 && p0.m_tiles >= 4;
+  if (pair) cs = 2;
   using KernelT = void (*)(TcParams, const CUtensorMap, const CUtensorMap);
   KernelT kernel;
   int variant;
   if (!tma) {
     kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, false, 1>, variant = 0;
+  } else if constexpr (B_PRE && !A_T && BN % 32 == 0) {
+    if (pair)
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 2, true>, variant = 4;
+    else if (cs == 4)
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 4>, variant = 3;
+    else if (cs == 2)
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 2>, variant = 2;
+    else
+      kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 1>, variant = 1;
   } else if constexpr (B_PRE) {
     if (cs == 4)
       kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 4>, variant = 3;
@@ -1144,8 +1266,9 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     kernel = gemm_tc_kernel<A_T, B_T, BN, STAGES, B_PRE, true, 1>, variant = 1;
   }
   // the single-CTA TMA + weight-image kernel runs the ring layout
-  const size_t smem = (B_PRE && variant == 1) ? Cfg::kSmemRing : Cfg::kSmem;
-  static thread_local bool attr[4] = {false, false, false, false};
+  const size_t smem = variant == 4 ? Cfg::kSmemPair
+                                    : ((B_PRE && variant == 1) ? Cfg::kSmemRing : Cfg::kSmem);
+  static thread_local bool attr[5] = {false, false, false, false, false};
   if (!attr[variant]) {
     PK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
@@ -1164,7 +1287,8 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     PK_LAUNCH("gemm tcgen05 b image");
     p.b_image = img.p;
   }
-  const i64 tiles = static_cast<i64>(p.m_tiles) * p.n_tiles * p.splits;
+  const i64 tiles = pair ? 2 * ((p.m_tiles + 1) / 2)  // one CTA per half of a pair tile
+                        : static_cast<i64>(p.m_tiles) * p.n_tiles * p.splits;
   int grid = static_cast<int>(std::min<i64>(tiles, sm_count()));
   if (cs > 1) {
     grid = std::max(cs, grid / cs * cs);

@@ -149,11 +149,16 @@ def test_gemm_cluster_multicast_matches_single_cta(cuda, tmp_path):
     """Weight-image multicast across 2- and 4-CTA clusters (with phantom
     tiles: 149 and 37 m tiles) gives the single-CTA results bit for bit; the
     register-staged fallback (PK_TC_TMA=0) stays within the 3xTF32 bound."""
-    one = _variant(tmp_path, "cs1", {"PK_TC_CLUSTER": "1"})
+    one = _variant(tmp_path, "cs1", {"PK_TC_CLUSTER": "1", "PK_TC_PAIR": "1"})  # CTA pairs
     for cs in ("2", "4"):
-        got = _variant(tmp_path, "cs" + cs, {"PK_TC_CLUSTER": cs})
+        got = _variant(tmp_path, "cs" + cs, {"PK_TC_CLUSTER": cs, "PK_TC_PAIR": "0"})
         for key in one:
             assert np.array_equal(got[key].view(np.uint32), one[key].view(np.uint32)), (cs, key)
+    # CTA pairs (cta_group::2, M = 256) accumulate every element in the same k
+    # order as one CTA: bit-identical too
+    single = _variant(tmp_path, "nopair", {"PK_TC_PAIR": "0", "PK_TC_CLUSTER": "1"})
+    for key in one:
+        assert np.array_equal(single[key].view(np.uint32), one[key].view(np.uint32)), key
     reg = _variant(tmp_path, "reg", {"PK_TC_TMA": "0"})
     for key in one:
         den = np.linalg.norm(one[key].astype(np.float64)) or 1.0
