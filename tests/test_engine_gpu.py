@@ -61,6 +61,26 @@ def test_single_pass_matches_serial_trainer(cuda, hidden):
     eng.close()
 
 
+def test_single_pass_unaligned_widths(cuda):
+    """Feature / hidden widths that are not multiples of 4 (10, 14, 6): the
+    SpMMs run over the zero-padded width (16-B vectors); logits stay
+    bit-identical to the reference serial pass, gradients within 1e-5."""
+    graph, tr = _mods()
+    pre = build(10, 9000, 10, 5, seed=4)
+    rpre = ref.synth_rmat(10, 9000, 10, 5, seed=4).preprocess(4)
+    want = rpre.serial(hidden=(14, 6), seed=0).forward_backward(0)
+    opts = tr.TrainOptions(hidden_dims=[14, 6], mode=tr.PK_MODE_PARITY, hub_threshold=64)
+    eng = tr.RankEngine(pre.n, pre.feat_dim, pre.num_classes, tr.GridConfig(1, 1, 1), 0, opts)
+    eng.load(pre)
+    loss, acc = eng.forward_backward(0)
+    logits = eng.tensor(tr.PK_T_FOUT).cpu().numpy()
+    assert np.array_equal(logits.view(np.uint32), want["logits"].view(np.uint32))
+    for l, w in enumerate(want["dw"]):
+        assert nrel(eng.tensor(tr.PK_T_DW, l).cpu().numpy(), w) <= 1e-5, l
+    assert nrel(eng.tensor(tr.PK_T_DF0).cpu().numpy(), want["df0"]) <= 1e-5
+    eng.close()
+
+
 def test_weights_and_features_slices_at_init(cuda):
     from paper_2505_04083_b200.philox import init_weights
     _, tr = _mods()
