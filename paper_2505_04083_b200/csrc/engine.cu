@@ -25,20 +25,6 @@ i64 pad4(i64 c) { return c <= 0 ? 4 : (c + 3) / 4 * 4; }
 
 // 8 B per nonzero (u32 col + f32 val) + 8 B per row_ptr entry
 // + one gathered feature row per nonzero + one written output row per row.
-// SpMM run width. A row width that is not a multiple of 4 floats runs over
-// its 16-B padded width when both leading dimensions cover it: engine
-// buffers are zero-filled past their columns and nothing reads the extra
-// output columns, so the gathers stay 16-B vectors instead of 8-B ones
-// (C3's 602 input features). PK_SPMM_PAD=0 runs the exact width.
-i64 spmm_width(i64 d, i64 ldx, i64 ldy) {
-  static const bool pad = [] {
-    const char* e = std::getenv("PK_SPMM_PAD");
-    return !(e && e[0] == '0');
-  }();
-  const i64 p4 = (d + 3) / 4 * 4;
-  return (pad && p4 != d && ldx >= p4 && ldy >= p4) ? p4 : d;
-}
-
 double spmm_alg_bytes(i64 rows, u64 nnz, i64 d) {
   return 8.0 * nnz + 8.0 * (rows + 1) + 4.0 * nnz * d + 4.0 * rows * d;
 }
@@ -561,8 +547,7 @@ void Engine::forward_layer(int l, bool fault) {
       sh.a.rows, blocks,
       [&](i64 r0, i64 r1) {
         clock_.begin(0, st_);
-        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, spmm_width(s.f_cols, ldf, h.ld),
-                 hpart + r0 * h.ld, h.ld, st_);
+        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, hpart + r0 * h.ld, h.ld, st_);
         spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
         spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
         ++b;
@@ -765,9 +750,9 @@ void Engine::backward_layer(int l) {
       sh.at.rows, comm_chunks(sh.at.rows, lay.row),
       [&](i64 r0, i64 r1) {
         clock_.begin(5, st_);
-        const i64 w = mask_spmm ? s.f_cols : spmm_width(s.f_cols, lddh, lddf);
-        spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, w, dfpart + r0 * lddf, lddf,
-                 st_, mask_spmm ? act->p() + r0 * act->ld : nullptr, mask_spmm ? act->ld : 0);
+        spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, s.f_cols, dfpart + r0 * lddf,
+                 lddf, st_, mask_spmm ? act->p() + r0 * act->ld : nullptr,
+                 mask_spmm ? act->ld : 0);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {

@@ -63,8 +63,9 @@ def test_single_pass_matches_serial_trainer(cuda, hidden):
 
 def test_single_pass_unaligned_widths(cuda):
     """Feature / hidden widths that are not multiples of 4 (10, 14, 6): the
-    SpMMs run over the zero-padded width (16-B vectors); logits stay
-    bit-identical to the reference serial pass, gradients within 1e-5."""
+    SpMMs take their 8-B / 4-B vector paths; logits stay bit-identical to the
+    reference serial pass, gradients within 1e-5. (Running such rows over the
+    16-B padded width was measured slower on C3: 137.6 vs 93.9 ms.)"""
     graph, tr = _mods()
     pre = build(10, 9000, 10, 5, seed=4)
     rpre = ref.synth_rmat(10, 9000, 10, 5, seed=4).preprocess(4)
