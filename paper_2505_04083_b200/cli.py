@@ -1,5 +1,5 @@
 """Command line front end mirroring the reference's tools/main.cpp
-(preprocess / train / rank-configs) over this package. f32 only: the device
+(preprocess / train / rank-configs / validate) over this package. f32 only: the device
 path computes in fp32 (`--precision f64` is refused, exit code 2).
 
     python -m paper_2505_04083_b200 preprocess --synth rmat:scale=17,edges=2000000 \\
@@ -262,6 +262,64 @@ def cmd_rank_configs(a):
     return EXIT_OK
 
 
+def cmd_validate(a):
+    """validate (main.cpp:469-512): every factorization of the world size
+    trains the same dataset; each loss curve must match the single-rank
+    1x1x1 run within --tolerance (relative, per epoch). Run under torchrun
+    with --nproc-per-node G (one process per GPU); fp32 here, so the default
+    tolerance is 1e-5 (the reference's f64 sweep uses 1e-9). PARITY mode:
+    the ordered reductions keep the forward bit-identical across grids."""
+    import torch
+    import torch.distributed as dist
+
+    from . import distributed as D, graph, shard_io, trainer
+    from .layout import GridConfig, enumerate_configs
+    rank, world = D.init_control_plane()
+    _, _, local = D.dist_env()
+    torch.cuda.set_device(local)
+    if a.manifest:
+        pre = shard_io.load_preprocessed(shard_io.load_manifest(a.manifest))
+    elif a.synth:
+        kind, p = parse_synth(a.synth)
+        if kind != "rmat":
+            raise CliError(EXIT_INPUT, f"unknown synth kind '{kind}' (this build: rmat)")
+        pre = graph.preprocess(graph.synth_rmat(int(p.get("scale", 10)), int(p.get("edges", 0)),
+                                                a.feat_dim, a.classes, a.seed), a.seed)
+    else:
+        raise CliError(EXIT_INPUT, "validate needs --manifest or --synth")
+    opts = trainer.TrainOptions(hidden_dims=_ints(a.layers), epochs=a.epochs, lr=a.lr,
+                                seed=a.seed, mode=trainer.PK_MODE_PARITY,
+                                fault_epoch=0 if a.inject_fault else -1)
+    serial = None
+    if rank == 0:  # the single-rank reference curve on this GPU
+        eng = trainer.RankEngine(pre.n, pre.feat_dim, pre.num_classes, GridConfig(1, 1, 1), 0,
+                                 opts, local)
+        eng.load(pre)
+        serial = [eng.train_epoch(e)["loss"] for e in range(a.epochs)]
+        eng.close()
+        print(f"single-rank reference: {a.epochs} epochs, final loss {serial[-1]}")
+    all_ok = True
+    for shape in enumerate_configs(world):
+        res = D.train_distributed(lambda: pre, GridConfig(*shape), opts,
+                                  reassemble_params=False)
+        if rank != 0:
+            continue
+        dev = [abs(m["loss"] - s_) / max(abs(s_), abs(m["loss"]), 1e-300)
+               for m, s_ in zip(res.global_metrics, serial)]
+        worst = max(dev)
+        ok = worst <= a.tolerance
+        all_ok = all_ok and ok
+        print(f"{'PASS' if ok else 'FAIL'} config ({shape[0]}x{shape[1]}x{shape[2]}): max rel "
+              f"loss deviation {worst} at epoch {dev.index(worst)}")
+    if world > 1:
+        flag = torch.tensor([1 if all_ok else 0], dtype=torch.int32)
+        dist.broadcast(flag, 0)
+        all_ok = bool(flag.item())
+    if rank == 0:
+        print("validation passed" if all_ok else "validation FAILED")
+    return EXIT_OK if all_ok else EXIT_VALIDATION
+
+
 def build_parser():
     ap = argparse.ArgumentParser(prog="paper_2505_04083_b200",
                                  description="3D tensor-parallel full-graph GCN training on B200")
@@ -307,6 +365,18 @@ def build_parser():
     r.add_argument("--fit-samples", default="")
     r.add_argument("--coeffs-out", default="")
     r.add_argument("--csv", default="")
+    v = sub.add_parser("validate", help="every grid of the world size vs the 1x1x1 run")
+    v.add_argument("--manifest", default="")
+    v.add_argument("--synth", default="")
+    v.add_argument("--feat-dim", type=int, default=16)
+    v.add_argument("--classes", type=int, default=32)
+    v.add_argument("--epochs", type=int, default=10)
+    v.add_argument("--layers", default="16")
+    v.add_argument("--seed", type=int, default=0)
+    v.add_argument("--lr", type=float, default=1e-2)
+    v.add_argument("--tolerance", type=float, default=1e-5)
+    v.add_argument("--inject-fault", action="store_true",
+                   help="skip a reduction in epoch 0 (the check must then fail)")
     return ap
 
 
@@ -315,7 +385,7 @@ def main(argv=None):
     a = build_parser().parse_args(argv)
     try:
         return {"preprocess": cmd_preprocess, "train": cmd_train,
-                "rank-configs": cmd_rank_configs}[a.cmd](a)
+                "rank-configs": cmd_rank_configs, "validate": cmd_validate}[a.cmd](a)
     except CliError as e:
         print(f"error: {e}", file=sys.stderr)
         return e.code

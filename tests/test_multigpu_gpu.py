@@ -110,3 +110,18 @@ def test_two_gpu_engines_from_shard_files(cuda, grid, tmp_path):
     reference's distributed pass and train_distributed."""
     rep = _run(2, "--grid", grid, "--files", str(tmp_path / "shards"), "--shard-grid", "2,3")
     assert rep["logits_bitwise"]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("fault", [False, True])
+def test_two_gpu_cli_validate(cuda, fault):
+    """cli validate (main.cpp:469-512): every 2-rank grid against the 1x1x1
+    curve; an injected fault (a skipped reduction) must fail it (exit 1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", "-m", "paper_2505_04083_b200",
+           "validate", "--synth", "rmat:scale=10,edges=8000", "--feat-dim", "12", "--classes",
+           "5", "--epochs", "3", "--layers", "16"] + (["--inject-fault"] if fault else [])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert p.returncode == (1 if fault else 0), p.stdout[-2000:] + p.stderr[-2000:]
+    assert ("validation FAILED" if fault else "validation passed") in p.stdout
