@@ -258,14 +258,19 @@ constexpr int kListUnroll = PK_LIST_UNROLL;
 #ifndef PK_LIST_MINB8M
 #define PK_LIST_MINB8M 4
 #endif
-template <int VEC, int NV, bool MASK>
+// (The tuned one-vector, full-warp forms above; wider rows carry NV
+// accumulators and NV x U gathers per lane and narrower groups more gathers
+// per lane, so those trade residency for registers instead of spilling.)
+template <int VEC, int LANES, int NV, bool MASK>
 constexpr int list_min_blocks() {
-  return NV == 2 ? 3 : (VEC == 8 ? (MASK ? PK_LIST_MINB8M : PK_LIST_MINB8) : PK_LIST_MINB1);
+  if (NV >= 3 || (NV == 2 && VEC == 8)) return 2;
+  if (NV == 2 || LANES < 32) return 3;
+  return VEC == 8 ? (MASK ? PK_LIST_MINB8M : PK_LIST_MINB8) : PK_LIST_MINB1;
 }
 // MASK: the relu_backward epilogue variant (its own instantiation, so the
 // plain kernel's register allocation is untouched)
 template <int VEC, int LANES, int NV, int U, bool MASK>
-__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, NV, MASK>())
+__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, LANES, NV, MASK>())
 spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
                  int* __restrict__ counters) {
   using V = typename Vec<VEC>::T;
@@ -637,8 +642,11 @@ struct ListWorkspace {
 
 template <int VEC, int LANES, int NV>
 void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
-  constexpr int U0 =
-      NV >= 4 ? 2 : (NV == 2 ? PK_LIST_U2 : (VEC == 8 ? PK_LIST_U8 : PK_LIST_U1));
+  // gathers in flight per lane: U groups x NV vectors, double-buffered —
+  // kept to what fits the residency's register budget without spills
+  constexpr int U0 = NV >= 3 ? 2
+                             : (NV == 2 ? (VEC >= 4 ? 2 : PK_LIST_U2)
+                                        : (VEC == 8 ? PK_LIST_U8 : PK_LIST_U1));
   constexpr int U = U0 < LANES ? U0 : LANES / 2;
   const bool masked = a.mask != nullptr;
   auto kernel = masked ? spmm_list_kernel<VEC, LANES, NV, U, true>
@@ -701,8 +709,30 @@ void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream
     launch_list<VEC, 32, 1>(a, i0, i1, rpc, st);
   else if (nv <= 64)
     launch_list<VEC, 32, 2>(a, i0, i1, rpc, st);
-  else
-    launch_list<VEC, 32, 4>(a, i0, i1, rpc, st);  // wider rows split across blockIdx.y
+  else {
+    // wider rows: as few column slices (blockIdx.y, each re-streaming the
+    // nonzeros) as 6 vectors per lane allow, each slice as even as possible
+    // (C3's 602 features at 8 B: 2 slices of 160 instead of 128+128+45)
+    // (vectors per lane capped so the accumulators and gathers fit without
+    // spills: 6 below 16-B vectors, 4 at 16 B, 2 at 32 B)
+    constexpr int kMaxNV = VEC <= 2 ? 6 : (VEC == 4 ? 4 : 2);
+    const int slices = (nv + 32 * kMaxNV - 1) / (32 * kMaxNV);
+    const int per_lane = (nv + 32 * slices - 1) / (32 * slices);
+    if (per_lane <= 2) {
+      launch_list<VEC, 32, 2>(a, i0, i1, rpc, st);
+    } else if constexpr (kMaxNV >= 4) {
+      if (per_lane <= 3)
+        launch_list<VEC, 32, 3>(a, i0, i1, rpc, st);
+      else if (per_lane <= 4 || kMaxNV == 4)
+        launch_list<VEC, 32, 4>(a, i0, i1, rpc, st);
+      else if constexpr (kMaxNV >= 6) {
+        if (per_lane <= 5)
+          launch_list<VEC, 32, 5>(a, i0, i1, rpc, st);
+        else
+          launch_list<VEC, 32, 6>(a, i0, i1, rpc, st);
+      }
+    }
+  }
 }
 
 int pick_vec(const float* x, i64 ldx, const float* y, i64 ldy, i64 d, bool allow8) {

@@ -87,8 +87,11 @@ def test_spmm_flops_and_shape_error(cuda):
         k.spmm(bad, torch.zeros(2, 2, device=cuda))
 
 
-@pytest.mark.parametrize("d", [1, 2, 3, 5, 8, 13, 16, 25, 32, 47, 50, 64, 100, 128, 256, 301])
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 8, 13, 16, 25, 32, 47, 50, 64, 100, 128, 256, 301,
+                               520, 602, 777, 1000, 1200])
 def test_spmm_bitwise_random(cuda, d):
+    """Every vector width and lane-group form, including wide rows split
+    into balanced column slices (520, 602, 777, 1000, 1200)."""
     rng = np.random.default_rng(d)
     rows, cols = 300, 257
     rp, ci, v = random_csr(rows, cols, 0.08, rng)
@@ -302,7 +305,7 @@ def test_adam_bitwise(cuda):
 # ---------------------------------------------------------------------------
 # FAST SpMM plans: hub rows cut into segments, fixed-order combine
 
-@pytest.mark.parametrize("d", [1, 7, 64, 100, 256])
+@pytest.mark.parametrize("d", [1, 7, 64, 100, 256, 602])
 def test_spmm_fast_plan_segments_tolerance(cuda, d):
     """Hub rows (>= threshold) are summed as 2048-nonzero segments combined
     in a fixed order: within fp32 rounding of the reference's single chain,
