@@ -238,9 +238,6 @@ __device__ __forceinline__ unsigned end_mask(const u32* __restrict__ bits, u64 k
 #define PK_LIST_UNROLL 16
 #endif
 constexpr int kListUnroll = PK_LIST_UNROLL;
-#ifndef PK_LIST_HALF32
-#define PK_LIST_HALF32 0
-#endif
 
 // Minimum resident blocks per SM for the register allocation: three for
 // the 2-vector (D <= 256) form, where the extra warps' gathers outweigh the
@@ -703,8 +700,6 @@ void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream
     launch_list<VEC, 8, 1>(a, i0, i1, rpc, st);
   else if (nv <= 16)
     launch_list<VEC, 16, 1>(a, i0, i1, rpc, st);
-  else if (nv <= 32 && PK_LIST_HALF32)
-    launch_list<VEC, 16, 2>(a, i0, i1, rpc, st);  // two rows per warp instruction
   else if (nv <= 32)
     launch_list<VEC, 32, 1>(a, i0, i1, rpc, st);
   else if (nv <= 64)
