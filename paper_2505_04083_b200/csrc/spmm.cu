@@ -649,9 +649,14 @@ void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t
   auto kernel = masked ? spmm_list_kernel<VEC, LANES, NV, U, true>
                        : spmm_list_kernel<VEC, LANES, NV, U, false>;
   const int slices = ceil_div(a.nvec, NV * LANES);
-  // ~1-2K nonzeros per chunk at the products shape; never more chunks than rows
+  // ~1-2K nonzeros per chunk at the products shape; never more chunks than
+  // rows (PK_LIST_CHUNKS: chunks per SM, experiments)
+  static const i64 per_sm = [] {
+    const char* e = std::getenv("PK_LIST_CHUNKS");
+    return e ? std::max<i64>(1, std::atoll(e)) : i64{512};
+  }();
   const i64 nchunks64 =
-      std::max<i64>(1, std::min<i64>(i1 - i0, static_cast<i64>(sm_count()) * 512));
+      std::max<i64>(1, std::min<i64>(i1 - i0, static_cast<i64>(sm_count()) * per_sm));
   const int nchunks = static_cast<int>(nchunks64);
   static thread_local ListWorkspace ws;
   ws.bounds.ensure(nchunks + 1);
