@@ -100,14 +100,15 @@ class ClockSampler:
 
     def __init__(self, device):
         self.device = device
-        self.rows = []
+        self.rows = []  # (host receive time, fields)
         self.proc = None
+        self.window = None  # (t0, t1) host times of the timed region
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -117,7 +118,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.monotonic(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -128,9 +132,20 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        """Samples inside the timed region; a region shorter than the
+        sampler's first readings falls back to warm-up + timed (the GPU is
+        under the same load), and says so in `window`."""
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows = self.rows
+        window = "timed"
+        if self.window:
+            inside = [r for r in rows if self.window[0] <= r[0] <= self.window[1] + 0.1]
+            if len(inside) >= 2:
+                rows = inside
+            else:
+                window = "warmup+timed"
+        for _, r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = float(r[2])
@@ -140,7 +155,7 @@ class ClockSampler:
             except Exception:
                 continue
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def build_dataset(cfg, device):
@@ -252,6 +267,7 @@ def run_ours(args):
     eng.load(pre)
     stream = torch.cuda.ExternalStream(eng.stream_ptr())
 
+    clocks = ClockSampler(local).__enter__()  # started early: nvidia-smi needs a moment
     for e in range(args.warmup):
         eng.train_epoch(e)
     if world > 1:
@@ -259,11 +275,13 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _capi.lib().pk_kernel_launch_count()
-    with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        metrics = [eng.train_epoch(args.warmup + e) for e in range(args.steps)]
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    t_timed0 = time.monotonic()
+    ev0.record(stream)
+    metrics = [eng.train_epoch(args.warmup + e) for e in range(args.steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark(t_timed0, time.monotonic())
+    clocks.__exit__(None, None, None)
     launches = _capi.lib().pk_kernel_launch_count() - launches0
     ms_total = ev0.elapsed_time(ev1)
     if world > 1:
