@@ -308,6 +308,21 @@ def run_ours(args):
     phases = {k: float(np.mean([m[k] for m in metrics])) * 1e3 for k in
               ("forward_spmm_s", "forward_gemm_s", "backward_s", "optimizer_s", "collectives_s")}
     losses = [m["loss"] for m in metrics]
+    # collective bus bandwidth: the reference's ring-model bytes (= NCCL bus
+    # bytes, cluster.hpp:300-333) over the device time of this rank's
+    # reductions / gathers (max over ranks of the time)
+    coll = None
+    if world > 1:
+        ring = float(np.mean([m["allreduce_bytes"] + m["allgather_bytes"] +
+                              m["reducescatter_bytes"] for m in metrics]))
+        ctime = float(np.mean([m["collectives_s"] for m in metrics]))
+        t = torch.tensor([ctime], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ctime = float(t.item())
+        coll = {"ms_per_epoch": ctime * 1e3, "ring_bytes_per_epoch": ring,
+                "bus_gbs": ring / ctime / 1e9 if ctime > 0 else None,
+                "nvlink_gbs_per_direction": 900.0,
+                "note": "ordered peer-memory reductions (csrc/lsa.cu) + NCCL all-gathers"}
     # closed before the e2e run; its device blocks stay in the library's
     # allocation cache (memory.cu) for the next engine, like a process that
     # re-builds its engine
@@ -396,6 +411,7 @@ def run_ours(args):
                                  "(8nnz + 8(rows+1) + 4nnz*D + 4rows*D per SpMM) / "
                                  "measured SpMM time"},
             "phases_ms": phases,
+            "collectives": coll,
             "losses": losses,
             "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches // max(1, args.steps)),
