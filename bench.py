@@ -407,6 +407,10 @@ def run_ours(args):
                                            if traffic and spmm_s > 0 else None),
                          "dram_frac": (traffic / spmm_s / 1e9 / peak
                                        if traffic and spmm_s > 0 else None),
+                         # against the 8 TB/s HBM3e spec sheet figure as well
+                         "spec_peak": 8000.0,
+                         "dram_frac_spec": (traffic / spmm_s / 1e9 / 8000.0
+                                            if traffic and spmm_s > 0 else None),
                          "note": "achieved = SURVEY 8(d) algorithmic bytes "
                                  "(8nnz + 8(rows+1) + 4nnz*D + 4rows*D per SpMM) / "
                                  "measured SpMM time"},
