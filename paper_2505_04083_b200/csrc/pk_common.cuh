@@ -6,9 +6,11 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "plexus_b200.h"
 
@@ -111,6 +113,41 @@ struct DevBuf {
     n = 0;
     return q;
   }
+};
+
+// Device scratch for setup work (SpMM plans, transposes): one buffer per
+// host thread, grown to the largest need and kept, bump-allocated, reset by
+// each user at its start. Setup then allocates only its results — the
+// temporaries' cudaMalloc/cudaFree pairs were most of the engine's load time.
+class Scratch {
+ public:
+  static Scratch& get() {
+    static thread_local Scratch s;
+    return s;
+  }
+  void reset(size_t reserve) {
+    extra_.clear();
+    if (buf_.n < reserve) buf_.alloc(reserve);
+    off_ = 0;
+  }
+  template <typename T>
+  T* take(size_t count) {
+    const size_t b = (std::max<size_t>(count, 1) * sizeof(T) + 255) / 256 * 256;
+    if (off_ + b > buf_.n) {  // beyond the reservation: a dedicated buffer until reset
+      extra_.emplace_back(b);
+      return reinterpret_cast<T*>(extra_.back().p);
+    }
+    T* p = reinterpret_cast<T*>(buf_.p + off_);
+    off_ += b;
+    return p;
+  }
+  size_t mark() const { return off_; }
+  void release_to(size_t m) { off_ = m; }
+
+ private:
+  DevBuf<unsigned char> buf_;
+  size_t off_ = 0;
+  std::vector<DevBuf<unsigned char>> extra_;
 };
 
 inline int sm_count() {

@@ -214,24 +214,60 @@ __global__ void low_words(const u64* keys, u64 n, u32* out) {
 void csr_transpose(const pk_csr& a, pk_csr_owned* out, cudaStream_t st) {
   alloc_owned(out, a.cols, a.rows, a.nnz);
   const u64 n = a.nnz;
-  DevBuf<u64> counts(a.cols + 1);
-  PK_CUDA(cudaMemsetAsync(counts.p, 0, counts.n * sizeof(u64), st));
+  // temporaries from the per-thread scratch arena (row ids, iota, sorted
+  // keys, permutation, counts, cub workspaces): nothing to allocate per call
+  Scratch& sc = Scratch::get();
+  auto cub_temp = [&](auto&& f) {  // cub call with its workspace in the arena
+    size_t bytes = 0;
+    PK_CUDA(f(nullptr, bytes));
+    const size_t m = sc.mark();
+    PK_CUDA(f(sc.take<unsigned char>(bytes), bytes));
+    PK_CUDA(cudaStreamSynchronize(st));
+    sc.release_to(m);
+  };
+  size_t sort_bytes = 0;
+  if (n)
+    PK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, a.col_idx, (u32*)nullptr,
+                                            (u32*)nullptr, (u32*)nullptr, static_cast<i64>(n),
+                                            0, 32, st));
+  sc.reset(5 * (n + 1) * sizeof(u32) + (a.cols + 1) * sizeof(u64) + sort_bytes +
+           (size_t{64} << 20));
+  u64* counts = sc.take<u64>(a.cols + 1);
+  PK_CUDA(cudaMemsetAsync(counts, 0, (a.cols + 1) * sizeof(u64), st));
   if (n) {
-    histogram_u32<<<grid_for(n), 256, 0, st>>>(a.col_idx, n, counts.p);
+    histogram_u32<<<grid_for(n), 256, 0, st>>>(a.col_idx, n, counts);
     PK_LAUNCH("transpose histogram");
   }
-  counts_to_row_ptr(counts.p, a.cols, out->row_ptr, st);
+  cub_temp([&](void* t, size_t& bytes) {
+    return cub::DeviceScan::ExclusiveSum(t, bytes, counts, out->row_ptr,
+                                         static_cast<i64>(a.cols + 1), st);
+  });
   if (!n) return;
-  DevBuf<u32> rows = expand_rows(a, 0, a.rows, st);
-  DevBuf<u32> idx(n), keys_out(n), perm(n);
-  iota_u32<<<grid_for(n), 256, 0, st>>>(idx.p, n);
+  // row id of every entry (expand_rows, in the arena)
+  u32* marks = sc.take<u32>(n);
+  u32* rows = sc.take<u32>(n);
+  PK_CUDA(cudaMemsetAsync(marks, 0, n * sizeof(u32), st));
+  if (a.rows > 1) {
+    u64 base = 0;
+    PK_CUDA(cudaMemcpyAsync(&base, a.row_ptr, sizeof(u64), cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    row_start_marks<<<grid_for(a.rows), 256, 0, st>>>(a.row_ptr, a.rows, base, n, marks);
+    PK_LAUNCH("row start marks");
+  }
+  cub_temp([&](void* t, size_t& bytes) {
+    return cub::DeviceScan::InclusiveSum(t, bytes, marks, rows, static_cast<i64>(n), st);
+  });
+  u32* idx = sc.take<u32>(n);
+  u32* keys_out = sc.take<u32>(n);
+  u32* perm = sc.take<u32>(n);
+  iota_u32<<<grid_for(n), 256, 0, st>>>(idx, n);
   PK_LAUNCH("iota");
   const int end_bit = bits_for(a.cols > 0 ? a.cols - 1 : 0);
-  cub_call([&](void* t, size_t& bytes) {
-    return cub::DeviceRadixSort::SortPairs(t, bytes, a.col_idx, keys_out.p, idx.p, perm.p,
+  cub_temp([&](void* t, size_t& bytes) {
+    return cub::DeviceRadixSort::SortPairs(t, bytes, a.col_idx, keys_out, idx, perm,
                                            static_cast<i64>(n), 0, end_bit, st);
-  }, st);
-  transpose_scatter<<<grid_for(n), 256, 0, st>>>(perm.p, rows.p, a.values, n, out->col_idx,
+  });
+  transpose_scatter<<<grid_for(n), 256, 0, st>>>(perm, rows, a.values, n, out->col_idx,
                                                  out->values);
   PK_LAUNCH("transpose scatter");
   PK_CUDA(cudaStreamSynchronize(st));

@@ -867,41 +867,6 @@ unsigned blocks_for(i64 n, int per = 256) {
   return static_cast<unsigned>(std::max<i64>(1, std::min<i64>((n + per - 1) / per, 1 << 16)));
 }
 
-// Device scratch for plan construction: one buffer per host thread, grown to
-// the largest plan's need and kept, bump-allocated. Building a plan then
-// allocates only the plan's own arrays — the ~15 cudaMalloc/cudaFree pairs
-// of temporaries per plan were most of the engine's load time.
-class Scratch {
- public:
-  static Scratch& get() {
-    static thread_local Scratch s;
-    return s;
-  }
-  void reset(size_t reserve) {
-    extra_.clear();
-    if (buf_.n < reserve) buf_.alloc(reserve);
-    off_ = 0;
-  }
-  template <typename T>
-  T* take(size_t count) {
-    const size_t b = (std::max<size_t>(count, 1) * sizeof(T) + 255) / 256 * 256;
-    if (off_ + b > buf_.n) {  // beyond the reservation: a dedicated buffer until reset
-      extra_.emplace_back(b);
-      return reinterpret_cast<T*>(extra_.back().p);
-    }
-    T* p = reinterpret_cast<T*>(buf_.p + off_);
-    off_ += b;
-    return p;
-  }
-  size_t mark() const { return off_; }
-  void release_to(size_t m) { off_ = m; }
-
- private:
-  DevBuf<unsigned char> buf_;
-  size_t off_ = 0;
-  std::vector<DevBuf<unsigned char>> extra_;
-};
-
 template <typename F>
 void cub_run(F&& f, cudaStream_t st) {
   size_t bytes = 0;
