@@ -52,15 +52,14 @@ void upload_block(DMat& m, const float* host, i64 cols, cudaStream_t st) {
 
 }  // namespace
 
-void DMat::alloc(i64 r, i64 c) {
+void DMat::alloc(i64 r, i64 c, cudaStream_t st) {
   rows = r;
   cols = c;
   ld = pad4(c);
   buf.alloc(static_cast<size_t>(std::max<i64>(1, r) * ld));
-  // legacy-stream memset, completed before any engine stream touches the
-  // block (the allocator hands back reused, non-zero blocks)
-  PK_CUDA(cudaMemset(buf.p, 0, buf.n * sizeof(float)));
-  PK_CUDA(cudaStreamSynchronize(0));
+  // zero-filled (the allocator hands back reused, non-zero blocks): on the
+  // engine stream that will use the block, so no host wait is needed
+  PK_CUDA(cudaMemsetAsync(buf.p, 0, buf.n * sizeof(float), st));
 }
 
 const std::vector<u64>& AdjShard::blocks_nnz(int blocks, cudaStream_t st) {
@@ -231,7 +230,7 @@ void Engine::finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, M
 // F0 shard from device rows of width feature_slice's column count (ld given)
 void Engine::set_f0(const float* src, i64 ld) {
   const Slice fs = feature_slice(grid_, c_, cfg_.n, dims_[0]);
-  f0_.alloc(fs.r1 - fs.r0, fs.c1 - fs.c0);
+  f0_.alloc(fs.r1 - fs.r0, fs.c1 - fs.c0, st_);
   if (f0_.rows && f0_.cols) {
     if (f0_.ld == f0_.cols && ld == f0_.cols)
       PK_CUDA(cudaMemcpyAsync(f0_.p(), src, f0_.rows * f0_.cols * sizeof(float),
@@ -239,9 +238,9 @@ void Engine::set_f0(const float* src, i64 ld) {
     else
       copy_block_launch(src, ld, f0_.rows, f0_.cols, f0_.p(), f0_.ld, st_);
   }
-  f0_m_.alloc(f0_.rows, f0_.cols);
-  f0_v_.alloc(f0_.rows, f0_.cols);
-  df0_.alloc(f0_.rows, f0_.cols);
+  f0_m_.alloc(f0_.rows, f0_.cols, st_);
+  f0_v_.alloc(f0_.rows, f0_.cols, st_);
+  df0_.alloc(f0_.rows, f0_.cols, st_);
   f0_step_ = 0;
 }
 
@@ -254,24 +253,24 @@ void Engine::alloc_params() {
   for (int l = 0; l < L_; ++l) {
     const Shapes& s = shapes_[l];
     const Slice ws = weight_slice(grid_, lays_[l], c_, dims_[l], dims_[l + 1]);
-    w_[l].alloc(ws.r1 - ws.r0, ws.c1 - ws.c0);
+    w_[l].alloc(ws.r1 - ws.r0, ws.c1 - ws.c0, st_);
     auto blk = init_weight_block(cfg_.seed, l, dims_[l], dims_[l + 1], ws);
     upload_block(w_[l], blk.data(), w_[l].cols, st_);
     PK_CUDA(cudaStreamSynchronize(st_));
-    w_m_[l].alloc(w_[l].rows, w_[l].cols);
-    w_v_[l].alloc(w_[l].rows, w_[l].cols);
-    dw_[l].alloc(w_[l].rows, w_[l].cols);
-    wfull_[l].alloc(s.f_cols, s.w_cols);
-    dwp_[l].alloc(s.f_cols, s.w_cols);
-    h_[l].alloc(s.h_rows, s.h_cols);
-    q_[l].alloc(s.q_rows, s.q_cols);
-    if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols);
+    w_m_[l].alloc(w_[l].rows, w_[l].cols, st_);
+    w_v_[l].alloc(w_[l].rows, w_[l].cols, st_);
+    dw_[l].alloc(w_[l].rows, w_[l].cols, st_);
+    wfull_[l].alloc(s.f_cols, s.w_cols, st_);
+    dwp_[l].alloc(s.f_cols, s.w_cols, st_);
+    h_[l].alloc(s.h_rows, s.h_cols, st_);
+    q_[l].alloc(s.q_rows, s.q_cols, st_);
+    if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols, st_);
     max_dq = std::max(max_dq, s.q_rows * pad4(s.q_cols));
     max_dh = std::max(max_dh, s.h_rows * pad4(s.h_cols));
     max_df = std::max(max_df, s.a_cols * pad4(s.f_cols));
   }
   w_step_ = 0;
-  f0g_.alloc(shapes_[0].f_rows, shapes_[0].f_cols);
+  f0g_.alloc(shapes_[0].f_rows, shapes_[0].f_cols, st_);
   dq_.buf.alloc(max_dq);
   dh_.buf.alloc(max_dh);
   df_.buf.alloc(max_df);
@@ -296,9 +295,9 @@ void Engine::set_labels(const u32* labels, const u8* mask, i64 lrows, u64 global
     PK_CUDA(cudaMemcpyAsync(mask_.p, mask, lrows, cudaMemcpyDeviceToDevice, st_));
   }
   mask_count_ = global_count;
-  logits_.alloc(sl.a_rows, dims_[L_]);
-  dl_.alloc(sl.a_rows, dims_[L_]);
-  stage_.alloc(sl.a_rows, dims_[L_]);
+  logits_.alloc(sl.a_rows, dims_[L_], st_);
+  dl_.alloc(sl.a_rows, dims_[L_], st_);
+  stage_.alloc(sl.a_rows, dims_[L_], st_);
   // DMat::alloc zeroes on the legacy stream: drain everything before use
   PK_CUDA(cudaDeviceSynchronize());
 }

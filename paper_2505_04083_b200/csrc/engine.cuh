@@ -23,7 +23,7 @@ struct DMat {
   DevBuf<float> buf;
   i64 rows = 0, cols = 0, ld = 0;
   float* p() const { return buf.p; }
-  void alloc(i64 r, i64 c);
+  void alloc(i64 r, i64 c, cudaStream_t st);  // zero-filled on `st`
   i64 elems() const { return rows * ld; }
 };
 
