@@ -200,6 +200,7 @@ struct ListArgs {
   float* part = nullptr;        // FAST plan: segment sums (target bit 31 set)
   i64 ldp = 0;
   int nvec = 0;
+  i64 xrows = 0;                // rows of x the nonzeros gather from
   const float* mask = nullptr;  // optional relu_backward mask, rows like y
   i64 ldm = 0;
 };
@@ -704,6 +705,33 @@ void launch_hub(const SpmmArgs& a, cudaStream_t st) {
   PK_LAUNCH("spmm hub kernel");
 }
 
+// Wide rows over a gathered matrix larger than L2 (C3: 262K rows x 602
+// features = 631 MB): one column slice of 32 (or 16) lanes per grid.y, so the
+// slices run one after another and each slice's columns of x (262K x 256 B =
+// 67 MB at 32 lanes of 8 B) stay L2-resident while the nonzeros are
+// re-streamed (8 B per nonzero per slice against LANES*4*VEC B of gathers).
+// Returns the slice's lane count, or 0 for the balanced wide form.
+// PK_SPMM_L2_MB: the slice's L2 budget (0 = off); PK_SPMM_L2_LANES=32|16
+// forces the form on every wide row (tests).
+inline int l2_slice_lanes(const ListArgs& a, int vec) {
+  static const double budget = [] {
+    const char* e = std::getenv("PK_SPMM_L2_MB");
+    return (e ? std::atof(e) : 96.0) * (1 << 20);
+  }();
+  static const int forced = [] {
+    const char* e = std::getenv("PK_SPMM_L2_LANES");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (a.nvec <= 32) return 0;
+  if (forced == 32 || forced == 16) return forced;
+  if (budget <= 0) return 0;
+  const double row_bytes = 4.0 * vec;
+  if (static_cast<double>(a.xrows) * a.nvec * row_bytes <= budget) return 0;
+  for (int lanes = 32; lanes >= 16; lanes /= 2)
+    if (static_cast<double>(a.xrows) * lanes * row_bytes <= budget) return lanes;
+  return 0;
+}
+
 template <int VEC>
 void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
   const int nv = a.nvec;
@@ -716,6 +744,10 @@ void dispatch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream
     launch_list<VEC, 16, 1>(a, i0, i1, rpc, st);
   else if (nv <= 32)
     launch_list<VEC, 32, 1>(a, i0, i1, rpc, st);
+  else if (const int sl = l2_slice_lanes(a, VEC); sl == 32)
+    launch_list<VEC, 32, 1>(a, i0, i1, rpc, st);
+  else if (sl == 16)
+    launch_list<VEC, 16, 1>(a, i0, i1, rpc, st);
   else if (nv <= 64)
     launch_list<VEC, 32, 2>(a, i0, i1, rpc, st);
   else {
@@ -1134,6 +1166,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     ListArgs la;
     la.cv = plan.cv.p, la.rl = plan.rl.p, la.rpc = plan.rpc.p, la.endbits = plan.endbits.p;
     la.x = x, la.ldx = ldx, la.y = y, la.ldy = ldy, la.r0 = r0, la.nvec = nvec;
+    la.xrows = static_cast<i64>(a.cols);
     la.mask = mask, la.ldm = ldm;
     if (plan.segment && plan.segments) {
       la.ldp = (d + 7) / 8 * 8;  // 32-B aligned rows for the widest slices

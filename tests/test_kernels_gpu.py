@@ -363,3 +363,41 @@ def test_spmm_relu_backward_fused(cuda, d, mode):
         want = k.relu_backward(mask[r0:r1], plain)
         got = k.spmm_rows_relu_backward(a, x, r0, r1, mask[r0:r1], plan)
         assert torch.equal(got.view(torch.int32), want.view(torch.int32)), (r0, r1)
+
+
+_L2_SLICED_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import restate
+from paper_2505_04083_b200 import kernels as k
+sys.path.insert(0, sys.argv[1] + "/tests")
+from test_kernels_gpu import random_csr, skewed_csr
+for d in (33, 100, 301, 602, 1000):
+    rng = np.random.default_rng(500 + d)
+    for rows, cols in ((300, 257), (800, 3000)):
+        rp, ci, v = (random_csr(rows, cols, 0.08, rng) if rows == 300
+                     else skewed_csr(rows, cols, rng, hubs=((3, 2500),)))
+        x = rng.uniform(-1, 1, size=(cols, d)).astype(np.float32)
+        want = restate.spmm_rows(rp, ci, v, x, 0, rows)
+        a = k.DeviceCsr.from_host(rows, cols, rp, ci, v)
+        got = k.spmm(a, torch.from_numpy(x).cuda()).cpu().numpy()
+        want = np.ascontiguousarray(want, dtype=np.float32)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (d, rows)
+print("ok")
+"""
+
+
+def test_spmm_l2_sliced_form_bitwise(cuda):
+    """The L2-sliced wide-row form (one 32-lane column slice per grid.y,
+    spmm.cu l2_slice_lanes) is forced with PK_SPMM_L2_LANES at 32 and 16
+    lanes; rows stay bit-identical with the reference chain. The variable is
+    read once per process, hence the child processes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for lanes in ("32", "16"):
+        env = dict(os.environ, PK_SPMM_L2_LANES=lanes)
+        r = subprocess.run([sys.executable, "-c", _L2_SLICED_CHILD, root], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
