@@ -706,7 +706,7 @@ void launch_hub(const SpmmArgs& a, cudaStream_t st) {
 }
 
 // Wide rows over a gathered matrix larger than L2 (C3: 262K rows x 602
-// features = 631 MB): one column slice of 32 (or 16) lanes per grid.y, so the
+// features = 631 MB): one column slice of 32 lanes per grid.y, so the
 // slices run one after another and each slice's columns of x (262K x 256 B =
 // 67 MB at 32 lanes of 8 B) stay L2-resident while the nonzeros are
 // re-streamed (8 B per nonzero per slice against LANES*4*VEC B of gathers).
@@ -727,8 +727,10 @@ inline int l2_slice_lanes(const ListArgs& a, int vec) {
   if (budget <= 0) return 0;
   const double row_bytes = 4.0 * vec;
   if (static_cast<double>(a.xrows) * a.nvec * row_bytes <= budget) return 0;
-  for (int lanes = 32; lanes >= 16; lanes /= 2)
-    if (static_cast<double>(a.xrows) * lanes * row_bytes <= budget) return lanes;
+  // 32 lanes of at least 8 B: narrower slices (16 lanes, or 4-B gathers)
+  // measured slower than the balanced form (C3: 121 vs 94 ms at 16 lanes on
+  // 1 GPU; 65.8 vs 38.2 ms with 4-B gathers at D = 301 on 2 GPUs)
+  if (vec >= 2 && static_cast<double>(a.xrows) * 32 * row_bytes <= budget) return 32;
   return 0;
 }
 
