@@ -61,16 +61,19 @@ def test_single_pass_matches_serial_trainer(cuda, hidden):
     eng.close()
 
 
-def test_single_pass_unaligned_widths(cuda):
-    """Feature / hidden widths that are not multiples of 4 (10, 14, 6): the
-    SpMMs take their 8-B / 4-B vector paths; logits stay bit-identical to the
-    reference serial pass, gradients within 1e-5. (Running such rows over the
-    16-B padded width was measured slower on C3: 137.6 vs 93.9 ms.)"""
+@pytest.mark.parametrize("feat,hidden", [(10, (14, 6)), (9, (13, 7))])
+def test_single_pass_unaligned_widths(cuda, feat, hidden):
+    """Feature / hidden widths that are not multiples of 4: even ones (10,
+    14, 6) take the 8-B vector path, odd ones (9, 13, 7) the 4-B path. Logits
+    stay bit-identical to the reference serial pass, gradients within 1e-5.
+    (Running such rows over the 16-B padded width was measured slower twice:
+    C3 137.6 vs 93.9 ms on 1 GPU at 602 features; 44.5 vs 38.1 ms on 2 GPUs
+    at 301 features per rank — profiles/r1_pad_ab_c3_n2.log.)"""
     graph, tr = _mods()
-    pre = build(10, 9000, 10, 5, seed=4)
-    rpre = ref.synth_rmat(10, 9000, 10, 5, seed=4).preprocess(4)
-    want = rpre.serial(hidden=(14, 6), seed=0).forward_backward(0)
-    opts = tr.TrainOptions(hidden_dims=[14, 6], mode=tr.PK_MODE_PARITY, hub_threshold=64)
+    pre = build(10, 9000, feat, 5, seed=4)
+    rpre = ref.synth_rmat(10, 9000, feat, 5, seed=4).preprocess(4)
+    want = rpre.serial(hidden=hidden, seed=0).forward_backward(0)
+    opts = tr.TrainOptions(hidden_dims=list(hidden), mode=tr.PK_MODE_PARITY, hub_threshold=64)
     eng = tr.RankEngine(pre.n, pre.feat_dim, pre.num_classes, tr.GridConfig(1, 1, 1), 0, opts)
     eng.load(pre)
     loss, acc = eng.forward_backward(0)
