@@ -651,9 +651,13 @@ template <int VEC, int LANES, int NV>
 void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
   // gathers in flight per lane: U groups x NV vectors, double-buffered —
   // kept to what fits the residency's register budget without spills
+#ifndef PK_LIST_U2V
+#define PK_LIST_U2V 4
+#endif
   constexpr int U0 = NV >= 3 ? 2
                              : (NV == 2 ? (VEC >= 4 ? 2 : PK_LIST_U2)
-                                        : (VEC == 8 ? PK_LIST_U8 : PK_LIST_U1));
+                                        : (VEC == 8 ? PK_LIST_U8
+                                                    : (VEC == 2 ? PK_LIST_U2V : PK_LIST_U1)));
   constexpr int U = U0 < LANES ? U0 : LANES / 2;
   const bool masked = a.mask != nullptr;
   auto kernel = masked ? spmm_list_kernel<VEC, LANES, NV, U, true>
