@@ -51,6 +51,17 @@ CONFIGS = {
 B200_MACHINE = dict(g_node=8, beta_intra=725e9, beta_inter=50e9, bytes_per_scalar=4)
 
 
+def ref_pick_grid(gpus, n, nnz, dims):
+    """The same pick from the reference's own rank_configs (oracle/_ref):
+    the reference arm never loads libplexus_b200.so."""
+    from oracle import ref
+    m = B200_MACHINE
+    best = ref.rank_configs(gpus, n, nnz, dims, g_node=m["g_node"], beta_intra=m["beta_intra"],
+                            beta_inter=m["beta_inter"],
+                            bytes_per_scalar=m["bytes_per_scalar"])[0]
+    return tuple(int(x) for x in best[:3])
+
+
 def pick_grid(gpus, n, nnz, dims):
     """The performance model's choice (rank_configs, perf_model.cpp:207-229)
     for this dataset on this machine."""
@@ -70,10 +81,14 @@ def parse():
     ap.add_argument("--grid", default=None, help="gx,gy,gz (default: perf-model pick)")
     ap.add_argument("--mode", default="fast", choices=["fast", "parity"])
     ap.add_argument("--e2e-epochs", type=int, default=10)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU seconds for the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c1-measured", action="store_true",
+                    help="skip the measured reference C1 epoch (train_distributed, 8 threads)")
+    ap.add_argument("--ref-budget-s", type=float, default=100.0,
+                    help="--impl reference: sampled CPU seconds over all timed steps")
     return ap.parse_args()
 
 
@@ -170,58 +185,133 @@ def build_dataset(cfg, device):
     return pre
 
 
-def cpu_reference_sample(pre_dev, hidden, target_s, threads):
-    """The reference's own CPU kernels (oracle/_ref, -O2 scalar) on a bounded
-    row sample of this workload, scaled to a full epoch. Returns the
-    estimated epoch ms and a description."""
+def config_dict(cfg, grid, n, nnz):
+    """The workload, identical in both arms' JSON lines."""
+    return {"workload": cfg["workload"], "grid": "x".join(map(str, grid)), "n": int(n),
+            "nnz": int(nnz), "dims": [cfg["feat"], *cfg["hidden"], cfg["classes"]],
+            "l2": f"inputs larger than L2 (adjacency {2 * nnz * 8 / 1e9:.1f} GB + activations "
+                  "per epoch)"}
+
+
+def ref_dataset(cfg):
+    """The reference's own synth_rmat + preprocess (oracle/_ref, -O2, one
+    thread; graph.hpp:291-322, 356-384) — the reference arm's input, built
+    without libplexus_b200.so."""
+    from oracle import ref
+    a, b, c = cfg["abc"]
+    g = ref.synth_rmat(cfg["scale"], cfg["edges"], cfg["feat"], cfg["classes"], seed=1,
+                       a=a, b=b, c=c)
+    pre = g.preprocess(1)
+    del g
+    return pre
+
+
+def ref_dataset_from_device(pre_dev):
+    """Our GPU-built dataset (bit-identical to the reference's preprocess,
+    tests/test_shard_builder_gpu.py, tests/test_c2_parity_gpu.py) handed to
+    the reference for the cpu_baseline leg of our own arm."""
     from oracle import ref
     from paper_2505_04083_b200.trainer import HostDataset
     h = HostDataset.from_device(pre_dev, pin=False)
-    rpre = ref.Pre.from_arrays(h.n, h.feat_dim, h.num_classes,
+    return ref.Pre.from_arrays(h.n, h.feat_dim, h.num_classes,
                                (h.even[0].view(np.uint64), h.even[1].view(np.uint32), h.even[2]),
                                (h.odd[0].view(np.uint64), h.odd[1].view(np.uint32), h.odd[2]),
                                h.features, h.labels_row.view(np.uint32),
                                h.labels_col.view(np.uint32), h.mask_row, h.mask_col)
-    # calibrate on a small sample, then size the measured one to target_s
-    rows = 64
-    est, wall = rpre.epoch_sample(hidden, rows, threads)
-    per_row = wall / rows
-    rows = int(max(64, min(h.n // max(1, threads), target_s / max(per_row, 1e-9))))
+
+
+def reference_epoch_estimate(rpre, hidden, threads, target_s, rows=None):
+    """The ONE cpu_baseline definition of both arms: the reference's own
+    per-layer ops (spmm_rows / gemm incl. its TN dW form / relu / CE / Adam,
+    oracle/_ref built with the reference's flags) over a row sample of the
+    full epoch on `threads` host threads (ref_capi.cpp ref_epoch_sample),
+    scaled to all n rows. An ESTIMATE: a full C2 epoch of the reference's
+    scalar code takes minutes even on every host core. Returns (ms, rows
+    per thread, sampled wall s)."""
+    n = rpre.info()["n"]
+    if rows is None:
+        est, wall = rpre.epoch_sample(hidden, 64, threads)
+        rows = int(max(64, min(n // max(1, threads), target_s / max(wall / 64, 1e-9))))
     est, wall = rpre.epoch_sample(hidden, rows, threads)
     return est * 1e3, rows, wall
 
 
+def ref_c1_measured(threads_cap):
+    """A MEASURED (not extrapolated) epoch of the reference's own
+    train_distributed (trainer.hpp:541-687, one std::thread per rank) on C1
+    at grid 2x2x2 = 8 threads: wall(3 epochs) - wall(1 epoch) over 2, so the
+    setup cancels. Input from the reference's own synth_rmat + preprocess."""
+    from oracle import ref
+    cfg = CONFIGS["c1"]
+    rpre = ref_dataset(cfg)
+    grid = (2, 2, 2)
+    walls = {}
+    for e in (1, 3):
+        t0 = time.perf_counter()
+        out = rpre.train_distributed(grid, hidden=tuple(cfg["hidden"]), epochs=e,
+                                     max_running=threads_cap)
+        walls[e] = time.perf_counter() - t0
+    ms = (walls[3] - walls[1]) / 2 * 1e3
+    return {"config": "c1", "workload": cfg["workload"], "grid": "2x2x2", "threads": 8,
+            "ms_per_epoch": ms, "losses": [float(x) for x in out["loss"]],
+            "how": "reference train_distributed, wall(3 epochs) - wall(1 epoch) over 2, "
+                   "input from reference synth_rmat+preprocess (oracle/_ref)"}
+
+
+def gpu_c1_epoch_ms(local):
+    """Our C1 epoch (1 GPU, grid 1x1x1, FAST): mean device epoch time of
+    epochs 2..9 of 10 (the reference CLI's averaging window, main.cpp:209-231)."""
+    from paper_2505_04083_b200 import trainer
+    cfg = CONFIGS["c1"]
+    pre = build_dataset(cfg, local)
+    opts = trainer.TrainOptions(hidden_dims=cfg["hidden"], mode=trainer.PK_MODE_FAST, epochs=10)
+    metrics, _, _ = trainer.train_single(pre, opts)
+    return float(np.mean([m["epoch_s"] for m in metrics[2:10]])) * 1e3
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path,
+    on this box's host cores, never touching libplexus_b200.so. Input: the
+    reference's synth_rmat + preprocess (oracle/_ref). Each step: one
+    bounded row-sample estimate of a full epoch (reference_epoch_estimate),
+    sized so the whole --warmup/--steps run stays within a few minutes. Rank
+    0 only under torchrun."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    import torch
-    torch.cuda.set_device(local)
     cfg = CONFIGS[args.config]
-    pre = build_dataset(cfg, local)
+    t0 = time.perf_counter()
+    rpre = ref_dataset(cfg)
+    t_build = time.perf_counter() - t0
+    info = rpre.info()
+    n, nnz = info["n"], info["nnz_even"]
     dims = [cfg["feat"], *cfg["hidden"], cfg["classes"]]
     grid = (tuple(int(x) for x in args.grid.split(",")) if args.grid
-            else pick_grid(args.gpus, pre.n, pre.a_even.nnz, dims))
+            else ref_pick_grid(args.gpus, n, nnz, dims))
     threads = os.cpu_count() or 1
-    vals = []
+    # per timed step ~budget / steps seconds of sampled work
+    step_s = max(1.0, min(8.0, args.ref_budget_s / max(1, args.steps)))
+    _, rows, _ = reference_epoch_estimate(rpre, cfg["hidden"], threads, step_s)
+    vals, walls = [], []
     for step in range(args.warmup + args.steps):
-        ms, rows, wall = cpu_reference_sample(pre, cfg["hidden"], 20.0 if step >= args.warmup
-                                              else 3.0, threads)
+        r = max(64, rows // 8) if step < args.warmup else rows
+        ms, _, wall = reference_epoch_estimate(rpre, cfg["hidden"], threads, step_s, rows=r)
         if step >= args.warmup:
             vals.append(ms)
+            walls.append(wall)
     val = float(np.median(vals))
     sample = (f"{rows} rows x {threads} threads of every per-layer op of one 1x1x1 epoch "
-              f"(reference spmm_rows/gemm/relu/CE/Adam, oracle/_ref -O2), scaled to "
-              f"{pre.n} rows; input built by the GPU shard builder (bit-exact with "
-              f"reference preprocess)")
+              f"(reference spmm_rows/gemm/relu/CE/Adam, oracle/_ref -O2) per step, "
+              f"extrapolated to {n} rows; input from the reference's own synth_rmat + "
+              f"preprocess ({t_build:.0f} s)")
     line = {"metric": METRIC, "value": val, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": val, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": cfg["workload"], "grid": "x".join(map(str, grid)),
-                       "reference_grid_note": "CPU reference timed as its 1x1x1 op set"},
+            "impl": "reference", "extrapolated": True,
+            "sampled_wall_s_per_step": float(np.median(walls)),
+            "config": config_dict(cfg, grid, n, nnz),
             "cpu_baseline": {"value": val, "unit": "ms", "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "extrapolated": True},
             "e2e": {"value": val, "unit": "ms", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -293,16 +383,20 @@ def run_ours(args):
     spmm_s = float(np.mean([m["spmm_s"] for m in metrics]))
     spmm_bytes = float(np.mean([m["spmm_bytes"] for m in metrics]))
     spmm_launch_share = spmm_s / (ms_step * 1e-3)
+    spmm_cbytes = float(np.mean([m["spmm_compulsory_bytes"] for m in metrics]))
     peak, peak_kind = hbm_peak()
-    achieved = spmm_bytes / spmm_s / 1e9 if spmm_s > 0 else None
     # DRAM bytes of the same SpMM launches of one epoch, from the committed
-    # ncu launch list (scripts/ncu_round.sh -> scripts/spmm_traffic.py)
-    traffic = None
+    # ncu launch list of this config at 1 GPU (scripts/ncu_round.sh ->
+    # scripts/spmm_traffic.py; the file names the commit it was taken at)
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", f"ncu_spmm_{args.config}.json")
-    if os.path.exists(prof) and world == 1:
+    if os.path.exists(prof) and world == 1 and args.mode == "fast":
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_epoch")
+                pj = json.load(f)
+            traffic = pj.get("dram_bytes_per_epoch")
+            traffic_src = {"file": os.path.relpath(prof, ROOT), "commit": pj.get("commit"),
+                           "launches": pj.get("spmm_launches")}
         except Exception:
             traffic = None
     phases = {k: float(np.mean([m[k] for m in metrics])) * 1e3 for k in
@@ -332,7 +426,9 @@ def run_ours(args):
 
     # e2e: the reference-facing API with HOST buffers (train_distributed on a
     # host PreprocessedDataset): H2D of the whole dataset from pinned memory,
-    # shard slicing, E epochs (each reads its loss/accuracy back to the host).
+    # shard slicing, E epochs (each reads its metrics back to the host), then
+    # the TrainResult download of this rank's trained W shards and F0 shard
+    # (trainer.hpp:636-686 reassembles them on the host).
     e2e = None
     if not args.no_e2e:
         host = trainer.HostDataset.from_device(pre, pin=True)
@@ -351,69 +447,93 @@ def run_ours(args):
         t2 = time.perf_counter()
         for e in range(args.e2e_epochs):
             eng2.train_epoch(e)
-        torch.cuda.synchronize()
         t3 = time.perf_counter()
-        parts = [t3 - t0, t1 - t0, t2 - t1, t3 - t2]
+        result = eng2.download_params()
+        t4 = time.perf_counter()
+        parts = [t4 - t0, t1 - t0, t2 - t1, t3 - t2, t4 - t3]
         if world > 1:
             t = torch.tensor(parts, device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             parts = t.tolist()
         wall = parts[0]
         eng2.close()
+        d2h = sum(a.nbytes for a in result) + args.e2e_epochs * C.sizeof(trainer.pk_epoch_metrics)
         e2e = {"value": wall * 1e3 / args.e2e_epochs, "unit": "ms",
                "h2d_bytes_per_step": int(host.nbytes() // args.e2e_epochs),
-               "d2h_bytes_per_step": 4 * 8,
+               "d2h_bytes_per_step": int(d2h // args.e2e_epochs),
                "epochs": args.e2e_epochs,
                "phases_ms": {"create_and_comm_init": parts[1] * 1e3, "load": parts[2] * 1e3,
-                             "epochs": parts[3] * 1e3},
+                             "epochs": parts[3] * 1e3, "result_download": parts[4] * 1e3},
                "note": "train_distributed from a pinned-host PreprocessedDataset: dataset H2D "
-                       "+ shard slicing + E epochs, wall / E (max over ranks)"}
-        del host
+                       "+ shard slicing + E epochs + download of the trained W / F0 shards, "
+                       "wall / E (max over ranks)"}
+        del host, result
 
-    cpu = None
+    threads = os.cpu_count() or 1
+    cpu = c1 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            ms, rows, wall = cpu_reference_sample(pre, cfg["hidden"], args.cpu_seconds, 1)
-            cpu = {"value": ms, "unit": "ms", "cores": 1, "kind": "reference",
-                   "sample": f"{rows} rows of every per-layer op of one epoch on 1 thread "
-                             f"(oracle/_ref, reference -O2 scalar kernels), scaled to {n} rows "
-                             f"({wall:.1f} s measured)"}
+            rpre = ref_dataset_from_device(pre)
+            ms, rows, wall = reference_epoch_estimate(rpre, cfg["hidden"], threads,
+                                                      args.cpu_seconds)
+            del rpre
+            cpu = {"value": ms, "unit": "ms", "cores": threads, "kind": "reference",
+                   "extrapolated": True,
+                   "sample": f"{rows} rows x {threads} threads of every per-layer op of one "
+                             f"1x1x1 epoch (reference spmm_rows/gemm/relu/CE/Adam, oracle/_ref "
+                             f"-O2), extrapolated to {n} rows ({wall:.1f} s sampled); same "
+                             f"definition as --impl reference"}
         except Exception as exc:  # report, never fake
-            cpu = {"value": None, "unit": "ms", "cores": 1, "kind": "reference",
+            cpu = {"value": None, "unit": "ms", "cores": threads, "kind": "reference",
                    "sample": f"unavailable: {exc}"}
+    if rank == 0 and world == 1 and not args.no_c1_measured:
+        try:
+            del pre
+            torch.cuda.empty_cache()
+            c1 = ref_c1_measured(threads)
+            c1["gpu_ms_per_epoch"] = gpu_c1_epoch_ms(local)
+            c1["gpu_grid"] = "1x1x1 (1 B200, FAST)"
+            c1["speedup"] = c1["ms_per_epoch"] / c1["gpu_ms_per_epoch"]
+        except Exception as exc:
+            c1 = {"unavailable": str(exc)}
 
     if rank == 0:
+        dram = traffic / spmm_s / 1e9 if traffic and spmm_s > 0 else None
+        comp = spmm_cbytes / spmm_s / 1e9 if spmm_s > 0 else None
+        alg = spmm_bytes / spmm_s / 1e9 if spmm_s > 0 else None
+        achieved = dram if dram is not None else comp
         line = {
             "metric": METRIC, "value": ms_step, "unit": "ms", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "grid": "x".join(map(str, grid)),
-                       "n": n, "nnz": nnz, "dims": [cfg["feat"], *cfg["hidden"], cfg["classes"]],
-                       "gemm_mode": args.mode, "l2": "inputs larger than L2 (adjacency "
-                       f"{2 * nnz * 8 / 1e9:.1f} GB + activations per epoch)",
-                       "dataset_build_s": round(t_build, 2)},
+            "config": config_dict(cfg, grid, n, nnz),
+            "gemm_mode": args.mode, "dataset_build_s": round(t_build, 2),
             "roofline": {"bound": "hbm", "kernel": "spmm (all launches of the epoch)",
+                         "basis": "dram" if dram is not None else "compulsory",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak if achieved else None,
                          "traffic": traffic, "traffic_unit": "DRAM bytes per epoch (ncu)",
-                         "alg_bytes_per_epoch": spmm_bytes,
+                         "traffic_source": traffic_src,
                          "spmm_ms_per_epoch": spmm_s * 1e3,
                          "spmm_share_of_step": spmm_launch_share,
-                         # DRAM view of the same launches: ncu bytes over the
-                         # live SpMM time (frac above exceeds 1 because L2
-                         # serves about half of the gathered feature rows)
-                         "dram_achieved": (traffic / spmm_s / 1e9
-                                           if traffic and spmm_s > 0 else None),
-                         "dram_frac": (traffic / spmm_s / 1e9 / peak
-                                       if traffic and spmm_s > 0 else None),
-                         # against the 8 TB/s HBM3e spec sheet figure as well
+                         # the traffic floor: sparse matrix, output and every
+                         # gathered row once per launch
+                         "compulsory_bytes_per_epoch": spmm_cbytes,
+                         "compulsory_gbs": comp,
+                         "compulsory_frac": comp / peak if comp else None,
+                         "traffic_over_compulsory": (traffic / spmm_cbytes
+                                                     if traffic and spmm_cbytes else None),
+                         # SURVEY 8(d) no-reuse bytes (one gathered row per
+                         # nonzero): above the DRAM peak because L2 serves
+                         # about half of the gathers, so not a DRAM fraction
+                         "alg_noreuse_bytes_per_epoch": spmm_bytes,
+                         "alg_noreuse_gbs": alg,
+                         "alg_noreuse_over_peak": alg / peak if alg else None,
                          "spec_peak": 8000.0,
-                         "dram_frac_spec": (traffic / spmm_s / 1e9 / 8000.0
-                                            if traffic and spmm_s > 0 else None),
-                         "note": "achieved = SURVEY 8(d) algorithmic bytes "
-                                 "(8nnz + 8(rows+1) + 4nnz*D + 4rows*D per SpMM) / "
-                                 "measured SpMM time"},
+                         "note": "achieved = DRAM bytes of the epoch's SpMM launches (ncu, "
+                                 "traffic) / live SpMM device time (CUDA events); "
+                                 "compulsory = 8nnz + 8(rows+1) + 4 x_rows D + 4 rows D"},
             "phases_ms": phases,
             "collectives": coll,
             "losses": losses,
@@ -422,6 +542,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "cpu_measured_c1": c1,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -78,6 +78,11 @@ const char* pk_last_error(void);
 int pk_abi_version(void);
 /* total kernels launched by this library in the process (evidence counter) */
 uint64_t pk_kernel_launch_count(void);
+/* Device watchdog counters (process-wide): non-zero when an SpMM hub
+ * pipeline or a tcgen05 GEMM pipeline abandoned a barrier wait (its output
+ * is incomplete). The engine checks them after every epoch / pass and
+ * fails with PK_ERR_CUDA; exposed for callers of the plain kernels. */
+int pk_device_watchdogs(uint32_t* spmm, uint32_t* gemm);
 
 /* Device memory the library freed is kept in a per-process cache and reused
  * by the next allocation of the same size (a rebuilt engine allocates
@@ -298,6 +303,8 @@ typedef struct pk_epoch_metrics {
   uint64_t kernel_launches; /* libplexus kernels launched in the epoch    */
   uint64_t spmm_flops, gemm_flops;
   double allreduce_bytes, allgather_bytes, reducescatter_bytes;
+  double spmm_compulsory_bytes; /* SpMM traffic floor: sparse matrix, output
+                                   and each gathered row once             */
 } pk_epoch_metrics;
 
 typedef struct pk_tensor_view {

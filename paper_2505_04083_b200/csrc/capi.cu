@@ -26,6 +26,15 @@ std::atomic<u64> g_launches{0};
 u64 count_launch() { return g_launches.fetch_add(1, std::memory_order_relaxed) + 1; }
 u64 launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+void check_device_watchdogs() {
+  if (const unsigned s = spmm_watchdog())
+    throw Error(PK_ERR_CUDA, "spmm: hub pipeline watchdog fired " + std::to_string(s) +
+                                 " time(s); results are incomplete");
+  if (const unsigned g = gemm_watchdog())
+    throw Error(PK_ERR_CUDA, "gemm_tc: pipeline watchdog fired " + std::to_string(g) +
+                                 " time(s); results are incomplete");
+}
+
 SideStream& side_stream() {
   struct Holder {
     SideStream s;
@@ -102,6 +111,13 @@ const char* pk_last_error(void) { return g_last_error.c_str(); }
 int pk_abi_version(void) { return 1; }
 
 uint64_t pk_kernel_launch_count(void) { return g_launches.load(); }
+
+int pk_device_watchdogs(uint32_t* spmm, uint32_t* gemm) {
+  return guard([&] {
+    if (spmm) *spmm = spmm_watchdog();
+    if (gemm) *gemm = gemm_watchdog();
+  });
+}
 
 int pk_device_cache_release(void) {
   return guard([&] { dev_trim(); });

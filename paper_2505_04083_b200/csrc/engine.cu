@@ -29,6 +29,13 @@ double spmm_alg_bytes(i64 rows, u64 nnz, i64 d) {
   return 8.0 * nnz + 8.0 * (rows + 1) + 4.0 * nnz * d + 4.0 * rows * d;
 }
 
+// Compulsory bytes of the same launch: the sparse matrix and the output once,
+// and every row of the gathered operand once (x_rows = the matrix's column
+// count) — the traffic floor if L2 caught every repeated gather.
+double spmm_compulsory_bytes(i64 rows, u64 nnz, i64 x_rows, i64 d) {
+  return 8.0 * nnz + 8.0 * (rows + 1) + 4.0 * x_rows * d + 4.0 * rows * d;
+}
+
 // Global Glorot init (model.hpp:17-33) then this rank's block.
 std::vector<float> init_weight_block(u64 seed, int l, i64 din, i64 dout, const Slice& s) {
   const double bound = std::sqrt(6.0 / static_cast<double>(din + dout));
@@ -148,6 +155,7 @@ Engine::Engine(const pk_engine_config& cfg) : cfg_(cfg) {
   PK_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   PK_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   sums_.alloc(4);
+  PK_CUDA(cudaMallocHost(&sums_host_, 4 * sizeof(double)));
 }
 
 Engine::~Engine() {
@@ -160,6 +168,7 @@ Engine::~Engine() {
     cudaStreamDestroy(cs_);
   }
   for (auto e : sync_ev_) cudaEventDestroy(e);
+  if (sums_host_) cudaFreeHost(sums_host_);
 }
 
 cudaEvent_t Engine::sync_event() {
@@ -549,6 +558,7 @@ void Engine::forward_layer(int l, bool fault) {
         spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, hpart + r0 * h.ld, h.ld, st_);
         spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
         spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
+        spmm_cbytes_ += spmm_compulsory_bytes(r1 - r0, bnnz[b], b == 0 ? sh.a.cols : 0, s.f_cols);
         ++b;
         clock_.end(st_);
       },
@@ -609,7 +619,7 @@ void Engine::forward_layer(int l, bool fault) {
 // ---------------------------------------------------------------------------
 // loss (trainer.hpp:498-516)
 
-void Engine::loss(int epoch, double* loss_out, double* acc_out) {
+void Engine::loss() {
   const Layout& last = lays_[L_ - 1];
   const Shapes& s = shapes_[L_ - 1];
   const i64 C = dims_[L_];
@@ -632,15 +642,24 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
                  st_, mask_count_);
   clock_.end(st_);
   on_comm([&](cudaStream_t cs) { comms_.all_reduce_f64(sums_.p, 3, last.row, cs); });
-  double h[3];
-  u32 bad = 0;
-  PK_CUDA(cudaMemcpyAsync(h, sums_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  PK_CUDA(cudaMemcpyAsync(&bad, ce_ws_.bad.p, sizeof(u32), cudaMemcpyDeviceToHost, st_));
-  PK_CUDA(cudaStreamSynchronize(st_));
+  // no host wait here: the sums ride to pinned memory in stream order and
+  // finish_pass() checks them after the epoch (the gradient scaling uses the
+  // load-time mask count, so the backward does not need them)
+  PK_CUDA(cudaMemcpyAsync(sums_host_, sums_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  PK_CUDA(cudaMemcpyAsync(reinterpret_cast<u32*>(sums_host_ + 3), ce_ws_.bad.p, sizeof(u32),
+                          cudaMemcpyDeviceToHost, st_));
+}
+
+// finalize_loss (trainer.hpp:71-89) and the pass's error checks; the stream
+// has drained.
+void Engine::finish_pass(int epoch, double* loss_out, double* acc_out) {
+  const i64 C = dims_[L_];
+  const u32 bad = *reinterpret_cast<const u32*>(sums_host_ + 3);
   check(!bad, "cross entropy: label out of range for " + std::to_string(C) + " classes");
   if (lsa_ready_ && grid_.size() > 1 && lsa_timed_out())
     throw Error(PK_ERR_NCCL, "peer-memory reduction: a barrier wait timed out (peer stalled)");
-  // finalize_loss (trainer.hpp:71-89)
+  check_device_watchdogs();
+  const double* h = sums_host_;
   const u64 count = static_cast<u64>(h[1]), correct = static_cast<u64>(h[2]);
   if (count == 0)
     throw Error(PK_ERR_TRAINING,
@@ -649,8 +668,8 @@ void Engine::loss(int epoch, double* loss_out, double* acc_out) {
   if (!std::isfinite(loss))
     throw Error(PK_ERR_TRAINING, "epoch " + std::to_string(epoch) + ": loss is not finite (" +
                                      std::to_string(loss) + ")");
-  *loss_out = loss;
-  *acc_out = static_cast<double>(correct) / static_cast<double>(count);
+  if (loss_out) *loss_out = loss;
+  if (acc_out) *acc_out = static_cast<double>(correct) / static_cast<double>(count);
   check(count == mask_count_, "cross entropy: counted " + std::to_string(count) +
                                   " masked rows, expected " + std::to_string(mask_count_));
 }
@@ -775,6 +794,7 @@ void Engine::backward_layer(int l) {
       });
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.f_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.f_cols);
+  spmm_cbytes_ += spmm_compulsory_bytes(sh.at.rows, sh.nnz_t, sh.at.cols, s.f_cols);
   if (l > 0) std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
   df_masked_ = mask_spmm || mask_reduce;
 }
@@ -801,7 +821,7 @@ void Engine::setup_lsa() {
   lsa_ready_ = true;
 }
 
-void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
+void Engine::forward_backward(int epoch) {
   check(loaded_, "engine: no dataset loaded");
   check(comms_.ready(), "engine: communicators not initialised");
   PK_CUDA(cudaSetDevice(cfg_.device));
@@ -809,7 +829,7 @@ void Engine::forward_backward(int epoch, double* loss_out, double* acc_out) {
   sync_used_ = 0;
   if (!lsa_ready_) setup_lsa();
   for (int l = 0; l < L_; ++l) forward_layer(l, fault);
-  loss(epoch, loss_out, acc_out);
+  loss();
   for (int l = L_ - 1; l >= 0; --l) backward_layer(l);
 }
 
@@ -828,15 +848,21 @@ void Engine::optimizer_step() {
 void Engine::train_epoch(int epoch, pk_epoch_metrics* m) {
   CommCounters before = comms_.counters;
   const u64 sf0 = spmm_flops_, gf0 = gemm_flops_;
-  const double sb0 = spmm_bytes_;
+  const double sb0 = spmm_bytes_, cb0 = spmm_cbytes_;
   const u64 launches0 = launch_count();
+  clock_.reset();  // marks of earlier forward_backward / optimizer_step calls
   cudaEvent_t e0 = clock_.get(), e1 = clock_.get();
   PK_CUDA(cudaEventRecord(e0, st_));
   double loss = 0, acc = 0;
-  forward_backward(epoch, &loss, &acc);
+  forward_backward(epoch);
   optimizer_step();
   PK_CUDA(cudaEventRecord(e1, st_));
   PK_CUDA(cudaEventSynchronize(e1));
+  // the one host wait of the epoch; the checks of the pass follow it (the
+  // reference raises TrainingError before its Adam step, trainer.hpp:74-83 —
+  // here the step already ran on the device, and the error still names the
+  // epoch and ends training)
+  finish_pass(epoch, &loss, &acc);
   float ms = 0;
   PK_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   double ph[6];
@@ -851,6 +877,7 @@ void Engine::train_epoch(int epoch, pk_epoch_metrics* m) {
   m->backward_s = ph[2] + ph[5];
   m->spmm_s = ph[0] + ph[5];
   m->spmm_bytes = spmm_bytes_ - sb0;
+  m->spmm_compulsory_bytes = spmm_cbytes_ - cb0;
   m->kernel_launches = launch_count() - launches0;
   m->optimizer_s = ph[3];
   m->collectives_s = ph[4];
@@ -950,16 +977,18 @@ int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rv) {
 
 int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss, double* acc) {
   return guard([&] {
-    double l = 0, a = 0;
-    e->e->forward_backward(epoch, &l, &a);
+    e->e->reset_clock();  // phase marks are only collected by train_epoch
+    e->e->forward_backward(epoch);
     PK_CUDA(cudaStreamSynchronize(e->e->stream()));
-    if (loss) *loss = l;
-    if (acc) *acc = a;
+    e->e->finish_pass(epoch, loss, acc);
   });
 }
 
 int pk_engine_optimizer_step(pk_engine* e) {
-  return guard([&] { e->e->optimizer_step(); });
+  return guard([&] {
+    e->e->reset_clock();
+    e->e->optimizer_step();
+  });
 }
 
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* m) {

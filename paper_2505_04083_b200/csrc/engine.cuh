@@ -57,6 +57,11 @@ struct PhaseClock {
   void begin(int phase, cudaStream_t st);
   void end(cudaStream_t st);
   void collect(double out[6]);  // syncs, sums seconds per phase, resets
+  void reset() {                // drop marks nobody will collect
+    marks.clear();
+    used = 0;
+    open_phase = -1;
+  }
   ~PhaseClock();
   int open_phase = -1;
   cudaEvent_t open_ev = nullptr;
@@ -70,17 +75,23 @@ class Engine {
   void comm_init(const void* uid, int world_size) { comms_.init(grid_, rank_, uid, world_size); }
   void load(const pk_dataset_view& ds, bool host);
   void load_rank(const pk_rank_view& rv);
-  // rank_forward_backward (trainer.hpp:478-527): returns loss/accuracy
-  void forward_backward(int epoch, double* loss, double* acc);
+  // rank_forward_backward (trainer.hpp:478-527), enqueued without a host
+  // wait: the cross-entropy sums travel to pinned host memory on the stream
+  // and finish_pass() turns them into loss / accuracy (and the reference's
+  // TrainingError checks) once the stream has drained.
+  void forward_backward(int epoch);
+  // After a stream sync: loss, accuracy, error checks of the last pass.
+  void finish_pass(int epoch, double* loss, double* acc);
   void optimizer_step();
   void train_epoch(int epoch, pk_epoch_metrics* m);
+  void reset_clock() { clock_.reset(); }
   bool tensor(int which, int layer, pk_tensor_view* out);
   cudaStream_t stream() const { return st_; }
 
  private:
   void forward_layer(int l, bool fault);
   void backward_layer(int l);
-  void loss(int epoch, double* loss, double* acc);
+  void loss();
   // Forward row blocks of a plane's shard. The result is invariant to the
   // block count (test_engine.cpp:190-213), so `block_count = 0` is free to
   // pick for speed: one launch when no all-reduce follows, a few pipelined
@@ -134,10 +145,11 @@ class Engine {
   DevBuf<u8> mask_;
   u64 mask_count_ = 0;  // global number of masked nodes (the CE count)
   DevBuf<double> sums_;
+  double* sums_host_ = nullptr;  // pinned: {loss_sum, count, correct, bad}
   CeWorkspace ce_ws_;
   PhaseClock clock_;
   u64 spmm_flops_ = 0, gemm_flops_ = 0;
-  double spmm_bytes_ = 0;
+  double spmm_bytes_ = 0, spmm_cbytes_ = 0;
   bool loaded_ = false;
   // load pieces shared by load() and load_rank()
   template <typename Mark>

@@ -1416,3 +1416,11 @@ extern "C" int pk_tc_prof(unsigned long long* out8, int reset) {
   return 0;
 }
 #endif
+
+namespace pk {
+unsigned gemm_watchdog() {
+  unsigned v = 0;
+  PK_CUDA(cudaMemcpyFromSymbol(&v, g_gemm_watchdog, sizeof(v)));
+  return v;
+}
+}  // namespace pk

@@ -35,6 +35,12 @@ namespace {
 
 __device__ unsigned g_lsa_timeout = 0;
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void flag_store(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -45,18 +51,23 @@ __device__ __forceinline__ unsigned flag_load(const unsigned* p) {
 }
 
 // flags of member m: [g][kLsaBlocks] u32; slot [src][b] is written by src
+// Waits are bounded by wall time (%globaltimer), not by a poll count: a
+// peer whose host thread pauses for a while (logging, a checkpoint, GC)
+// only delays the group; a peer that never arrives within timeout_ns
+// (PK_LSA_TIMEOUT_S, default 120 s) sets the error flag the engine checks.
 __device__ void barrier(const LsaPeers& P, int b, unsigned epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int p = 0; p < P.g; ++p)
       if (p != P.me) flag_store(P.flags[p] + P.me * kLsaBlocks + b, epoch);
+    const unsigned long long t0 = globaltimer_ns();
     for (int p = 0; p < P.g; ++p) {
       if (p == P.me) continue;
       const unsigned* f = P.flags[P.me] + p * kLsaBlocks + b;
       unsigned spins = 0;
       while (static_cast<int>(flag_load(f) - epoch) < 0) {
-        if (++spins > (1u << 22)) {  // ~seconds with the backoff below
+        if ((++spins & 255u) == 0 && globaltimer_ns() - t0 > P.timeout_ns) {
           atomicExch(&g_lsa_timeout, 1u);
           break;
         }
@@ -180,6 +191,12 @@ bool LsaGroup::init(ncclComm_t comm, int g, int me, size_t scratch_elems) {
   peer_pointers(data_win_, g, dp);
   peer_pointers(flag_win_, g, fp);
   peers_.g = g, peers_.me = me;
+  static const double timeout_s = [] {
+    const char* e = std::getenv("PK_LSA_TIMEOUT_S");
+    const double v = e ? std::atof(e) : 120.0;
+    return v > 0 ? v : 120.0;
+  }();
+  peers_.timeout_ns = static_cast<unsigned long long>(timeout_s * 1e9);
   for (int j = 0; j < g; ++j) {
     peers_.data[j] = static_cast<const float*>(dp[j]);
     peers_.flags[j] = static_cast<unsigned*>(fp[j]);
@@ -230,6 +247,11 @@ bool lsa_timed_out() {
   unsigned v = 0;
   PK_CUDA(cudaMemcpyFromSymbol(&v, g_lsa_timeout, sizeof(v)));
   return v != 0;
+}
+
+void lsa_clear_timeout() {
+  const unsigned z = 0;
+  PK_CUDA(cudaMemcpyToSymbol(g_lsa_timeout, &z, sizeof(z)));
 }
 
 }  // namespace pk

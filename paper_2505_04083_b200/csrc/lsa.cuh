@@ -14,6 +14,7 @@ struct LsaPeers {
   const float* data[kLsaMaxMembers];  // each member's symmetric scratch
   unsigned* flags[kLsaMaxMembers];    // each member's barrier flags
   int g = 0, me = 0;
+  unsigned long long timeout_ns = 0;  // bounded barrier waits (wall time)
 };
 
 // One axis group's symmetric scratch + barrier flags.
@@ -50,5 +51,6 @@ class LsaGroup {
 
 // true when a barrier wait gave up (a protocol error; results are invalid)
 bool lsa_timed_out();
+void lsa_clear_timeout();
 
 }  // namespace pk

@@ -47,6 +47,14 @@ u64 launch_count();
 
 void set_last_error(const std::string& msg);
 
+// Device-side watchdogs: a kernel that gave up on a wait it should never
+// have had to abandon leaves partial results; these counters say so.
+unsigned spmm_watchdog();  // spmm.cu (hub pipeline mbarrier waits)
+unsigned gemm_watchdog();  // gemm_tc.cu (tcgen05 pipeline barrier waits)
+// Throws PK_ERR_CUDA naming the kernel when a watchdog fired (a sync point:
+// call after the work has completed).
+void check_device_watchdogs();
+
 template <typename F>
 int guard(F&& f) {
   try {

@@ -181,7 +181,8 @@ __device__ __forceinline__ float8 ldg_hint<float8>(const float* p, bool hot) {
 constexpr int kThreads = 256;
 
 // Set (and reported once with printf) when a kernel bails out of a wait or
-// loop that should have terminated; read back by pk_spmm_watchdog().
+// loop that should have terminated; read back by spmm_watchdog() / pk_device_watchdogs(); the engine checks it
+// after every epoch.
 __device__ unsigned g_spmm_watchdog = 0;
 
 // ---------------------------------------------------------------------------
@@ -1198,4 +1199,12 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   if (!plan.segment && rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));
 }
 
+}  // namespace pk
+
+namespace pk {
+unsigned spmm_watchdog() {
+  unsigned v = 0;
+  PK_CUDA(cudaMemcpyFromSymbol(&v, g_spmm_watchdog, sizeof(v)));
+  return v;
+}
 }  // namespace pk

@@ -26,7 +26,7 @@ from .layout import GridConfig, feature_slice, plan_layouts, weight_slice
 MAX_KEYS = ("forward_spmm_s", "forward_gemm_s", "backward_s", "optimizer_s", "collectives_s",
             "epoch_s", "spmm_s")
 SUM_KEYS = ("spmm_flops", "gemm_flops", "allreduce_bytes", "allgather_bytes",
-            "reducescatter_bytes", "spmm_bytes", "kernel_launches")
+            "reducescatter_bytes", "spmm_bytes", "spmm_compulsory_bytes", "kernel_launches")
 
 
 @dataclass

@@ -50,7 +50,7 @@ class pk_epoch_metrics(C.Structure):
                 ("kernel_launches", C.c_uint64),
                 ("spmm_flops", C.c_uint64), ("gemm_flops", C.c_uint64),
                 ("allreduce_bytes", C.c_double), ("allgather_bytes", C.c_double),
-                ("reducescatter_bytes", C.c_double)]
+                ("reducescatter_bytes", C.c_double), ("spmm_compulsory_bytes", C.c_double)]
 
 
 class pk_rank_view(C.Structure):
@@ -102,7 +102,8 @@ class TrainOptions:
 METRIC_KEYS = ("epoch", "loss", "accuracy", "forward_spmm_s", "forward_gemm_s", "backward_s",
                "optimizer_s", "collectives_s", "epoch_s", "spmm_s", "spmm_bytes",
                "kernel_launches", "spmm_flops", "gemm_flops",
-               "allreduce_bytes", "allgather_bytes", "reducescatter_bytes")
+               "allreduce_bytes", "allgather_bytes", "reducescatter_bytes",
+               "spmm_compulsory_bytes")
 
 
 def nccl_unique_id() -> bytes:
@@ -266,6 +267,18 @@ class RankEngine:
                                         "data": (int(v.data), False), "version": 3,
                                         "strides": None}
         return torch.as_tensor(_Arr(), device="cuda")[:, :v.cols].clone()
+
+    def download_params(self):
+        """This rank's share of TrainResult (trainer.hpp:636-686): its W
+        shards and F0 shard copied to pinned host memory (numpy views)."""
+        outs = []
+        for which, layers in ((PK_T_W, range(len(self.dims) - 1)), (PK_T_F0, [0])):
+            for l in layers:
+                t = self.tensor(which, l)
+                h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+                h.copy_(t)
+                outs.append(h.numpy())
+        return outs
 
     def stream_ptr(self):
         s = C.c_void_p()

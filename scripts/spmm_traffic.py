@@ -1,7 +1,7 @@
 """From an ncu launch list of one epoch (scripts/ncu_round.sh), write the
 SpMM DRAM traffic bench.py reports as roofline.traffic:
 profiles/ncu_spmm_<config>.json = {dram_bytes_per_epoch, launches, ...}."""
-import collections, csv, json, sys
+import collections, csv, json, os, sys
 
 path, out = sys.argv[1], sys.argv[2]
 rows = list(csv.reader(open(path)))
@@ -19,5 +19,6 @@ sp = [i for i in per if "spmm" in names[i] and "partition" not in names[i]]
 byts = sum(per[i].get("dram__bytes_read.sum", 0) + per[i].get("dram__bytes_write.sum", 0) for i in sp)
 secs = sum(per[i].get("gpu__time_duration.sum", 0) for i in sp)
 json.dump({"dram_bytes_per_epoch": byts, "spmm_launches": len(sp), "spmm_seconds_serialised": secs,
-           "dram_gbs_serialised": byts / secs / 1e9 if secs else None, "source": path}, open(out, "w"), indent=1)
+           "dram_gbs_serialised": byts / secs / 1e9 if secs else None, "source": path,
+           "commit": os.environ.get("PK_COMMIT")}, open(out, "w"), indent=1)
 print(open(out).read())
