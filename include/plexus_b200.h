@@ -37,6 +37,8 @@ typedef enum pk_status {
   PK_ERR_NCCL = 3,     /* NCCL failure                                */
   PK_ERR_MEMORY = 4,   /* MemoryError (common.hpp:22-26), device OOM  */
   PK_ERR_TRAINING = 5, /* TrainingError (trainer.hpp:26-29)           */
+  PK_ERR_ABORTED = 6,  /* ClusterAborted (cluster.hpp:67-71): another
+                          rank of the grid failed                      */
   /* IoError (common.hpp:28-41): 10 + IoErrorCode                        */
   PK_ERR_IO_MISSING = 10,   /* MissingFile                              */
   PK_ERR_IO_TRUNCATED = 11, /* TruncatedFile                            */
@@ -75,7 +77,7 @@ typedef struct pk_csr_owned {
 } pk_csr_owned;
 
 const char* pk_last_error(void);
-int pk_abi_version(void);
+int pk_abi_version(void); /* 2 */
 /* total kernels launched by this library in the process (evidence counter) */
 uint64_t pk_kernel_launch_count(void);
 /* Device watchdog counters (process-wide): non-zero when an SpMM hub
@@ -332,6 +334,23 @@ int pk_nccl_unique_id(void* out128);
 int pk_engine_create(const pk_engine_config* cfg, pk_engine** out);
 /* world_size 1 needs no call; otherwise every rank passes rank 0's id. */
 int pk_engine_comm_init(pk_engine* e, const void* unique_id128, int world_size);
+/* In-process cluster (Cluster, cluster.hpp:188-250, 405-442): every rank
+ * of the grid is a host thread of this process with its own engine; several
+ * ranks may share one GPU. Collectives are ordered device sums / copies
+ * sequenced by CUDA events the members swap at a host rendezvous
+ * (GroupChannel::exchange, cluster.hpp:140-168) — the reference's
+ * coordinate-order combine bit for bit for any group size. When a rank's
+ * load / pass / epoch fails, its cluster aborts: every other rank's pending
+ * or next collective returns PK_ERR_ABORTED naming the failed rank
+ * (ClusterAborted, cluster.hpp:67-71, 240, 434). */
+typedef struct pk_cluster pk_cluster;
+int pk_cluster_create(int gx, int gy, int gz, pk_cluster** out);
+int pk_cluster_abort(pk_cluster* c, int rank, const char* why);
+int pk_cluster_aborted(pk_cluster* c, int* aborted);
+/* after every engine of the cluster is destroyed */
+int pk_cluster_destroy(pk_cluster* c);
+/* instead of pk_engine_comm_init: this engine is rank cfg.rank of `c` */
+int pk_engine_comm_init_local(pk_engine* e, pk_cluster* c);
 int pk_engine_load(pk_engine* e, const pk_dataset_view* ds);
 int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds_host);
 /* The file_handle path (trainer.hpp:461-466): this rank's tensors only
@@ -342,6 +361,42 @@ int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rank_tensors);
 int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss_host,
                                double* accuracy_host);
 int pk_engine_optimizer_step(pk_engine* e);
+
+/* rank_forward_backward one piece at a time (forward_layer, engine.hpp:
+ * 158-206; backward_layer, engine.hpp:214-259): begin_pass; forward_layer
+ * l = 0..L-1 (fault = EngineOptions.fault_skip_h_allreduce); loss (logits
+ * column gather + CE + the 1x3 sums all-reduce, trainer.hpp:498-516);
+ * backward_layer l = L-1..0; finish_pass (stream sync, finalize_loss checks,
+ * loss / accuracy). The same as pk_engine_forward_backward. The layer's
+ * tensors (PK_T_H / PK_T_Q / PK_T_ACT / PK_T_DW) are readable after it. */
+int pk_engine_begin_pass(pk_engine* e);
+int pk_engine_forward_layer(pk_engine* e, int layer, int fault);
+int pk_engine_loss(pk_engine* e);
+int pk_engine_backward_layer(pk_engine* e, int layer);
+int pk_engine_finish_pass(pk_engine* e, int epoch, double* loss_host,
+                          double* accuracy_host);
+
+/* RankCtx collectives (cluster.hpp:265-340) over this rank's axis group
+ * (axis 0/1/2 = X/Y/Z; members in ascending coordinate order), on device
+ * buffers, enqueued on `stream`; singleton axes short-circuit but are still
+ * counted, like the reference. Every member of the group must make the same
+ * call. Sums are the reference's coordinate-order combine (in-process
+ * clusters and peer-memory groups) or NCCL's sum (two-member axes: equal).
+ *   all_reduce     (cluster.hpp:307-321): buf rows x cols (ld) summed in place
+ *   all_gather     (cluster.hpp:268-305): member j's block (chunk_size(out_rows
+ *                  or out_cols, g, j) rows / columns) concatenated by rows
+ *                  (concat_cols = 0) or columns (1) into out
+ *   reduce_scatter (cluster.hpp:323-340): sum of buf (rows x cols), this
+ *                  member keeps row chunk chunk_start(rows, g, pos).. in out */
+int pk_engine_all_reduce_f32(pk_engine* e, int axis, float* buf, int64_t rows,
+                             int64_t cols, int64_t ld, void* stream);
+int pk_engine_all_gather_f32(pk_engine* e, int axis, int concat_cols,
+                             const float* local, int64_t local_ld, float* out,
+                             int64_t out_rows, int64_t out_cols, int64_t out_ld,
+                             void* stream);
+int pk_engine_reduce_scatter_f32(pk_engine* e, int axis, float* buf, int64_t rows,
+                                 int64_t cols, int64_t ld, float* out,
+                                 void* stream);
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* out_host);
 int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out);
 int pk_engine_stream(pk_engine* e, void** stream_out);

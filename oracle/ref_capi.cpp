@@ -11,8 +11,10 @@
 // arrays into the reference's types and calls the reference entry point named
 // in its comment.
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -1012,6 +1014,121 @@ int ref_epoch_sample(void* pre, const u64* hidden, int nh, u64 rows, int threads
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     out[0] = wall * static_cast<double>(n) / (static_cast<double>(threads) * rows);
     out[1] = wall;
+  });
+}
+
+// SerialTrainer::forward_backward (trainer.hpp:137-169) with the reference's
+// own kernels composed over `threads` row blocks — the checker for passes too
+// large for one thread (C2: 116.6M nonzeros, 100-256-256-47). Row-local ops
+// (spmm_rows, the NN / NT gemms, relu, per-row CE) are bitwise those of the
+// serial pass: every output row is the same loop over the same operands.
+// The two cross-row reductions are not: the CE loss_sum (double; blocks
+// summed in order) and dW = H^T dQ over K = n rows, which is returned in
+// double (the reference's gemm at T = double on the fp32 operands, block
+// partials summed in double) — at K = 2M rows the serial fp32 chain's own
+// rounding is ~1e-4 normwise, so dW is gated against this fp64 value.
+// Outputs: loss, accuracy, logits (n x C), dW (f64) concatenated, dF0
+// (n x F), H of layer 0.
+int ref_serial_pass_parallel(void* pre, const u64* hidden, int nh, u64 seed, int threads,
+                             double* loss, double* acc, float* logits, double* dw_cat,
+                             float* df0, float* h0) {
+  auto* p = static_cast<Pre*>(pre);
+  return guarded([&] {
+    check(!p->f64, "ref_serial_pass_parallel: float datasets only");
+    const auto& d = p->f;
+    std::vector<std::size_t> dims{d.feat_dim};
+    for (int i = 0; i < nh; ++i) dims.push_back(hidden[i]);
+    dims.push_back(d.num_classes);
+    const int L = static_cast<int>(dims.size()) - 1;
+    const std::size_t n = d.n;
+    const int T = std::max(1, threads);
+    auto ws = init_weights<float>(dims, seed);
+    const CsrMatrix<float> at_even = d.a_even.transpose(), at_odd = d.a_odd.transpose();
+    auto par = [&](auto&& body) {
+      std::vector<std::thread> pool;
+      for (int t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+          const std::size_t r0 = n * t / T, r1 = n * (t + 1) / T;
+          body(t, r0, r1);
+        });
+      for (auto& th : pool) th.join();
+    };
+    auto put = [&](DenseMatrix<float>& dst, std::size_t r0, const DenseMatrix<float>& blk) {
+      if (blk.size()) std::memcpy(dst.data() + r0 * dst.cols(), blk.data(), blk.size() * sizeof(float));
+    };
+    std::vector<DenseMatrix<float>> h(L), q(L);
+    DenseMatrix<float> f = d.features;
+    for (int l = 0; l < L; ++l) {
+      const auto& a = l % 2 ? d.a_odd : d.a_even;
+      h[l] = DenseMatrix<float>::zeros(n, dims[l]);
+      q[l] = DenseMatrix<float>::zeros(n, dims[l + 1]);
+      DenseMatrix<float> fn = l + 1 < L ? DenseMatrix<float>::zeros(n, dims[l + 1])
+                                        : DenseMatrix<float>();
+      par([&](int, std::size_t r0, std::size_t r1) {
+        auto hb = spmm_rows(a, f, r0, r1);
+        auto qb = gemm(hb, ws[l]);
+        put(h[l], r0, hb);
+        put(q[l], r0, qb);
+        if (l + 1 < L) put(fn, r0, relu_forward(qb));
+      });
+      if (l + 1 < L) f = std::move(fn);
+    }
+    const int parity = final_output_parity(L);
+    const auto& labels = d.labels_for_parity(parity);
+    const auto& mask = d.mask_for_parity(parity);
+    std::vector<double> lsum(T);
+    std::vector<u64> cnt(T), cor(T);
+    auto df = DenseMatrix<float>::zeros(n, dims[L]);
+    par([&](int t, std::size_t r0, std::size_t r1) {
+      auto s = softmax_cross_entropy_sums(
+          q[L - 1].block(r0, r1, 0, dims[L]),
+          std::vector<u32>(labels.begin() + r0, labels.begin() + r1),
+          std::vector<u8>(mask.begin() + r0, mask.begin() + r1));
+      lsum[t] = s.loss_sum, cnt[t] = s.count, cor[t] = s.correct;
+      put(df, r0, s.dlogits);
+    });
+    double sum = 0;
+    u64 count = 0, correct = 0;
+    for (int t = 0; t < T; ++t) sum += lsum[t], count += cnt[t], correct += cor[t];
+    CrossEntropySums<float> all;
+    all.dlogits = std::move(df);
+    auto lr = detail::finalize_loss<float>(std::move(all), sum, count, correct, 0);
+    *loss = lr.loss;
+    *acc = lr.accuracy;
+    std::memcpy(logits, q[L - 1].data(), q[L - 1].size() * sizeof(float));
+    if (h0) std::memcpy(h0, h[0].data(), h[0].size() * sizeof(float));
+    df = std::move(lr.dlogits);
+    std::vector<std::size_t> off(L, 0);
+    for (int l = 1; l < L; ++l) off[l] = off[l - 1] + dims[l - 1] * dims[l];
+    for (int l = L - 1; l >= 0; --l) {
+      const auto& at = l % 2 ? at_odd : at_even;
+      auto dq = l == L - 1 ? std::move(df) : DenseMatrix<float>::zeros(n, dims[l + 1]);
+      auto dh = DenseMatrix<float>::zeros(n, dims[l]);
+      std::vector<DenseMatrix<double>> dwp(T);
+      par([&](int t, std::size_t r0, std::size_t r1) {
+        DenseMatrix<float> dqb = l == L - 1 ? dq.block(r0, r1, 0, dims[l + 1])
+                                            : relu_backward(q[l].block(r0, r1, 0, dims[l + 1]),
+                                                            df.block(r0, r1, 0, dims[l + 1]));
+        if (l != L - 1) put(dq, r0, dqb);
+        // dW = H^T dQ in T = double: the reference's own gemm at double
+        // precision on the fp32 operands, block partials summed in double
+        auto hb = h[l].block(r0, r1, 0, dims[l]);
+        dwp[t] = gemm(DenseMatrix<double>(hb.rows(), hb.cols(),
+                                          std::vector<double>(hb.data(), hb.data() + hb.size())),
+                      DenseMatrix<double>(dqb.rows(), dqb.cols(),
+                                          std::vector<double>(dqb.data(), dqb.data() + dqb.size())),
+                      true, false);
+        put(dh, r0, gemm(dqb, ws[l], false, true));
+      });
+      DenseMatrix<double> dw = std::move(dwp[0]);
+      for (int t = 1; t < T; ++t)
+        for (std::size_t i = 0; i < dw.size(); ++i) dw.data()[i] += dwp[t].data()[i];
+      for (std::size_t i = 0; i < dw.size(); ++i) dw_cat[off[l] + i] = dw.data()[i];
+      auto dfn = DenseMatrix<float>::zeros(n, dims[l]);
+      par([&](int, std::size_t r0, std::size_t r1) { put(dfn, r0, spmm_rows(at, dh, r0, r1)); });
+      df = std::move(dfn);
+    }
+    std::memcpy(df0, df.data(), df.size() * sizeof(float));
   });
 }
 

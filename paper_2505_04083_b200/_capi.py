@@ -11,7 +11,8 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libplexus_b200.so")
 
-PK_OK, PK_ERR_CONTRACT, PK_ERR_CUDA, PK_ERR_NCCL, PK_ERR_MEMORY, PK_ERR_TRAINING = range(6)
+(PK_OK, PK_ERR_CONTRACT, PK_ERR_CUDA, PK_ERR_NCCL, PK_ERR_MEMORY, PK_ERR_TRAINING,
+ PK_ERR_ABORTED) = range(7)
 PK_MODE_PARITY, PK_MODE_FAST = 0, 1
 
 
@@ -35,6 +36,10 @@ class NcclError(RuntimeError):
     pass
 
 
+class ClusterAborted(RuntimeError):
+    """plexuskit::ClusterAborted (cluster.hpp:67-71): another rank failed."""
+
+
 class IoError(RuntimeError):
     """plexuskit::IoError (common.hpp:28-41); `code` is the IoErrorCode name."""
     CODES = {10: "MissingFile", 11: "TruncatedFile", 12: "ChecksumMismatch",
@@ -50,7 +55,8 @@ def _io_error(rc):
 
 
 _ERRORS = {PK_ERR_CONTRACT: ContractError, PK_ERR_CUDA: CudaError, PK_ERR_NCCL: NcclError,
-           PK_ERR_MEMORY: MemoryError_, PK_ERR_TRAINING: TrainingError}
+           PK_ERR_MEMORY: MemoryError_, PK_ERR_TRAINING: TrainingError,
+           PK_ERR_ABORTED: ClusterAborted}
 _ERRORS.update({rc: _io_error(rc) for rc in IoError.CODES})
 
 

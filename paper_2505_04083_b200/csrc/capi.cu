@@ -108,7 +108,7 @@ extern "C" {
 
 const char* pk_last_error(void) { return g_last_error.c_str(); }
 
-int pk_abi_version(void) { return 1; }
+int pk_abi_version(void) { return 2; }  // 2: pk_epoch_metrics.spmm_compulsory_bytes, clusters, per-layer calls
 
 uint64_t pk_kernel_launch_count(void) { return g_launches.load(); }
 

@@ -138,6 +138,39 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
   axes_ = set_->axes;
 }
 
+void Comms::init_local(const Grid& grid, int rank, LocalCluster* cluster) {
+  check(cluster != nullptr, "comm init: null cluster");
+  const Grid& cg = cluster->grid();
+  check(cg.g[0] == grid.g[0] && cg.g[1] == grid.g[1] && cg.g[2] == grid.g[2],
+        "comm init: the cluster's grid differs from the engine's");
+  grid_ = grid;
+  coords_ = grid.coords_of(rank);
+  local_ = true;
+  lc_.init(cluster, grid, rank);
+}
+
+void Comms::abort_nccl() {
+  if (!set_) return;
+  // ncclCommAbort ends in-flight operations instead of waiting for them;
+  // the set leaves the process cache so no later engine reuses it
+  for (auto& c : set_->axes)
+    if (c) {
+      ncclCommAbort(c);
+      c = nullptr;
+    }
+  if (set_->world) {
+    ncclCommAbort(set_->world);
+    set_->world = nullptr;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    for (auto it = g_comm_cache.begin(); it != g_comm_cache.end();)
+      it = it->second == set_ ? g_comm_cache.erase(it) : std::next(it);
+  }
+  world_ = nullptr;
+  axes_ = {nullptr, nullptr, nullptr};
+}
+
 LsaGroup* Comms::lsa(int axis, size_t elems) {
   const int g = grid_.extent(axis);
   if (g == 1 || !set_) return nullptr;
@@ -177,14 +210,18 @@ void Comms::all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaS
   const int g = grid_.extent(axis);
   counters.calls[axis][kAllReduce]++;
   counters.ring_numer[axis][kAllReduce] += 2 * static_cast<u64>(g - 1) * logical_bytes;
-  if (g == 1 || count == 0) return;
+  if (g == 1) return;
+  if (local_) return lc_.all_reduce<float>(axis, buf, 1, count, count, st);
+  if (count == 0) return;
   PK_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, axes_[axis], st));
 }
 
 void Comms::all_reduce_f64(double* buf, i64 count, int axis, cudaStream_t st) {
   const int g = grid_.extent(axis);
   counters.calls[axis][kAllReduce]++;  // loss stats are not part of the modeled volume
-  if (g == 1 || count == 0) return;
+  if (g == 1) return;
+  if (local_) return lc_.all_reduce<double>(axis, buf, 1, count, count, st);
+  if (count == 0) return;
   PK_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, axes_[axis], st));
 }
 
@@ -201,6 +238,7 @@ void Comms::all_gather_rows(const float* local, float* out, i64 total_rows, i64 
                               cudaMemcpyDeviceToDevice, st));
     return;
   }
+  if (local_) return lc_.all_gather_rows(axis, local, out, total_rows, ld, st);
   PK_NCCL(ncclGroupStart());
   for (int j = 0; j < g; ++j) {
     const i64 off = chunk_start(total_rows, g, j), rows = chunk_size(total_rows, g, j);
@@ -217,6 +255,7 @@ void Comms::all_gather_cols(const float* local, i64 ld_in, float* out, i64 ld_ou
   counters.calls[axis][kAllGather]++;
   counters.ring_numer[axis][kAllGather] +=
       static_cast<u64>(g - 1) * static_cast<u64>(rows) * total_cols * sizeof(float);
+  if (g > 1 && local_) return lc_.all_gather_cols(axis, local, ld_in, out, ld_out, rows, total_cols, st);
   if (rows == 0 || total_cols == 0) return;
   if (g == 1) {
     copy_block_kernel<<<small_grid(rows * total_cols), 256, 0, st>>>(local, ld_in, rows,
@@ -256,6 +295,7 @@ void Comms::reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int ax
                               cudaMemcpyDeviceToDevice, st));
     return;
   }
+  if (local_) return lc_.ordered_sum<float>(axis, buf, ld, own0, own0 + own_rows, logical_cols, out, ld, st);
   PK_NCCL(ncclGroupStart());
   for (int j = 0; j < g; ++j) {
     const i64 off = chunk_start(rows, g, j), cnt = chunk_size(rows, g, j);
@@ -277,6 +317,10 @@ void Comms::reduce_scatter_rows_range(float* buf, float* out, i64 rows, i64 ld, 
       PK_CUDA(cudaMemcpyAsync(out + (r0 - own0) * ld, buf + r0 * ld, (r1 - r0) * ld * sizeof(float),
                               cudaMemcpyDeviceToDevice, st));
     return;
+  }
+  if (local_) {
+    const i64 a = std::max(r0, own0), b = std::max(a, std::min(r1, own1));
+    return lc_.ordered_sum<float>(axis, buf, ld, a, b, logical_cols, out + (a - own0) * ld, ld, st);
   }
   PK_NCCL(ncclGroupStart());
   for (int j = 0; j < g; ++j) {

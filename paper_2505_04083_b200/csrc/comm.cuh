@@ -20,6 +20,7 @@
 #include <memory>
 
 #include "layout.h"
+#include "local.cuh"
 #include "lsa.cuh"
 #include "pk_common.cuh"
 
@@ -52,7 +53,13 @@ class Comms {
   // world_size == 1: no NCCL at all. Otherwise `uid` is the 128-byte
   // ncclUniqueId from rank 0.
   void init(const Grid& grid, int rank, const void* uid, int world_size);
-  bool ready() const { return world_ != nullptr || grid_.size() == 1; }
+  // In-process cluster (local.cuh): the ranks are threads of this process.
+  void init_local(const Grid& grid, int rank, LocalCluster* cluster);
+  bool ready() const { return world_ != nullptr || local_ || grid_.size() == 1; }
+  LocalCluster* local_cluster() const { return local_ ? lc_.cluster() : nullptr; }
+  // Tear down after a failure (ClusterAborted semantics): NCCL
+  // communicators are aborted so no later call can block on them.
+  void abort_nccl();
   int size(int axis) const { return grid_.extent(axis); }
   int pos(int axis) const { return coords_.along(axis); }
 
@@ -92,6 +99,8 @@ class Comms {
 
  private:
   ncclComm_t axis_comm(int axis) const { return axes_[axis]; }
+  bool local_ = false;
+  LocalComm lc_;
   Grid grid_;
   Coords coords_;
   ncclComm_t world_ = nullptr;

@@ -821,13 +821,17 @@ void Engine::setup_lsa() {
   lsa_ready_ = true;
 }
 
-void Engine::forward_backward(int epoch) {
+void Engine::begin_pass() {
   check(loaded_, "engine: no dataset loaded");
   check(comms_.ready(), "engine: communicators not initialised");
   PK_CUDA(cudaSetDevice(cfg_.device));
-  const bool fault = epoch == cfg_.fault_epoch;
   sync_used_ = 0;
   if (!lsa_ready_) setup_lsa();
+}
+
+void Engine::forward_backward(int epoch) {
+  const bool fault = epoch == cfg_.fault_epoch;
+  begin_pass();
   for (int l = 0; l < L_; ++l) forward_layer(l, fault);
   loss();
   for (int l = L_ - 1; l >= 0; --l) backward_layer(l);
@@ -895,6 +899,10 @@ void Engine::train_epoch(int epoch, pk_epoch_metrics* m) {
   }
 }
 
+void Engine::on_failure(const std::string& why) {
+  if (LocalCluster* cl = comms_.local_cluster()) cl->abort(rank_, why);
+}
+
 bool Engine::tensor(int which, int layer, pk_tensor_view* out) {
   auto fill = [&](const DMat& m, i64 cols) {
     out->data = m.p();
@@ -929,7 +937,27 @@ struct pk_engine {
   std::unique_ptr<pk::Engine> e;
 };
 
+struct pk_cluster {
+  std::unique_ptr<pk::LocalCluster> c;
+};
+
 using namespace pk;
+
+namespace {
+// Entry points that run the rank's collective program: a failure here is a
+// rank failure and aborts the rank's cluster (ClusterAborted on the peers).
+template <typename F>
+int guard_rank(pk_engine* e, F&& f) {
+  const int rc = guard(std::forward<F>(f));
+  if (rc != PK_OK && rc != PK_ERR_ABORTED && e && e->e) {
+    try {
+      e->e->on_failure(pk_last_error());
+    } catch (...) {
+    }
+  }
+  return rc;
+}
+}  // namespace
 
 extern "C" {
 
@@ -960,23 +988,54 @@ int pk_engine_comm_init(pk_engine* e, const void* uid, int world_size) {
   return guard([&] { e->e->comm_init(uid, world_size); });
 }
 
+int pk_cluster_create(int gx, int gy, int gz, pk_cluster** out) {
+  return guard([&] {
+    check(out != nullptr, "cluster: null argument");
+    Grid g;
+    g.g[0] = gx, g.g[1] = gy, g.g[2] = gz;
+    check(gx >= 1 && gy >= 1 && gz >= 1, "grid: all dimensions must be >= 1");
+    auto* h = new pk_cluster;
+    h->c = std::make_unique<LocalCluster>(g);
+    *out = h;
+  });
+}
+
+int pk_cluster_abort(pk_cluster* c, int rank, const char* why) {
+  return guard([&] { c->c->abort(rank, why ? why : "aborted by the host"); });
+}
+
+int pk_cluster_aborted(pk_cluster* c, int* aborted) {
+  return guard([&] { *aborted = c->c->aborted() ? 1 : 0; });
+}
+
+int pk_cluster_destroy(pk_cluster* c) {
+  return guard([&] { delete c; });
+}
+
+int pk_engine_comm_init_local(pk_engine* e, pk_cluster* c) {
+  return guard([&] {
+    check(e && c, "comm init: null argument");
+    e->e->comm_init_local(c->c.get());
+  });
+}
+
 int pk_engine_load(pk_engine* e, const pk_dataset_view* ds) {
-  return guard([&] { e->e->load(*ds, false); });
+  return guard_rank(e, [&] { e->e->load(*ds, false); });
 }
 
 int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds) {
-  return guard([&] { e->e->load(*ds, true); });
+  return guard_rank(e, [&] { e->e->load(*ds, true); });
 }
 
 int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rv) {
-  return guard([&] {
+  return guard_rank(e, [&] {
     check(e && rv, "engine load_rank: null argument");
     e->e->load_rank(*rv);
   });
 }
 
 int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss, double* acc) {
-  return guard([&] {
+  return guard_rank(e, [&] {
     e->e->reset_clock();  // phase marks are only collected by train_epoch
     e->e->forward_backward(epoch);
     PK_CUDA(cudaStreamSynchronize(e->e->stream()));
@@ -984,15 +1043,85 @@ int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss, double* ac
   });
 }
 
+int pk_engine_begin_pass(pk_engine* e) {
+  return guard_rank(e, [&] {
+    e->e->reset_clock();
+    e->e->begin_pass();
+  });
+}
+
+int pk_engine_forward_layer(pk_engine* e, int layer, int fault) {
+  return guard_rank(e, [&] {
+    check(layer >= 0 && layer < e->e->num_layers(), "engine: layer out of range");
+    e->e->layer_forward(layer, fault != 0);
+  });
+}
+
+int pk_engine_loss(pk_engine* e) {
+  return guard_rank(e, [&] { e->e->pass_loss(); });
+}
+
+int pk_engine_backward_layer(pk_engine* e, int layer) {
+  return guard_rank(e, [&] {
+    check(layer >= 0 && layer < e->e->num_layers(), "engine: layer out of range");
+    e->e->layer_backward(layer);
+  });
+}
+
+int pk_engine_finish_pass(pk_engine* e, int epoch, double* loss, double* acc) {
+  return guard_rank(e, [&] {
+    PK_CUDA(cudaStreamSynchronize(e->e->stream()));
+    e->e->finish_pass(epoch, loss, acc);
+  });
+}
+
+// RankCtx collectives (cluster.hpp:265-340) on this rank's axis groups.
+int pk_engine_all_reduce_f32(pk_engine* e, int axis, float* buf, int64_t rows, int64_t cols,
+                             int64_t ld, void* stream) {
+  return guard_rank(e, [&] {
+    check(axis >= 0 && axis < 3, "all_reduce: axis out of range");
+    check(rows >= 0 && cols >= 0 && ld >= cols, "all_reduce: bad shape");
+    e->e->comms().all_reduce(buf, rows * ld, axis, rows * cols * 4, as_stream(stream));
+  });
+}
+
+int pk_engine_all_gather_f32(pk_engine* e, int axis, int concat_cols, const float* local,
+                             int64_t local_ld, float* out, int64_t out_rows, int64_t out_cols,
+                             int64_t out_ld, void* stream) {
+  return guard_rank(e, [&] {
+    check(axis >= 0 && axis < 3, "all_gather: axis out of range");
+    Comms& c = e->e->comms();
+    const int g = c.size(axis);
+    if (concat_cols) {
+      DevBuf<float> stage(static_cast<size_t>(std::max<i64>(1, out_rows * out_cols)));
+      c.all_gather_cols(local, local_ld, out, out_ld, out_rows, out_cols, axis, stage.p,
+                        as_stream(stream));
+      PK_CUDA(cudaStreamSynchronize(as_stream(stream)));  // stage dies here
+    } else {
+      check(local_ld == out_ld, "all_gather: rows are concatenated with one row stride");
+      (void)g;
+      c.all_gather_rows(local, out, out_rows, out_ld, axis, out_cols, as_stream(stream));
+    }
+  });
+}
+
+int pk_engine_reduce_scatter_f32(pk_engine* e, int axis, float* buf, int64_t rows, int64_t cols,
+                                 int64_t ld, float* out, void* stream) {
+  return guard_rank(e, [&] {
+    check(axis >= 0 && axis < 3, "reduce_scatter: axis out of range");
+    e->e->comms().reduce_scatter_rows(buf, out, rows, ld, axis, cols, as_stream(stream));
+  });
+}
+
 int pk_engine_optimizer_step(pk_engine* e) {
-  return guard([&] {
+  return guard_rank(e, [&] {
     e->e->reset_clock();
     e->e->optimizer_step();
   });
 }
 
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* m) {
-  return guard([&] { e->e->train_epoch(epoch, m); });
+  return guard_rank(e, [&] { e->e->train_epoch(epoch, m); });
 }
 
 int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out) {

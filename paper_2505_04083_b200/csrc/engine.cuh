@@ -73,6 +73,10 @@ class Engine {
   ~Engine();
 
   void comm_init(const void* uid, int world_size) { comms_.init(grid_, rank_, uid, world_size); }
+  void comm_init_local(LocalCluster* cl) { comms_.init_local(grid_, rank_, cl); }
+  // A failed rank takes its cluster down (cluster.hpp:240, 434): peers
+  // blocked in (or later entering) a collective fail with ClusterAborted.
+  void on_failure(const std::string& why);
   void load(const pk_dataset_view& ds, bool host);
   void load_rank(const pk_rank_view& rv);
   // rank_forward_backward (trainer.hpp:478-527), enqueued without a host
@@ -85,6 +89,16 @@ class Engine {
   void optimizer_step();
   void train_epoch(int epoch, pk_epoch_metrics* m);
   void reset_clock() { clock_.reset(); }
+  // forward_layer / backward_layer (engine.hpp:158-259) one at a time, for
+  // callers that drive rank_forward_backward themselves (the C++ shim):
+  // begin_pass, forward_layer(0..L-1), loss, backward_layer(L-1..0), then a
+  // stream sync and finish_pass give exactly forward_backward.
+  void begin_pass();
+  void layer_forward(int l, bool fault) { forward_layer(l, fault); }
+  void pass_loss() { loss(); }
+  void layer_backward(int l) { backward_layer(l); }
+  int num_layers() const { return L_; }
+  Comms& comms() { return comms_; }
   bool tensor(int which, int layer, pk_tensor_view* out);
   cudaStream_t stream() const { return st_; }
 

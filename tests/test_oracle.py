@@ -126,4 +126,4 @@ def test_capi_exports_every_declared_symbol():
     missing = [s for s in sorted(declared) if not hasattr(lib, s)]
     assert not missing, missing
     assert set(_capi.SIGNATURES) <= declared | {"pk_last_error"}
-    assert lib.pk_abi_version() == 1
+    assert lib.pk_abi_version() == 2
