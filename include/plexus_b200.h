@@ -237,6 +237,54 @@ int pk_degree_quantile_labels(const uint32_t* edges_uv, uint64_t num_edges,
                               void* stream);
 
 /* ------------------------------------------------------------------ */
+/* Per-rank shard generation (billion-edge grids): one rank's blocks,    */
+/* features and labels straight from synth_rmat's indexable Philox       */
+/* streams, bit-identical to synth_rmat -> preprocess ->                 */
+/* build_adjacency_shards / slice_rank_tensors (graph.hpp:40-148, 291-384,*/
+/* engine.hpp:96-113, trainer.hpp:234-250) without the global graph.     */
+
+/* RmatParams (graph.hpp:189-193) + the dataset's orientation: synth_rmat
+ * always symmetrises (graph.hpp:23); undirected = 0 keeps the drawn
+ * orientation with row degrees (the papers-shaped C4, SURVEY 8e'). */
+typedef struct pk_rmat_spec {
+  int scale;
+  int undirected;
+  uint64_t edges; /* 0 = 8 * 2^scale (graph.hpp:298) */
+  double a, b, c;
+  uint64_t seed;
+} pk_rmat_spec;
+
+/* Degrees of nodes [node0, node1) (device u32 out). kind 0: the degree
+ * normalize_adjacency uses (distinct row entries incl. the self loop,
+ * graph.hpp:44-61); kind 1: degree_quantile_labels' distinct undirected
+ * neighbours without self loops (graph.hpp:197-210). Ranks compute their
+ * node ranges and all-gather. */
+int pk_rmat_node_degrees(const pk_rmat_spec* spec, int kind, int64_t node0,
+                         int64_t node1, uint32_t* degree, void* stream);
+/* inv[perm[i]] = i (invert_permutation, graph.hpp:95-99) */
+int pk_invert_permutation(const uint32_t* perm, int64_t n, uint32_t* inv,
+                          void* stream);
+/* Block [r0, r1) x [c0, c1) of A_even (parity 0) or A_odd (1) with local
+ * column ids — variant.block(...) of the reference (engine.hpp:108) —
+ * from the permutation pair, its inverses and the all-gathered kind-0
+ * degrees (device arrays of n). Allocates out (pk_csr_free). */
+int pk_rmat_block(const pk_rmat_spec* spec, int parity, const uint32_t* row_perm,
+                  const uint32_t* col_perm, const uint32_t* inv_row,
+                  const uint32_t* inv_col, const uint32_t* norm_degree, int64_t r0,
+                  int64_t r1, int64_t c0, int64_t c1, pk_csr_owned* out, void* stream);
+/* features in permuted order (graph.hpp:233-236, 373-376): out[i - r0, j - c0]
+ * = (float) next_double number perm[i] * feat_dim + j of Philox(seed, 3) */
+int pk_rmat_features_permuted(uint64_t seed, int64_t feat_dim, const uint32_t* perm,
+                              int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                              float* out, int64_t ldo, void* stream);
+/* degree_quantile_labels (graph.hpp:212-221) from all n kind-1 degrees */
+int pk_labels_from_degrees(const uint32_t* label_degree, int64_t n, uint32_t classes,
+                           uint32_t* labels, void* stream);
+/* out[i] = src[idx[i]] (labels / masks into a permuted order) */
+int pk_gather_u32(const uint32_t* src, const uint32_t* idx, int64_t n, uint32_t* out,
+                  void* stream);
+
+/* ------------------------------------------------------------------ */
 /* 3D-parallel GCN engine: one per rank (one per GPU)                   */
 /*                                                                     */
 /* Replaces the per-rank body of train_distributed (trainer.hpp:562-633):*/
@@ -398,6 +446,15 @@ int pk_engine_reduce_scatter_f32(pk_engine* e, int axis, float* buf, int64_t row
                                  int64_t cols, int64_t ld, float* out,
                                  void* stream);
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* out_host);
+/* This rank failed outside the library (e.g. its host code threw): take the
+ * grid down like the reference's Cluster does (cluster.hpp:240, 434). In
+ * an in-process cluster every other rank's collectives return
+ * PK_ERR_ABORTED; across processes (pk_engine_comm_init) the failure is
+ * published in a node-local shared-memory block named after the NCCL unique
+ * id, every rank aborts its communicators and peer-memory waits, and their
+ * pending epoch returns PK_ERR_ABORTED naming this rank. Failures inside
+ * pk_engine_load* / forward_backward / train_epoch do this on their own. */
+int pk_engine_abort(pk_engine* e, const char* why);
 int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out);
 int pk_engine_stream(pk_engine* e, void** stream_out);
 int pk_engine_destroy(pk_engine* e);

@@ -230,9 +230,9 @@ inline CsrMatrix<float> transpose(const CsrMatrix<float>& a) {
     detail::cuda(cudaMemcpy(ci.data(), t.col_idx, t.nnz * 4, cudaMemcpyDeviceToHost), "download");
     detail::cuda(cudaMemcpy(v.data(), t.values, t.nnz * 4, cudaMemcpyDeviceToHost), "download");
   }
+  const auto rows = static_cast<std::size_t>(t.rows), cols = static_cast<std::size_t>(t.cols);
   pk_csr_free(&t);
-  return CsrMatrix<float>(static_cast<std::size_t>(t.rows), static_cast<std::size_t>(t.cols),
-                          std::move(rp), std::move(ci), std::move(v));
+  return CsrMatrix<float>(rows, cols, std::move(rp), std::move(ci), std::move(v));
 }
 
 // ---------------------------------------------------------------------------

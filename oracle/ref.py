@@ -222,7 +222,7 @@ class Pre(_Handle):
                                       C.c_int(threads), _p(out)))
         return float(out[0]), float(out[1])
 
-    def serial_pass_parallel(self, hidden, threads, seed=0, want_h0=False):
+    def serial_pass_parallel(self, hidden, threads, seed=0, want_h0=False, sample_cols=0):
         """SerialTrainer::forward_backward(0) composed from the reference
         kernels over `threads` row blocks (ref_serial_pass_parallel): rows
         bitwise the serial pass's, the CE loss sum reduced blockwise, dW in
@@ -236,11 +236,20 @@ class Pre(_Handle):
         dw = np.empty(sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1)), np.float64)
         df0 = np.empty((n, dims[0]), np.float32)
         h0 = np.empty((n, dims[0]), np.float32) if want_h0 else None
+        L = len(dims) - 1
+        dmax = max(dims)
+        dws = np.zeros((L, dmax, sample_cols), np.float32) if sample_cols else None
         _check(lib().ref_serial_pass_parallel(
             self.h, _p(hid), C.c_int(len(hidden)), C.c_uint64(seed), C.c_int(threads),
-            C.byref(loss), C.byref(acc), _p(logits), _p(dw), _p(df0), _p(h0)))
-        return dict(loss=loss.value, accuracy=acc.value, logits=logits,
-                    dw=split_weights(dw, dims), df0=df0, h0=h0)
+            C.byref(loss), C.byref(acc), _p(logits), _p(dw), _p(df0), _p(h0),
+            C.c_int(sample_cols), _p(dws)))
+        out = dict(loss=loss.value, accuracy=acc.value, logits=logits,
+                   dw=split_weights(dw, dims), df0=df0, h0=h0)
+        if sample_cols:
+            # serial fp32 chain dW[:, :sample_cols] per layer
+            out["dw_serial_cols"] = [dws[l, :dims[l], :min(sample_cols, dims[l + 1])]
+                                     for l in range(L)]
+        return out
 
     def distributed_pass(self, grid, hidden=(128, 128), seed=0, block_count=0):
         i = self.info()

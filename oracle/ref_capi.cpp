@@ -1031,7 +1031,7 @@ int ref_epoch_sample(void* pre, const u64* hidden, int nh, u64 rows, int threads
 // (n x F), H of layer 0.
 int ref_serial_pass_parallel(void* pre, const u64* hidden, int nh, u64 seed, int threads,
                              double* loss, double* acc, float* logits, double* dw_cat,
-                             float* df0, float* h0) {
+                             float* df0, float* h0, int sample_cols, float* dw_serial) {
   auto* p = static_cast<Pre*>(pre);
   return guarded([&] {
     check(!p->f64, "ref_serial_pass_parallel: float datasets only");
@@ -1042,6 +1042,8 @@ int ref_serial_pass_parallel(void* pre, const u64* hidden, int nh, u64 seed, int
     const int L = static_cast<int>(dims.size()) - 1;
     const std::size_t n = d.n;
     const int T = std::max(1, threads);
+    std::size_t dims_max_ = 0;
+    for (auto x : dims) dims_max_ = std::max(dims_max_, x);
     auto ws = init_weights<float>(dims, seed);
     const CsrMatrix<float> at_even = d.a_even.transpose(), at_odd = d.a_odd.transpose();
     auto par = [&](auto&& body) {
@@ -1120,6 +1122,20 @@ int ref_serial_pass_parallel(void* pre, const u64* hidden, int nh, u64 seed, int
                       true, false);
         put(dh, r0, gemm(dqb, ws[l], false, true));
       });
+      // the serial trainer's own fp32 dW for the first `sample_cols`
+      // columns: gemm(h, dq[:, j], true) over all n rows in one k chain,
+      // one column per thread (trainer.hpp:163)
+      if (dw_serial && sample_cols > 0) {
+        const int sc = std::min<int>(sample_cols, static_cast<int>(dims[l + 1]));
+        std::vector<std::thread> cols;
+        std::vector<DenseMatrix<float>> res(sc);
+        for (int j = 0; j < sc; ++j)
+          cols.emplace_back([&, j] { res[j] = gemm(h[l], dq.block(0, n, j, j + 1), true, false); });
+        for (auto& th : cols) th.join();
+        float* dst = dw_serial + l * dims_max_ * sample_cols;
+        for (int j = 0; j < sc; ++j)
+          for (std::size_t i = 0; i < dims[l]; ++i) dst[i * sample_cols + j] = res[j].at(i, 0);
+      }
       DenseMatrix<double> dw = std::move(dwp[0]);
       for (int t = 1; t < T; ++t)
         for (std::size_t i = 0; i < dw.size(); ++i) dw.data()[i] += dwp[t].data()[i];

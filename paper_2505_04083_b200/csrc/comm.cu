@@ -1,11 +1,18 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 
 #include "comm.cuh"
 
@@ -59,6 +66,20 @@ void copy_block_launch(const float* src, i64 ld_src, i64 rows, i64 cols, float* 
   PK_LAUNCH("copy block");
 }
 
+// Abort propagation across the processes of one node (ClusterAborted,
+// cluster.hpp:67-71, 240, 434, for one process per GPU): a small POSIX
+// shared-memory block named after the NCCL unique id. A rank that fails
+// publishes itself there; every rank's monitor thread sees it within a
+// millisecond and aborts its communicators (NCCL kernels waiting on the dead
+// peer exit) and raises the peer-memory reductions' abort flag (their
+// barrier waits exit), so blocked host waits return and the engine raises
+// PK_ERR_ABORTED naming the failed rank instead of hanging.
+struct AbortBlock {
+  unsigned flag;  // 0 = running; set once, by the first failing rank
+  int rank;
+  char why[504];
+};
+
 struct CommSet {
   ncclComm_t world = nullptr;
   std::array<ncclComm_t, 3> axes{nullptr, nullptr, nullptr};
@@ -67,12 +88,71 @@ struct CommSet {
   std::array<std::unique_ptr<LsaGroup>, 3> lsa;
   std::array<size_t, 3> lsa_elems{0, 0, 0};
   std::array<bool, 3> lsa_failed{false, false, false};
-  ~CommSet() {
+  AbortBlock* ab = nullptr;
+  std::thread monitor;
+  std::atomic<bool> stop{false}, dead{false};
+  std::mutex mu;
+
+  void kill() {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dead.exchange(true)) return;
+    lsa_signal_abort();
     for (auto& c : axes)
-      if (c) ncclCommDestroy(c);
-    if (world) ncclCommDestroy(world);
+      if (c) ncclCommAbort(c), c = nullptr;
+    if (world) ncclCommAbort(world), world = nullptr;
+  }
+  std::string why() const {
+    if (!ab) return "cluster aborted";
+    char buf[sizeof(ab->why) + 1];
+    std::memcpy(buf, ab->why, sizeof(ab->why));
+    buf[sizeof(ab->why)] = 0;
+    return "cluster aborted: rank " + std::to_string(ab->rank) + " failed: " + buf;
+  }
+  void publish(int rank, const std::string& msg) {
+    if (!ab) return;
+    unsigned zero = 0;
+    if (__atomic_compare_exchange_n(&ab->flag, &zero, 2u, false, __ATOMIC_ACQ_REL,
+                                    __ATOMIC_ACQUIRE)) {
+      ab->rank = rank;
+      std::strncpy(ab->why, msg.c_str(), sizeof(ab->why) - 1);
+      __atomic_store_n(&ab->flag, 1u, __ATOMIC_RELEASE);
+    }
+  }
+  ~CommSet() {
+    stop = true;
+    if (monitor.joinable()) monitor.join();
+    if (!dead) {
+      for (auto& c : axes)
+        if (c) ncclCommDestroy(c);
+      if (world) ncclCommDestroy(world);
+    }
+    if (ab) munmap(ab, sizeof(AbortBlock));
   }
 };
+
+namespace {
+std::string abort_block_name(const void* uid) {
+  // FNV-1a of the 128-byte unique id
+  unsigned long long h = 1469598103934665603ull;
+  const auto* p = static_cast<const unsigned char*>(uid);
+  for (int i = 0; i < 128; ++i) h = (h ^ p[i]) * 1099511628211ull;
+  char name[64];
+  std::snprintf(name, sizeof(name), "/pk_abort_%016llx", h);
+  return name;
+}
+
+AbortBlock* open_abort_block(const std::string& name) {
+  const int fd = shm_open(name.c_str(), O_CREAT | O_RDWR, 0600);
+  if (fd < 0) return nullptr;
+  if (ftruncate(fd, sizeof(AbortBlock)) != 0) {
+    close(fd);
+    return nullptr;
+  }
+  void* p = mmap(nullptr, sizeof(AbortBlock), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  return p == MAP_FAILED ? nullptr : static_cast<AbortBlock*>(p);
+}
+}  // namespace
 
 namespace {
 std::mutex g_comm_mu;
@@ -109,6 +189,10 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
     auto fresh = std::make_shared<CommSet>();
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
+    // every rank maps the block before the (collective) init; rank 0 unlinks
+    // the name once init has returned on all ranks — the mappings stay
+    const std::string ab_name = abort_block_name(uid);
+    fresh->ab = open_abort_block(ab_name);
     // NCCL's CTAs share the SMs with the SpMM / GEMM they overlap.
     // PK_NCCL_MAX_CTAS caps them; the default (NCCL's own choice) measured
     // best: a 16-CTA cap slowed the 2-GPU epoch from 52.9 to 56.6 ms.
@@ -127,6 +211,19 @@ void Comms::init(const Grid& grid, int rank, const void* uid, int world_size) {
       PK_NCCL(ncclCommCount(fresh->axes[a], &n));
       PK_NCCL(ncclCommUserRank(fresh->axes[a], &r));
       check(n == grid.extent(a) && r == coords_.along(a), "comm split: inconsistent axis group");
+    }
+    if (rank == 0) shm_unlink(ab_name.c_str());
+    if (fresh->ab) {
+      CommSet* cs = fresh.get();
+      cs->monitor = std::thread([cs] {
+        while (!cs->stop.load()) {
+          if (__atomic_load_n(&cs->ab->flag, __ATOMIC_ACQUIRE) == 1u) {
+            cs->kill();
+            return;
+          }
+          std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        }
+      });
     }
     set_ = fresh;
     if (comm_cache_on()) {
@@ -149,19 +246,21 @@ void Comms::init_local(const Grid& grid, int rank, LocalCluster* cluster) {
   lc_.init(cluster, grid, rank);
 }
 
+void Comms::signal_abort(int rank, const std::string& why) {
+  if (!set_) return;
+  set_->publish(rank, why);
+  abort_nccl();
+}
+
+void Comms::check_alive() const {
+  if (set_ && set_->dead.load()) throw Error(PK_ERR_ABORTED, set_->why());
+}
+
 void Comms::abort_nccl() {
   if (!set_) return;
   // ncclCommAbort ends in-flight operations instead of waiting for them;
   // the set leaves the process cache so no later engine reuses it
-  for (auto& c : set_->axes)
-    if (c) {
-      ncclCommAbort(c);
-      c = nullptr;
-    }
-  if (set_->world) {
-    ncclCommAbort(set_->world);
-    set_->world = nullptr;
-  }
+  set_->kill();
   {
     std::lock_guard<std::mutex> lk(g_comm_mu);
     for (auto it = g_comm_cache.begin(); it != g_comm_cache.end();)
@@ -213,15 +312,20 @@ void Comms::all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaS
   if (g == 1) return;
   if (local_) return lc_.all_reduce<float>(axis, buf, 1, count, count, st);
   if (count == 0) return;
+  check_alive();
   PK_NCCL(ncclAllReduce(buf, buf, count, ncclFloat32, ncclSum, axes_[axis], st));
 }
 
 void Comms::all_reduce_f64(double* buf, i64 count, int axis, cudaStream_t st) {
   const int g = grid_.extent(axis);
-  counters.calls[axis][kAllReduce]++;  // loss stats are not part of the modeled volume
+  // the reference counts the loss sums' 1x3 all-reduce like any other
+  // (cluster.hpp:316: 2 (g - 1) x its bytes)
+  counters.calls[axis][kAllReduce]++;
+  counters.ring_numer[axis][kAllReduce] += 2 * static_cast<u64>(g - 1) * count * sizeof(double);
   if (g == 1) return;
   if (local_) return lc_.all_reduce<double>(axis, buf, 1, count, count, st);
   if (count == 0) return;
+  check_alive();
   PK_NCCL(ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, axes_[axis], st));
 }
 
@@ -239,6 +343,7 @@ void Comms::all_gather_rows(const float* local, float* out, i64 total_rows, i64 
     return;
   }
   if (local_) return lc_.all_gather_rows(axis, local, out, total_rows, ld, st);
+  check_alive();
   PK_NCCL(ncclGroupStart());
   for (int j = 0; j < g; ++j) {
     const i64 off = chunk_start(total_rows, g, j), rows = chunk_size(total_rows, g, j);

@@ -60,6 +60,11 @@ class Comms {
   // Tear down after a failure (ClusterAborted semantics): NCCL
   // communicators are aborted so no later call can block on them.
   void abort_nccl();
+  // This rank failed: tell every rank of the node (shared-memory abort
+  // block) and abort the communicators.
+  void signal_abort(int rank, const std::string& why);
+  // Throws PK_ERR_ABORTED when a rank of the communicator set failed.
+  void check_alive() const;
   int size(int axis) const { return grid_.extent(axis); }
   int pos(int axis) const { return coords_.along(axis); }
 

@@ -653,6 +653,7 @@ void Engine::loss() {
 // finalize_loss (trainer.hpp:71-89) and the pass's error checks; the stream
 // has drained.
 void Engine::finish_pass(int epoch, double* loss_out, double* acc_out) {
+  comms_.check_alive();  // a peer failed: its ClusterAborted, not our partial sums
   const i64 C = dims_[L_];
   const u32 bad = *reinterpret_cast<const u32*>(sums_host_ + 3);
   check(!bad, "cross entropy: label out of range for " + std::to_string(C) + " classes");
@@ -901,6 +902,7 @@ void Engine::train_epoch(int epoch, pk_epoch_metrics* m) {
 
 void Engine::on_failure(const std::string& why) {
   if (LocalCluster* cl = comms_.local_cluster()) cl->abort(rank_, why);
+  else comms_.signal_abort(rank_, why);
 }
 
 bool Engine::tensor(int which, int layer, pk_tensor_view* out) {
@@ -1122,6 +1124,10 @@ int pk_engine_optimizer_step(pk_engine* e) {
 
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* m) {
   return guard_rank(e, [&] { e->e->train_epoch(epoch, m); });
+}
+
+int pk_engine_abort(pk_engine* e, const char* why) {
+  return guard([&] { e->e->on_failure(why ? why : "aborted by the host"); });
 }
 
 int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out) {

@@ -23,6 +23,7 @@
 #include <nccl_device.h>
 
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 #include <cstdlib>
 #include <cstring>
@@ -67,7 +68,8 @@ __device__ void barrier(const LsaPeers& P, int b, unsigned epoch) {
       const unsigned* f = P.flags[P.me] + p * kLsaBlocks + b;
       unsigned spins = 0;
       while (static_cast<int>(flag_load(f) - epoch) < 0) {
-        if ((++spins & 255u) == 0 && globaltimer_ns() - t0 > P.timeout_ns) {
+        if ((++spins & 255u) == 0 &&
+            (globaltimer_ns() - t0 > P.timeout_ns || (P.abort && *P.abort))) {
           atomicExch(&g_lsa_timeout, 1u);
           break;
         }
@@ -162,7 +164,27 @@ void peer_pointers(ncclWindow_t win, int g, void** host_out) {
   PK_CUDA(cudaFree(d));
 }
 
+// one host-mapped abort word per process (zero until a rank fails)
+unsigned* g_abort_host = nullptr;
+std::mutex g_abort_mu;
+
+const volatile unsigned* abort_flag_device() {
+  std::lock_guard<std::mutex> lk(g_abort_mu);
+  if (!g_abort_host) {
+    PK_CUDA(cudaHostAlloc(&g_abort_host, sizeof(unsigned), cudaHostAllocMapped));
+    *g_abort_host = 0;
+  }
+  unsigned* d = nullptr;
+  PK_CUDA(cudaHostGetDevicePointer(&d, g_abort_host, 0));
+  return d;
+}
+
 }  // namespace
+
+void lsa_signal_abort() {
+  std::lock_guard<std::mutex> lk(g_abort_mu);
+  if (g_abort_host) __atomic_store_n(g_abort_host, 1u, __ATOMIC_RELEASE);
+}
 
 LsaGroup::~LsaGroup() {
   // windows and ncclMemAlloc buffers are released with the communicator
@@ -197,6 +219,7 @@ bool LsaGroup::init(ncclComm_t comm, int g, int me, size_t scratch_elems) {
     return v > 0 ? v : 120.0;
   }();
   peers_.timeout_ns = static_cast<unsigned long long>(timeout_s * 1e9);
+  peers_.abort = abort_flag_device();
   for (int j = 0; j < g; ++j) {
     peers_.data[j] = static_cast<const float*>(dp[j]);
     peers_.flags[j] = static_cast<unsigned*>(fp[j]);

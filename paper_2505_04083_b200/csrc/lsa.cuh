@@ -15,6 +15,7 @@ struct LsaPeers {
   unsigned* flags[kLsaMaxMembers];    // each member's barrier flags
   int g = 0, me = 0;
   unsigned long long timeout_ns = 0;  // bounded barrier waits (wall time)
+  const volatile unsigned* abort = nullptr;  // host-mapped: a rank failed
 };
 
 // One axis group's symmetric scratch + barrier flags.
@@ -51,6 +52,8 @@ class LsaGroup {
 
 // true when a barrier wait gave up (a protocol error; results are invalid)
 bool lsa_timed_out();
+// Raise the process's abort flag: every peer-memory barrier wait exits.
+void lsa_signal_abort();
 void lsa_clear_timeout();
 
 }  // namespace pk

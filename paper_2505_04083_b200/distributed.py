@@ -100,7 +100,8 @@ def reassemble(grid: GridConfig, n: int, dims: List[int], w_shards: List[List[np
 
 def train_distributed(load_dataset: Callable[[], object], grid: GridConfig, opts,
                       engine_factory: Optional[Callable] = None,
-                      reassemble_params: bool = True) -> TrainResult:
+                      reassemble_params: bool = True,
+                      epoch_hook: Optional[Callable[[int], None]] = None) -> TrainResult:
     """Collective call on every rank (world size == grid.size). Returns the
     reassembled TrainResult on rank 0 and per-rank metrics everywhere."""
     import torch.distributed as dist
@@ -123,7 +124,19 @@ def train_distributed(load_dataset: Callable[[], object], grid: GridConfig, opts
             e.load(pre_)
             return e
     eng = engine_factory(pre, grid, rank, opts)
-    mine = [eng.train_epoch(e) for e in range(opts.epochs)]
+    mine = []
+    try:
+        for e in range(opts.epochs):
+            mine.append(eng.train_epoch(e))
+            if epoch_hook is not None:
+                epoch_hook(e)
+    except Exception as exc:
+        # a failure on this rank takes the grid down (cluster.hpp:240, 434):
+        # peers blocked in their epoch raise ClusterAborted instead of hanging
+        from ._capi import ClusterAborted
+        if not isinstance(exc, ClusterAborted) and hasattr(eng, "abort"):
+            eng.abort(f"{type(exc).__name__}: {exc}")
+        raise
     L = len(eng.dims) - 1
     w_mine = [np.asarray(_host(eng.tensor(0, l))) for l in range(L)] if reassemble_params else []
     f_mine = np.asarray(_host(eng.tensor(2))) if reassemble_params else None

@@ -78,6 +78,7 @@ _SIGS = {
     "pk_engine_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(pk_tensor_view)]),
     "pk_engine_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pk_engine_destroy": (C.c_int, [C.c_void_p]),
+    "pk_engine_abort": (C.c_int, [C.c_void_p, C.c_char_p]),
 }
 _capi.register(_SIGS)
 
@@ -254,6 +255,11 @@ class RankEngine:
         m = pk_epoch_metrics()
         call("pk_engine_train_epoch", self.h, epoch, C.byref(m))
         return {k: getattr(m, k) for k in METRIC_KEYS}
+
+    def abort(self, why: str):
+        """This rank failed: take the grid down (pk_engine_abort) — the other
+        ranks' pending epoch fails with ClusterAborted naming this rank."""
+        call("pk_engine_abort", self.h, str(why).encode()[:500])
 
     def tensor(self, which, layer=0) -> torch.Tensor:
         """Copy of an engine tensor (rows x cols) as a CUDA tensor."""

@@ -13,12 +13,12 @@ Checker: the compiled, unmodified reference (oracle/_ref):
       2,097,152 rows returned in float64). From the same W and F0: PARITY
       logits and dF0 bit-identical, FAST logits / dW / dF0 within 1e-4
       normwise, loss within 1e-6 relative (expf / logf ulps). PARITY dW is
-      the reference's own sequential fp32 k-chain (the serial trainer's
-      order, bit-identical at smaller K in test_kernels_gpu / test_engine_gpu);
-      at K = 2.1M that chain's rounding alone is ~5e-4 normwise from the
-      fp64 value, so PARITY dW is gated at 1e-3 — the tensor-core path, which
-      folds its TMEM partial every 512 k with round-to-nearest adds, must
-      meet 1e-4;
+      the reference's own sequential fp32 k-chain: bit-identical to the
+      serial trainer's gemm(h, dq, true) on the columns the checker also runs
+      serially (one k chain of 2.1M terms per column); that chain's own
+      rounding is up to ~2e-3 normwise from the fp64 value (last layer), so
+      its fp64 gate is 5e-3 — the tensor-core path, which folds its TMEM
+      partial every 512 k with round-to-nearest adds, must meet 1e-4;
   (c) the FAST SpMM plan's segmented hub rows at C2's real degrees (rows of
       up to 155,518 nonzeros = 76 fixed 2048-nonzero segments): H of layer 0
       bit-identical on every non-hub row, hub rows within 1e-6 normwise.
@@ -86,7 +86,7 @@ def ref_pass(c2):
     rpre, _ = c2
     threads = os.cpu_count() or 1
     t0 = time.time()
-    out = rpre.serial_pass_parallel(HIDDEN, threads, seed=0, want_h0=True)
+    out = rpre.serial_pass_parallel(HIDDEN, threads, seed=0, want_h0=True, sample_cols=4)
     print(f"\nC2 reference forward_backward on {threads} threads: {time.time() - t0:.1f} s")
     return out
 
@@ -113,9 +113,15 @@ def test_c2_parity_pass_logits_bitwise(c2, ref_pass):
     assert np.array_equal(got["logits"].view(np.uint32), ref_pass["logits"].view(np.uint32))
     assert got["accuracy"] == ref_pass["accuracy"]
     assert abs(got["loss"] - ref_pass["loss"]) <= 1e-6 * abs(ref_pass["loss"])
+    # dW: the serial trainer's own fp32 k chain over all 2,097,152 rows,
+    # bit for bit, on the columns the reference computed serially
+    for l in range(3):
+        ser = ref_pass["dw_serial_cols"][l]
+        assert np.array_equal(np.ascontiguousarray(got["dw"][l][:, :ser.shape[1]]).view(np.uint32),
+                              ser.view(np.uint32)), l
     errs = [nrel(got["dw"][l], ref_pass["dw"][l]) for l in range(3)]
-    print(f"\nC2 PARITY dW vs fp64 (normwise): {errs}")
-    assert max(errs) <= 1e-3, errs
+    print(f"\nC2 PARITY (= serial fp32 chain) dW vs fp64 (normwise): {errs}")
+    assert max(errs) <= 5e-3, errs
     assert np.array_equal(got["df0"].view(np.uint32), ref_pass["df0"].view(np.uint32))
     # every H row of layer 0 is one exact chain in PARITY plans
     assert np.array_equal(got["h0"].view(np.uint32), ref_pass["h0"].view(np.uint32))

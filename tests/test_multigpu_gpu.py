@@ -125,3 +125,19 @@ def test_two_gpu_cli_validate(cuda, fault):
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert p.returncode == (1 if fault else 0), p.stdout[-2000:] + p.stderr[-2000:]
     assert ("validation FAILED" if fault else "validation passed") in p.stdout
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("grid", ["2,1,1", "1,1,2"])
+def test_two_gpu_rank_failure_aborts_peers(cuda, grid):
+    """One process per GPU: rank 1's host code fails after epoch 1; rank 0,
+    blocked in its next epoch's NCCL / peer-memory collectives, must end with
+    ClusterAborted naming rank 1 (node-local abort block, csrc/comm.cu)
+    instead of hanging."""
+    worker = os.path.join(HERE, "mp", "abort_worker.py")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", worker, "--grid", grid]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    res = [l for l in p.stdout.splitlines() if l.startswith("ABORTRESULT")]
+    assert len(res) == 2, p.stdout[-3000:] + p.stderr[-3000:]
+    assert all("ok=1" in l for l in res), res
