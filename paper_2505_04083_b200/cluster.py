@@ -170,4 +170,36 @@ def train_distributed(pre, grid: GridConfig, opts, devices=None) -> TrainResult:
     return res
 
 
-__all__ = ["Cluster", "ClusterAborted", "distributed_pass", "train_distributed"]
+
+
+
+def train_distributed_generated(spec, grid: GridConfig, opts, devices=None) -> TrainResult:
+    """train_distributed with the file_handle-style per-rank loader replaced
+    by per-rank generation (rank_gen.generate_rank_tensors): no rank, and no
+    host, ever holds the global graph."""
+    from . import rank_gen, trainer
+    cl = Cluster(grid, devices)
+    dims = trainer.model_dims(spec.feat_dim, list(opts.hidden_dims), spec.classes)
+    L = len(dims) - 1
+    pieces = rank_gen.global_pieces(spec, 0, grid.size)
+
+    def rank_train(r):
+        e = cl.engine(spec.n, spec.feat_dim, spec.classes, r, opts)
+        try:
+            e.load_rank(rank_gen.generate_rank_tensors(spec, grid, r, L, pieces))
+            metrics = [e.train_epoch(ep) for ep in range(opts.epochs)]
+            w = [e.tensor(trainer.PK_T_W, l).cpu().numpy() for l in range(L)]
+            f = e.tensor(trainer.PK_T_F0).cpu().numpy()
+            return metrics, w, f
+        finally:
+            e.close()
+    try:
+        per = cl.run(rank_train)
+    finally:
+        cl.close()
+    res = TrainResult(per_rank=[p[0] for p in per])
+    res.global_metrics = reduce_epoch_metrics(res.per_rank)
+    res.weights, res.features = reassemble(grid, spec.n, dims, [p[1] for p in per],
+                                           [p[2] for p in per])
+    return res
+__all__ = ["Cluster", "ClusterAborted", "distributed_pass", "train_distributed", "train_distributed_generated"]
