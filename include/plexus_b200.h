@@ -399,6 +399,12 @@ int pk_cluster_aborted(pk_cluster* c, int* aborted);
 int pk_cluster_destroy(pk_cluster* c);
 /* instead of pk_engine_comm_init: this engine is rank cfg.rank of `c` */
 int pk_engine_comm_init_local(pk_engine* e, pk_cluster* c);
+/* Measurement mode: rank cfg.rank of a grid larger than the machine runs
+ * alone — every collective only puts this rank's own contribution in place
+ * (results are NOT the GCN's), the ring-model byte counters still follow the
+ * real grid. Measures one rank's memory and compute share (e.g. one rank of
+ * 2x2x2 at billion-edge scale on one GPU). */
+int pk_engine_comm_init_solo(pk_engine* e);
 int pk_engine_load(pk_engine* e, const pk_dataset_view* ds);
 int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds_host);
 /* The file_handle path (trainer.hpp:461-466): this rank's tensors only

@@ -246,6 +246,12 @@ void Comms::init_local(const Grid& grid, int rank, LocalCluster* cluster) {
   lc_.init(cluster, grid, rank);
 }
 
+void Comms::init_solo(const Grid& grid, int rank) {
+  grid_ = grid;
+  coords_ = grid.coords_of(rank);
+  solo_ = true;
+}
+
 void Comms::signal_abort(int rank, const std::string& why) {
   if (!set_) return;
   set_->publish(rank, why);
@@ -309,7 +315,7 @@ void Comms::all_reduce(float* buf, i64 count, int axis, i64 logical_bytes, cudaS
   const int g = grid_.extent(axis);
   counters.calls[axis][kAllReduce]++;
   counters.ring_numer[axis][kAllReduce] += 2 * static_cast<u64>(g - 1) * logical_bytes;
-  if (g == 1) return;
+  if (g == 1 || solo_) return;
   if (local_) return lc_.all_reduce<float>(axis, buf, 1, count, count, st);
   if (count == 0) return;
   check_alive();
@@ -322,7 +328,7 @@ void Comms::all_reduce_f64(double* buf, i64 count, int axis, cudaStream_t st) {
   // (cluster.hpp:316: 2 (g - 1) x its bytes)
   counters.calls[axis][kAllReduce]++;
   counters.ring_numer[axis][kAllReduce] += 2 * static_cast<u64>(g - 1) * count * sizeof(double);
-  if (g == 1) return;
+  if (g == 1 || solo_) return;
   if (local_) return lc_.all_reduce<double>(axis, buf, 1, count, count, st);
   if (count == 0) return;
   check_alive();
@@ -336,9 +342,9 @@ void Comms::all_gather_rows(const float* local, float* out, i64 total_rows, i64 
   counters.ring_numer[axis][kAllGather] +=
       static_cast<u64>(g - 1) * static_cast<u64>(total_rows) * logical_cols * sizeof(float);
   const i64 own0 = chunk_start(total_rows, g, pos), own_rows = chunk_size(total_rows, g, pos);
-  if (g == 1) {
-    if (local != out && own_rows)
-      PK_CUDA(cudaMemcpyAsync(out, local, own_rows * ld * sizeof(float),
+  if (g == 1 || solo_) {
+    if (local != out + own0 * ld && own_rows)
+      PK_CUDA(cudaMemcpyAsync(out + own0 * ld, local, own_rows * ld * sizeof(float),
                               cudaMemcpyDeviceToDevice, st));
     return;
   }
@@ -355,7 +361,8 @@ void Comms::all_gather_rows(const float* local, float* out, i64 total_rows, i64 
 }
 
 void Comms::all_gather_cols(const float* local, i64 ld_in, float* out, i64 ld_out, i64 rows,
-                            i64 total_cols, int axis, float* stage, cudaStream_t st) {
+                            i64 total_cols, int axis, float* stage, i64 stage_rows,
+                            cudaStream_t st) {
   const int g = grid_.extent(axis), pos = coords_.along(axis);
   counters.calls[axis][kAllGather]++;
   counters.ring_numer[axis][kAllGather] +=
@@ -368,23 +375,38 @@ void Comms::all_gather_cols(const float* local, i64 ld_in, float* out, i64 ld_ou
     PK_LAUNCH("gather cols copy");
     return;
   }
-  // own block -> its contiguous slot of `stage`, then broadcasts, then pack
+  if (solo_) {
+    const i64 c0 = chunk_start(total_cols, g, pos), cj = chunk_size(total_cols, g, pos);
+    if (cj) {
+      copy_block_kernel<<<small_grid(rows * cj), 256, 0, st>>>(local, ld_in, rows, cj, out + c0,
+                                                               ld_out);
+      PK_LAUNCH("gather cols copy");
+    }
+    return;
+  }
+  check_alive();
+  // per row chunk: own block -> its contiguous slot of `stage`, grouped
+  // broadcasts of every member's slot, then pack into the output columns
   const i64 my_c0 = chunk_start(total_cols, g, pos), my_c = chunk_size(total_cols, g, pos);
-  if (my_c) {
-    copy_block_kernel<<<small_grid(rows * my_c), 256, 0, st>>>(local, ld_in, rows, my_c,
-                                                               stage + rows * my_c0, my_c);
-    PK_LAUNCH("gather cols stage");
+  const i64 step = stage_rows > 0 ? stage_rows : rows;
+  for (i64 q0 = 0; q0 < rows; q0 += step) {
+    const i64 nr = std::min(step, rows - q0);
+    if (my_c) {
+      copy_block_kernel<<<small_grid(nr * my_c), 256, 0, st>>>(local + q0 * ld_in, ld_in, nr,
+                                                               my_c, stage + nr * my_c0, my_c);
+      PK_LAUNCH("gather cols stage");
+    }
+    PK_NCCL(ncclGroupStart());
+    for (int j = 0; j < g; ++j) {
+      const i64 c0 = chunk_start(total_cols, g, j), cj = chunk_size(total_cols, g, j);
+      float* slot = stage + nr * c0;
+      PK_NCCL(ncclBroadcast(slot, slot, nr * cj, ncclFloat32, j, axes_[axis], st));
+    }
+    PK_NCCL(ncclGroupEnd());
+    pack_cols_kernel<<<small_grid(nr * total_cols), 256, 0, st>>>(stage, nr, total_cols, g,
+                                                                  out + q0 * ld_out, ld_out);
+    PK_LAUNCH("gather cols pack");
   }
-  PK_NCCL(ncclGroupStart());
-  for (int j = 0; j < g; ++j) {
-    const i64 c0 = chunk_start(total_cols, g, j), cj = chunk_size(total_cols, g, j);
-    float* slot = stage + rows * c0;
-    PK_NCCL(ncclBroadcast(slot, slot, rows * cj, ncclFloat32, j, axes_[axis], st));
-  }
-  PK_NCCL(ncclGroupEnd());
-  pack_cols_kernel<<<small_grid(rows * total_cols), 256, 0, st>>>(stage, rows, total_cols, g, out,
-                                                                  ld_out);
-  PK_LAUNCH("gather cols pack");
 }
 
 void Comms::reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int axis,
@@ -394,7 +416,7 @@ void Comms::reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int ax
   counters.ring_numer[axis][kReduceScatter] +=
       static_cast<u64>(g - 1) * static_cast<u64>(rows) * logical_cols * sizeof(float);
   const i64 own0 = chunk_start(rows, g, pos), own_rows = chunk_size(rows, g, pos);
-  if (g == 1) {
+  if (g == 1 || solo_) {
     if (buf != out && own_rows)
       PK_CUDA(cudaMemcpyAsync(out, buf + own0 * ld, own_rows * ld * sizeof(float),
                               cudaMemcpyDeviceToDevice, st));
@@ -417,9 +439,10 @@ void Comms::reduce_scatter_rows_range(float* buf, float* out, i64 rows, i64 ld, 
   counters.ring_numer[axis][kReduceScatter] +=
       static_cast<u64>(g - 1) * static_cast<u64>(r1 - r0) * logical_cols * sizeof(float);
   const i64 own0 = chunk_start(rows, g, pos), own1 = chunk_start(rows, g, pos + 1);
-  if (g == 1) {
-    if (buf != out && r1 > r0)
-      PK_CUDA(cudaMemcpyAsync(out + (r0 - own0) * ld, buf + r0 * ld, (r1 - r0) * ld * sizeof(float),
+  if (g == 1 || solo_) {
+    const i64 a = std::max(r0, own0), b = std::min(r1, own1);
+    if (buf != out && b > a)
+      PK_CUDA(cudaMemcpyAsync(out + (a - own0) * ld, buf + a * ld, (b - a) * ld * sizeof(float),
                               cudaMemcpyDeviceToDevice, st));
     return;
   }

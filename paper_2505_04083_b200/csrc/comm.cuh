@@ -55,7 +55,12 @@ class Comms {
   void init(const Grid& grid, int rank, const void* uid, int world_size);
   // In-process cluster (local.cuh): the ranks are threads of this process.
   void init_local(const Grid& grid, int rank, LocalCluster* cluster);
-  bool ready() const { return world_ != nullptr || local_ || grid_.size() == 1; }
+  // Measurement mode: this rank of `grid` runs alone; every collective
+  // puts only the rank's own contribution in place (results are not the
+  // GCN's) while the byte counters still follow the real grid. Used to
+  // measure one rank's share of a grid larger than the machine at hand.
+  void init_solo(const Grid& grid, int rank);
+  bool ready() const { return world_ != nullptr || local_ || solo_ || grid_.size() == 1; }
   LocalCluster* local_cluster() const { return local_ ? lc_.cluster() : nullptr; }
   // Tear down after a failure (ClusterAborted semantics): NCCL
   // communicators are aborted so no later call can block on them.
@@ -78,9 +83,10 @@ class Comms {
                        i64 logical_cols, cudaStream_t st);
   // Column concatenation (trainer.hpp:499): member j holds rows x c_j
   // (ld_in) with c_j = chunk_size(total_cols, g, j); output rows x total_cols
-  // (ld_out). `stage` must hold rows * total_cols floats.
+  // (ld_out). `stage` holds stage_rows * total_cols floats; the rows go
+  // through it in chunks of stage_rows (0 = all at once).
   void all_gather_cols(const float* local, i64 ld_in, float* out, i64 ld_out, i64 rows,
-                       i64 total_cols, int axis, float* stage, cudaStream_t st);
+                       i64 total_cols, int axis, float* stage, i64 stage_rows, cudaStream_t st);
   // Sum over the group, keep this member's row chunk (cluster.hpp:323-340):
   // buf is rows x ld (clobbered); out receives chunk rows x ld.
   void reduce_scatter_rows(float* buf, float* out, i64 rows, i64 ld, int axis, i64 logical_cols,
@@ -104,7 +110,7 @@ class Comms {
 
  private:
   ncclComm_t axis_comm(int axis) const { return axes_[axis]; }
-  bool local_ = false;
+  bool local_ = false, solo_ = false;
   LocalComm lc_;
   Grid grid_;
   Coords coords_;

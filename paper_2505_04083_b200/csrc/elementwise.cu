@@ -82,7 +82,7 @@ __host__ __device__ inline int ce_stride(int classes) { return classes | 1; }
 __global__ void __launch_bounds__(kCeRows)
 ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
           const u32* __restrict__ labels, const u8* __restrict__ mask,
-          float* __restrict__ dl, i64 ldd, double* __restrict__ partial,
+          float* __restrict__ dl, i64 ldd, int dc0, int dc1, double* __restrict__ partial,
           u32* __restrict__ bad_label, u64 scale_count) {
   extern __shared__ float tile[];  // [kCeRows][ce_stride(classes)]
   // (T)1 / (T)global_count (trainer.hpp:84), applied as the reference's
@@ -139,9 +139,12 @@ ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
       }
     }
     __syncthreads();
-    for (int e = t; e < elems; e += kCeRows) {
-      const int rr = e / classes, c = e - rr * classes;
-      __stcs(dl + (r0 + rr) * ldd + c, tile[rr * stride + c]);
+    // only the class window [dc0, dc1) of dlogits leaves the CTA: the rank's
+    // own chunk of the last layer's classes (trainer.hpp:517-520)
+    const int w = dc1 - dc0;
+    for (int e = t; e < nr * w; e += kCeRows) {
+      const int rr = e / w, c = e - rr * w;
+      __stcs(dl + (r0 + rr) * ldd + c, tile[rr * stride + dc0 + c]);
     }
     __syncthreads();
   }
@@ -268,7 +271,9 @@ void relu_backward_launch(const float* q, i64 ldq, const float* df, i64 lddf, i6
 
 void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
                     const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
-                    cudaStream_t st, u64 scale_count) {
+                    cudaStream_t st, u64 scale_count, i64 dc0, i64 dc1) {
+  if (dc1 < 0) dc1 = classes;
+  check(0 <= dc0 && dc0 <= dc1 && dc1 <= classes, "cross entropy: bad class window");
   const size_t smem = sizeof(float) * kCeRows * ce_stride(static_cast<int>(classes));
   check(classes <= kCeMaxClasses, "cross entropy: at most " + std::to_string(kCeMaxClasses) +
                                       " classes supported");
@@ -288,7 +293,9 @@ void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u
   PK_CUDA(cudaMemsetAsync(ws.bad.p, 0, sizeof(u32), st));
   if (rows > 0 && classes > 0) {
     ce_kernel<<<blocks, kCeRows, smem, st>>>(logits, ldl, rows, static_cast<int>(classes), labels,
-                                             mask, dl, ldd, ws.partial.p, ws.bad.p, scale_count);
+                                             mask, dl, ldd, static_cast<int>(dc0),
+                                             static_cast<int>(dc1), ws.partial.p, ws.bad.p,
+                                             scale_count);
     PK_LAUNCH("cross entropy");
     ce_finish_kernel<<<1, kCeFinishThreads, 0, st>>>(ws.partial.p, blocks, sums);
   } else {

@@ -18,10 +18,12 @@ struct CeWorkspace {
 // sums = {loss_sum, count, correct} as doubles on the device.
 // scale: 0 writes the unscaled softmax - onehot; otherwise the gradient is
 // multiplied by (float)1/(float)scale in the same pass (finalize_loss,
-// trainer.hpp:84-87, with the global count known in advance).
+// trainer.hpp:84-87, with the global count known in advance). Only the
+// class columns [dc0, dc1) of dlogits are written (dl column 0 = class dc0);
+// dc1 < 0 = all classes.
 void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
                     const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
-                    cudaStream_t st, u64 scale_count = 0);
+                    cudaStream_t st, u64 scale_count = 0, i64 dc0 = 0, i64 dc1 = -1);
 void scale_by_count_launch(float* d, i64 ldd, i64 rows, i64 cols, const double* sums,
                            cudaStream_t st);
 

@@ -233,6 +233,24 @@ void Engine::finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, M
   spmm_plan_build(sh->plan_at, view(sh->at), static_cast<u64>(cfg_.hub_threshold), st_, seg);
   mark("spmm plans");
   sh->nnz_t = sh->at.nnz;
+  // A FAST plan carries every nonzero of its matrix (packed (col, val)
+  // pairs, hub rows as segments), so the CSR's columns and values are dead
+  // weight from here on: 8 B per nonzero for A and again for A^T (20 GB per
+  // rank at C4 scale). Only row_ptr stays (block edges). PK_KEEP_CSR=1 keeps
+  // them.
+  static const bool keep_csr = [] {
+    const char* e = std::getenv("PK_KEEP_CSR");
+    return e && e[0] == '1';
+  }();
+  if (seg && !keep_csr) {
+    PK_CUDA(cudaStreamSynchronize(st_));
+    for (pk_csr_owned* m : {&sh->a, &sh->at}) {
+      if (m->col_idx) dev_free(m->col_idx);
+      if (m->values) dev_free(m->values);
+      m->col_idx = nullptr;
+      m->values = nullptr;
+    }
+  }
   shards_[plane * 2 + parity] = std::move(sh);
 }
 
@@ -272,7 +290,9 @@ void Engine::alloc_params() {
     wfull_[l].alloc(s.f_cols, s.w_cols, st_);
     dwp_[l].alloc(s.f_cols, s.w_cols, st_);
     h_[l].alloc(s.h_rows, s.h_cols, st_);
-    q_[l].alloc(s.q_rows, s.q_cols, st_);
+    // a hidden layer's Q exists only where the engine materialises it (the
+    // NCCL fallback of a split col_shard): allocated on first use
+    if (l + 1 == L_) q_[l].alloc(s.q_rows, s.q_cols, st_);
     if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols, st_);
     max_dq = std::max(max_dq, s.q_rows * pad4(s.q_cols));
     max_dh = std::max(max_dh, s.h_rows * pad4(s.h_cols));
@@ -304,9 +324,18 @@ void Engine::set_labels(const u32* labels, const u8* mask, i64 lrows, u64 global
     PK_CUDA(cudaMemcpyAsync(mask_.p, mask, lrows, cudaMemcpyDeviceToDevice, st_));
   }
   mask_count_ = global_count;
-  logits_.alloc(sl.a_rows, dims_[L_], st_);
-  dl_.alloc(sl.a_rows, dims_[L_], st_);
-  stage_.alloc(sl.a_rows, dims_[L_], st_);
+  // the gathered logits and their gather stage exist only when the classes
+  // are split (inner > 1); the stage is bounded (row chunks); dlogits keeps
+  // only this rank's class chunk — at C4 scale (2x2x2, s26) the three full
+  // a_rows x C buffers were 69 GB per rank
+  const Layout& last = lays_[L_ - 1];
+  const int gi = grid_.extent(last.inner);
+  if (gi > 1) {
+    logits_.alloc(sl.a_rows, dims_[L_], st_);
+    stage_rows_ = std::max<i64>(1, std::min<i64>(sl.a_rows, (i64{256} << 20) / 4 / dims_[L_]));
+    stage_.alloc(stage_rows_, dims_[L_], st_);
+  }
+  dl_.alloc(sl.a_rows, chunk_size(dims_[L_], gi, c_.along(last.inner)), st_);
   // DMat::alloc zeroes on the legacy stream: drain everything before use
   PK_CUDA(cudaDeviceSynchronize());
 }
@@ -565,7 +594,7 @@ void Engine::forward_layer(int l, bool fault) {
       [&](i64 r0, i64 r1) {
         if (fault) return;
         if (lsa_h) {
-          lsa_h->reduce(r0, r1, s.f_cols, h.ld, h.p(), r0, h.ld, cs_);
+          lsa_h->all_reduce(r0, r1, s.f_cols, h.ld, h.p(), r0, h.ld, cs_);
           comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.f_cols * 4);
         } else {
           comms_.all_reduce(h.p() + r0 * h.ld, (r1 - r0) * h.ld, lay.inner,
@@ -585,6 +614,7 @@ void Engine::forward_layer(int l, bool fault) {
   const bool col_single = comms_.size(lay.col) == 1;
   LsaGroup* lsa_q = comms_.lsa(lay.col);
   DMat& qout = hidden && (col_single || lsa_q) ? fout_[l] : q_[l];
+  if (qout.buf.p == nullptr) qout.alloc(s.q_rows, s.q_cols, st_);
   float* qpart = lsa_q ? lsa_q->scratch() : qout.p();
   pipelined(
       s.h_rows, comm_chunks(s.h_rows, lay.col),
@@ -597,7 +627,7 @@ void Engine::forward_layer(int l, bool fault) {
       },
       [&](i64 r0, i64 r1) {
         if (lsa_q) {
-          lsa_q->reduce(r0, r1, s.q_cols, qout.ld, qout.p(), r0, qout.ld, cs_, hidden);
+          lsa_q->all_reduce(r0, r1, s.q_cols, qout.ld, qout.p(), r0, qout.ld, cs_, hidden);
           comms_.count(kAllReduce, lay.col, (r1 - r0) * s.q_cols * 4);
         } else {
           comms_.all_reduce(qout.p() + r0 * qout.ld, (r1 - r0) * qout.ld, lay.col,
@@ -630,7 +660,7 @@ void Engine::loss() {
   if (comms_.size(last.inner) > 1) {
     on_comm([&](cudaStream_t cs) {
       comms_.all_gather_cols(q_[L_ - 1].p(), q_[L_ - 1].ld, logits_.p(), logits_.ld, s.a_rows,
-                             C, last.inner, stage_.p(), cs);
+                             C, last.inner, stage_.p(), stage_rows_, cs);
     });
     logits = logits_.p();
     ldl = logits_.ld;
@@ -638,8 +668,9 @@ void Engine::loss() {
     comms_.counters.calls[last.inner][kAllGather]++;  // the reference still counts the call
   }
   clock_.begin(2, st_);
+  const int gi = comms_.size(last.inner), pi = c_.along(last.inner);
   ce_sums_launch(logits, ldl, s.a_rows, C, labels_.p, mask_.p, dl_.p(), dl_.ld, sums_.p, ce_ws_,
-                 st_, mask_count_);
+                 st_, mask_count_, chunk_start(C, gi, pi), chunk_start(C, gi, pi + 1));
   clock_.end(st_);
   on_comm([&](cudaStream_t cs) { comms_.all_reduce_f64(sums_.p, 3, last.row, cs); });
   // no host wait here: the sums ride to pinned memory in stream order and
@@ -688,9 +719,8 @@ void Engine::backward_layer(int l) {
   const float* dq;
   i64 lddq;
   clock_.begin(2, st_);
-  if (is_last) {
-    const i64 c0 = chunk_start(dims_[L_], comms_.size(lay.inner), c_.along(lay.inner));
-    dq = dl_.p() + c0;
+  if (is_last) {  // dlogits holds exactly this rank's class chunk
+    dq = dl_.p();
     lddq = dl_.ld;
   } else if (df_masked_) {
     // relu_backward already applied by the SpMM^T / reduction that made dF
@@ -737,7 +767,7 @@ void Engine::backward_layer(int l) {
       },
       [&](i64 r0, i64 r1) {
         if (lsa_dh) {
-          lsa_dh->reduce(r0, r1, s.h_cols, lddh, dh_.p(), r0, lddh, cs_);
+          lsa_dh->all_reduce(r0, r1, s.h_cols, lddh, dh_.p(), r0, lddh, cs_);
           comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
         } else {
           comms_.all_reduce(dh_.p() + r0 * lddh, (r1 - r0) * lddh, lay.inner,
@@ -781,7 +811,7 @@ void Engine::backward_layer(int l) {
             lsa_df->reduce(a, std::max(a, b), s.f_cols, lddf, df0_.p(), a - own0, df0_.ld, cs_);
             comms_.count(kReduceScatter, lay.row, (r1 - r0) * s.f_cols * 4);
           } else {
-            lsa_df->reduce(r0, r1, s.f_cols, lddf, df_.p(), r0, lddf, cs_, false,
+            lsa_df->all_reduce(r0, r1, s.f_cols, lddf, df_.p(), r0, lddf, cs_, false,
                            mask_reduce ? act->p() : nullptr, mask_reduce ? act->ld : 0);
             comms_.count(kAllReduce, lay.row, (r1 - r0) * s.f_cols * 4);
           }
@@ -813,7 +843,7 @@ void Engine::setup_lsa() {
     auto grow = [&](int axis, size_t e) { need[axis] = std::max(need[axis], e); };
     grow(lay.inner, static_cast<size_t>(s.a_rows) * h_[l].ld);
     grow(lay.inner, static_cast<size_t>(s.q_rows) * pad4(s.h_cols));
-    grow(lay.col, static_cast<size_t>(s.h_rows) * q_[l].ld);
+    grow(lay.col, static_cast<size_t>(s.h_rows) * pad4(s.q_cols));
     grow(lay.row, static_cast<size_t>(s.a_cols) * pad4(s.f_cols));
     grow(lay.row, static_cast<size_t>(s.f_cols) * dwp_[l].ld);
   }
@@ -1021,6 +1051,10 @@ int pk_engine_comm_init_local(pk_engine* e, pk_cluster* c) {
   });
 }
 
+int pk_engine_comm_init_solo(pk_engine* e) {
+  return guard([&] { e->e->comm_init_solo(); });
+}
+
 int pk_engine_load(pk_engine* e, const pk_dataset_view* ds) {
   return guard_rank(e, [&] { e->e->load(*ds, false); });
 }
@@ -1096,7 +1130,7 @@ int pk_engine_all_gather_f32(pk_engine* e, int axis, int concat_cols, const floa
     const int g = c.size(axis);
     if (concat_cols) {
       DevBuf<float> stage(static_cast<size_t>(std::max<i64>(1, out_rows * out_cols)));
-      c.all_gather_cols(local, local_ld, out, out_ld, out_rows, out_cols, axis, stage.p,
+      c.all_gather_cols(local, local_ld, out, out_ld, out_rows, out_cols, axis, stage.p, 0,
                         as_stream(stream));
       PK_CUDA(cudaStreamSynchronize(as_stream(stream)));  // stage dies here
     } else {

@@ -74,6 +74,7 @@ class Engine {
 
   void comm_init(const void* uid, int world_size) { comms_.init(grid_, rank_, uid, world_size); }
   void comm_init_local(LocalCluster* cl) { comms_.init_local(grid_, rank_, cl); }
+  void comm_init_solo() { comms_.init_solo(grid_, rank_); }
   // A failed rank takes its cluster down (cluster.hpp:240, 434): peers
   // blocked in (or later entering) a collective fail with ClusterAborted.
   void on_failure(const std::string& why);
@@ -155,6 +156,7 @@ class Engine {
   std::vector<DMat> wfull_, dwp_;      // gathered W and dW partial per layer
   DMat dq_, dh_, df_, df_prev_;        // backward workspaces (max shapes)
   DMat logits_, dl_, stage_;
+  i64 stage_rows_ = 0;
   DevBuf<u32> labels_;
   DevBuf<u8> mask_;
   u64 mask_count_ = 0;  // global number of masked nodes (the CE count)

@@ -150,6 +150,105 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
   barrier(P, blockIdx.x, epoch + 1);
 }
 
+// All-reduce at ring cost: 2 (g - 1) / g x M NVLink bytes per member instead
+// of the all-pull reduce's (g - 1) x M. Rows [r0, r1) are ceil-split over
+// the members; member i
+//   phase 1: sums its own chunk over all members' partials (coordinate order,
+//            the reference's sum_combine), applies the fused relu / mask,
+//            stores the result to its output and pushes it into every
+//            peer's scratch at the same place (posted NVLink stores; a peer
+//            only ever reads its own chunk there, and only in phase 1);
+//   barrier;
+//   phase 2: copies the other members' chunks out of its own scratch.
+// Element e of a chunk is handled by CTA (e mod stride) / blockDim in both
+// phases on every member, so the per-CTA barrier orders each phase-2 read
+// after the phase-1 store that produced it. Two barriers, like the reduce.
+template <int VEC, int G>
+__global__ void __launch_bounds__(256) lsa_allreduce_kernel(LsaPeers P, i64 r0, i64 r1, i64 cols,
+                                                            i64 ld_p, float* __restrict__ out,
+                                                            i64 out_r0, i64 ld_o, int relu,
+                                                            const float* __restrict__ mask,
+                                                            i64 ldm, unsigned epoch) {
+  using V = typename std::conditional<VEC == 4, float4, float>::type;
+  barrier(P, blockIdx.x, epoch);
+  const i64 cv = cols / VEC;
+  const i64 stride = static_cast<i64>(gridDim.x) * blockDim.x;
+  const i64 rows = r1 - r0;
+  const i64 base_rows = rows / P.g, rem = rows % P.g;
+  auto chunk0 = [&](int k) { return r0 + k * base_rows + (k < rem ? k : rem); };
+  const i64 a = chunk0(P.me), b = chunk0(P.me + 1);
+  {
+    const i64 total = (b - a) * cv;
+    constexpr int kUnroll = 4;
+    for (i64 base = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; base < total;
+         base += stride * kUnroll) {
+      V x[kUnroll][G];
+      i64 off[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const i64 i = base + u * stride;
+        const i64 r = a + i / cv, c = (i % cv) * VEC;
+        off[u] = i < total ? r * ld_p + c : -1;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (j < P.g && off[u] >= 0) x[u][j] = __ldcg(reinterpret_cast<const V*>(P.data[j] + off[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (off[u] < 0) continue;
+        const i64 i = base + u * stride;
+        const i64 r = a + i / cv, c = (i % cv) * VEC;
+        V acc = x[u][0];
+#pragma unroll
+        for (int j = 1; j < G; ++j) {
+          if (j >= P.g) break;
+          if constexpr (VEC == 4) {
+            acc.x = __fadd_rn(acc.x, x[u][j].x), acc.y = __fadd_rn(acc.y, x[u][j].y);
+            acc.z = __fadd_rn(acc.z, x[u][j].z), acc.w = __fadd_rn(acc.w, x[u][j].w);
+          } else {
+            acc = __fadd_rn(acc, x[u][j]);
+          }
+        }
+        const i64 ro = r - r0 + out_r0;
+        if (relu) {
+          if constexpr (VEC == 4) {
+            acc.x = acc.x > 0.f ? acc.x : 0.f, acc.y = acc.y > 0.f ? acc.y : 0.f;
+            acc.z = acc.z > 0.f ? acc.z : 0.f, acc.w = acc.w > 0.f ? acc.w : 0.f;
+          } else {
+            acc = acc > 0.f ? acc : 0.f;
+          }
+        }
+        if (mask) {
+          const V m = *reinterpret_cast<const V*>(mask + ro * ldm + c);
+          if constexpr (VEC == 4) {
+            acc.x = m.x > 0.f ? acc.x : 0.f, acc.y = m.y > 0.f ? acc.y : 0.f;
+            acc.z = m.z > 0.f ? acc.z : 0.f, acc.w = m.w > 0.f ? acc.w : 0.f;
+          } else {
+            acc = m > 0.f ? acc : 0.f;
+          }
+        }
+        *reinterpret_cast<V*>(out + ro * ld_o + c) = acc;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (j < P.g && j != P.me)
+            __stcg(reinterpret_cast<V*>(const_cast<float*>(P.data[j]) + off[u]), acc);
+      }
+    }
+  }
+  __threadfence_system();  // every thread's pushes before the CTA's arrival
+  barrier(P, blockIdx.x, epoch + 1);
+  for (int k = 0; k < P.g; ++k) {
+    if (k == P.me) continue;
+    const i64 ka = chunk0(k), kb = chunk0(k + 1);
+    const i64 total = (kb - ka) * cv;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+      const i64 r = ka + i / cv, c = (i % cv) * VEC;
+      *reinterpret_cast<V*>(out + (r - r0 + out_r0) * ld_o + c) =
+          __ldcg(reinterpret_cast<const V*>(P.data[P.me] + r * ld_p + c));
+    }
+  }
+}
+
 __global__ void lsa_peer_ptrs_kernel(ncclWindow_t win, int g, void** out) {
   const int j = threadIdx.x;
   if (j < g) out[j] = ncclGetLsaPointer(win, 0, j);
@@ -264,6 +363,47 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
     else launch(V1{}, std::integral_constant<int, 8>{});
   }
   PK_LAUNCH("lsa ordered reduce");
+}
+
+void LsaGroup::all_reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
+                          cudaStream_t st, bool relu, const float* mask, i64 ldm) {
+  // PK_LSA_PUSH=0: the all-pull reduce over every row on every member
+  static const bool push = [] {
+    const char* e = std::getenv("PK_LSA_PUSH");
+    return !(e && e[0] == '0');
+  }();
+  if (!push) return reduce(r0, r1, cols, ld_p, out, out_r0, ld_o, st, relu, mask, ldm);
+  check(ready_, "lsa all_reduce: group not initialised");
+  check((r1 > 0 ? r1 : 0) * ld_p * sizeof(float) <= scratch_bytes_,
+        "lsa all_reduce: partial exceeds the symmetric scratch");
+  const unsigned epoch = epoch_;
+  epoch_ += 2;
+  const bool v4 = cols % 4 == 0 && ld_p % 4 == 0 && ld_o % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                  (!mask || (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0));
+  static const int ctas = [] {
+    const char* e = std::getenv("PK_LSA_CTAS");
+    const int v = e ? std::atoi(e) : kLsaBlocks / 2;
+    return std::max(1, std::min(v, kLsaBlocks));
+  }();
+  auto launch = [&](auto vec_tag, auto g_tag) {
+    constexpr int V = decltype(vec_tag)::value, Gm = decltype(g_tag)::value;
+    lsa_allreduce_kernel<V, Gm><<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0,
+                                                     ld_o, relu ? 1 : 0, mask, ldm, epoch);
+  };
+  using V4 = std::integral_constant<int, 4>;
+  using V1 = std::integral_constant<int, 1>;
+  if (g_ <= 2) {
+    if (v4) launch(V4{}, std::integral_constant<int, 2>{});
+    else launch(V1{}, std::integral_constant<int, 2>{});
+  } else if (g_ <= 4) {
+    if (v4) launch(V4{}, std::integral_constant<int, 4>{});
+    else launch(V1{}, std::integral_constant<int, 4>{});
+  } else {
+    if (v4) launch(V4{}, std::integral_constant<int, 8>{});
+    else launch(V1{}, std::integral_constant<int, 8>{});
+  }
+  PK_LAUNCH("lsa ring all-reduce");
 }
 
 bool lsa_timed_out() {

@@ -38,6 +38,12 @@ class LsaGroup {
   // into the dF reduction).
   void reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
               cudaStream_t st, bool relu = false, const float* mask = nullptr, i64 ldm = 0);
+  // The same result for a row range every member passes identically (an
+  // all-reduce), at ring cost: each member sums its own ceil-split chunk and
+  // pushes it to the peers (lsa.cu). The scratch then holds the reduced
+  // rows of the other members' chunks. Bit-identical to reduce().
+  void all_reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
+                  cudaStream_t st, bool relu = false, const float* mask = nullptr, i64 ldm = 0);
 
  private:
   int g_ = 0, me_ = 0;

@@ -79,6 +79,7 @@ _SIGS = {
     "pk_engine_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pk_engine_destroy": (C.c_int, [C.c_void_p]),
     "pk_engine_abort": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "pk_engine_comm_init_solo": (C.c_int, [C.c_void_p]),
 }
 _capi.register(_SIGS)
 
@@ -210,6 +211,11 @@ class RankEngine:
     def comm_init(self, uid: bytes, world_size: int):
         buf = (C.c_ubyte * 128).from_buffer_copy(uid)
         call("pk_engine_comm_init", self.h, C.cast(buf, C.c_void_p), world_size)
+
+    def comm_init_solo(self):
+        """Measurement mode (pk_engine_comm_init_solo): this rank alone;
+        collectives keep only its own contribution."""
+        call("pk_engine_comm_init_solo", self.h)
 
     def load(self, pre):
         """A PreprocessedDataset (device), a HostDataset (pinned host), or a
