@@ -412,6 +412,13 @@ int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds_host);
  * summed over the last layer's row_shard group (comm_init first when the
  * grid has more than one rank). */
 int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rank_tensors);
+/* The same, taking over the blocks in `blocks[plane * 2 + parity]` (arrays
+ * allocated by this library, e.g. pk_rmat_block / pk_csr_block) instead of
+ * copying them — a billion-edge rank cannot hold its blocks twice. Taken
+ * entries are zeroed; entries left with a NULL row_ptr are copied from
+ * rank_tensors->adj as usual. */
+int pk_engine_load_rank_adopt(pk_engine* e, const pk_rank_view* rank_tensors,
+                              pk_csr_owned* blocks);
 int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss_host,
                                double* accuracy_host);
 int pk_engine_optimizer_step(pk_engine* e);

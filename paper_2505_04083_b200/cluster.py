@@ -186,7 +186,7 @@ def train_distributed_generated(spec, grid: GridConfig, opts, devices=None) -> T
     def rank_train(r):
         e = cl.engine(spec.n, spec.feat_dim, spec.classes, r, opts)
         try:
-            e.load_rank(rank_gen.generate_rank_tensors(spec, grid, r, L, pieces))
+            e.load_rank(rank_gen.generate_rank_tensors(spec, grid, r, L, pieces), adopt=True)
             metrics = [e.train_epoch(ep) for ep in range(opts.epochs)]
             w = [e.tensor(trainer.PK_T_W, l).cpu().numpy() for l in range(L)]
             f = e.tensor(trainer.PK_T_F0).cpu().numpy()

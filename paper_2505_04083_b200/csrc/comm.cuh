@@ -62,6 +62,7 @@ class Comms {
   void init_solo(const Grid& grid, int rank);
   bool ready() const { return world_ != nullptr || local_ || solo_ || grid_.size() == 1; }
   LocalCluster* local_cluster() const { return local_ ? lc_.cluster() : nullptr; }
+  bool solo() const { return solo_; }
   // Tear down after a failure (ClusterAborted semantics): NCCL
   // communicators are aborted so no later call can block on them.
   void abort_nccl();

@@ -276,7 +276,7 @@ void Engine::set_f0(const float* src, i64 ld) {
 void Engine::alloc_params() {
   w_.resize(L_), w_m_.resize(L_), w_v_.resize(L_), dw_.resize(L_);
   wfull_.resize(L_), dwp_.resize(L_), h_.resize(L_), q_.resize(L_), fout_.resize(L_);
-  i64 max_dq = 1, max_dh = 1, max_df = 1;
+  i64 max_dh = 1, max_df = 1;
   for (int l = 0; l < L_; ++l) {
     const Shapes& s = shapes_[l];
     const Slice ws = weight_slice(grid_, lays_[l], c_, dims_[l], dims_[l + 1]);
@@ -294,17 +294,14 @@ void Engine::alloc_params() {
     // NCCL fallback of a split col_shard): allocated on first use
     if (l + 1 == L_) q_[l].alloc(s.q_rows, s.q_cols, st_);
     if (l + 1 < L_) fout_[l].alloc(s.q_rows, s.q_cols, st_);
-    max_dq = std::max(max_dq, s.q_rows * pad4(s.q_cols));
     max_dh = std::max(max_dh, s.h_rows * pad4(s.h_cols));
     max_df = std::max(max_df, s.a_cols * pad4(s.f_cols));
   }
   w_step_ = 0;
   f0g_.alloc(shapes_[0].f_rows, shapes_[0].f_cols, st_);
-  dq_.buf.alloc(max_dq);
   dh_.buf.alloc(max_dh);
   df_.buf.alloc(max_df);
   df_prev_.buf.alloc(max_df);
-  PK_CUDA(cudaMemset(dq_.buf.p, 0, dq_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
@@ -473,7 +470,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
 }
 
 // The file_handle path (trainer.hpp:461-466): the rank's own tensors.
-void Engine::load_rank(const pk_rank_view& rv) {
+void Engine::load_rank(const pk_rank_view& rv, pk_csr_owned* adopt) {
   PK_CUDA(cudaSetDevice(cfg_.device));
   const i64 n = cfg_.n;
   auto mark = [](const char*) {};
@@ -496,7 +493,13 @@ void Engine::load_rank(const pk_rank_view& rv) {
     }
     auto sh = std::make_shared<AdjShard>();
     sh->parity = parity, sh->r0 = r.r0, sh->r1 = r.r1, sh->c0 = r.c0, sh->c1 = r.c1;
-    csr_block(b, 0, b.rows, 0, b.cols, &sh->a, st_);  // an all-columns block: a plain copy
+    pk_csr_owned* own = adopt ? &adopt[plane * 2 + parity] : nullptr;
+    if (own && own->row_ptr) {  // library-allocated block: taken over, no copy
+      sh->a = *own;
+      *own = pk_csr_owned{};
+    } else {
+      csr_block(b, 0, b.rows, 0, b.cols, &sh->a, st_);  // an all-columns block: a plain copy
+    }
     finish_shard(std::move(sh), plane, parity, mark);
   }
   const Slice fs = feature_slice(grid_, c_, n, dims_[0]);
@@ -613,7 +616,10 @@ void Engine::forward_layer(int l, bool fault) {
   const bool hidden = l + 1 < L_;
   const bool col_single = comms_.size(lay.col) == 1;
   LsaGroup* lsa_q = comms_.lsa(lay.col);
-  DMat& qout = hidden && (col_single || lsa_q) ? fout_[l] : q_[l];
+  // measurement mode stands in for the peer-memory path: relu in place
+  // where the ordered reduction would have fused it
+  const bool solo = comms_.solo();
+  DMat& qout = hidden && (col_single || lsa_q || solo) ? fout_[l] : q_[l];
   if (qout.buf.p == nullptr) qout.alloc(s.q_rows, s.q_cols, st_);
   float* qpart = lsa_q ? lsa_q->scratch() : qout.p();
   pipelined(
@@ -632,6 +638,9 @@ void Engine::forward_layer(int l, bool fault) {
         } else {
           comms_.all_reduce(qout.p() + r0 * qout.ld, (r1 - r0) * qout.ld, lay.col,
                             (r1 - r0) * s.q_cols * 4, cs_);
+          if (solo && hidden && !col_single)
+            relu_forward_launch(qout.p() + r0 * qout.ld, qout.ld, r1 - r0, s.q_cols,
+                                qout.p() + r0 * qout.ld, qout.ld, cs_);
         }
       });
   gemm_flops_ += 2 * static_cast<u64>(s.h_rows) * s.w_cols * s.h_cols;
@@ -728,10 +737,11 @@ void Engine::backward_layer(int l) {
     dq = df_prev_.p();
   } else {
     lddq = pad4(s.q_cols);
-    // relu'(Q) from the stored activation: relu(Q) > 0 exactly where Q > 0
+    // relu'(Q) from the stored activation: relu(Q) > 0 exactly where Q > 0;
+    // in place — dF_out is dead once dQ exists (no separate dQ workspace)
     relu_backward_launch(fout_[l].p(), fout_[l].ld, df_prev_.p(), pad4(s.q_cols), s.q_rows,
-                         s.q_cols, dq_.p(), lddq, st_);
-    dq = dq_.p();
+                         s.q_cols, df_prev_.p(), lddq, st_);
+    dq = df_prev_.p();
   }
   // dW = (dQ^T H)^T computed as H^T dQ: same products, same k order
   LsaGroup* lsa_dw = comms_.lsa(lay.row);
@@ -1066,7 +1076,14 @@ int pk_engine_load_host(pk_engine* e, const pk_dataset_view* ds) {
 int pk_engine_load_rank(pk_engine* e, const pk_rank_view* rv) {
   return guard_rank(e, [&] {
     check(e && rv, "engine load_rank: null argument");
-    e->e->load_rank(*rv);
+    e->e->load_rank(*rv, nullptr);
+  });
+}
+
+int pk_engine_load_rank_adopt(pk_engine* e, const pk_rank_view* rv, pk_csr_owned* blocks) {
+  return guard_rank(e, [&] {
+    check(e && rv && blocks, "engine load_rank: null argument");
+    e->e->load_rank(*rv, blocks);
   });
 }
 

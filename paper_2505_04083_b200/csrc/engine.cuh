@@ -79,7 +79,9 @@ class Engine {
   // blocked in (or later entering) a collective fail with ClusterAborted.
   void on_failure(const std::string& why);
   void load(const pk_dataset_view& ds, bool host);
-  void load_rank(const pk_rank_view& rv);
+  // adopt (optional, [6] like rv.adj): library-allocated blocks the engine
+  // takes over instead of copying (entries are zeroed when taken)
+  void load_rank(const pk_rank_view& rv, pk_csr_owned* adopt);
   // rank_forward_backward (trainer.hpp:478-527), enqueued without a host
   // wait: the cross-entropy sums travel to pinned host memory on the stream
   // and finish_pass() turns them into loss / accuracy (and the reference's
@@ -154,7 +156,7 @@ class Engine {
   std::vector<char> q_kept_;           // hidden layer's Q materialised last forward
   bool df_masked_ = false;             // df_prev_ already carries relu_backward
   std::vector<DMat> wfull_, dwp_;      // gathered W and dW partial per layer
-  DMat dq_, dh_, df_, df_prev_;        // backward workspaces (max shapes)
+  DMat dh_, df_, df_prev_;             // backward workspaces (max shapes)
   DMat logits_, dl_, stage_;
   i64 stage_rows_ = 0;
   DevBuf<u32> labels_;

@@ -71,6 +71,8 @@ _SIGS = {
     "pk_engine_load": (C.c_int, [C.c_void_p, C.POINTER(pk_dataset_view)]),
     "pk_engine_load_host": (C.c_int, [C.c_void_p, C.POINTER(pk_dataset_view)]),
     "pk_engine_load_rank": (C.c_int, [C.c_void_p, C.POINTER(pk_rank_view)]),
+    "pk_engine_load_rank_adopt": (C.c_int, [C.c_void_p, C.POINTER(pk_rank_view),
+                                            C.POINTER(_capi.pk_csr_owned)]),
     "pk_engine_forward_backward": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double),
                                              C.POINTER(C.c_double)]),
     "pk_engine_optimizer_step": (C.c_int, [C.c_void_p]),
@@ -235,8 +237,11 @@ class RankEngine:
             torch.cuda.synchronize()
             call("pk_engine_load", self.h, C.byref(v))
 
-    def load_rank(self, rt):
-        """RankTensors (shard_io.RankTensors) -> pk_engine_load_rank."""
+    def load_rank(self, rt, adopt=False):
+        """RankTensors (shard_io.RankTensors) -> pk_engine_load_rank. With
+        adopt=True, library-allocated blocks (rank_gen / shard builder
+        outputs) are handed to the engine instead of copied
+        (pk_engine_load_rank_adopt); those DeviceCsr objects are spent."""
         v = pk_rank_view()
         for (plane, parity), (blk, _) in rt.adj.items():
             v.adj[plane * 2 + parity] = blk._view
@@ -247,7 +252,21 @@ class RankEngine:
         v.mask = rt.mask.data_ptr() if rt.mask.numel() else None
         v.label_rows = rt.labels.numel()
         torch.cuda.synchronize()
-        call("pk_engine_load_rank", self.h, C.byref(v))
+        if not adopt:
+            call("pk_engine_load_rank", self.h, C.byref(v))
+            return
+        owned = (_capi.pk_csr_owned * 6)()
+        taken, seen = [], set()
+        for (plane, parity), (blk, _) in rt.adj.items():
+            keep = getattr(blk, "_owned", None)
+            if keep is None or id(keep) in seen or not keep.owned.row_ptr:
+                continue
+            seen.add(id(keep))
+            owned[plane * 2 + parity] = keep.owned
+            taken.append(keep)
+        call("pk_engine_load_rank_adopt", self.h, C.byref(v), owned)
+        for keep in taken:  # the engine owns those arrays now
+            keep.owned = _capi.pk_csr_owned()
 
     def forward_backward(self, epoch=0):
         loss, acc = C.c_double(), C.c_double()

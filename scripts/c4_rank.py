@@ -54,6 +54,8 @@ def main():
                        f"{'undirected' if args.undirected else 'directed'} edges, "
                        f"GCN 128-128-128-172, grid {args.grid}, rank {args.rank} of {grid.size} "
                        "measured alone (pk_engine_comm_init_solo)"}
+    def note(what):
+        print(f"[c4] {what}: {used_gb()[0]:.1f} GB in use", file=sys.stderr, flush=True)
     t0 = time.perf_counter()
     pieces = rank_gen.global_pieces(spec, args.rank, grid.size)  # every degree range here
     torch.cuda.synchronize()
@@ -66,16 +68,18 @@ def main():
     del pieces
     torch.cuda.empty_cache()
     out["gen_mem_gb"] = used_gb()[0]
+    note("shards generated")
     opts = trainer.TrainOptions(hidden_dims=[128, 128], mode=trainer.PK_MODE_FAST)
     eng = trainer.RankEngine(spec.n, 128, 172, grid, args.rank, opts, 0)
     eng.comm_init_solo()
     t0 = time.perf_counter()
-    eng.load_rank(rt)
+    eng.load_rank(rt, adopt=True)
     torch.cuda.synchronize()
     out["load_s"] = time.perf_counter() - t0
     del rt
     torch.cuda.empty_cache()
     _capi.lib().pk_device_cache_release()
+    note("engine loaded")
     for e in range(args.warmup):
         eng.train_epoch(e)
     ms = [eng.train_epoch(args.warmup + e) for e in range(args.epochs)]
