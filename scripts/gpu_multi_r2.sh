@@ -23,3 +23,13 @@ for push in 1 0; do
   run 4 4,1,1 $push n4_411_push$push
   run 4 1,4,1 $push n4_141_push$push
 done
+# scaling on the performance model's grids (default push), full bench line
+for n in 1 2 4; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n \
+    --master-addr 127.0.0.1 --master-port $((29800 + n)) bench.py --gpus $n \
+    --steps 10 --warmup 3 --no-cpu-baseline --no-c1-measured > gpurun_out/scale_c2_n$n.log 2>&1
+  echo "scale n=$n rc=$? $(grep -o '"value": [0-9.]*' gpurun_out/scale_c2_n$n.log | head -2 | tr '\n' ' ') $(grep -o '"grid": "[0-9x]*"' gpurun_out/scale_c2_n$n.log | head -1)"
+done
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+  --master-port 29911 scripts/grid_sweep.py --epochs 3 > gpurun_out/grid_sweep_n4.log 2>&1
+echo "sweep rc=$?"; tail -3 gpurun_out/grid_sweep_n4.log
