@@ -443,6 +443,7 @@ def run_ours(args):
             eng2.comm_init(uid, world)
         t1 = time.perf_counter()
         eng2.load(host)
+        eng2.prepare_result_buffers()  # host-side, overlaps the epochs
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         for e in range(args.e2e_epochs):

@@ -238,12 +238,20 @@ void Engine::finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, M
   // weight from here on: 8 B per nonzero for A and again for A^T (20 GB per
   // rank at C4 scale). Only row_ptr stays (block edges). PK_KEEP_CSR=1 keeps
   // them.
+  // (dropped in drop_csr_arrays() once the whole load has drained: a free
+  // synchronises the device, which here would stall the staged uploads)
+  shards_[plane * 2 + parity] = std::move(sh);
+}
+
+void Engine::drop_csr_arrays() {
   static const bool keep_csr = [] {
     const char* e = std::getenv("PK_KEEP_CSR");
     return e && e[0] == '1';
   }();
-  if (seg && !keep_csr) {
-    PK_CUDA(cudaStreamSynchronize(st_));
+  if (cfg_.mode != PK_MODE_FAST || spmm_fast_segment() == 0 || keep_csr) return;
+  PK_CUDA(cudaStreamSynchronize(st_));
+  for (auto& sh : shards_) {
+    if (!sh) continue;
     for (pk_csr_owned* m : {&sh->a, &sh->at}) {
       if (m->col_idx) dev_free(m->col_idx);
       if (m->values) dev_free(m->values);
@@ -251,7 +259,6 @@ void Engine::finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, M
       m->values = nullptr;
     }
   }
-  shards_[plane * 2 + parity] = std::move(sh);
 }
 
 // F0 shard from device rows of width feature_slice's column count (ld given)
@@ -466,6 +473,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   PK_CUDA(cudaStreamSynchronize(cs_));  // the staged uploads are released with this scope
   for (auto& e : staged)
     if (e) cudaEventDestroy(e);
+  drop_csr_arrays();
   loaded_ = true;
 }
 
@@ -526,6 +534,7 @@ void Engine::load_rank(const pk_rank_view& rv, pk_csr_owned* adopt) {
     PK_CUDA(cudaStreamSynchronize(st_));
   }
   set_labels(rv.labels, rv.mask, rv.label_rows, static_cast<u64>(count));
+  drop_csr_arrays();
   loaded_ = true;
 }
 

@@ -173,6 +173,9 @@ class Engine {
   template <typename Mark>
   void finish_shard(std::shared_ptr<AdjShard> sh, int plane, int parity, Mark& mark);
   void set_f0(const float* src, i64 ld);
+  // FAST plans hold every nonzero: free the shards' CSR columns / values
+  // (8 B per nonzero for A and A^T) once the load has drained
+  void drop_csr_arrays();
   void alloc_params();
   void set_labels(const u32* labels, const u8* mask, i64 lrows, u64 global_count);
 };

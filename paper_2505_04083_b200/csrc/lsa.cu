@@ -367,12 +367,17 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
 
 void LsaGroup::all_reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
                           cudaStream_t st, bool relu, const float* mask, i64 ldm) {
-  // PK_LSA_PUSH=0: the all-pull reduce over every row on every member
-  static const bool push = [] {
+  // Owner-push pays off from three members up: C2 at 4 GPUs, collectives
+  // per epoch 1x1x4 26.3 -> 19.5 ms, 4x1x1 28.7 -> 19.5, 1x4x1 42.5 ->
+  // 29.5; with two members both move M per member and the all-pull is
+  // faster (2x1x1 10.6 vs 13.0 ms; profiles/r2_lsa_push_ab_n4.log).
+  // PK_LSA_PUSH=0 never pushes, 1 always, default from g >= 3.
+  static const int push = [] {
     const char* e = std::getenv("PK_LSA_PUSH");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : -1;
   }();
-  if (!push) return reduce(r0, r1, cols, ld_p, out, out_r0, ld_o, st, relu, mask, ldm);
+  if (push == 0 || (push < 0 && g_ < 3))
+    return reduce(r0, r1, cols, ld_p, out, out_r0, ld_o, st, relu, mask, ldm);
   check(ready_, "lsa all_reduce: group not initialised");
   check((r1 > 0 ? r1 : 0) * ld_p * sizeof(float) <= scratch_bytes_,
         "lsa all_reduce: partial exceeds the symmetric scratch");

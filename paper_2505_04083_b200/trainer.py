@@ -299,13 +299,44 @@ class RankEngine:
                                         "strides": None}
         return torch.as_tensor(_Arr(), device="cuda")[:, :v.cols].clone()
 
+    def _result_shapes(self):
+        out = []
+        for which, layers in ((PK_T_W, range(len(self.dims) - 1)), (PK_T_F0, [0])):
+            for l in layers:
+                v = pk_tensor_view()
+                call("pk_engine_tensor", self.h, which, l, C.byref(v))
+                out.append((which, l, int(v.rows), int(v.cols)))
+        return out
+
+    def prepare_result_buffers(self):
+        """Allocate (pin) the host buffers of this rank's TrainResult share on
+        a helper thread while the GPU trains: page-locking ~1 GB of fresh
+        host memory takes longer than the copy itself, and it does not need
+        to wait for the device."""
+        import threading
+        shapes = self._result_shapes()
+        self._result_bufs = None
+
+        def alloc():
+            self._result_bufs = [torch.empty((r, c), dtype=torch.float32, pin_memory=True)
+                                 for _, _, r, c in shapes]
+        self._result_thread = threading.Thread(target=alloc, daemon=True)
+        self._result_thread.start()
+
     def download_params(self):
         """This rank's share of TrainResult (trainer.hpp:636-686): its W
-        shards and F0 shard as host numpy arrays (pageable: pinning a fresh
-        839 MB buffer costs more than the staged copy saves)."""
-        return [self.tensor(which, l).cpu().numpy()
-                for which, layers in ((PK_T_W, range(len(self.dims) - 1)), (PK_T_F0, [0]))
-                for l in layers]
+        shards and F0 shard as host numpy arrays (into the pinned buffers of
+        prepare_result_buffers when they exist)."""
+        t = getattr(self, "_result_thread", None)
+        if t is None:
+            return [self.tensor(which, l).cpu().numpy()
+                    for which, l, _, _ in self._result_shapes()]
+        t.join()
+        out = []
+        for (which, l, _, _), h in zip(self._result_shapes(), self._result_bufs):
+            h.copy_(self.tensor(which, l))
+            out.append(h.numpy())
+        return out
 
     def stream_ptr(self):
         s = C.c_void_p()
