@@ -152,6 +152,21 @@ Engine::Engine(const pk_engine_config& cfg) : cfg_(cfg) {
   lays_ = plan_layouts(L_);
   for (int l = 0; l < L_; ++l)
     shapes_.push_back(layer_shapes(grid_, lays_[l], c_, cfg.n, dims_[l], dims_[l + 1]));
+  // Transform-first layers (FAST only): where the layer's inner axis is a
+  // single rank and it narrows (D_out < D_in), Q = A (F W) instead of
+  // (A F) W — both SpMMs of the layer then gather D_out-wide rows instead of
+  // D_in-wide ones (C2's last layer: 47 instead of 256; C3's first: 128
+  // instead of 602). Same products, another association: tolerance-level
+  // difference, so PARITY keeps the reference's order. PK_TRANSFORM_FIRST=0
+  // turns it off.
+  static const bool tf_on = [] {
+    const char* e = std::getenv("PK_TRANSFORM_FIRST");
+    return !(e && e[0] == '0');
+  }();
+  tf_.assign(L_, 0);
+  for (int l = 0; l < L_; ++l)
+    tf_[l] = tf_on && cfg.mode == PK_MODE_FAST && grid_.extent(lays_[l].inner) == 1 &&
+             dims_[l + 1] < dims_[l];
   PK_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   PK_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   sums_.alloc(4);
@@ -283,7 +298,7 @@ void Engine::set_f0(const float* src, i64 ld) {
 void Engine::alloc_params() {
   w_.resize(L_), w_m_.resize(L_), w_v_.resize(L_), dw_.resize(L_);
   wfull_.resize(L_), dwp_.resize(L_), h_.resize(L_), q_.resize(L_), fout_.resize(L_);
-  i64 max_dh = 1, max_df = 1;
+  i64 max_dh = 1, max_df = 1, max_tf = 0;
   for (int l = 0; l < L_; ++l) {
     const Shapes& s = shapes_[l];
     const Slice ws = weight_slice(grid_, lays_[l], c_, dims_[l], dims_[l + 1]);
@@ -296,7 +311,8 @@ void Engine::alloc_params() {
     dw_[l].alloc(w_[l].rows, w_[l].cols, st_);
     wfull_[l].alloc(s.f_cols, s.w_cols, st_);
     dwp_[l].alloc(s.f_cols, s.w_cols, st_);
-    h_[l].alloc(s.h_rows, s.h_cols, st_);
+    if (!tf_[l]) h_[l].alloc(s.h_rows, s.h_cols, st_);  // a transform-first layer keeps no H
+    else max_tf = std::max(max_tf, s.a_cols * pad4(s.w_cols));
     // a hidden layer's Q exists only where the engine materialises it (the
     // NCCL fallback of a split col_shard): allocated on first use
     if (l + 1 == L_) q_[l].alloc(s.q_rows, s.q_cols, st_);
@@ -309,6 +325,7 @@ void Engine::alloc_params() {
   dh_.buf.alloc(max_dh);
   df_.buf.alloc(max_df);
   df_prev_.buf.alloc(max_df);
+  if (max_tf) tfbuf_.buf.alloc(max_tf);  // P = F W forward, dP = A^T dQ backward
   PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
@@ -562,6 +579,7 @@ void Engine::on_comm(const std::function<void(cudaStream_t)>& f) {
 }
 
 void Engine::forward_layer(int l, bool fault) {
+  if (tf_[l]) return forward_layer_tf(l);
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
   AdjShard& sh = const_cast<AdjShard&>(shard(lay));
@@ -728,6 +746,7 @@ void Engine::finish_pass(int epoch, double* loss_out, double* acc_out) {
 // backward_layer (engine.hpp:214-259)
 
 void Engine::backward_layer(int l) {
+  if (tf_[l]) return backward_layer_tf(l);
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
   AdjShard& sh = const_cast<AdjShard&>(shard(lay));
@@ -849,6 +868,146 @@ void Engine::backward_layer(int l) {
   df_masked_ = mask_spmm || mask_reduce;
 }
 
+// ---------------------------------------------------------------------------
+// transform-first layers (inner axis a single rank, D_out < D_in; FAST)
+//
+// forward:  P = F W_full  (a_cols x w_cols, partial over col_shard: its
+//           all-reduce replaces Q's), Q = A P (complete: inner is one rank)
+// backward: dP = A^T dQ (partial over row_shard: all-reduced, replacing
+//           dF's), dW = F^T dP restricted to this rank's stored rows (no
+//           reduce-scatter: dP is complete and F holds every row), dF = dP
+//           W_full^T (complete; at layer 0 only this rank's F0 rows)
+// The fault hook (skip the aggregation all-reduce) has nothing to skip here:
+// inner is a single rank.
+
+void Engine::forward_layer_tf(int l) {
+  const Layout& lay = lays_[l];
+  const Shapes& s = shapes_[l];
+  AdjShard& sh = const_cast<AdjShard&>(shard(lay));
+  const float* f;
+  i64 ldf;
+  if (l == 0) {
+    on_comm([&](cudaStream_t cs) {
+      comms_.all_gather_rows(f0_.p(), f0g_.p(), s.f_rows, f0g_.ld, lay.row, s.f_cols, cs);
+    });
+    f = f0g_.p();
+    ldf = f0g_.ld;
+  } else {
+    f = fout_[l - 1].p();
+    ldf = fout_[l - 1].ld;
+  }
+  check(sh.a.cols == s.f_rows, "forward layer " + std::to_string(l) + ": adjacency shard " +
+                                   shape(sh.a.rows, sh.a.cols) + " does not match features " +
+                                   shape(s.f_rows, s.f_cols));
+  comms_.counters.calls[lay.inner][kAllReduce]++;  // the singleton H all-reduce
+  on_comm([&](cudaStream_t cs) {
+    comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
+                           cs);
+  });
+  const i64 ldp = pad4(s.w_cols);
+  LsaGroup* lsa_p = comms_.lsa(lay.col);
+  float* ppart = lsa_p ? lsa_p->scratch() : tfbuf_.p();
+  clock_.begin(1, st_);
+  gemm_launch(false, false, s.f_rows, s.w_cols, s.f_cols, f, ldf, wfull_[l].p(), wfull_[l].ld,
+              ppart, ldp, cfg_.mode, st_);
+  clock_.end(st_);
+  gemm_flops_ += 2 * static_cast<u64>(s.f_rows) * s.w_cols * s.f_cols;
+  if (comms_.size(lay.col) > 1) {
+    on_comm([&](cudaStream_t cs) {
+      if (lsa_p) {
+        lsa_p->all_reduce(0, s.f_rows, s.w_cols, ldp, tfbuf_.p(), 0, ldp, cs);
+        comms_.count(kAllReduce, lay.col, s.f_rows * s.w_cols * 4);
+      } else {
+        comms_.all_reduce(tfbuf_.p(), s.f_rows * ldp, lay.col, s.f_rows * s.w_cols * 4, cs);
+      }
+    });
+  } else {
+    comms_.counters.calls[lay.col][kAllReduce]++;
+  }
+  const bool hidden = l + 1 < L_;
+  DMat& qout = hidden ? fout_[l] : q_[l];
+  clock_.begin(0, st_);
+  spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, s.w_cols, qout.p(), qout.ld,
+           st_);
+  spmm_flops_ += 2 * sh.a.nnz * static_cast<u64>(s.w_cols);
+  spmm_bytes_ += spmm_alg_bytes(sh.a.rows, sh.a.nnz, s.w_cols);
+  spmm_cbytes_ += spmm_compulsory_bytes(sh.a.rows, sh.a.nnz, sh.a.cols, s.w_cols);
+  if (hidden) relu_forward_launch(qout.p(), qout.ld, s.q_rows, s.q_cols, qout.p(), qout.ld, st_);
+  clock_.end(st_);
+  if (hidden) {
+    if (q_kept_.size() < static_cast<size_t>(L_)) q_kept_.assign(L_, 0);
+    q_kept_[l] = 0;
+  }
+}
+
+void Engine::backward_layer_tf(int l) {
+  const Layout& lay = lays_[l];
+  const Shapes& s = shapes_[l];
+  AdjShard& sh = const_cast<AdjShard&>(shard(lay));
+  const bool is_last = l == L_ - 1;
+  const float* dq;
+  i64 lddq;
+  clock_.begin(2, st_);
+  if (is_last) {  // inner is one rank: dlogits holds every class
+    dq = dl_.p();
+    lddq = dl_.ld;
+  } else {
+    lddq = pad4(s.q_cols);
+    if (!df_masked_)
+      relu_backward_launch(fout_[l].p(), fout_[l].ld, df_prev_.p(), lddq, s.q_rows, s.q_cols,
+                           df_prev_.p(), lddq, st_);
+    dq = df_prev_.p();
+  }
+  clock_.end(st_);
+  const i64 ldp = pad4(s.w_cols);
+  LsaGroup* lsa_r = comms_.lsa(lay.row);
+  float* dpp = lsa_r ? lsa_r->scratch() : tfbuf_.p();
+  clock_.begin(5, st_);
+  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, s.w_cols, dpp, ldp, st_);
+  clock_.end(st_);
+  spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.w_cols);
+  spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.w_cols);
+  spmm_cbytes_ += spmm_compulsory_bytes(sh.at.rows, sh.nnz_t, sh.at.cols, s.w_cols);
+  const int gr = grid_.extent(lay.row), pr = c_.along(lay.row);
+  if (gr > 1) {
+    on_comm([&](cudaStream_t cs) {
+      if (lsa_r) {
+        lsa_r->all_reduce(0, s.a_cols, s.w_cols, ldp, tfbuf_.p(), 0, ldp, cs);
+        comms_.count(kAllReduce, lay.row, s.a_cols * s.w_cols * 4);
+      } else {
+        comms_.all_reduce(tfbuf_.p(), s.a_cols * ldp, lay.row, s.a_cols * s.w_cols * 4, cs);
+      }
+    });
+  } else {
+    comms_.counters.calls[lay.row][kAllReduce]++;
+  }
+  const float* dp = tfbuf_.p();
+  const float* f = l == 0 ? f0g_.p() : fout_[l - 1].p();
+  const i64 ldf = l == 0 ? f0g_.ld : fout_[l - 1].ld;
+  clock_.begin(2, st_);
+  // dW: this rank's stored rows of W (weight_slice: the f_cols chunk split
+  // again by row_shard) = F[:, o0:o1]^T dP over all a_cols rows
+  const i64 o0 = chunk_start(s.f_cols, gr, pr), o1 = chunk_start(s.f_cols, gr, pr + 1);
+  gemm_launch(true, false, o1 - o0, s.w_cols, s.f_rows, f + o0, ldf, dp, ldp, dw_[l].p(),
+              dw_[l].ld, cfg_.mode, st_);
+  gemm_flops_ += 2 * static_cast<u64>(o1 - o0) * s.w_cols * s.f_rows;
+  if (l > 0) {
+    const i64 lddf = pad4(s.f_cols);
+    gemm_launch(false, true, s.f_rows, s.f_cols, s.w_cols, dp, ldp, wfull_[l].p(), wfull_[l].ld,
+                df_.p(), lddf, cfg_.mode, st_);
+    gemm_flops_ += 2 * static_cast<u64>(s.f_rows) * s.f_cols * s.w_cols;
+    std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
+  } else {
+    // this rank's F0 rows: the row_shard chunk of the gathered input rows
+    const i64 own0 = chunk_start(s.a_cols, gr, pr), own1 = chunk_start(s.a_cols, gr, pr + 1);
+    gemm_launch(false, true, own1 - own0, s.f_cols, s.w_cols, dp + own0 * ldp, ldp,
+                wfull_[l].p(), wfull_[l].ld, df0_.p(), df0_.ld, cfg_.mode, st_);
+    gemm_flops_ += 2 * static_cast<u64>(own1 - own0) * s.f_cols * s.w_cols;
+  }
+  clock_.end(st_);
+  df_masked_ = false;
+}
+
 // Symmetric scratch for the ordered peer-memory reductions: per axis the
 // largest partial it reduces (H and dH along inner, Q along col_shard, dF
 // along row_shard). Collective; every member of a group computes the same
@@ -865,6 +1024,10 @@ void Engine::setup_lsa() {
     grow(lay.col, static_cast<size_t>(s.h_rows) * pad4(s.q_cols));
     grow(lay.row, static_cast<size_t>(s.a_cols) * pad4(s.f_cols));
     grow(lay.row, static_cast<size_t>(s.f_cols) * dwp_[l].ld);
+    if (tf_[l]) {  // P along col_shard, dP along row_shard
+      grow(lay.col, static_cast<size_t>(s.a_cols) * pad4(s.w_cols));
+      grow(lay.row, static_cast<size_t>(s.a_cols) * pad4(s.w_cols));
+    }
   }
   for (int a = 0; a < 3; ++a)
     if (need[a] && grid_.extent(a) > 1) comms_.lsa(a, need[a]);

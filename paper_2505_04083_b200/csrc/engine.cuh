@@ -108,6 +108,9 @@ class Engine {
  private:
   void forward_layer(int l, bool fault);
   void backward_layer(int l);
+  void forward_layer_tf(int l);
+  void backward_layer_tf(int l);
+  std::vector<char> tf_;  // transform-first layers (see engine.cu)
   void loss();
   // Forward row blocks of a plane's shard. The result is invariant to the
   // block count (test_engine.cpp:190-213), so `block_count = 0` is free to
@@ -157,6 +160,7 @@ class Engine {
   bool df_masked_ = false;             // df_prev_ already carries relu_backward
   std::vector<DMat> wfull_, dwp_;      // gathered W and dW partial per layer
   DMat dh_, df_, df_prev_;             // backward workspaces (max shapes)
+  DMat tfbuf_;                         // transform-first: P forward, dP backward
   DMat logits_, dl_, stage_;
   i64 stage_rows_ = 0;
   DevBuf<u32> labels_;
