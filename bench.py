@@ -318,6 +318,15 @@ def run_reference(args):
     return 0
 
 
+def transform_first_layers(grid, dims, mode):
+    from paper_2505_04083_b200 import layout
+    if mode != "fast" or os.environ.get("PK_TRANSFORM_FIRST", "1") == "0":
+        return []
+    lays = layout.plan_layouts(len(dims) - 1)
+    return [l for l, lay in enumerate(lays)
+            if grid.extent(lay.inner) == 1 and dims[l + 1] < dims[l]]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -510,6 +519,9 @@ def run_ours(args):
             "dtype": "f32", "data": "synthetic",
             "config": config_dict(cfg, grid, n, nnz),
             "gemm_mode": args.mode, "dataset_build_s": round(t_build, 2),
+            # layers run as Q = A (F W) (engine.cu, transform-first: inner
+            # axis one rank and D_out < D_in, FAST only)
+            "transform_first_layers": transform_first_layers(gridc, dims, args.mode),
             "roofline": {"bound": "hbm", "kernel": "spmm (all launches of the epoch)",
                          "basis": "dram" if dram is not None else "compulsory",
                          "achieved": achieved, "peak": peak, "peak_kind": peak_kind,

@@ -325,7 +325,10 @@ void Engine::alloc_params() {
   dh_.buf.alloc(max_dh);
   df_.buf.alloc(max_df);
   df_prev_.buf.alloc(max_df);
-  if (max_tf) tfbuf_.buf.alloc(max_tf);  // P = F W forward, dP = A^T dQ backward
+  if (max_tf) {  // P = F W forward, dP = A^T dQ backward; padding stays 0
+    tfbuf_.buf.alloc(max_tf);
+    PK_CUDA(cudaMemset(tfbuf_.buf.p, 0, tfbuf_.buf.n * sizeof(float)));
+  }
   PK_CUDA(cudaMemset(dh_.buf.p, 0, dh_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_.buf.p, 0, df_.buf.n * sizeof(float)));
   PK_CUDA(cudaMemset(df_prev_.buf.p, 0, df_prev_.buf.n * sizeof(float)));
@@ -927,8 +930,10 @@ void Engine::forward_layer_tf(int l) {
   const bool hidden = l + 1 < L_;
   DMat& qout = hidden ? fout_[l] : q_[l];
   clock_.begin(0, st_);
-  spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, s.w_cols, qout.p(), qout.ld,
-           st_);
+  // the SpMM runs over the padded width (47 -> 48): 16-B gathers instead of
+  // 4-B ones; P's padding columns are zero, so the extra output column is
+  // exactly +0 — the padding the output keeps anyway
+  spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, ldp, qout.p(), qout.ld, st_);
   spmm_flops_ += 2 * sh.a.nnz * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.a.rows, sh.a.nnz, s.w_cols);
   spmm_cbytes_ += spmm_compulsory_bytes(sh.a.rows, sh.a.nnz, sh.a.cols, s.w_cols);
@@ -963,7 +968,8 @@ void Engine::backward_layer_tf(int l) {
   LsaGroup* lsa_r = comms_.lsa(lay.row);
   float* dpp = lsa_r ? lsa_r->scratch() : tfbuf_.p();
   clock_.begin(5, st_);
-  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, s.w_cols, dpp, ldp, st_);
+  // padded width as in the forward: dQ's padding columns are zero
+  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, ldp, dpp, ldp, st_);
   clock_.end(st_);
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.w_cols);

@@ -309,17 +309,22 @@ class RankEngine:
         return out
 
     def prepare_result_buffers(self):
-        """Allocate (pin) the host buffers of this rank's TrainResult share on
-        a helper thread while the GPU trains: page-locking ~1 GB of fresh
-        host memory takes longer than the copy itself, and it does not need
-        to wait for the device."""
+        """Allocate the host buffers of this rank's TrainResult share on a
+        helper thread while the GPU trains, and fault their pages in: first
+        touch of ~1 GB of fresh host memory costs more than the copy. (Not
+        pinned: cudaHostAlloc holds the driver lock and stalls the training
+        thread's launches for as long as it runs.)"""
         import threading
         shapes = self._result_shapes()
         self._result_bufs = None
 
         def alloc():
-            self._result_bufs = [torch.empty((r, c), dtype=torch.float32, pin_memory=True)
-                                 for _, _, r, c in shapes]
+            bufs = []
+            for _, _, r, c in shapes:
+                h = np.empty((r, c), np.float32)
+                h.fill(0)
+                bufs.append(torch.from_numpy(h))
+            self._result_bufs = bufs
         self._result_thread = threading.Thread(target=alloc, daemon=True)
         self._result_thread.start()
 
