@@ -564,6 +564,19 @@ int Engine::forward_blocks(i64 rows, const Layout& lay) const {
   return static_cast<int>(std::max<i64>(1, std::min<i64>(4, rows / 65536)));
 }
 
+// The producer-fused form of an axis' ordered reduction (lsa.cuh
+// slot_map / reduce_slots): FAST mode (plans without hub CTAs, the
+// tensor-core GEMM epilogue) with peer-memory groups. PK_FUSED_REDUCE=0
+// keeps the producer -> reduction kernels.
+LsaGroup* Engine::fused(int axis) const {
+  static const bool on = [] {
+    const char* e = std::getenv("PK_FUSED_REDUCE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || cfg_.mode != PK_MODE_FAST || spmm_fast_segment() == 0) return nullptr;
+  return comms_.lsa(axis);
+}
+
 // ---------------------------------------------------------------------------
 // forward_layer (engine.hpp:158-206)
 
@@ -605,7 +618,12 @@ void Engine::forward_layer(int l, bool fault) {
   DMat& h = h_[l];
   // blocked aggregation (engine.hpp:175-192): SpMM row block b, then its
   // all-reduce along inner — overlapped with block b+1's SpMM
-  const int blocks = forward_blocks(sh.a.rows, lay);
+  // fused: the SpMM stores each row straight into its owner's slot (one
+  // block — the transfer already overlaps the SpMM)
+  LsaGroup* fu_h = fault ? nullptr : fused(lay.inner);
+  RowMap map_h;
+  if (fu_h) map_h = fu_h->slot_map(sh.a.rows, h.ld);
+  const int blocks = fu_h ? 1 : forward_blocks(sh.a.rows, lay);
   const std::vector<u64>& bnnz = sh.blocks_nnz(blocks, st_);
   int b = 0;
   // partials go to the axis' symmetric scratch when the ordered peer-memory
@@ -617,7 +635,8 @@ void Engine::forward_layer(int l, bool fault) {
       sh.a.rows, blocks,
       [&](i64 r0, i64 r1) {
         clock_.begin(0, st_);
-        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, hpart + r0 * h.ld, h.ld, st_);
+        spmm_run(sh.plan_a, view(sh.a), r0, r1, f, ldf, s.f_cols, hpart + r0 * h.ld, h.ld, st_,
+                 nullptr, 0, fu_h ? &map_h : nullptr);
         spmm_flops_ += 2 * bnnz[b] * static_cast<u64>(s.f_cols);
         spmm_bytes_ += spmm_alg_bytes(r1 - r0, bnnz[b], s.f_cols);
         spmm_cbytes_ += spmm_compulsory_bytes(r1 - r0, bnnz[b], b == 0 ? sh.a.cols : 0, s.f_cols);
@@ -626,7 +645,10 @@ void Engine::forward_layer(int l, bool fault) {
       },
       [&](i64 r0, i64 r1) {
         if (fault) return;
-        if (lsa_h) {
+        if (fu_h) {
+          fu_h->reduce_slots(sh.a.rows, s.f_cols, h.ld, h.p(), h.ld, cs_);
+          comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.f_cols * 4);
+        } else if (lsa_h) {
           lsa_h->all_reduce(r0, r1, s.f_cols, h.ld, h.p(), r0, h.ld, cs_);
           comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.f_cols * 4);
         } else {
@@ -652,17 +674,24 @@ void Engine::forward_layer(int l, bool fault) {
   DMat& qout = hidden && (col_single || lsa_q || solo) ? fout_[l] : q_[l];
   if (qout.buf.p == nullptr) qout.alloc(s.q_rows, s.q_cols, st_);
   float* qpart = lsa_q ? lsa_q->scratch() : qout.p();
+  // fused when the epilogue stores each row once (k <= 512: one TMEM segment)
+  LsaGroup* fu_q = s.h_cols <= 512 ? fused(lay.col) : nullptr;
+  RowMap map_q;
+  if (fu_q) map_q = fu_q->slot_map(s.h_rows, qout.ld);
   pipelined(
-      s.h_rows, comm_chunks(s.h_rows, lay.col),
+      s.h_rows, fu_q ? 1 : comm_chunks(s.h_rows, lay.col),
       [&](i64 r0, i64 r1) {
         clock_.begin(1, st_);
         gemm_launch(false, false, r1 - r0, s.w_cols, s.h_cols, h.p() + r0 * h.ld, h.ld,
                     wfull_[l].p(), wfull_[l].ld, qpart + r0 * qout.ld, qout.ld, cfg_.mode, st_,
-                    hidden && col_single);
+                    hidden && col_single, fu_q ? &map_q : nullptr);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        if (lsa_q) {
+        if (fu_q) {
+          fu_q->reduce_slots(s.h_rows, s.q_cols, qout.ld, qout.p(), qout.ld, cs_, hidden);
+          comms_.count(kAllReduce, lay.col, (r1 - r0) * s.q_cols * 4);
+        } else if (lsa_q) {
           lsa_q->all_reduce(r0, r1, s.q_cols, qout.ld, qout.p(), r0, qout.ld, cs_, hidden);
           comms_.count(kAllReduce, lay.col, (r1 - r0) * s.q_cols * 4);
         } else {
@@ -798,16 +827,23 @@ void Engine::backward_layer(int l) {
   const i64 lddh = pad4(s.h_cols);
   LsaGroup* lsa_dh = comms_.lsa(lay.inner);
   float* dhpart = lsa_dh ? lsa_dh->scratch() : dh_.p();
+  LsaGroup* fu_dh = s.q_cols <= 512 ? fused(lay.inner) : nullptr;
+  RowMap map_dh;
+  if (fu_dh) map_dh = fu_dh->slot_map(s.q_rows, lddh);
   pipelined(
-      s.q_rows, comm_chunks(s.q_rows, lay.inner),
+      s.q_rows, fu_dh ? 1 : comm_chunks(s.q_rows, lay.inner),
       [&](i64 r0, i64 r1) {
         clock_.begin(2, st_);
         gemm_launch(false, true, r1 - r0, s.h_cols, s.q_cols, dq + r0 * lddq, lddq,
-                    wfull_[l].p(), wfull_[l].ld, dhpart + r0 * lddh, lddh, cfg_.mode, st_);
+                    wfull_[l].p(), wfull_[l].ld, dhpart + r0 * lddh, lddh, cfg_.mode, st_, false,
+                    fu_dh ? &map_dh : nullptr);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        if (lsa_dh) {
+        if (fu_dh) {
+          fu_dh->reduce_slots(s.q_rows, s.h_cols, lddh, dh_.p(), lddh, cs_);
+          comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
+        } else if (lsa_dh) {
           lsa_dh->all_reduce(r0, r1, s.h_cols, lddh, dh_.p(), r0, lddh, cs_);
           comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
         } else {
@@ -836,17 +872,30 @@ void Engine::backward_layer(int l) {
   const DMat* act = l > 0 && fuse > 0 ? &fout_[l - 1] : nullptr;
   const bool mask_spmm = act && gr == 1 && fuse >= 2;
   const bool mask_reduce = act && gr > 1 && lsa_df;
+  LsaGroup* fu_df = fused(lay.row);
+  RowMap map_df;
+  if (fu_df) map_df = fu_df->slot_map(sh.at.rows, lddf);
   pipelined(
-      sh.at.rows, comm_chunks(sh.at.rows, lay.row),
+      sh.at.rows, fu_df ? 1 : comm_chunks(sh.at.rows, lay.row),
       [&](i64 r0, i64 r1) {
         clock_.begin(5, st_);
         spmm_run(sh.plan_at, view(sh.at), r0, r1, dh_.p(), lddh, s.f_cols, dfpart + r0 * lddf,
                  lddf, st_, mask_spmm ? act->p() + r0 * act->ld : nullptr,
-                 mask_spmm ? act->ld : 0);
+                 mask_spmm ? act->ld : 0, fu_df ? &map_df : nullptr);
         clock_.end(st_);
       },
       [&](i64 r0, i64 r1) {
-        if (lsa_df) {
+        if (fu_df) {
+          if (l == 0) {  // reduce-scatter: the owner keeps its own rows only
+            fu_df->reduce_slots(sh.at.rows, s.f_cols, lddf, df0_.p(), df0_.ld, cs_, false,
+                                nullptr, 0, true);
+            comms_.count(kReduceScatter, lay.row, (r1 - r0) * s.f_cols * 4);
+          } else {
+            fu_df->reduce_slots(sh.at.rows, s.f_cols, lddf, df_.p(), lddf, cs_, false,
+                                mask_reduce ? act->p() : nullptr, mask_reduce ? act->ld : 0);
+            comms_.count(kAllReduce, lay.row, (r1 - r0) * s.f_cols * 4);
+          }
+        } else if (lsa_df) {
           if (l == 0) {  // reduce-scatter: this member sums only its own rows
             const i64 a = std::max(r0, own0), b = std::min(r1, own1);
             lsa_df->reduce(a, std::max(a, b), s.f_cols, lddf, df0_.p(), a - own0, df0_.ld, cs_);
@@ -910,14 +959,20 @@ void Engine::forward_layer_tf(int l) {
   const i64 ldp = pad4(s.w_cols);
   LsaGroup* lsa_p = comms_.lsa(lay.col);
   float* ppart = lsa_p ? lsa_p->scratch() : tfbuf_.p();
+  LsaGroup* fu_p = s.f_cols <= 512 ? fused(lay.col) : nullptr;
+  RowMap map_p;
+  if (fu_p) map_p = fu_p->slot_map(s.f_rows, ldp);
   clock_.begin(1, st_);
   gemm_launch(false, false, s.f_rows, s.w_cols, s.f_cols, f, ldf, wfull_[l].p(), wfull_[l].ld,
-              ppart, ldp, cfg_.mode, st_);
+              ppart, ldp, cfg_.mode, st_, false, fu_p ? &map_p : nullptr);
   clock_.end(st_);
   gemm_flops_ += 2 * static_cast<u64>(s.f_rows) * s.w_cols * s.f_cols;
   if (comms_.size(lay.col) > 1) {
     on_comm([&](cudaStream_t cs) {
-      if (lsa_p) {
+      if (fu_p) {
+        fu_p->reduce_slots(s.f_rows, s.w_cols, ldp, tfbuf_.p(), ldp, cs);
+        comms_.count(kAllReduce, lay.col, s.f_rows * s.w_cols * 4);
+      } else if (lsa_p) {
         lsa_p->all_reduce(0, s.f_rows, s.w_cols, ldp, tfbuf_.p(), 0, ldp, cs);
         comms_.count(kAllReduce, lay.col, s.f_rows * s.w_cols * 4);
       } else {
@@ -968,8 +1023,12 @@ void Engine::backward_layer_tf(int l) {
   const i64 ldp = pad4(s.w_cols);
   LsaGroup* lsa_r = comms_.lsa(lay.row);
   float* dpp = lsa_r ? lsa_r->scratch() : tfbuf_.p();
+  LsaGroup* fu_r = fused(lay.row);
+  RowMap map_r;
+  if (fu_r) map_r = fu_r->slot_map(sh.at.rows, ldp);
   clock_.begin(5, st_);
-  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, s.w_cols, dpp, ldp, st_);
+  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, s.w_cols, dpp, ldp, st_, nullptr, 0,
+           fu_r ? &map_r : nullptr);
   clock_.end(st_);
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.w_cols);
@@ -977,7 +1036,10 @@ void Engine::backward_layer_tf(int l) {
   const int gr = grid_.extent(lay.row), pr = c_.along(lay.row);
   if (gr > 1) {
     on_comm([&](cudaStream_t cs) {
-      if (lsa_r) {
+      if (fu_r) {
+        fu_r->reduce_slots(s.a_cols, s.w_cols, ldp, tfbuf_.p(), ldp, cs);
+        comms_.count(kAllReduce, lay.row, s.a_cols * s.w_cols * 4);
+      } else if (lsa_r) {
         lsa_r->all_reduce(0, s.a_cols, s.w_cols, ldp, tfbuf_.p(), 0, ldp, cs);
         comms_.count(kAllReduce, lay.row, s.a_cols * s.w_cols * 4);
       } else {
@@ -1036,7 +1098,12 @@ void Engine::setup_lsa() {
     }
   }
   for (int a = 0; a < 3; ++a)
-    if (need[a] && grid_.extent(a) > 1) comms_.lsa(a, need[a]);
+    if (need[a] && grid_.extent(a) > 1) {
+      // the fused form needs the owner slots (g x ceil(rows / g) rows) and a
+      // result region of all rows: ~2x the partial, plus the ceil slack
+      const size_t e = cfg_.mode == PK_MODE_FAST ? 2 * need[a] + (size_t{1} << 16) : need[a];
+      comms_.lsa(a, e);
+    }
   lsa_ready_ = true;
 }
 

@@ -127,6 +127,7 @@ class Engine {
   int comm_chunks(i64 rows, int axis) const;
   void on_comm(const std::function<void(cudaStream_t)>& f);
   void setup_lsa();
+  LsaGroup* fused(int axis) const;
   bool lsa_ready_ = false;
 
   pk_engine_config cfg_;

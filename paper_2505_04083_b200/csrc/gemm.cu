@@ -213,8 +213,15 @@ void gemm_simt_dispatch(i64 m, i64 n, i64 k, const float* a, i64 lda, const floa
 }  // namespace
 
 void gemm_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda, const float* b,
-                 i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st, bool relu) {
+                 i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st, bool relu,
+                 const RowMap* map) {
   if (m == 0 || n == 0) return;
+  if (map) {  // a reduction fused into the epilogue: tensor-core path only
+    check(mode == PK_MODE_FAST && k > 0 &&
+              gemm_tc_launch(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, st, relu, map),
+          "gemm: mapped output rows need the tensor-core path");
+    return;
+  }
   if (k == 0) {  // reference writes acc = 0 (kernels.hpp:84-89); relu(0) = 0
     zero_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(c, m, n, ldc);
     PK_LAUNCH("gemm zero fill");

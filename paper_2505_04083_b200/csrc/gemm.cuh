@@ -9,14 +9,15 @@ namespace pk {
 // (tb ? n x k : k x n). mode: PK_MODE_PARITY (bit-exact) or PK_MODE_FAST.
 // relu: store relu(C) instead (relu_forward, kernels.hpp:94-101), fused into
 // the tensor-core epilogue, else a separate in-place pass.
+// map (FAST only): output row r goes to map->row(c, ldc, r) (RowMap).
 void gemm_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
                  const float* b, i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st,
-                 bool relu = false);
+                 bool relu = false, const RowMap* map = nullptr);
 
 // Tensor-core (tcgen05, 3xTF32) path; returns false when the shape or
 // alignment is not covered and the caller should fall back.
 bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
                     const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st,
-                    bool relu = false);
+                    bool relu = false, const RowMap* map = nullptr);
 
 }  // namespace pk

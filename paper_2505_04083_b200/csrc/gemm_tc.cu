@@ -465,6 +465,7 @@ struct TcParams {
   i64 ldc;
   i64 split_stride; // elements between split partials
   int relu;         // 1: the final value is stored as relu(v) (v > 0 ? v : 0)
+  RowMap map;       // output row placement (g == 0: c + row * ldc)
 };
 
 template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE>
@@ -1057,7 +1058,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             tmem_ld8(taddr + static_cast<unsigned>(c0), v);
           }
           if (gm < p.m) {
-            float* dst = out + gm * p.ldc + n0 + c0;
+            float* dst = p.map.row(out, p.ldc, gm) + n0 + c0;
             const i64 left = p.n - (n0 + c0);
             if (vec_out && left >= CH) {
               float4* d4 = reinterpret_cast<float4*>(dst);
@@ -1339,9 +1340,14 @@ bool aligned16(const void* p, i64 ld) {
 }  // namespace
 
 bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
-                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st, bool relu) {
+                    const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st, bool relu,
+                    const RowMap* map) {
   if (ta && tb) return false;  // not used by the layer
   TcParams p{};
+  if (map) {
+    p.map = *map;
+    c = map->base[0];  // alignment of the slots (all 16-B aligned)
+  }
   p.m = m, p.n = n, p.k = k;
   p.relu = relu ? 1 : 0;
   // A: NN/NT -> K-major (storage m x k); TN -> MN-major (storage k x m)
@@ -1378,6 +1384,7 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
   p.k_chunk = ((k + splits - 1) / splits + kBK - 1) / kBK * kBK;
   splits = static_cast<int>((k + p.k_chunk - 1) / p.k_chunk);
   p.splits = splits;
+  check(!map || splits == 1, "gemm: mapped output rows need an unsplit k");
   static thread_local DevBuf<float> part;
   if (splits > 1) {
     const i64 ldp = static_cast<i64>(p.n_tiles) * bn;

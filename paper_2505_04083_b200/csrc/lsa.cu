@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "layout.h"
 #include "lsa.cuh"
 
 namespace pk {
@@ -249,6 +250,96 @@ __global__ void __launch_bounds__(256) lsa_allreduce_kernel(LsaPeers P, i64 r0, 
   }
 }
 
+// Producer-fused reduction (reduce_slots): member i's scratch holds g slots
+// of S rows (slot j = member j's partial of chunk i's rows) followed by a
+// result region indexed by global row. Phase 1 sums the slots of the own
+// chunk in coordinate order, stores out and (unless scatter) pushes to every
+// peer's result region; phase 2 copies the other chunks' results. Element e
+// of a chunk is handled by the same CTA slot in both phases on every member.
+template <int VEC, int G>
+__global__ void __launch_bounds__(256) lsa_slots_kernel(LsaPeers P, i64 rows, i64 cols, i64 ld,
+                                                        i64 S, float* __restrict__ out,
+                                                        i64 ld_o, int relu,
+                                                        const float* __restrict__ mask, i64 ldm,
+                                                        int scatter, unsigned epoch) {
+  using V = typename std::conditional<VEC == 4, float4, float>::type;
+  barrier(P, blockIdx.x, epoch);
+  const i64 cv = cols / VEC;
+  const i64 stride = static_cast<i64>(gridDim.x) * blockDim.x;
+  const i64 base_rows = rows / P.g, rem = rows % P.g;
+  auto chunk0 = [&](int k) { return k * base_rows + (k < rem ? k : rem); };
+  const i64 a = chunk0(P.me), b = chunk0(P.me + 1);
+  const float* mine = P.data[P.me];
+  const i64 res = static_cast<i64>(P.g) * S * ld;  // result region offset
+  {
+    const i64 total = (b - a) * cv;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+      const i64 lr = i / cv, c = (i % cv) * VEC;
+      V x[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (j < P.g) x[j] = __ldcg(reinterpret_cast<const V*>(mine + (j * S + lr) * ld + c));
+      V acc = x[0];
+#pragma unroll
+      for (int j = 1; j < G; ++j) {
+        if (j >= P.g) break;
+        if constexpr (VEC == 4) {
+          acc.x = __fadd_rn(acc.x, x[j].x), acc.y = __fadd_rn(acc.y, x[j].y);
+          acc.z = __fadd_rn(acc.z, x[j].z), acc.w = __fadd_rn(acc.w, x[j].w);
+        } else {
+          acc = __fadd_rn(acc, x[j]);
+        }
+      }
+      const i64 r = a + lr;
+      if (relu) {
+        if constexpr (VEC == 4) {
+          acc.x = acc.x > 0.f ? acc.x : 0.f, acc.y = acc.y > 0.f ? acc.y : 0.f;
+          acc.z = acc.z > 0.f ? acc.z : 0.f, acc.w = acc.w > 0.f ? acc.w : 0.f;
+        } else {
+          acc = acc > 0.f ? acc : 0.f;
+        }
+      }
+      if (mask) {
+        const V m = *reinterpret_cast<const V*>(mask + r * ldm + c);
+        if constexpr (VEC == 4) {
+          acc.x = m.x > 0.f ? acc.x : 0.f, acc.y = m.y > 0.f ? acc.y : 0.f;
+          acc.z = m.z > 0.f ? acc.z : 0.f, acc.w = m.w > 0.f ? acc.w : 0.f;
+        } else {
+          acc = m > 0.f ? acc : 0.f;
+        }
+      }
+      // scatter (a reduce-scatter): out holds only the own chunk's rows
+      *reinterpret_cast<V*>(out + (scatter ? lr : r) * ld_o + c) = acc;
+      if (!scatter) {
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (j < P.g && j != P.me)
+            __stcg(reinterpret_cast<V*>(const_cast<float*>(P.data[j]) + res + r * ld + c), acc);
+      }
+    }
+  }
+  if (scatter) {
+    barrier(P, blockIdx.x, epoch + 1);  // slots may be rewritten only after all reads
+    return;
+  }
+  __threadfence_system();
+  barrier(P, blockIdx.x, epoch + 1);
+  // (a trailing barrier follows phase 2: the next producer writes into the
+  // peers' scratch without a barrier of its own, and a later reduction's
+  // slots may overlap this one's result region)
+  for (int k = 0; k < P.g; ++k) {
+    if (k == P.me) continue;
+    const i64 ka = chunk0(k), kb = chunk0(k + 1);
+    const i64 total = (kb - ka) * cv;
+    for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+      const i64 r = ka + i / cv, c = (i % cv) * VEC;
+      *reinterpret_cast<V*>(out + r * ld_o + c) =
+          __ldcg(reinterpret_cast<const V*>(mine + res + r * ld + c));
+    }
+  }
+  barrier(P, blockIdx.x, epoch + 2);
+}
+
 __global__ void lsa_peer_ptrs_kernel(ncclWindow_t win, int g, void** out) {
   const int j = threadIdx.x;
   if (j < g) out[j] = ncclGetLsaPointer(win, 0, j);
@@ -409,6 +500,57 @@ void LsaGroup::all_reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 ou
     else launch(V1{}, std::integral_constant<int, 8>{});
   }
   PK_LAUNCH("lsa ring all-reduce");
+}
+
+RowMap LsaGroup::slot_map(i64 rows, i64 ld) const {
+  RowMap m;
+  m.g = g_;
+  const i64 S = (rows + g_ - 1) / g_;
+  for (int k = 0; k <= g_; ++k) m.start[k] = chunk_start(rows, g_, k);
+  for (int k = 0; k < g_; ++k)
+    m.base[k] = const_cast<float*>(peers_.data[k]) + static_cast<i64>(me_) * S * ld;
+  return m;
+}
+
+i64 LsaGroup::slot_scratch_elems(i64 rows, i64 ld) const {
+  const i64 S = (rows + g_ - 1) / g_;
+  return (static_cast<i64>(g_) * S + rows) * ld;
+}
+
+void LsaGroup::reduce_slots(i64 rows, i64 cols, i64 ld, float* out, i64 ld_o, cudaStream_t st,
+                            bool relu, const float* mask, i64 ldm, bool scatter) {
+  check(ready_, "lsa reduce_slots: group not initialised");
+  check(slot_scratch_elems(rows, ld) * sizeof(float) <= scratch_bytes_,
+        "lsa reduce_slots: slots exceed the symmetric scratch");
+  const unsigned epoch = epoch_;
+  epoch_ += 3;
+  const i64 S = (rows + g_ - 1) / g_;
+  const bool v4 = cols % 4 == 0 && ld % 4 == 0 && ld_o % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                  (!mask || (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0));
+  static const int ctas = [] {
+    const char* e = std::getenv("PK_LSA_CTAS");
+    const int v = e ? std::atoi(e) : kLsaBlocks / 2;
+    return std::max(1, std::min(v, kLsaBlocks));
+  }();
+  auto launch = [&](auto vec_tag, auto g_tag) {
+    constexpr int V = decltype(vec_tag)::value, Gm = decltype(g_tag)::value;
+    lsa_slots_kernel<V, Gm><<<ctas, 256, 0, st>>>(peers_, rows, cols, ld, S, out, ld_o,
+                                                 relu ? 1 : 0, mask, ldm, scatter ? 1 : 0, epoch);
+  };
+  using V4 = std::integral_constant<int, 4>;
+  using V1 = std::integral_constant<int, 1>;
+  if (g_ <= 2) {
+    if (v4) launch(V4{}, std::integral_constant<int, 2>{});
+    else launch(V1{}, std::integral_constant<int, 2>{});
+  } else if (g_ <= 4) {
+    if (v4) launch(V4{}, std::integral_constant<int, 4>{});
+    else launch(V1{}, std::integral_constant<int, 4>{});
+  } else {
+    if (v4) launch(V4{}, std::integral_constant<int, 8>{});
+    else launch(V1{}, std::integral_constant<int, 8>{});
+  }
+  PK_LAUNCH("lsa slot reduce");
 }
 
 bool lsa_timed_out() {

@@ -45,6 +45,22 @@ class LsaGroup {
   void all_reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0, i64 ld_o,
                   cudaStream_t st, bool relu = false, const float* mask = nullptr, i64 ldm = 0);
 
+  // Producer-fused reduction over rows [0, rows) (ld floats per row). The
+  // producer (SpMM / GEMM epilogue) stores its partial of row r straight into
+  // the scratch of the member owning r's ceil-split chunk, at this member's
+  // slot: slot_map() is that RowMap. reduce_slots() then sums each owner's
+  // slots locally in coordinate order (the reference's combine, bit for
+  // bit), applies relu / mask, stores the owner's rows and — unless only
+  // this member's rows are wanted (scatter: a reduce-scatter) — pushes them
+  // to every peer, which copies the other chunks out of its own HBM. NVLink
+  // then carries the partials while the producer runs and only the reduced
+  // chunks afterwards.
+  RowMap slot_map(i64 rows, i64 ld) const;
+  i64 slot_scratch_elems(i64 rows, i64 ld) const;  // what slot_map + results need
+  void reduce_slots(i64 rows, i64 cols, i64 ld, float* out, i64 ld_o, cudaStream_t st,
+                    bool relu = false, const float* mask = nullptr, i64 ldm = 0,
+                    bool scatter = false);
+
  private:
   int g_ = 0, me_ = 0;
   bool ready_ = false;

@@ -74,6 +74,29 @@ int guard(F&& f) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Where a producer kernel stores output row lr (0-based in its output): its
+// own buffer (g == 0: y + lr * ld), or — for a reduction fused into the
+// producer — the slot this rank owns in the symmetric scratch of the member
+// that owns the row's chunk: base[k] + (lr - start[k]) * ld for the k with
+// start[k] <= lr < start[k + 1] (lsa.cu; remote rows travel over NVLink as
+// the producer writes them).
+constexpr int kMaxRowOwners = 8;
+struct RowMap {
+  float* base[kMaxRowOwners] = {};
+  i64 start[kMaxRowOwners + 1] = {};
+  int g = 0;
+#ifdef __CUDACC__
+  __device__ __forceinline__ float* row(float* y, i64 ld, i64 lr) const {
+    if (g == 0) return y + lr * ld;
+    int k = 0;
+#pragma unroll
+    for (int j = 1; j < kMaxRowOwners; ++j)
+      if (j < g && lr >= start[j]) k = j;
+    return base[k] + (lr - start[k]) * ld;
+  }
+#endif
+};
+
 inline std::string shape(i64 r, i64 c) {
   return std::to_string(r) + "x" + std::to_string(c);
 }

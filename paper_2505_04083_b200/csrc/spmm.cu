@@ -204,6 +204,7 @@ struct ListArgs {
   i64 xrows = 0;                // rows of x the nonzeros gather from
   const float* mask = nullptr;  // optional relu_backward mask, rows like y
   i64 ldm = 0;
+  RowMap map;                   // where output rows go (g == 0: y)
 };
 
 // chunk bounds over list entries [i0, i1), ~equal nonzeros per chunk
@@ -330,7 +331,7 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
       const u32 row = __shfl_sync(gmask, rid, rn, LANES);
       const bool seg = (row & 0x80000000u) != 0;
       float* yrow = seg ? a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp
-                        : a.y + (static_cast<i64>(row) - a.r0) * a.ldy;
+                        : a.map.row(a.y, a.ldy, static_cast<i64>(row) - a.r0);
       yrow += (vbase + lane) * VEC;
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
@@ -431,7 +432,7 @@ __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* 
                                         const u32* __restrict__ nseg, i64 nh, i64 r0,
                                         const float* __restrict__ part, i64 ldp, float* y,
                                         i64 ldy, i64 d, const float* __restrict__ mask,
-                                        i64 ldm) {
+                                        i64 ldm, RowMap map) {
   const i64 total = nh * d;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<i64>(gridDim.x) * blockDim.x) {
@@ -440,17 +441,17 @@ __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* 
     float acc = part[s0 * ldp + c];
     for (u32 k = 1; k < nseg[h]; ++k) acc = __fadd_rn(acc, part[(s0 + k) * ldp + c]);
     const i64 rr = static_cast<i64>(hub[h]) - r0;
-    y[rr * ldy + c] = mask ? keep(acc, mask[rr * ldm + c]) : acc;
+    map.row(y, ldy, rr)[c] = mask ? keep(acc, mask[rr * ldm + c]) : acc;
   }
 }
 
 // y rows listed in `rows` (absolute ids) := 0 over d columns
 __global__ void zero_rows_kernel(const u32* __restrict__ rows, i64 n, i64 r0, float* y, i64 ldy,
-                                 i64 d) {
+                                 i64 d, RowMap map) {
   const i64 total = n * d;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<i64>(gridDim.x) * blockDim.x)
-    y[(static_cast<i64>(rows[i / d]) - r0) * ldy + i % d] = 0.f;
+    map.row(y, ldy, static_cast<i64>(rows[i / d]) - r0)[i % d] = 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -1131,9 +1132,14 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 }
 
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
-              float* y, i64 ldy, cudaStream_t st, const float* mask, i64 ldm) {
+              float* y, i64 ldy, cudaStream_t st, const float* mask, i64 ldm,
+              const RowMap* map) {
   if (r1 <= r0 || d == 0) return;
   SpmmPlan::Range& rg = plan_range(plan, r0, r1, st);
+  const RowMap rmap = map ? *map : RowMap{};
+  check(rmap.g == 0 || plan.segment || rg.hubs == 0,
+        "spmm: mapped output rows need a FAST plan (no hub CTAs)");
+  if (rmap.g) y = rmap.base[0];  // alignment of the slots (all 16-B aligned)
   // 32-B slices for the list kernel; the exact plan's hub kernel stages
   // 16-B cp.async pieces, so a plan with hub CTAs stays at 16 B
   // the mask is read with y's vector width: it must share y's alignment
@@ -1166,7 +1172,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   if (rg.e1 > rg.e0) {
     const i64 ne = rg.e1 - rg.e0;
     zero_rows_kernel<<<blocks_for(ne * d), 256, 0, st>>>(plan.empty_rows.p + rg.e0, ne, r0, y,
-                                                         ldy, d);
+                                                         ldy, d, rmap);
     PK_LAUNCH("spmm zero rows");
   }
   if (rg.i1 > rg.i0) {
@@ -1175,6 +1181,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     la.x = x, la.ldx = ldx, la.y = y, la.ldy = ldy, la.r0 = r0, la.nvec = nvec;
     la.xrows = static_cast<i64>(a.cols);
     la.mask = mask, la.ldm = ldm;
+    la.map = rmap;
     if (plan.segment && plan.segments) {
       la.ldp = (d + 7) / 8 * 8;  // 32-B aligned rows for the widest slices
       plan.partial.ensure(plan.segments * la.ldp);
@@ -1193,7 +1200,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
     const i64 nh = rg.h1 - rg.h0;
     combine_segments_kernel<<<blocks_for(nh * d), 256, 0, st>>>(
         plan.hub_asc.p + rg.h0, plan.hub_seg0.p + rg.h0, plan.hub_nseg.p + rg.h0, nh, r0,
-        plan.partial.p, (d + 7) / 8 * 8, y, ldy, d, mask, ldm);
+        plan.partial.p, (d + 7) / 8 * 8, y, ldy, d, mask, ldm, rmap);
     PK_LAUNCH("spmm combine segments");
   }
   if (!plan.segment && rg.hubs > 0) PK_CUDA(cudaStreamWaitEvent(st, side.join, 0));

@@ -84,8 +84,11 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 // mask (optional, rows laid out like y, ld = ldm): every stored row value
 // becomes mask > 0 ? value : 0 — relu_backward (kernels.hpp:103-111) of the
 // previous layer fused into this SpMM^T's epilogue.
+// map (optional, FAST / hub-free plans only): output row lr = row - r0 goes
+// to map->row(y, ldy, lr) — a reduction's owner slots (RowMap).
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
-              float* y, i64 ldy, cudaStream_t st, const float* mask = nullptr, i64 ldm = 0);
+              float* y, i64 ldy, cudaStream_t st, const float* mask = nullptr, i64 ldm = 0,
+              const RowMap* map = nullptr);
 
 // Per-thread fork/join stream used to overlap hub CTAs with the list kernel.
 struct SideStream {

@@ -60,6 +60,19 @@ def test_two_gpu_fast_mode_and_blocks(cuda):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("grid", _grids(2) + (_grids(4) if torch.cuda.device_count() >= 4 else []))
+def test_fast_mode_every_grid(cuda, grid, fused):
+    """FAST mode (tcgen05 GEMMs, segmented plans, transform-first layers
+    where the inner axis is one rank) on every grid of 2 and 4 ranks, with
+    the producer-fused reductions (the SpMM / GEMM epilogues store each row
+    into its owner's peer-memory slot; csrc/lsa.cu reduce_slots) and
+    without: within 1e-4 of the reference's distributed pass and curve."""
+    n = 2 if grid in _grids(2) else 4
+    _run(n, "--grid", grid, "--mode", "fast", env={"PK_FUSED_REDUCE": fused})
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("grid", _grids(2))
 def test_two_gpu_nccl_reductions(cuda, grid):
     """The NCCL path the engine falls back to without peer-memory access
