@@ -24,11 +24,14 @@ def _port():
 
 
 def _run(nproc, *args, env=None):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           WORKER, *args]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                       env={**os.environ, **(env or {})})
+    for attempt in range(3):  # a probed free port can be taken before torchrun binds it
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1",
+               f"--master-port={_port()}", WORKER, *args]
+        p = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           env={**os.environ, **(env or {})})
+        if "EADDRINUSE" not in p.stderr + p.stdout:
+            break
     lines = [l for l in p.stdout.splitlines() if l.startswith("MPRESULT ")]
     assert lines, p.stdout[-3000:] + p.stderr[-3000:]
     rep = json.loads(lines[-1][len("MPRESULT "):])
