@@ -932,6 +932,14 @@ void Engine::backward_layer(int l) {
 // The fault hook (skip the aggregation all-reduce) has nothing to skip here:
 // inner is a single rank.
 
+int Engine::tf_vec() {
+  static const int v = [] {
+    const char* e = std::getenv("PK_TF_VEC");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 void Engine::forward_layer_tf(int l) {
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
@@ -985,11 +993,15 @@ void Engine::forward_layer_tf(int l) {
   const bool hidden = l + 1 < L_;
   DMat& qout = hidden ? fout_[l] : q_[l];
   clock_.begin(0, st_);
-  // over the exact width: the padded one (47 -> 48) takes the 16-lane group
-  // form, measured slower (2 x 5.6 vs 2 x 3.9 ms per C2 epoch) than 32
-  // lanes of 4-B gathers
-  spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, s.w_cols, qout.p(), qout.ld,
-           st_);
+  // Width of the narrow SpMMs (PK_TF_VEC): 0 = the exact width (47: 32
+  // lanes of 4-B gathers); v > 0 = the padded width (48; P's and dQ's
+  // padding columns are zero, so the extra output column is exactly +0)
+  // with gathers of at most v floats. The padded width at 16 B takes the
+  // 16-lane group form, measured slower (2 x 5.6 vs 2 x 3.9 ms per C2
+  // epoch).
+  const int tfv = tf_vec();
+  spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, tfv ? ldp : s.w_cols,
+           qout.p(), qout.ld, st_, nullptr, 0, nullptr, tfv ? tfv : 8);
   spmm_flops_ += 2 * sh.a.nnz * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.a.rows, sh.a.nnz, s.w_cols);
   spmm_cbytes_ += spmm_compulsory_bytes(sh.a.rows, sh.a.nnz, sh.a.cols, s.w_cols);
@@ -1027,8 +1039,9 @@ void Engine::backward_layer_tf(int l) {
   RowMap map_r;
   if (fu_r) map_r = fu_r->slot_map(sh.at.rows, ldp);
   clock_.begin(5, st_);
-  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, s.w_cols, dpp, ldp, st_, nullptr, 0,
-           fu_r ? &map_r : nullptr);
+  const int tfv = tf_vec();
+  spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, tfv ? ldp : s.w_cols, dpp, ldp, st_,
+           nullptr, 0, fu_r ? &map_r : nullptr, tfv ? tfv : 8);
   clock_.end(st_);
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.w_cols);

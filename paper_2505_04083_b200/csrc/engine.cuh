@@ -109,6 +109,7 @@ class Engine {
   void forward_layer(int l, bool fault);
   void backward_layer(int l);
   void forward_layer_tf(int l);
+  static int tf_vec();
   void backward_layer_tf(int l);
   std::vector<char> tf_;  // transform-first layers (see engine.cu)
   void loss();

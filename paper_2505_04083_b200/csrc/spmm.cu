@@ -1133,7 +1133,7 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
               float* y, i64 ldy, cudaStream_t st, const float* mask, i64 ldm,
-              const RowMap* map) {
+              const RowMap* map, int max_vec) {
   if (r1 <= r0 || d == 0) return;
   SpmmPlan::Range& rg = plan_range(plan, r0, r1, st);
   const RowMap rmap = map ? *map : RowMap{};
@@ -1144,6 +1144,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   // 16-B cp.async pieces, so a plan with hub CTAs stays at 16 B
   // the mask is read with y's vector width: it must share y's alignment
   int vec = pick_vec(x, ldx, y, ldy, d, plan.segment || rg.hubs == 0);
+  while (vec > max_vec) vec /= 2;
   if (mask)
     while (vec > 1 && (ldm % vec || (reinterpret_cast<uintptr_t>(mask) % (vec * 4)))) vec /= 2;
   const int nvec = static_cast<int>(d / vec);
