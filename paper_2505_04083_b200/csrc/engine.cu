@@ -566,14 +566,22 @@ int Engine::forward_blocks(i64 rows, const Layout& lay) const {
 
 // The producer-fused form of an axis' ordered reduction (lsa.cuh
 // slot_map / reduce_slots): FAST mode (plans without hub CTAs, the
-// tensor-core GEMM epilogue) with peer-memory groups. PK_FUSED_REDUCE=0
-// keeps the producer -> reduction kernels.
-LsaGroup* Engine::fused(int axis) const {
-  static const bool on = [] {
+// tensor-core GEMM epilogue) with peer-memory groups. PK_FUSED_REDUCE is a
+// mask of the producers that store into the owners' slots: 1 = SpMM, 2 =
+// GEMM. Default 1: the SpMM stores whole rows per lane group, while the
+// GEMM epilogue stores 32 B per thread per row — over NVLink that measured
+// 9.2 vs 2.5 ms for C2's forward GEMMs at 2 GPUs (profiles/r2_fused_ab_n4.log).
+int Engine::fused_mask() {
+  static const int m = [] {
     const char* e = std::getenv("PK_FUSED_REDUCE");
-    return !(e && e[0] == '0');
+    return e ? std::atoi(e) : 1;
   }();
-  if (!on || cfg_.mode != PK_MODE_FAST || spmm_fast_segment() == 0) return nullptr;
+  return m;
+}
+
+LsaGroup* Engine::fused(int axis, int producer) const {
+  if (!(fused_mask() & producer) || cfg_.mode != PK_MODE_FAST || spmm_fast_segment() == 0)
+    return nullptr;
   return comms_.lsa(axis);
 }
 
@@ -620,7 +628,7 @@ void Engine::forward_layer(int l, bool fault) {
   // all-reduce along inner — overlapped with block b+1's SpMM
   // fused: the SpMM stores each row straight into its owner's slot (one
   // block — the transfer already overlaps the SpMM)
-  LsaGroup* fu_h = fault ? nullptr : fused(lay.inner);
+  LsaGroup* fu_h = fault ? nullptr : fused(lay.inner, kFuseSpmm);
   RowMap map_h;
   if (fu_h) map_h = fu_h->slot_map(sh.a.rows, h.ld);
   const int blocks = fu_h ? 1 : forward_blocks(sh.a.rows, lay);
@@ -675,7 +683,7 @@ void Engine::forward_layer(int l, bool fault) {
   if (qout.buf.p == nullptr) qout.alloc(s.q_rows, s.q_cols, st_);
   float* qpart = lsa_q ? lsa_q->scratch() : qout.p();
   // fused when the epilogue stores each row once (k <= 512: one TMEM segment)
-  LsaGroup* fu_q = s.h_cols <= 512 ? fused(lay.col) : nullptr;
+  LsaGroup* fu_q = s.h_cols <= 512 ? fused(lay.col, kFuseGemm) : nullptr;
   RowMap map_q;
   if (fu_q) map_q = fu_q->slot_map(s.h_rows, qout.ld);
   pipelined(
@@ -827,7 +835,7 @@ void Engine::backward_layer(int l) {
   const i64 lddh = pad4(s.h_cols);
   LsaGroup* lsa_dh = comms_.lsa(lay.inner);
   float* dhpart = lsa_dh ? lsa_dh->scratch() : dh_.p();
-  LsaGroup* fu_dh = s.q_cols <= 512 ? fused(lay.inner) : nullptr;
+  LsaGroup* fu_dh = s.q_cols <= 512 ? fused(lay.inner, kFuseGemm) : nullptr;
   RowMap map_dh;
   if (fu_dh) map_dh = fu_dh->slot_map(s.q_rows, lddh);
   pipelined(
@@ -872,7 +880,7 @@ void Engine::backward_layer(int l) {
   const DMat* act = l > 0 && fuse > 0 ? &fout_[l - 1] : nullptr;
   const bool mask_spmm = act && gr == 1 && fuse >= 2;
   const bool mask_reduce = act && gr > 1 && lsa_df;
-  LsaGroup* fu_df = fused(lay.row);
+  LsaGroup* fu_df = fused(lay.row, kFuseSpmm);
   RowMap map_df;
   if (fu_df) map_df = fu_df->slot_map(sh.at.rows, lddf);
   pipelined(
@@ -967,7 +975,7 @@ void Engine::forward_layer_tf(int l) {
   const i64 ldp = pad4(s.w_cols);
   LsaGroup* lsa_p = comms_.lsa(lay.col);
   float* ppart = lsa_p ? lsa_p->scratch() : tfbuf_.p();
-  LsaGroup* fu_p = s.f_cols <= 512 ? fused(lay.col) : nullptr;
+  LsaGroup* fu_p = s.f_cols <= 512 ? fused(lay.col, kFuseGemm) : nullptr;
   RowMap map_p;
   if (fu_p) map_p = fu_p->slot_map(s.f_rows, ldp);
   clock_.begin(1, st_);
@@ -1035,7 +1043,7 @@ void Engine::backward_layer_tf(int l) {
   const i64 ldp = pad4(s.w_cols);
   LsaGroup* lsa_r = comms_.lsa(lay.row);
   float* dpp = lsa_r ? lsa_r->scratch() : tfbuf_.p();
-  LsaGroup* fu_r = fused(lay.row);
+  LsaGroup* fu_r = fused(lay.row, kFuseSpmm);
   RowMap map_r;
   if (fu_r) map_r = fu_r->slot_map(sh.at.rows, ldp);
   clock_.begin(5, st_);

@@ -128,7 +128,9 @@ class Engine {
   int comm_chunks(i64 rows, int axis) const;
   void on_comm(const std::function<void(cudaStream_t)>& f);
   void setup_lsa();
-  LsaGroup* fused(int axis) const;
+  static constexpr int kFuseSpmm = 1, kFuseGemm = 2;
+  LsaGroup* fused(int axis, int producer) const;
+  static int fused_mask();
   bool lsa_ready_ = false;
 
   pk_engine_config cfg_;

@@ -63,7 +63,7 @@ def test_two_gpu_fast_mode_and_blocks(cuda):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("fused", ["3", "0"])
 @pytest.mark.parametrize("grid", _grids(2) + (_grids(4) if torch.cuda.device_count() >= 4 else []))
 def test_fast_mode_every_grid(cuda, grid, fused):
     """FAST mode (tcgen05 GEMMs, segmented plans, transform-first layers
