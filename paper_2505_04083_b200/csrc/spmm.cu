@@ -276,12 +276,15 @@ constexpr int list_min_blocks() {
   if (NV == 2 || LANES < 32) return 3;
   return VEC == 8 ? (MASK ? PK_LIST_MINB8M : PK_LIST_MINB8) : PK_LIST_MINB1;
 }
-// MASK: the relu_backward epilogue variant (its own instantiation, so the
-// plain kernel's register allocation is untouched)
-template <int VEC, int LANES, int NV, int U, bool MASK>
-__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, LANES, NV, MASK>())
+// EPI: 0 plain; 1 the relu_backward epilogue (MASK); 2 mapped output rows
+// (a reduction's owner slots, RowMap). Each its own instantiation, so the
+// plain kernel's registers and code stay untouched (the row mapping inlined
+// at every row end grew the plain kernel by 20 % and cost 8 ms per C2 epoch).
+template <int VEC, int LANES, int NV, int U, int EPI>
+__global__ void __launch_bounds__(kThreads, list_min_blocks<VEC, LANES, NV, EPI == 1>())
 spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
                  int* __restrict__ counters) {
+  constexpr bool MASK = EPI == 1, MAPPED = EPI == 2;
   using V = typename Vec<VEC>::T;
   const int lane = threadIdx.x % LANES;
   const unsigned gmask =
@@ -330,8 +333,14 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
     auto row_done = [&]() {
       const u32 row = __shfl_sync(gmask, rid, rn, LANES);
       const bool seg = (row & 0x80000000u) != 0;
-      float* yrow = seg ? a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp
-                        : a.map.row(a.y, a.ldy, static_cast<i64>(row) - a.r0);
+      float* yrow;
+      if (seg) {
+        yrow = a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp;
+      } else if constexpr (MAPPED) {
+        yrow = a.map.row(a.y, a.ldy, static_cast<i64>(row) - a.r0);
+      } else {
+        yrow = a.y + (static_cast<i64>(row) - a.r0) * a.ldy;
+      }
       yrow += (vbase + lane) * VEC;
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
@@ -662,8 +671,10 @@ void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t
                                                     : (VEC == 2 ? PK_LIST_U2V : PK_LIST_U1)));
   constexpr int U = U0 < LANES ? U0 : LANES / 2;
   const bool masked = a.mask != nullptr;
-  auto kernel = masked ? spmm_list_kernel<VEC, LANES, NV, U, true>
-                       : spmm_list_kernel<VEC, LANES, NV, U, false>;
+  check(!(masked && a.map.g), "spmm: a mask epilogue with mapped rows is not supported");
+  auto kernel = masked   ? spmm_list_kernel<VEC, LANES, NV, U, 1>
+                : a.map.g ? spmm_list_kernel<VEC, LANES, NV, U, 2>
+                          : spmm_list_kernel<VEC, LANES, NV, U, 0>;
   const int slices = ceil_div(a.nvec, NV * LANES);
   // ~1-2K nonzeros per chunk at the products shape; never more chunks than
   // rows (PK_LIST_CHUNKS: chunks per SM, experiments)
@@ -681,8 +692,8 @@ void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t
                                                                     ws.bounds.p, ws.counters.p,
                                                                     slices);
   PK_LAUNCH("spmm list partition");
-  static thread_local int occs[2] = {0, 0};
-  int& occ = occs[masked ? 1 : 0];
+  static thread_local int occs[3] = {0, 0, 0};
+  int& occ = occs[masked ? 1 : (a.map.g ? 2 : 0)];
   if (occ == 0) {
     PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0));
     occ = std::max(occ, 1);
