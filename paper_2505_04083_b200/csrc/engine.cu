@@ -568,13 +568,16 @@ int Engine::forward_blocks(i64 rows, const Layout& lay) const {
 // slot_map / reduce_slots): FAST mode (plans without hub CTAs, the
 // tensor-core GEMM epilogue) with peer-memory groups. PK_FUSED_REDUCE is a
 // mask of the producers that store into the owners' slots: 1 = SpMM, 2 =
-// GEMM. Default 1: the SpMM stores whole rows per lane group, while the
-// GEMM epilogue stores 32 B per thread per row — over NVLink that measured
-// 9.2 vs 2.5 ms for C2's forward GEMMs at 2 GPUs (profiles/r2_fused_ab_n4.log).
+// GEMM. Measured and off by default (correct on every grid of 2 and 4,
+// tests/test_multigpu_gpu.py): C2 at 2 GPUs (2x1x1) 40.6 vs 37.0 ms — the
+// SpMMs' remote row stores cost 2.7 ms more SpMM time than the 0.7 ms of
+// reduction they save (profiles/r2_fused_ab_trees_n2.log), and the GEMM
+// epilogue's 32-B-per-thread row stores over NVLink are slower still (9.2 vs
+// 2.5 ms for the forward GEMMs, profiles/r2_fused_ab_n4.log).
 int Engine::fused_mask() {
   static const int m = [] {
     const char* e = std::getenv("PK_FUSED_REDUCE");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   return m;
 }

@@ -437,6 +437,7 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
 }
 
 // FAST plan: y[hub row] = fold of its segment sums in segment order
+template <bool MAPPED>
 __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* __restrict__ seg0,
                                         const u32* __restrict__ nseg, i64 nh, i64 r0,
                                         const float* __restrict__ part, i64 ldp, float* y,
@@ -450,17 +451,21 @@ __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* 
     float acc = part[s0 * ldp + c];
     for (u32 k = 1; k < nseg[h]; ++k) acc = __fadd_rn(acc, part[(s0 + k) * ldp + c]);
     const i64 rr = static_cast<i64>(hub[h]) - r0;
-    map.row(y, ldy, rr)[c] = mask ? keep(acc, mask[rr * ldm + c]) : acc;
+    float* yr = MAPPED ? map.row(y, ldy, rr) : y + rr * ldy;
+    yr[c] = mask ? keep(acc, mask[rr * ldm + c]) : acc;
   }
 }
 
 // y rows listed in `rows` (absolute ids) := 0 over d columns
+template <bool MAPPED>
 __global__ void zero_rows_kernel(const u32* __restrict__ rows, i64 n, i64 r0, float* y, i64 ldy,
                                  i64 d, RowMap map) {
   const i64 total = n * d;
   for (i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<i64>(gridDim.x) * blockDim.x)
-    map.row(y, ldy, static_cast<i64>(rows[i / d]) - r0)[i % d] = 0.f;
+       i += static_cast<i64>(gridDim.x) * blockDim.x) {
+    const i64 lr = static_cast<i64>(rows[i / d]) - r0;
+    (MAPPED ? map.row(y, ldy, lr) : y + lr * ldy)[i % d] = 0.f;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1183,8 +1188,8 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   }
   if (rg.e1 > rg.e0) {
     const i64 ne = rg.e1 - rg.e0;
-    zero_rows_kernel<<<blocks_for(ne * d), 256, 0, st>>>(plan.empty_rows.p + rg.e0, ne, r0, y,
-                                                         ldy, d, rmap);
+    (rmap.g ? zero_rows_kernel<true> : zero_rows_kernel<false>)<<<blocks_for(ne * d), 256, 0, st>>>(
+        plan.empty_rows.p + rg.e0, ne, r0, y, ldy, d, rmap);
     PK_LAUNCH("spmm zero rows");
   }
   if (rg.i1 > rg.i0) {
@@ -1210,7 +1215,7 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   }
   if (plan.segment && rg.h1 > rg.h0) {
     const i64 nh = rg.h1 - rg.h0;
-    combine_segments_kernel<<<blocks_for(nh * d), 256, 0, st>>>(
+    (rmap.g ? combine_segments_kernel<true> : combine_segments_kernel<false>)<<<blocks_for(nh * d), 256, 0, st>>>(
         plan.hub_asc.p + rg.h0, plan.hub_seg0.p + rg.h0, plan.hub_nseg.p + rg.h0, nh, r0,
         plan.partial.p, (d + 7) / 8 * 8, y, ldy, d, mask, ldm, rmap);
     PK_LAUNCH("spmm combine segments");
