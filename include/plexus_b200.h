@@ -459,6 +459,12 @@ int pk_engine_reduce_scatter_f32(pk_engine* e, int axis, float* buf, int64_t row
                                  int64_t cols, int64_t ld, float* out,
                                  void* stream);
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* out_host);
+/* `count` epochs (first_epoch, first_epoch + 1, ...) enqueued back to back
+ * with one host wait at the end (no per-epoch sync bubble); out_host[count]
+ * receives each epoch's metrics, and the first epoch that fails the loss
+ * checks raises (PK_ERR_TRAINING naming it) after the wait. */
+int pk_engine_train_epochs(pk_engine* e, int first_epoch, int count,
+                           pk_epoch_metrics* out_host);
 /* This rank failed outside the library (e.g. its host code threw): take the
  * grid down like the reference's Cluster does (cluster.hpp:240, 434). In
  * an in-process cluster every other rank's collectives return

@@ -184,6 +184,7 @@ Engine::~Engine() {
   }
   for (auto e : sync_ev_) cudaEventDestroy(e);
   if (sums_host_) cudaFreeHost(sums_host_);
+  if (sums_ring_) cudaFreeHost(sums_ring_);
 }
 
 cudaEvent_t Engine::sync_event() {
@@ -755,22 +756,24 @@ void Engine::loss() {
   // no host wait here: the sums ride to pinned memory in stream order and
   // finish_pass() checks them after the epoch (the gradient scaling uses the
   // load-time mask count, so the backward does not need them)
-  PK_CUDA(cudaMemcpyAsync(sums_host_, sums_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  PK_CUDA(cudaMemcpyAsync(reinterpret_cast<u32*>(sums_host_ + 3), ce_ws_.bad.p, sizeof(u32),
+  double* dst = sums_dst_ ? sums_dst_ : sums_host_;
+  PK_CUDA(cudaMemcpyAsync(dst, sums_.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  PK_CUDA(cudaMemcpyAsync(reinterpret_cast<u32*>(dst + 3), ce_ws_.bad.p, sizeof(u32),
                           cudaMemcpyDeviceToHost, st_));
 }
 
 // finalize_loss (trainer.hpp:71-89) and the pass's error checks; the stream
 // has drained.
-void Engine::finish_pass(int epoch, double* loss_out, double* acc_out) {
+void Engine::finish_pass(int epoch, double* loss_out, double* acc_out, const double* slot) {
   comms_.check_alive();  // a peer failed: its ClusterAborted, not our partial sums
   const i64 C = dims_[L_];
-  const u32 bad = *reinterpret_cast<const u32*>(sums_host_ + 3);
+  const double* sums = slot ? slot : sums_host_;
+  const u32 bad = *reinterpret_cast<const u32*>(sums + 3);
   check(!bad, "cross entropy: label out of range for " + std::to_string(C) + " classes");
   if (lsa_ready_ && grid_.size() > 1 && lsa_timed_out())
     throw Error(PK_ERR_NCCL, "peer-memory reduction: a barrier wait timed out (peer stalled)");
   check_device_watchdogs();
-  const double* h = sums_host_;
+  const double* h = sums;
   const u64 count = static_cast<u64>(h[1]), correct = static_cast<u64>(h[2]);
   if (count == 0)
     throw Error(PK_ERR_TRAINING,
@@ -1214,6 +1217,91 @@ void Engine::on_failure(const std::string& why) {
   else comms_.signal_abort(rank_, why);
 }
 
+// `count` epochs enqueued back to back with one host wait at the end: the
+// host runs ahead of the device (no per-epoch sync bubble), each epoch's CE
+// sums land in their own pinned slot, and the checks / metrics of every
+// epoch follow the wait in epoch order (the first failing epoch raises, as
+// train_epoch would have).
+void Engine::train_epochs(int first, int count, pk_epoch_metrics* out) {
+  check(count >= 1, "train_epochs: count must be >= 1");
+  if (sums_ring_n_ < count) {
+    if (sums_ring_) cudaFreeHost(sums_ring_);
+    PK_CUDA(cudaMallocHost(&sums_ring_, sizeof(double) * 4 * count));
+    sums_ring_n_ = count;
+  }
+  clock_.reset();
+  struct Snap {
+    CommCounters c;
+    u64 sf, gf, launches;
+    double sb, cb;
+    size_t mark0;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Snap> snaps(count);
+  for (int i = 0; i < count; ++i) {
+    Snap& sn = snaps[i];
+    sn.c = comms_.counters, sn.sf = spmm_flops_, sn.gf = gemm_flops_;
+    sn.sb = spmm_bytes_, sn.cb = spmm_cbytes_, sn.launches = launch_count();
+    sn.e0 = clock_.get();
+    sn.e1 = clock_.get();
+    sn.mark0 = clock_.marks.size();
+    PK_CUDA(cudaEventRecord(sn.e0, st_));
+    sums_dst_ = sums_ring_ + 4 * i;
+    forward_backward(first + i);
+    optimizer_step();
+    PK_CUDA(cudaEventRecord(sn.e1, st_));
+  }
+  sums_dst_ = nullptr;
+  const u64 sf_end = spmm_flops_, gf_end = gemm_flops_, l_end = launch_count();
+  const double sb_end = spmm_bytes_, cb_end = spmm_cbytes_;
+  const CommCounters c_end = comms_.counters;
+  PK_CUDA(cudaEventSynchronize(snaps[count - 1].e1));
+  for (int i = 0; i < count; ++i) {
+    const Snap& sn = snaps[i];
+    double loss = 0, acc = 0;
+    finish_pass(first + i, &loss, &acc, sums_ring_ + 4 * i);
+    double ph[6] = {0, 0, 0, 0, 0, 0};
+    const size_t mark1 = i + 1 < count ? snaps[i + 1].mark0 : clock_.marks.size();
+    for (size_t k = sn.mark0; k < mark1; ++k) {
+      float t = 0;
+      PK_CUDA(cudaEventElapsedTime(&t, clock_.marks[k].a, clock_.marks[k].b));
+      ph[clock_.marks[k].phase] += t * 1e-3;
+    }
+    float ms = 0;
+    PK_CUDA(cudaEventElapsedTime(&ms, sn.e0, sn.e1));
+    const bool last = i + 1 == count;
+    const Snap* nx = last ? nullptr : &snaps[i + 1];
+    pk_epoch_metrics* m = out + i;
+    std::memset(m, 0, sizeof(*m));
+    m->epoch = first + i;
+    m->loss = loss;
+    m->accuracy = acc;
+    m->forward_spmm_s = ph[0];
+    m->forward_gemm_s = ph[1];
+    m->backward_s = ph[2] + ph[5];
+    m->spmm_s = ph[0] + ph[5];
+    m->optimizer_s = ph[3];
+    m->collectives_s = ph[4];
+    m->epoch_s = ms * 1e-3;
+    m->spmm_bytes = (last ? sb_end : nx->sb) - sn.sb;
+    m->spmm_compulsory_bytes = (last ? cb_end : nx->cb) - sn.cb;
+    m->kernel_launches = (last ? l_end : nx->launches) - sn.launches;
+    m->spmm_flops = (last ? sf_end : nx->sf) - sn.sf;
+    m->gemm_flops = (last ? gf_end : nx->gf) - sn.gf;
+    const CommCounters& ce = last ? c_end : nx->c;
+    for (int a = 0; a < 3; ++a) {
+      const double g = grid_.extent(a);
+      auto delta = [&](int op) {
+        return static_cast<double>(ce.ring_numer[a][op] - sn.c.ring_numer[a][op]) / g;
+      };
+      m->allreduce_bytes += delta(kAllReduce);
+      m->allgather_bytes += delta(kAllGather);
+      m->reducescatter_bytes += delta(kReduceScatter);
+    }
+  }
+  clock_.reset();
+}
+
 bool Engine::tensor(int which, int layer, pk_tensor_view* out) {
   auto fill = [&](const DMat& m, i64 cols) {
     out->data = m.p();
@@ -1439,6 +1527,13 @@ int pk_engine_optimizer_step(pk_engine* e) {
   return guard_rank(e, [&] {
     e->e->reset_clock();
     e->e->optimizer_step();
+  });
+}
+
+int pk_engine_train_epochs(pk_engine* e, int first_epoch, int count, pk_epoch_metrics* out) {
+  return guard_rank(e, [&] {
+    check(out != nullptr, "train_epochs: null metrics array");
+    e->e->train_epochs(first_epoch, count, out);
   });
 }
 

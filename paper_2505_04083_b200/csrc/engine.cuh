@@ -87,8 +87,10 @@ class Engine {
   // and finish_pass() turns them into loss / accuracy (and the reference's
   // TrainingError checks) once the stream has drained.
   void forward_backward(int epoch);
-  // After a stream sync: loss, accuracy, error checks of the last pass.
-  void finish_pass(int epoch, double* loss, double* acc);
+  // After a stream sync: loss, accuracy, error checks of the last pass (or
+  // of the pass whose sums went to `slot`).
+  void finish_pass(int epoch, double* loss, double* acc, const double* slot = nullptr);
+  void train_epochs(int first, int count, pk_epoch_metrics* out);
   void optimizer_step();
   void train_epoch(int epoch, pk_epoch_metrics* m);
   void reset_clock() { clock_.reset(); }
@@ -172,6 +174,9 @@ class Engine {
   u64 mask_count_ = 0;  // global number of masked nodes (the CE count)
   DevBuf<double> sums_;
   double* sums_host_ = nullptr;  // pinned: {loss_sum, count, correct, bad}
+  double* sums_dst_ = nullptr;   // where loss() sends them (null: sums_host_)
+  double* sums_ring_ = nullptr;  // train_epochs: one pinned slot per epoch
+  int sums_ring_n_ = 0;
   CeWorkspace ce_ws_;
   PhaseClock clock_;
   u64 spmm_flops_ = 0, gemm_flops_ = 0;

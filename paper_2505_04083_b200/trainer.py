@@ -77,6 +77,8 @@ _SIGS = {
                                              C.POINTER(C.c_double)]),
     "pk_engine_optimizer_step": (C.c_int, [C.c_void_p]),
     "pk_engine_train_epoch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(pk_epoch_metrics)]),
+    "pk_engine_train_epochs": (C.c_int, [C.c_void_p, C.c_int, C.c_int,
+                                         C.POINTER(pk_epoch_metrics)]),
     "pk_engine_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(pk_tensor_view)]),
     "pk_engine_stream": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pk_engine_destroy": (C.c_int, [C.c_void_p]),
@@ -285,6 +287,12 @@ class RankEngine:
         """This rank failed: take the grid down (pk_engine_abort) — the other
         ranks' pending epoch fails with ClusterAborted naming this rank."""
         call("pk_engine_abort", self.h, str(why).encode()[:500])
+
+    def train_epochs(self, first, count):
+        """`count` epochs with one host wait (pk_engine_train_epochs)."""
+        arr = (pk_epoch_metrics * count)()
+        call("pk_engine_train_epochs", self.h, first, count, arr)
+        return [{k: getattr(m, k) for k in METRIC_KEYS} for m in arr]
 
     def tensor(self, which, layer=0) -> torch.Tensor:
         """Copy of an engine tensor (rows x cols) as a CUDA tensor."""

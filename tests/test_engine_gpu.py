@@ -182,3 +182,28 @@ def test_training_error_on_empty_mask(cuda):
     with pytest.raises(TrainingError, match="epoch 3"):
         eng.train_epoch(3)
     eng.close()
+
+
+def test_train_epochs_batch_equals_single_epochs(cuda):
+    """pk_engine_train_epochs (K epochs, one host wait) is the same
+    computation as K train_epoch calls: identical losses, counters and
+    final weights."""
+    graph, tr = _mods()
+    pre = build(10, 12000, 8, 4, seed=3)
+    opts = tr.TrainOptions(hidden_dims=[16, 16], mode=tr.PK_MODE_FAST, hub_threshold=64)
+    a = tr.RankEngine(pre.n, pre.feat_dim, pre.num_classes, tr.GridConfig(1, 1, 1), 0, opts)
+    b = tr.RankEngine(pre.n, pre.feat_dim, pre.num_classes, tr.GridConfig(1, 1, 1), 0, opts)
+    a.load(pre)
+    b.load(pre)
+    one = [a.train_epoch(e) for e in range(5)]
+    many = b.train_epochs(0, 5)
+    for x, y in zip(one, many):
+        assert x["epoch"] == y["epoch"] and x["loss"] == y["loss"]
+        assert x["accuracy"] == y["accuracy"]
+        for k in ("spmm_flops", "gemm_flops", "kernel_launches", "spmm_bytes"):
+            assert x[k] == y[k], k
+        assert y["epoch_s"] > 0 and y["spmm_s"] > 0
+    for l in range(3):
+        assert torch.equal(a.tensor(tr.PK_T_W, l), b.tensor(tr.PK_T_W, l))
+    a.close()
+    b.close()
