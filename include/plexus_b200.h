@@ -283,6 +283,15 @@ int pk_labels_from_degrees(const uint32_t* label_degree, int64_t n, uint32_t cla
 /* out[i] = src[idx[i]] (labels / masks into a permuted order) */
 int pk_gather_u32(const uint32_t* src, const uint32_t* idx, int64_t n, uint32_t* out,
                   void* stream);
+int pk_gather_u8(const uint8_t* src, const uint32_t* idx, int64_t n, uint8_t* out,
+                 void* stream);
+/* dst row i = src row idx[i] (cols floats): preprocess' feature alignment,
+ * features in col_perm order (graph.hpp:373-376) */
+int pk_gather_rows_f32(const float* src, int64_t ld_src, const uint32_t* idx, int64_t n,
+                       int64_t cols, float* dst, int64_t ld_dst, void* stream);
+/* balance_metric (graph.hpp:157-172): max / mean nonzeros over the p x q
+ * ceil-split block partition, counted on the device */
+int pk_balance_metric(const pk_csr* a, int p, int q, double* out_host, void* stream);
 
 /* ------------------------------------------------------------------ */
 /* 3D-parallel GCN engine: one per rank (one per GPU)                   */

@@ -128,6 +128,10 @@ SIGNATURES = {
     "pk_rmat_edges": (INT, [INT, U64, DBL, DBL, DBL, U64, P, U64P, P]),
     "pk_rmat_features": (INT, [U64, I64, I64, P, I64, P]),
     "pk_degree_quantile_labels": (INT, [P, U64, I64, U32, P, P]),
+    "pk_gather_rows_f32": (INT, [P, I64, P, I64, I64, P, I64, P]),
+    "pk_gather_u32": (INT, [P, P, I64, P, P]),
+    "pk_gather_u8": (INT, [P, P, I64, P, P]),
+    "pk_balance_metric": (INT, [C.POINTER(pk_csr), INT, INT, C.POINTER(DBL), P]),
 }
 
 _lib = None

@@ -418,3 +418,92 @@ int pk_gather_u32(const uint32_t* src, const uint32_t* idx, int64_t n, uint32_t*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// preprocess' attribute alignment (graph.hpp:373-380) and balance_metric
+// (graph.hpp:157-172) on the device
+
+namespace pk {
+namespace {
+
+__global__ void gather_rows_kernel(const float* __restrict__ src, i64 ld_src,
+                                   const u32* __restrict__ idx, i64 n, i64 cols,
+                                   float* __restrict__ dst, i64 ld_dst) {
+  const u64 total = static_cast<u64>(n) * cols;
+  for (u64 t = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const i64 i = static_cast<i64>(t / cols), j = static_cast<i64>(t % cols);
+    dst[i * ld_dst + j] = src[static_cast<i64>(idx[i]) * ld_src + j];
+  }
+}
+
+__global__ void gather_u8_kernel(const u8* __restrict__ src, const u32* __restrict__ idx, u64 n,
+                                 u8* __restrict__ out) {
+  for (u64 i = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<u64>(gridDim.x) * blockDim.x)
+    out[i] = src[idx[i]];
+}
+
+// chunk_index (graph.hpp:150-155)
+__device__ __forceinline__ u64 chunk_of(u64 total, u64 parts, u64 pos) {
+  const u64 base = total / parts, rem = total % parts;
+  if (pos < rem * (base + 1)) return pos / (base + 1);
+  return rem + (pos - rem * (base + 1)) / (base > 0 ? base : 1);
+}
+
+__global__ void block_nnz_kernel(const u64* __restrict__ rp, const u32* __restrict__ ci, u64 rows,
+                                 u64 cols, int p, int q, unsigned long long* __restrict__ counts) {
+  for (u64 r = blockIdx.x * static_cast<u64>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<u64>(gridDim.x) * blockDim.x) {
+    const u64 bi = chunk_of(rows, p, r);
+    for (u64 k = rp[r]; k < rp[r + 1]; ++k)
+      atomicAdd(&counts[bi * q + chunk_of(cols, q, ci[k])], 1ull);
+  }
+}
+
+}  // namespace
+}  // namespace pk
+
+extern "C" {
+
+int pk_gather_rows_f32(const float* src, int64_t ld_src, const uint32_t* idx, int64_t n,
+                       int64_t cols, float* dst, int64_t ld_dst, void* stream) {
+  return guard([&] {
+    if (n <= 0 || cols <= 0) return;
+    gather_rows_kernel<<<grid_for(static_cast<u64>(n) * cols), 256, 0, as_stream(stream)>>>(
+        src, ld_src, idx, n, cols, dst, ld_dst);
+    PK_LAUNCH("gather rows");
+  });
+}
+
+int pk_gather_u8(const uint8_t* src, const uint32_t* idx, int64_t n, uint8_t* out, void* stream) {
+  return guard([&] {
+    if (n <= 0) return;
+    gather_u8_kernel<<<grid_for(n), 256, 0, as_stream(stream)>>>(src, idx, static_cast<u64>(n),
+                                                               out);
+    PK_LAUNCH("gather u8");
+  });
+}
+
+int pk_balance_metric(const pk_csr* a, int p, int q, double* out_host, void* stream) {
+  return guard([&] {
+    check(p >= 1 && q >= 1, "balance_metric: p and q must be >= 1");
+    check(a && a->nnz > 0, "balance_metric: matrix has no nonzeros");
+    cudaStream_t st = as_stream(stream);
+    const size_t nb = static_cast<size_t>(p) * q;
+    DevBuf<unsigned long long> counts(nb);
+    PK_CUDA(cudaMemsetAsync(counts.p, 0, nb * sizeof(unsigned long long), st));
+    block_nnz_kernel<<<grid_for(a->rows), 256, 0, st>>>(a->row_ptr, a->col_idx,
+                                                        static_cast<u64>(a->rows),
+                                                        static_cast<u64>(a->cols), p, q, counts.p);
+    PK_LAUNCH("balance block counts");
+    std::vector<unsigned long long> h(nb);
+    PK_CUDA(cudaMemcpyAsync(h.data(), counts.p, nb * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    PK_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long mx = *std::max_element(h.begin(), h.end());
+    *out_host = static_cast<double>(mx) / (static_cast<double>(a->nnz) / static_cast<double>(nb));
+  });
+}
+
+}  // extern "C"

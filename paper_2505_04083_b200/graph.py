@@ -157,28 +157,32 @@ def preprocess(ds: GraphDataset, perm_seed) -> PreprocessedDataset:
     even = permute_csr(a, rp, cp)
     odd = permute_csr(a, cp, rp)
     del a
-    rpl, cpl = rp.long(), cp.long()
+    # attribute alignment (graph.hpp:373-380): library gathers, so a C++
+    # caller can run the whole preprocess through the ABI
+    n, d0 = ds.num_nodes, ds.features.shape[1]
+    feats = torch.empty((n, d0), dtype=torch.float32, device=dev)
+    f_src = ds.features.contiguous()
+    call("pk_gather_rows_f32", _ptr(f_src), d0, _ptr(cp), n, d0, _ptr(feats), d0, _stream())
+    lab = ds.labels.contiguous()
+    msk = ds.train_mask.contiguous()
+    out = {}
+    for name, perm in (("row", rp), ("col", cp)):
+        lo = torch.empty(n, dtype=torch.int32, device=dev)
+        mo = torch.empty(n, dtype=torch.uint8, device=dev)
+        call("pk_gather_u32", _ptr(lab), _ptr(perm), n, _ptr(lo), _stream())
+        call("pk_gather_u8", _ptr(msk), _ptr(perm), n, _ptr(mo), _stream())
+        out[name] = (lo, mo)
     return PreprocessedDataset(
-        n=ds.num_nodes, feat_dim=ds.features.shape[1], num_classes=ds.num_classes,
-        perm_seed=perm_seed, a_even=even, a_odd=odd,
-        features=ds.features.index_select(0, cpl).contiguous(),
-        labels_row_order=ds.labels.index_select(0, rpl), labels_col_order=ds.labels.index_select(0, cpl),
-        mask_row_order=ds.train_mask.index_select(0, rpl),
-        mask_col_order=ds.train_mask.index_select(0, cpl),
+        n=n, feat_dim=d0, num_classes=ds.num_classes,
+        perm_seed=perm_seed, a_even=even, a_odd=odd, features=feats,
+        labels_row_order=out["row"][0], labels_col_order=out["col"][0],
+        mask_row_order=out["row"][1], mask_col_order=out["col"][1],
         row_perm=rperm, col_perm=cperm)
 
 
 def balance_metric(a: DeviceCsr, p, q):
     """balance_metric (graph.hpp:157-172): max/mean nnz over a p x q
-    ceil-split block partition (report only; host numpy over the CSR)."""
-    from .layout import chunk_index_array
-    if p < 1 or q < 1:
-        raise ContractError("balance_metric: p and q must be >= 1")
-    if a.nnz == 0:
-        raise ContractError("balance_metric: matrix has no nonzeros")
-    rp, ci, _ = a.to_host()
-    rows = np.repeat(np.arange(a.rows, dtype=np.int64), np.diff(rp.astype(np.int64)))
-    bi = chunk_index_array(a.rows, p, rows)
-    bj = chunk_index_array(a.cols, q, ci.astype(np.int64))
-    counts = np.bincount(bi * q + bj, minlength=p * q)
-    return counts.max() / (a.nnz / (p * q))
+    ceil-split block partition, counted on the device (pk_balance_metric)."""
+    out = C.c_double()
+    call("pk_balance_metric", a.view(), p, q, C.byref(out), _stream())
+    return out.value
