@@ -949,7 +949,7 @@ void Engine::backward_layer(int l) {
 int Engine::tf_vec() {
   static const int v = [] {
     const char* e = std::getenv("PK_TF_VEC");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 2;
   }();
   return v;
 }
@@ -1008,11 +1008,11 @@ void Engine::forward_layer_tf(int l) {
   DMat& qout = hidden ? fout_[l] : q_[l];
   clock_.begin(0, st_);
   // Width of the narrow SpMMs (PK_TF_VEC): 0 = the exact width (47: 32
-  // lanes of 4-B gathers); v > 0 = the padded width (48; P's and dQ's
+  // lanes x 2 of 4-B gathers); v > 0 = the padded width (48; P's and dQ's
   // padding columns are zero, so the extra output column is exactly +0)
-  // with gathers of at most v floats. The padded width at 16 B takes the
-  // 16-lane group form, measured slower (2 x 5.6 vs 2 x 3.9 ms per C2
-  // epoch).
+  // with gathers of at most v floats. Default 2: 24 lanes of 8-B gathers,
+  // C2 epoch 52.2 vs 52.8 ms; at 16 B the padded width takes the 16-lane
+  // group form, measured slower (2 x 5.6 vs 2 x 3.9 ms per C2 epoch).
   const int tfv = tf_vec();
   spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, tfv ? ldp : s.w_cols,
            qout.p(), qout.ld, st_, nullptr, 0, nullptr, tfv ? tfv : 8);
