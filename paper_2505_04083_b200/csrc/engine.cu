@@ -1128,7 +1128,8 @@ void Engine::setup_lsa() {
     if (need[a] && grid_.extent(a) > 1) {
       // the fused form needs the owner slots (g x ceil(rows / g) rows) and a
       // result region of all rows: ~2x the partial, plus the ceil slack
-      const size_t e = cfg_.mode == PK_MODE_FAST ? 2 * need[a] + (size_t{1} << 16) : need[a];
+      const size_t e = fused_mask() && cfg_.mode == PK_MODE_FAST
+                           ? 2 * need[a] + (size_t{1} << 16) : need[a];
       comms_.lsa(a, e);
     }
   lsa_ready_ = true;
