@@ -483,6 +483,11 @@ int pk_engine_train_epochs(pk_engine* e, int first_epoch, int count,
  * pending epoch returns PK_ERR_ABORTED naming this rank. Failures inside
  * pk_engine_load* / forward_backward / train_epoch do this on their own. */
 int pk_engine_abort(pk_engine* e, const char* why);
+/* CommStats (cluster.hpp:35-65) of this rank since its load: calls and
+ * ring-model bytes (CommStats::bytes, cluster.hpp:53-55) per [axis * 3 + op],
+ * op 0 all_gather, 1 all_reduce, 2 reduce_scatter — comm_stats.csv of the
+ * CLI (main.cpp:353-366). */
+int pk_engine_comm_stats(pk_engine* e, uint64_t* calls9, double* ring_bytes9);
 int pk_engine_tensor(pk_engine* e, int which, int layer, pk_tensor_view* out);
 int pk_engine_stream(pk_engine* e, void** stream_out);
 int pk_engine_destroy(pk_engine* e);

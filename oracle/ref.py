@@ -261,12 +261,15 @@ class Pre(_Handle):
         dw = np.empty(sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1)), dt)
         df0 = np.empty((i["n"], dims[0]), dt)
         flops = np.empty(2, np.uint64)
+        g = grid[0] * grid[1] * grid[2]
+        comm = np.empty((g, 3, 3, 2))
         _check(lib().ref_distributed_pass(
             self.h, *[C.c_int(g) for g in grid], _p(hid), C.c_int(len(hidden)),
             C.c_uint64(seed), C.c_int(block_count), C.byref(loss), C.byref(acc),
-            _p(logits), _p(dw), _p(df0), _p(flops)))
+            _p(logits), _p(dw), _p(df0), _p(flops), _p(comm)))
         return dict(loss=loss.value, accuracy=acc.value, logits=logits,
-                    dw=split_weights(dw, dims), df0=df0, flops=flops)
+                    dw=split_weights(dw, dims), df0=df0, flops=flops,
+                    comm_calls=comm[..., 0], comm_bytes=comm[..., 1])
 
 
 def split_weights(cat, dims):

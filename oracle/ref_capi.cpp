@@ -870,7 +870,7 @@ int ref_train_distributed(void* pre, int gx, int gy, int gz, const u64* hidden,
 int ref_distributed_pass(void* pre, int gx, int gy, int gz, const u64* hidden,
                          int nh, u64 seed, int block_count, double* loss,
                          double* acc, void* logits, void* dw_cat, void* df0,
-                         u64* flops2) {
+                         u64* flops2, double* comm) {
   auto* p = static_cast<Pre*>(pre);
   return guarded([&] {
     auto run = [&](auto& d, auto tag) {
@@ -937,6 +937,15 @@ int ref_distributed_pass(void* pre, int gx, int gy, int gz, const u64* hidden,
         flops2[0] = flops2[1] = 0;
         for (auto& s : stats) flops2[0] += s.spmm_flops, flops2[1] += s.gemm_flops;
       }
+      if (comm)  // per rank, [axis][op]: calls, ring bytes (CommStats::bytes)
+        for (std::size_t r = 0; r < stats.size(); ++r)
+          for (int a = 0; a < 3; ++a)
+            for (int o = 0; o < 3; ++o) {
+              const auto ax = static_cast<Axis>(a);
+              const auto op = static_cast<CollOp>(o);
+              comm[(r * 9 + a * 3 + o) * 2] = static_cast<double>(stats[r].at(ax, op).calls);
+              comm[(r * 9 + a * 3 + o) * 2 + 1] = stats[r].bytes(ax, op, grid);
+            }
     };
     if (p->f64)
       run(p->d, double{});

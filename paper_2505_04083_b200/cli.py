@@ -150,6 +150,12 @@ METRIC_COLS = ("loss", "accuracy", "load_s", "forward_spmm_s", "forward_gemm_s",
                "allgather_bytes", "reducescatter_bytes")
 
 
+def _fmt_bytes(x):
+    """the reference streams a double with default ostream formatting
+    (6 significant digits)"""
+    return f"{x:g}"
+
+
 def cmd_train(a):
     import torch
 
@@ -206,10 +212,21 @@ def cmd_train(a):
         f.write(f"{grid.gx}x{grid.gy}x{grid.gz},{a.epochs},{first},{avg['loss']},"
                 f"{avg['accuracy']},{avg['forward_spmm_s']},{avg['forward_gemm_s']},"
                 f"{avg['backward_s']},{avg['optimizer_s']},{avg['collectives_s']}\n")
+    # comm_stats.csv (main.cpp:353-366): per rank, axis and collective
+    with open(os.path.join(a.out, "comm_stats.csv"), "w") as f:
+        f.write("rank,axis,collective,calls,ring_bytes\n")
+        for r, st in enumerate(res.stats):
+            if st is None:
+                continue
+            calls, byts = st
+            for ax in range(3):
+                for op, name in enumerate(("all_gather", "all_reduce", "reduce_scatter")):
+                    f.write(f"{r},{'XYZ'[ax]},{name},{int(calls[ax][op])},"
+                            f"{_fmt_bytes(byts[ax][op])}\n")
     write_model_file(res.weights, res.features, os.path.join(a.out, "model.plxm"))
     print(f"trained {a.epochs} epochs on grid {grid.gx}x{grid.gy}x{grid.gz}: loss "
           f"{g[0]['loss']} -> {g[-1]['loss']}, accuracy {g[-1]['accuracy']}")
-    print(f"wrote metrics.csv, summary.csv, model.plxm to {a.out}")
+    print(f"wrote metrics.csv, summary.csv, comm_stats.csv, model.plxm to {a.out}")
     return EXIT_OK
 
 

@@ -128,7 +128,8 @@ def distributed_pass(pre, grid: GridConfig, opts, devices=None):
             loss, acc = e.forward_backward(0)
             return {"fout": e.tensor(trainer.PK_T_FOUT).cpu().numpy(),
                     "dw": [e.tensor(trainer.PK_T_DW, l).cpu().numpy() for l in range(L)],
-                    "df0": e.tensor(trainer.PK_T_DF0).cpu().numpy(), "loss": loss, "acc": acc}
+                    "df0": e.tensor(trainer.PK_T_DF0).cpu().numpy(), "loss": loss, "acc": acc,
+                    "comm": e.comm_stats()}
         finally:
             e.close()
     try:
@@ -137,7 +138,9 @@ def distributed_pass(pre, grid: GridConfig, opts, devices=None):
         cl.close()
     logits, dw, df0 = trainer.gather_rank_pass(per, grid, pre.n, dims)
     return dict(loss=per[0]["loss"], accuracy=per[0]["acc"], logits=logits, dw=dw, df0=df0,
-                rank_losses=[p["loss"] for p in per])
+                rank_losses=[p["loss"] for p in per],
+                comm_calls=np.array([p["comm"][0] for p in per]),
+                comm_bytes=np.array([p["comm"][1] for p in per]))
 
 
 def train_distributed(pre, grid: GridConfig, opts, devices=None) -> TrainResult:

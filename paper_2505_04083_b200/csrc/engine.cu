@@ -495,6 +495,7 @@ void Engine::load(const pk_dataset_view& dsin, bool host) {
   for (auto& e : staged)
     if (e) cudaEventDestroy(e);
   drop_csr_arrays();
+  comm_at_load_ = comms_.counters;  // CommStats count the training only
   loaded_ = true;
 }
 
@@ -556,6 +557,7 @@ void Engine::load_rank(const pk_rank_view& rv, pk_csr_owned* adopt) {
   }
   set_labels(rv.labels, rv.mask, rv.label_rows, static_cast<u64>(count));
   drop_csr_arrays();
+  comm_at_load_ = comms_.counters;  // CommStats count the training only
   loaded_ = true;
 }
 
@@ -1213,6 +1215,16 @@ void Engine::train_epoch(int epoch, pk_epoch_metrics* m) {
   }
 }
 
+void Engine::comm_stats(u64* calls9, double* bytes9) const {
+  for (int a = 0; a < 3; ++a)
+    for (int o = 0; o < 3; ++o) {
+      const u64 c = comms_.counters.calls[a][o] - comm_at_load_.calls[a][o];
+      const u64 r = comms_.counters.ring_numer[a][o] - comm_at_load_.ring_numer[a][o];
+      if (calls9) calls9[a * 3 + o] = c;
+      if (bytes9) bytes9[a * 3 + o] = static_cast<double>(r) / grid_.extent(a);
+    }
+}
+
 void Engine::on_failure(const std::string& why) {
   if (LocalCluster* cl = comms_.local_cluster()) cl->abort(rank_, why);
   else comms_.signal_abort(rank_, why);
@@ -1540,6 +1552,10 @@ int pk_engine_train_epochs(pk_engine* e, int first_epoch, int count, pk_epoch_me
 
 int pk_engine_train_epoch(pk_engine* e, int epoch, pk_epoch_metrics* m) {
   return guard_rank(e, [&] { e->e->train_epoch(epoch, m); });
+}
+
+int pk_engine_comm_stats(pk_engine* e, uint64_t* calls9, double* ring_bytes9) {
+  return guard([&] { e->e->comm_stats(calls9, ring_bytes9); });
 }
 
 int pk_engine_abort(pk_engine* e, const char* why) {

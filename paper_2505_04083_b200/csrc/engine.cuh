@@ -94,6 +94,9 @@ class Engine {
   void optimizer_step();
   void train_epoch(int epoch, pk_epoch_metrics* m);
   void reset_clock() { clock_.reset(); }
+  // CommStats (cluster.hpp:35-65) since the load: calls and ring bytes per
+  // [axis][op] (op: all_gather, all_reduce, reduce_scatter)
+  void comm_stats(u64* calls9, double* bytes9) const;
   // forward_layer / backward_layer (engine.hpp:158-259) one at a time, for
   // callers that drive rank_forward_backward themselves (the C++ shim):
   // begin_pass, forward_layer(0..L-1), loss, backward_layer(L-1..0), then a
@@ -149,6 +152,7 @@ class Engine {
   size_t sync_used_ = 0;
   cudaEvent_t sync_event();
   Comms comms_;
+  CommCounters comm_at_load_;
   // one per (plane, parity) key; keys whose block is the same range of the
   // same variant share one shard (at 1x1x1 planes 0 and 2 are both A_even)
   std::shared_ptr<AdjShard> shards_[6];

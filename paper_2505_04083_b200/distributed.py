@@ -36,6 +36,8 @@ class TrainResult:
     per_rank: List[List[Dict]] = field(default_factory=list)
     weights: List[np.ndarray] = field(default_factory=list)
     features: Optional[np.ndarray] = None
+    # CommStats per rank (cluster.hpp:35-65): (calls, ring bytes), [axis][op]
+    stats: List = field(default_factory=list)
 
 
 def dist_env():
@@ -141,13 +143,14 @@ def train_distributed(load_dataset: Callable[[], object], grid: GridConfig, opts
     w_mine = [np.asarray(_host(eng.tensor(0, l))) for l in range(L)] if reassemble_params else []
     f_mine = np.asarray(_host(eng.tensor(2))) if reassemble_params else None
     dims = list(eng.dims)
+    stats = eng.comm_stats() if hasattr(eng, "comm_stats") else None
     eng.close()
     if world > 1:
         gathered = [None] * world
-        dist.all_gather_object(gathered, (mine, w_mine, f_mine))
+        dist.all_gather_object(gathered, (mine, w_mine, f_mine, stats))
     else:
-        gathered = [(mine, w_mine, f_mine)]
-    res = TrainResult(per_rank=[g[0] for g in gathered])
+        gathered = [(mine, w_mine, f_mine, stats)]
+    res = TrainResult(per_rank=[g[0] for g in gathered], stats=[g[3] for g in gathered])
     res.global_metrics = reduce_epoch_metrics(res.per_rank)
     if reassemble_params:
         res.weights, res.features = reassemble(grid, pre.n, dims, [g[1] for g in gathered],

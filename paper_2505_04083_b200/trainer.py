@@ -84,6 +84,7 @@ _SIGS = {
     "pk_engine_destroy": (C.c_int, [C.c_void_p]),
     "pk_engine_abort": (C.c_int, [C.c_void_p, C.c_char_p]),
     "pk_engine_comm_init_solo": (C.c_int, [C.c_void_p]),
+    "pk_engine_comm_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 _capi.register(_SIGS)
 
@@ -215,6 +216,15 @@ class RankEngine:
     def comm_init(self, uid: bytes, world_size: int):
         buf = (C.c_ubyte * 128).from_buffer_copy(uid)
         call("pk_engine_comm_init", self.h, C.cast(buf, C.c_void_p), world_size)
+
+    def comm_stats(self):
+        """CommStats since the load: (calls, ring bytes), each [axis][op]
+        (op: all_gather, all_reduce, reduce_scatter)."""
+        calls = np.zeros(9, np.uint64)
+        byts = np.zeros(9, np.float64)
+        call("pk_engine_comm_stats", self.h, calls.ctypes.data_as(C.c_void_p),
+             byts.ctypes.data_as(C.c_void_p))
+        return calls.reshape(3, 3), byts.reshape(3, 3)
 
     def comm_init_solo(self):
         """Measurement mode (pk_engine_comm_init_solo): this rank alone;

@@ -39,6 +39,8 @@ def test_preprocess_then_train(cuda, tmp_path):
     rows = open(os.path.join(run, "metrics.csv")).read().splitlines()
     assert rows[0].startswith("epoch,rank,loss,accuracy") and len(rows) == 1 + 3 * 2
     assert os.path.exists(os.path.join(run, "summary.csv"))
+    comm = open(os.path.join(run, "comm_stats.csv")).read().splitlines()
+    assert comm[0] == "rank,axis,collective,calls,ring_bytes" and len(comm) == 1 + 9
     blob = open(os.path.join(run, "model.plxm"), "rb").read()
     assert blob[:4] == b"PLXM" and struct.unpack("<III", blob[4:16]) == (1, 4, 3)
     # the loss curve is the reference serial trainer's (PARITY, 1x1x1)

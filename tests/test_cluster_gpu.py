@@ -173,3 +173,21 @@ def test_cluster_abort_propagates(data):
     assert sorted(seen) == [0, 1, 3]
     assert all("rank 2" in m for m in seen.values())
     cl.close()
+
+
+@pytest.mark.parametrize("grid", [(2, 1, 1), (2, 2, 2), (1, 4, 2)],
+                         ids=lambda g: "x".join(map(str, g)))
+def test_cluster_comm_stats_match_reference(data, grid):
+    """CommStats (cluster.hpp:35-65) of one pass on every rank — calls and
+    ring-model bytes per axis and collective — equal the reference's, with
+    the blocked aggregation's block count fixed on both sides
+    (engine.hpp:135-138)."""
+    from paper_2505_04083_b200 import cluster, trainer
+    from paper_2505_04083_b200.layout import GridConfig
+    pre, rpre = data
+    opts = trainer.TrainOptions(hidden_dims=[16, 16], mode=trainer.PK_MODE_PARITY,
+                                hub_threshold=64, block_count=2)
+    got = cluster.distributed_pass(pre, GridConfig(*grid), opts)
+    want = rpre.distributed_pass(grid, hidden=[16, 16], seed=0, block_count=2)
+    assert np.array_equal(got["comm_calls"], want["comm_calls"].astype(np.uint64))
+    assert np.allclose(got["comm_bytes"], want["comm_bytes"], rtol=0, atol=0.5)
