@@ -433,7 +433,9 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   // the SMs the overlapped SpMM / GEMM keep.
   static const int ctas = [] {
     const char* e = std::getenv("PK_LSA_CTAS");
-    const int v = e ? std::atoi(e) : kLsaBlocks / 2;  // measured: 148 = NCCL speed, fewer SMs
+    // 296 (2 per SM): C2 at 2 GPUs 7.65 vs 8.46 ms of reductions at 148,
+    // 13.3 at 74; NCCL 8.25 (profiles/r2_lsa_ctas_ab_n2.log)
+    const int v = e ? std::atoi(e) : 296;
     return std::max(1, std::min(v, kLsaBlocks));
   }();
   auto launch = [&](auto vec_tag, auto g_tag) {
@@ -479,7 +481,7 @@ void LsaGroup::all_reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 ou
                   (!mask || (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0));
   static const int ctas = [] {
     const char* e = std::getenv("PK_LSA_CTAS");
-    const int v = e ? std::atoi(e) : kLsaBlocks / 2;
+    const int v = e ? std::atoi(e) : 296;
     return std::max(1, std::min(v, kLsaBlocks));
   }();
   auto launch = [&](auto vec_tag, auto g_tag) {
@@ -530,7 +532,7 @@ void LsaGroup::reduce_slots(i64 rows, i64 cols, i64 ld, float* out, i64 ld_o, cu
                   (!mask || (ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(mask) & 15) == 0));
   static const int ctas = [] {
     const char* e = std::getenv("PK_LSA_CTAS");
-    const int v = e ? std::atoi(e) : kLsaBlocks / 2;
+    const int v = e ? std::atoi(e) : 296;
     return std::max(1, std::min(v, kLsaBlocks));
   }();
   auto launch = [&](auto vec_tag, auto g_tag) {

@@ -8,7 +8,7 @@
 namespace pk {
 
 constexpr int kLsaMaxMembers = 8;
-constexpr int kLsaBlocks = 148 * 2;  // CTAs of every reduce (same on all members)
+constexpr int kLsaBlocks = 148 * 4;  // max CTAs of a reduce (barrier slots per member)
 
 struct LsaPeers {
   const float* data[kLsaMaxMembers];  // each member's symmetric scratch

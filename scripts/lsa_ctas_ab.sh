@@ -4,7 +4,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 for rep in 1 2; do
-for cfg in "PK_LSA_CTAS=148" "PK_LSA_CTAS=296" "PK_LSA_CTAS=74" "PK_LSA=0"; do
+for cfg in ${CFGS:-"PK_LSA_CTAS=148" "PK_LSA_CTAS=296" "PK_LSA_CTAS=74" "PK_LSA=0"}; do
   env $cfg timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
     --master-addr 127.0.0.1 --master-port $((29700 + RANDOM % 200)) bench.py --gpus 2 --grid 2,1,1 \
     --steps 20 --warmup 5 --no-cpu-baseline --no-c1-measured --no-e2e > gpurun_out/lsa_ab.log 2>&1
