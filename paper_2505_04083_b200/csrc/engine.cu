@@ -822,11 +822,12 @@ void Engine::backward_layer(int l) {
   // dW = (dQ^T H)^T computed as H^T dQ: same products, same k order
   LsaGroup* lsa_dw = comms_.lsa(lay.row);
   float* dwpart = lsa_dw ? lsa_dw->scratch() : dwp_[l].p();
-  gemm_launch(true, false, s.h_cols, s.q_cols, s.h_rows, h_[l].p(), h_[l].ld, dq, lddq, dwpart,
-              dwp_[l].ld, cfg_.mode, st_);
-  gemm_flops_ += 2 * static_cast<u64>(s.h_cols) * s.q_cols * s.h_rows;
-  clock_.end(st_);
-  on_comm([&](cudaStream_t cs) {
+  auto dw_gemm = [&]() {
+    gemm_launch(true, false, s.h_cols, s.q_cols, s.h_rows, h_[l].p(), h_[l].ld, dq, lddq, dwpart,
+                dwp_[l].ld, cfg_.mode, st_);
+    gemm_flops_ += 2 * static_cast<u64>(s.h_cols) * s.q_cols * s.h_rows;
+  };
+  auto dw_comm = [&](cudaStream_t cs) {
     if (lsa_dw) {  // reduce-scatter (engine.hpp:237): this member sums its own rows
       const int g = grid_.extent(lay.row), pos = c_.along(lay.row);
       const i64 o0 = chunk_start(s.f_cols, g, pos), o1 = chunk_start(s.f_cols, g, pos + 1);
@@ -838,7 +839,7 @@ void Engine::backward_layer(int l) {
     }
     comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
                            cs);
-  });
+  };
   // dH = dQ . W_full^T, then its all-reduce along inner, row-chunked
   const i64 lddh = pad4(s.h_cols);
   LsaGroup* lsa_dh = comms_.lsa(lay.inner);
@@ -846,27 +847,72 @@ void Engine::backward_layer(int l) {
   LsaGroup* fu_dh = s.q_cols <= 512 ? fused(lay.inner, kFuseGemm) : nullptr;
   RowMap map_dh;
   if (fu_dh) map_dh = fu_dh->slot_map(s.q_rows, lddh);
-  pipelined(
-      s.q_rows, fu_dh ? 1 : comm_chunks(s.q_rows, lay.inner),
-      [&](i64 r0, i64 r1) {
-        clock_.begin(2, st_);
-        gemm_launch(false, true, r1 - r0, s.h_cols, s.q_cols, dq + r0 * lddq, lddq,
-                    wfull_[l].p(), wfull_[l].ld, dhpart + r0 * lddh, lddh, cfg_.mode, st_, false,
-                    fu_dh ? &map_dh : nullptr);
-        clock_.end(st_);
-      },
-      [&](i64 r0, i64 r1) {
-        if (fu_dh) {
-          fu_dh->reduce_slots(s.q_rows, s.h_cols, lddh, dh_.p(), lddh, cs_);
-          comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
-        } else if (lsa_dh) {
-          lsa_dh->all_reduce(r0, r1, s.h_cols, lddh, dh_.p(), r0, lddh, cs_);
-          comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
-        } else {
-          comms_.all_reduce(dh_.p() + r0 * lddh, (r1 - r0) * lddh, lay.inner,
-                            (r1 - r0) * s.h_cols * 4, cs_);
-        }
-      });
+  auto dh_gemm = [&](i64 r0, i64 r1) {
+    clock_.begin(2, st_);
+    gemm_launch(false, true, r1 - r0, s.h_cols, s.q_cols, dq + r0 * lddq, lddq, wfull_[l].p(),
+                wfull_[l].ld, dhpart + r0 * lddh, lddh, cfg_.mode, st_, false,
+                fu_dh ? &map_dh : nullptr);
+    clock_.end(st_);
+  };
+  auto dh_reduce = [&](i64 r0, i64 r1) {
+    if (fu_dh) {
+      fu_dh->reduce_slots(s.q_rows, s.h_cols, lddh, dh_.p(), lddh, cs_);
+      comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
+    } else if (lsa_dh) {
+      lsa_dh->all_reduce(r0, r1, s.h_cols, lddh, dh_.p(), r0, lddh, cs_);
+      comms_.count(kAllReduce, lay.inner, (r1 - r0) * s.h_cols * 4);
+    } else {
+      comms_.all_reduce(dh_.p() + r0 * lddh, (r1 - r0) * lddh, lay.inner,
+                        (r1 - r0) * s.h_cols * 4, cs_);
+    }
+  };
+  // Order: when dH is reduced along a split inner axis, its GEMM goes first
+  // and the dW GEMM runs while dH crosses NVLink (the dW reduce-scatter and
+  // the W re-gather follow on the comm stream); otherwise the reference's
+  // order, with the dW reduce-scatter under the dH GEMM. PK_BWD_DH_FIRST=0
+  // keeps the reference's order everywhere.
+  static const bool dh_first_on = [] {
+    const char* e = std::getenv("PK_BWD_DH_FIRST");
+    return !(e && e[0] == '0');
+  }();
+  const bool dh_first = dh_first_on && comms_.size(lay.inner) > 1 && !fu_dh &&
+                        comm_chunks(s.q_rows, lay.inner) == 1;
+  cudaEvent_t bwd_comm_done = nullptr;
+  if (dh_first) {
+    clock_.end(st_);  // the dQ phase
+    dh_gemm(0, s.q_rows);
+    cudaEvent_t ready = sync_event();
+    PK_CUDA(cudaEventRecord(ready, st_));
+    PK_CUDA(cudaStreamWaitEvent(cs_, ready, 0));
+    cudaEvent_t c0 = clock_.stamp(cs_);
+    dh_reduce(0, s.q_rows);
+    clock_.add(4, c0, clock_.stamp(cs_));
+    cudaEvent_t dh_done = sync_event();
+    PK_CUDA(cudaEventRecord(dh_done, cs_));
+    clock_.begin(2, st_);
+    dw_gemm();
+    clock_.end(st_);
+    cudaEvent_t dw_ready = sync_event();
+    PK_CUDA(cudaEventRecord(dw_ready, st_));
+    PK_CUDA(cudaStreamWaitEvent(cs_, dw_ready, 0));
+    cudaEvent_t c1 = clock_.stamp(cs_);
+    dw_comm(cs_);
+    clock_.add(4, c1, clock_.stamp(cs_));
+    bwd_comm_done = sync_event();
+    PK_CUDA(cudaEventRecord(bwd_comm_done, cs_));
+    PK_CUDA(cudaStreamWaitEvent(st_, dh_done, 0));
+    // the dF partial below overwrites the row axis' scratch the dW
+    // reduce-scatter reads: then it waits for that too
+    if (lsa_dw) {
+      PK_CUDA(cudaStreamWaitEvent(st_, bwd_comm_done, 0));
+      bwd_comm_done = nullptr;
+    }
+  } else {
+    dw_gemm();
+    clock_.end(st_);
+    on_comm(dw_comm);
+    pipelined(s.q_rows, fu_dh ? 1 : comm_chunks(s.q_rows, lay.inner), dh_gemm, dh_reduce);
+  }
   gemm_flops_ += 2 * static_cast<u64>(s.q_rows) * s.h_cols * s.q_cols;
   // dF = A^T . dH, then reduce-scatter (layer 0) or all-reduce along
   // row_shard, row-chunked
@@ -934,6 +980,7 @@ void Engine::backward_layer(int l) {
   spmm_cbytes_ += spmm_compulsory_bytes(sh.at.rows, sh.nnz_t, sh.at.cols, s.f_cols);
   if (l > 0) std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
   df_masked_ = mask_spmm || mask_reduce;
+  if (bwd_comm_done) PK_CUDA(cudaStreamWaitEvent(st_, bwd_comm_done, 0));
 }
 
 // ---------------------------------------------------------------------------
