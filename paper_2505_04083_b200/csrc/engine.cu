@@ -608,6 +608,15 @@ void Engine::on_comm(const std::function<void(cudaStream_t)>& f) {
   PK_CUDA(cudaStreamWaitEvent(st_, done, 0));
 }
 
+void Engine::on_comm_nowait(const std::function<void(cudaStream_t)>& f) {
+  cudaEvent_t ready = sync_event();
+  PK_CUDA(cudaEventRecord(ready, st_));
+  PK_CUDA(cudaStreamWaitEvent(cs_, ready, 0));
+  cudaEvent_t a = clock_.stamp(cs_);
+  f(cs_);
+  clock_.add(4, a, clock_.stamp(cs_));
+}
+
 void Engine::forward_layer(int l, bool fault) {
   if (tf_[l]) return forward_layer_tf(l);
   const Layout& lay = lays_[l];
@@ -629,6 +638,13 @@ void Engine::forward_layer(int l, bool fault) {
   check(sh.a.cols == s.f_rows, "forward layer " + std::to_string(l) + ": adjacency shard " +
                                    shape(sh.a.rows, sh.a.cols) + " does not match features " +
                                    shape(s.f_rows, s.f_cols));
+  // W's all-gather goes out now, on the comm stream ahead of H's reduction,
+  // so it runs under the SpMM instead of between the reduction and the GEMM
+  // (the GEMM waits for the reduction, which follows it in stream order)
+  on_comm_nowait([&](cudaStream_t cs) {
+    comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
+                           cs);
+  });
   DMat& h = h_[l];
   // blocked aggregation (engine.hpp:175-192): SpMM row block b, then its
   // all-reduce along inner — overlapped with block b+1's SpMM
@@ -670,10 +686,6 @@ void Engine::forward_layer(int l, bool fault) {
                             (r1 - r0) * s.f_cols * 4, cs_);
         }
       });
-  on_comm([&](cudaStream_t cs) {
-    comms_.all_gather_rows(w_[l].p(), wfull_[l].p(), s.f_cols, wfull_[l].ld, lay.row, s.w_cols,
-                           cs);
-  });
   // Q = H . W_full, then its all-reduce along col_shard, row-chunked. Hidden
   // layers store only relu(Q) (the next layer's input and, since
   // relu(Q) > 0 <=> Q > 0, the backward's ReLU mask): the activation is

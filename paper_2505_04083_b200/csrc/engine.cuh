@@ -132,6 +132,9 @@ class Engine {
   void pipelined(i64 rows, int chunks, P&& produce, R&& reduce);
   int comm_chunks(i64 rows, int axis) const;
   void on_comm(const std::function<void(cudaStream_t)>& f);
+  // the same without making the compute stream wait: a later on_comm /
+  // pipelined reduction's completion covers it (comm stream order)
+  void on_comm_nowait(const std::function<void(cudaStream_t)>& f);
   void setup_lsa();
   static constexpr int kFuseSpmm = 1, kFuseGemm = 2;
   LsaGroup* fused(int axis, int producer) const;
