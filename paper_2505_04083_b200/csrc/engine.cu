@@ -1074,7 +1074,9 @@ void Engine::forward_layer_tf(int l) {
   // with gathers of at most v floats. Default 2: 24 lanes of 8-B gathers,
   // C2 epoch 52.2 vs 52.8 ms; at 16 B the padded width takes the 16-lane
   // group form, measured slower (2 x 5.6 vs 2 x 3.9 ms per C2 epoch).
-  const int tfv = tf_vec();
+  // (a width that is a multiple of 4 needs no padding and keeps 16-B and
+  // wider gathers: C3's 128)
+  const int tfv = s.w_cols % 4 ? tf_vec() : 0;
   spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, tfv ? ldp : s.w_cols,
            qout.p(), qout.ld, st_, nullptr, 0, nullptr, tfv ? tfv : 8);
   spmm_flops_ += 2 * sh.a.nnz * static_cast<u64>(s.w_cols);
@@ -1114,7 +1116,7 @@ void Engine::backward_layer_tf(int l) {
   RowMap map_r;
   if (fu_r) map_r = fu_r->slot_map(sh.at.rows, ldp);
   clock_.begin(5, st_);
-  const int tfv = tf_vec();
+  const int tfv = s.w_cols % 4 ? tf_vec() : 0;
   spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, tfv ? ldp : s.w_cols, dpp, ldp, st_,
            nullptr, 0, fu_r ? &map_r : nullptr, tfv ? tfv : 8);
   clock_.end(st_);
