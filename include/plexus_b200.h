@@ -136,6 +136,20 @@ int pk_spmm_plan_rows_relu_bwd_f32(const pk_spmm_plan* plan, const pk_csr* a,
                                    const float* mask, int64_t ldm, float* y,
                                    int64_t ldy, uint64_t* flops_host,
                                    void* stream);
+/* pk_spmm_plan_rows_f32 with flags. PK_SPMM_PAIRED (PK_MODE_FAST plans):
+ * rows of at most 16 gathered vectors (16-B, 8-B or 4-B, by alignment: up
+ * to 64 columns) are summed as two interleaved chains — the even and the
+ * odd nonzeros of each 32-nonzero window, each in the reference's order —
+ * added at the row end; a warp then gathers two rows per instruction.
+ * Deterministic; another association of the same sum (fp32-level
+ * difference, like the FAST plan's hub segments). Wider rows, and flags 0,
+ * are pk_spmm_plan_rows_f32. */
+#define PK_SPMM_PAIRED 1
+int pk_spmm_plan_rows_ex_f32(const pk_spmm_plan* plan, const pk_csr* a,
+                             int64_t r0, int64_t r1, const float* x,
+                             int64_t x_rows, int64_t ldx, int64_t d, float* y,
+                             int64_t ldy, int flags, uint64_t* flops_host,
+                             void* stream);
 /* number of hub rows and the hub threshold the plan chose */
 int pk_spmm_plan_info(const pk_spmm_plan* plan, int64_t* hub_rows,
                       int64_t* hub_threshold);

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libplexus_b200.so")
 (PK_OK, PK_ERR_CONTRACT, PK_ERR_CUDA, PK_ERR_NCCL, PK_ERR_MEMORY, PK_ERR_TRAINING,
  PK_ERR_ABORTED) = range(7)
 PK_MODE_PARITY, PK_MODE_FAST = 0, 1
+PK_SPMM_PAIRED = 1  # pk_spmm_plan_rows_ex_f32 flags
 
 
 class ContractError(RuntimeError):
@@ -100,6 +101,8 @@ SIGNATURES = {
                                     U64P, P]),
     "pk_spmm_plan_rows_relu_bwd_f32": (INT, [P, C.POINTER(pk_csr), I64, I64, P, I64, I64, I64,
                                              P, I64, P, I64, U64P, P]),
+    "pk_spmm_plan_rows_ex_f32": (INT, [P, C.POINTER(pk_csr), I64, I64, P, I64, I64, I64, P,
+                                       I64, INT, U64P, P]),
     "pk_spmm_plan_info": (INT, [P, I64P, I64P]),
     "pk_gemm_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),
     "pk_gemm_relu_f32": (INT, [INT, INT, I64, I64, I64, P, I64, P, I64, P, I64, INT, U64P, P]),

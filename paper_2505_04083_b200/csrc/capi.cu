@@ -76,7 +76,8 @@ u64 nnz_of_rows(const pk_csr* a, i64 r0, i64 r1, cudaStream_t st) {
 
 void spmm_common(const pk_csr* a, i64 r0, i64 r1, const float* x, i64 x_rows, i64 ldx, i64 d,
                  float* y, i64 ldy, u64* flops, cudaStream_t st, SpmmPlan* plan,
-                 const char* who, const float* mask = nullptr, i64 ldm = 0) {
+                 const char* who, const float* mask = nullptr, i64 ldm = 0,
+                 bool paired = false) {
   check_csr(a, who);
   check(a->cols == x_rows, std::string(who) + ": A is " + csr_shape(a) + " but X is " +
                                shape(x_rows, d));
@@ -84,7 +85,7 @@ void spmm_common(const pk_csr* a, i64 r0, i64 r1, const float* x, i64 x_rows, i6
   check(d >= 0 && ldx >= d && ldy >= d, std::string(who) + ": leading dimension smaller than width");
   check(!mask || ldm >= d, std::string(who) + ": mask leading dimension smaller than width");
   if (plan) {
-    spmm_run(*plan, *a, r0, r1, x, ldx, d, y, ldy, st, mask, ldm);
+    spmm_run(*plan, *a, r0, r1, x, ldx, d, y, ldy, st, mask, ldm, nullptr, 8, paired);
   } else {
     // a one-off call builds a throwaway plan (the engine keeps one per shard)
     SpmmPlan tmp;
@@ -204,6 +205,21 @@ int pk_spmm_plan_rows_relu_bwd_f32(const pk_spmm_plan* plan, const pk_csr* a, in
     check(mask != nullptr, "spmm relu_backward: null mask");
     spmm_common(a, r0, r1, x, x_rows, ldx, d, y, ldy, flops_host, as_stream(stream),
                 const_cast<SpmmPlan*>(&plan->plan), "spmm_rows_relu_backward", mask, ldm);
+  });
+}
+
+int pk_spmm_plan_rows_ex_f32(const pk_spmm_plan* plan, const pk_csr* a, int64_t r0, int64_t r1,
+                             const float* x, int64_t x_rows, int64_t ldx, int64_t d, float* y,
+                             int64_t ldy, int flags, uint64_t* flops_host, void* stream) {
+  return guard([&] {
+    check(plan != nullptr, "spmm plan: null plan");
+    check(a != nullptr && plan->plan.rows == a->rows, "spmm plan: plan built for another matrix");
+    check((flags & ~PK_SPMM_PAIRED) == 0, "spmm_rows_ex: unknown flags");
+    check(!(flags & PK_SPMM_PAIRED) || plan->plan.segment,
+          "spmm_rows_ex: PK_SPMM_PAIRED needs a PK_MODE_FAST plan");
+    spmm_common(a, r0, r1, x, x_rows, ldx, d, y, ldy, flops_host, as_stream(stream),
+                const_cast<SpmmPlan*>(&plan->plan), "spmm_rows_ex", nullptr, 0,
+                (flags & PK_SPMM_PAIRED) != 0);
   });
 }
 

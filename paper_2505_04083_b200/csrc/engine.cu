@@ -1015,6 +1015,17 @@ int Engine::tf_vec() {
   return v;
 }
 
+// The narrow SpMMs in the paired form (two nonzeros per warp gather,
+// spmm_pair_kernel) where the padded width allows it; PK_TF_PAIR=0 keeps
+// the list kernel.
+bool Engine::tf_pair() {
+  static const bool v = [] {
+    const char* e = std::getenv("PK_TF_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 void Engine::forward_layer_tf(int l) {
   const Layout& lay = lays_[l];
   const Shapes& s = shapes_[l];
@@ -1078,7 +1089,7 @@ void Engine::forward_layer_tf(int l) {
   // wider gathers: C3's 128)
   const int tfv = s.w_cols % 4 ? tf_vec() : 0;
   spmm_run(sh.plan_a, view(sh.a), 0, sh.a.rows, tfbuf_.p(), ldp, tfv ? ldp : s.w_cols,
-           qout.p(), qout.ld, st_, nullptr, 0, nullptr, tfv ? tfv : 8);
+           qout.p(), qout.ld, st_, nullptr, 0, nullptr, tfv ? tfv : 8, tf_pair());
   spmm_flops_ += 2 * sh.a.nnz * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.a.rows, sh.a.nnz, s.w_cols);
   spmm_cbytes_ += spmm_compulsory_bytes(sh.a.rows, sh.a.nnz, sh.a.cols, s.w_cols);
@@ -1118,7 +1129,7 @@ void Engine::backward_layer_tf(int l) {
   clock_.begin(5, st_);
   const int tfv = s.w_cols % 4 ? tf_vec() : 0;
   spmm_run(sh.plan_at, view(sh.at), 0, sh.at.rows, dq, lddq, tfv ? ldp : s.w_cols, dpp, ldp, st_,
-           nullptr, 0, fu_r ? &map_r : nullptr, tfv ? tfv : 8);
+           nullptr, 0, fu_r ? &map_r : nullptr, tfv ? tfv : 8, tf_pair());
   clock_.end(st_);
   spmm_flops_ += 2 * sh.nnz_t * static_cast<u64>(s.w_cols);
   spmm_bytes_ += spmm_alg_bytes(sh.at.rows, sh.nnz_t, s.w_cols);

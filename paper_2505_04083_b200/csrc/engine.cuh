@@ -115,6 +115,7 @@ class Engine {
   void backward_layer(int l);
   void forward_layer_tf(int l);
   static int tf_vec();
+  static bool tf_pair();
   void backward_layer_tf(int l);
   std::vector<char> tf_;  // transform-first layers (see engine.cu)
   void loss();

@@ -436,6 +436,148 @@ spmm_list_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
   }
 }
 
+// ---------------------------------------------------------------------------
+// paired narrow form (FAST, opt-in): rows of at most 16 vectors, e.g. the
+// transform-first layers' 48-wide P / dQ (engine.cu forward_layer_tf). The
+// plain form gives such a row one lane group per chunk, so a warp gather
+// moves one nonzero's 192 B and the pass is bound by gathers in flight (C2:
+// 1.6 TB/s DRAM, 3.9 ms per pass for 1 GB of compulsory bytes). Here a
+// warp's two halves take a window's even and odd nonzeros, so every gather
+// instruction moves two rows and half as many instructions cover a window.
+// Each half keeps a running chain (even / odd stream positions within the
+// chunk, each k-ascending, fl(acc + fl(v x)) like the reference); at a row
+// end the halves' chains are added (one shuffle) and the even half stores.
+// A two-chain sum is another association of the same row: tolerance-level
+// (FAST), deterministic (fixed chunks), so callers opt in (PK_SPMM_PAIRED).
+#ifndef PK_PAIR_U
+#define PK_PAIR_U 4
+#endif
+#ifndef PK_PAIR_MINB
+#define PK_PAIR_MINB 4
+#endif
+
+__device__ __forceinline__ float fold_halves(float a) {
+  return __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 16));
+}
+__device__ __forceinline__ float2 fold_halves(float2 a) {
+  return make_float2(fold_halves(a.x), fold_halves(a.y));
+}
+__device__ __forceinline__ float4 fold_halves(float4 a) {
+  return make_float4(fold_halves(a.x), fold_halves(a.y), fold_halves(a.z), fold_halves(a.w));
+}
+
+template <int VEC, int U, bool MAPPED>
+__global__ void __launch_bounds__(kThreads, PK_PAIR_MINB)
+spmm_pair_kernel(ListArgs a, const i64* __restrict__ bounds, int nchunks,
+                 int* __restrict__ counters) {
+  using V = typename Vec<VEC>::T;
+  constexpr unsigned kAll = 0xffffffffu;
+  constexpr int kSteps = 16;  // pair steps per 32-nonzero window
+  const int lane = threadIdx.x % 32, half = lane / 16, col = lane % 16;
+  const bool valid = col < a.nvec;
+  const float* xlane = a.x + col * VEC;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(counters, 1);
+    t = __shfl_sync(kAll, t, 0);
+    if (t >= nchunks) break;
+    const i64 is = bounds[t], ie = bounds[t + 1];
+    if (is >= ie) continue;
+    u64 k = __ldg(a.rpc + is);
+    const u64 kend = __ldg(a.rpc + ie);
+    i64 rb = is;
+    u32 rid = rb + lane < ie ? __ldg(a.rl + rb + lane) : 0u;
+    int rn = 0;
+    V acc = Vec<VEC>::zero();
+    auto row_done = [&]() {
+      const V tot = fold_halves(acc);
+      const u32 row = __shfl_sync(kAll, rid, rn);
+      if (half == 0 && valid) {
+        float* yrow;
+        if (row & 0x80000000u) {
+          yrow = a.part + static_cast<i64>(row & 0x7fffffffu) * a.ldp;
+        } else if constexpr (MAPPED) {
+          yrow = a.map.row(a.y, a.ldy, static_cast<i64>(row) - a.r0);
+        } else {
+          yrow = a.y + (static_cast<i64>(row) - a.r0) * a.ldy;
+        }
+        *reinterpret_cast<V*>(yrow + col * VEC) = tot;
+      }
+      acc = Vec<VEC>::zero();
+      if (++rn == 32) {
+        rn = 0;
+        rb += 32;
+        rid = rb + lane < ie ? __ldg(a.rl + rb + lane) : 0u;
+      }
+    };
+    // pair step s: this lane's nonzero is 2s + half of the window
+    auto step = [&](const V& xv, u32 wv, unsigned em, int s, bool odd_live) {
+      const float v = __uint_as_float(__shfl_sync(kAll, wv, 2 * s + half));
+      if (half == 0) madd(acc, v, xv);
+      if ((em >> (2 * s)) & 1u) row_done();
+      if (half == 1 && odd_live) madd(acc, v, xv);
+      if (odd_live && ((em >> (2 * s + 1)) & 1u)) row_done();
+    };
+    auto gather = [&](V (&xv)[U], u32 wc, int s0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const u32 c = __shfl_sync(kAll, wc, 2 * (s0 + u) + half);
+        xv[u] = valid ? ldg<V>(xlane + static_cast<i64>(c & 0x7fffffffu) * a.ldx)
+                      : Vec<VEC>::zero();
+      }
+    };
+    auto consume = [&](const V (&xv)[U], u32 wv, unsigned em, int s0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) step(xv[u], wv, em, s0 + u, true);
+    };
+    // the list kernel's software pipeline, over pair steps: the gathers of
+    // group g+1 (or the next window's group 0) are issued before group g is
+    // consumed
+    u64 w = k + lane < kend ? __ldcs(a.cv + k + lane) : 0ull;
+    V xa[U], xb[U];
+    bool primed = false;
+    while (k < kend) {
+      const int cnt = static_cast<int>(min(static_cast<u64>(32), kend - k));
+      const u64 wn = k + 32 + lane < kend ? __ldcs(a.cv + k + 32 + lane) : 0ull;
+      const unsigned em = end_mask(a.endbits, k);
+      const u32 wc = static_cast<u32>(w), wv = static_cast<u32>(w >> 32);
+      if (cnt == 32) {
+        if (!primed) gather(xa, wc, 0);
+        const bool next_full = k + 64 <= kend;
+#pragma unroll
+        for (int s = 0; s < kSteps; s += 2 * U) {
+          if (s + U < kSteps) gather(xb, wc, s + U);
+          else if (next_full) gather(xb, static_cast<u32>(wn), 0);
+          consume(xa, wv, em, s);
+          if (s + U < kSteps) {
+            if (s + 2 * U < kSteps) gather(xa, wc, s + 2 * U);
+            else if (next_full) gather(xa, static_cast<u32>(wn), 0);
+            consume(xb, wv, em, s + U);
+          }
+        }
+        primed = next_full && ((kSteps / U) % 2 == 0);
+        if (next_full && (kSteps / U) % 2 == 1) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) xa[u] = xb[u];
+          primed = true;
+        }
+      } else {
+        for (int s = 0; 2 * s < cnt; ++s) {
+          const int j = 2 * s + half;
+          const u32 c = __shfl_sync(kAll, wc, j);
+          const V xv = valid && j < cnt
+                           ? ldg<V>(xlane + static_cast<i64>(c & 0x7fffffffu) * a.ldx)
+                           : Vec<VEC>::zero();
+          step(xv, wv, em, s, 2 * s + 1 < cnt);
+        }
+        primed = false;
+      }
+      k += cnt;
+      w = wn;
+    }
+  }
+}
+
 // FAST plan: y[hub row] = fold of its segment sums in segment order
 template <bool MAPPED>
 __global__ void combine_segments_kernel(const u32* __restrict__ hub, const u32* __restrict__ seg0,
@@ -710,6 +852,37 @@ void launch_list(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t
   dim3 grid(static_cast<unsigned>(blocks), slices);
   kernel<<<grid, kThreads, 0, st>>>(a, ws.bounds.p, nchunks, ws.counters.p);
   PK_LAUNCH("spmm list kernel");
+}
+
+template <int VEC>
+void launch_pair(const ListArgs& a, i64 i0, i64 i1, const u64* rpc, cudaStream_t st) {
+  constexpr int U = PK_PAIR_U;
+  const bool mapped = a.map.g != 0;
+  auto kernel = mapped ? spmm_pair_kernel<VEC, U, true> : spmm_pair_kernel<VEC, U, false>;
+  static const i64 per_sm = [] {
+    const char* e = std::getenv("PK_LIST_CHUNKS");
+    return e ? std::max<i64>(1, std::atoll(e)) : i64{512};
+  }();
+  const int nchunks = static_cast<int>(
+      std::max<i64>(1, std::min<i64>(i1 - i0, static_cast<i64>(sm_count()) * per_sm)));
+  static thread_local ListWorkspace ws;
+  ws.bounds.ensure(nchunks + 1);
+  ws.counters.ensure(1);
+  list_partition_kernel<<<ceil_div(nchunks + 1, 256), 256, 0, st>>>(rpc, i0, i1, nchunks,
+                                                                    ws.bounds.p, ws.counters.p, 1);
+  PK_LAUNCH("spmm pair partition");
+  static thread_local int occs[2] = {0, 0};
+  int& occ = occs[mapped ? 1 : 0];
+  if (occ == 0) {
+    PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0));
+    occ = std::max(occ, 1);
+  }
+  const i64 warps = kThreads / 32;
+  const i64 blocks = std::max<i64>(
+      1, std::min<i64>(static_cast<i64>(sm_count()) * occ, (nchunks + warps - 1) / warps));
+  kernel<<<static_cast<unsigned>(blocks), kThreads, 0, st>>>(a, ws.bounds.p, nchunks,
+                                                             ws.counters.p);
+  PK_LAUNCH("spmm pair kernel");
 }
 
 template <int VEC>
@@ -1149,7 +1322,7 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
               float* y, i64 ldy, cudaStream_t st, const float* mask, i64 ldm,
-              const RowMap* map, int max_vec) {
+              const RowMap* map, int max_vec, bool paired) {
   if (r1 <= r0 || d == 0) return;
   SpmmPlan::Range& rg = plan_range(plan, r0, r1, st);
   const RowMap rmap = map ? *map : RowMap{};
@@ -1161,6 +1334,14 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   // the mask is read with y's vector width: it must share y's alignment
   int vec = pick_vec(x, ldx, y, ldy, d, plan.segment || rg.hubs == 0);
   while (vec > max_vec) vec /= 2;
+  // the paired narrow form: FAST plans, no epilogue mask, at most 16 vectors
+  // of up to 16 B per row
+  int pair_vec = 0;
+  if (paired && plan.segment && !mask) {
+    const int pv = pick_vec(x, ldx, y, ldy, d, false);
+    if (d / pv <= 16) pair_vec = pv;
+  }
+  if (pair_vec) vec = pair_vec;
   if (mask)
     while (vec > 1 && (ldm % vec || (reinterpret_cast<uintptr_t>(mask) % (vec * 4)))) vec /= 2;
   const int nvec = static_cast<int>(d / vec);
@@ -1204,7 +1385,13 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
       plan.partial.ensure(plan.segments * la.ldp);
       la.part = plan.partial.p;
     }
-    if (vec == 8)
+    if (pair_vec == 4)
+      launch_pair<4>(la, rg.i0, rg.i1, plan.rpc.p, st);
+    else if (pair_vec == 2)
+      launch_pair<2>(la, rg.i0, rg.i1, plan.rpc.p, st);
+    else if (pair_vec == 1)
+      launch_pair<1>(la, rg.i0, rg.i1, plan.rpc.p, st);
+    else if (vec == 8)
       dispatch_list<8>(la, rg.i0, rg.i1, plan.rpc.p, st);
     else if (vec == 4)
       dispatch_list<4>(la, rg.i0, rg.i1, plan.rpc.p, st);

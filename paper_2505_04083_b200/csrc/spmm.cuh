@@ -86,10 +86,12 @@ void spmm_plan_build(SpmmPlan& plan, const pk_csr& a, u64 threshold, cudaStream_
 // previous layer fused into this SpMM^T's epilogue.
 // map (optional, FAST / hub-free plans only): output row lr = row - r0 goes
 // to map->row(y, ldy, lr) — a reduction's owner slots (RowMap).
-// max_vec caps the gather width in floats (8 = no cap).
+// max_vec caps the gather width in floats (8 = no cap). paired (FAST plans,
+// rows of at most 16 vectors, no mask): each row summed as two interleaved
+// chains added at the row end (spmm_pair_kernel) — tolerance-level.
 void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i64 ldx, i64 d,
               float* y, i64 ldy, cudaStream_t st, const float* mask = nullptr, i64 ldm = 0,
-              const RowMap* map = nullptr, int max_vec = 8);
+              const RowMap* map = nullptr, int max_vec = 8, bool paired = false);
 
 // Per-thread fork/join stream used to overlap hub CTAs with the list kernel.
 struct SideStream {

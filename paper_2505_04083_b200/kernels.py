@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _capi
-from ._capi import PK_MODE_FAST, PK_MODE_PARITY, ContractError, call
+from ._capi import PK_MODE_FAST, PK_MODE_PARITY, PK_SPMM_PAIRED, ContractError, call
 
 __all__ = ["DeviceCsr", "spmm", "spmm_rows", "gemm", "relu_forward", "relu_backward",
            "softmax_cross_entropy_sums", "softmax_cross_entropy", "AdamParams", "AdamState",
@@ -151,8 +151,11 @@ def _flops_out(flops):
 
 
 def spmm_rows(a: DeviceCsr, x: torch.Tensor, r0: int, r1: int, flops=None, out=None,
-              plan=None, stream=None):
-    """spmm_rows (kernels.hpp:39-62): rows [r0, r1) of A . X, bit-exact."""
+              plan=None, stream=None, paired=False):
+    """spmm_rows (kernels.hpp:39-62): rows [r0, r1) of A . X, bit-exact.
+    paired=True (a PK_MODE_FAST plan; rows of <= 64 columns): each row as two
+    interleaved chains added at the row end (PK_SPMM_PAIRED) — fp32-level
+    difference, deterministic."""
     d = x.shape[1]
     if a.cols != x.shape[0]:
         raise ContractError(f"spmm_rows: A is {a.rows}x{a.cols} but X is {x.shape[0]}x{d}")
@@ -161,7 +164,11 @@ def spmm_rows(a: DeviceCsr, x: torch.Tensor, r0: int, r1: int, flops=None, out=N
     fl = _flops_out(flops)
     args = [a.view(), r0, r1, _ptr(x), x.shape[0], _ld(x), d, _ptr(out), _ld(out),
             C.byref(fl) if fl is not None else None, _stream(stream)]
-    if plan is not None:
+    if paired:
+        if plan is None:
+            raise ContractError("spmm_rows: paired=True needs a PK_MODE_FAST plan")
+        call("pk_spmm_plan_rows_ex_f32", plan.h, *args[:-2], PK_SPMM_PAIRED, *args[-2:])
+    elif plan is not None:
         call("pk_spmm_plan_rows_f32", plan.h, *args)
     else:
         call("pk_spmm_rows_f32", *args)
@@ -191,11 +198,13 @@ def spmm_rows_relu_backward(a: DeviceCsr, x: torch.Tensor, r0: int, r1: int, mas
     return out
 
 
-def spmm(a: DeviceCsr, x: torch.Tensor, flops=None, out=None, plan=None, stream=None):
-    """spmm (kernels.hpp:16-37): A . X, bit-exact."""
+def spmm(a: DeviceCsr, x: torch.Tensor, flops=None, out=None, plan=None, stream=None,
+         paired=False):
+    """spmm (kernels.hpp:16-37): A . X, bit-exact (paired: see spmm_rows)."""
     if a.cols != x.shape[0]:
         raise ContractError(f"spmm: A is {a.rows}x{a.cols} but X is {x.shape[0]}x{x.shape[1]}")
-    return spmm_rows(a, x, 0, a.rows, flops=flops, out=out, plan=plan, stream=stream)
+    return spmm_rows(a, x, 0, a.rows, flops=flops, out=out, plan=plan, stream=stream,
+                     paired=paired)
 
 
 def gemm(a, b, transpose_a=False, transpose_b=False, flops=None, mode=PK_MODE_PARITY, out=None,

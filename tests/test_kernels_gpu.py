@@ -335,6 +335,48 @@ def test_spmm_fast_plan_segments_tolerance(cuda, d):
     assert np.array_equal(part.view(np.uint32), got[50:160].view(np.uint32))
 
 
+@pytest.mark.parametrize("d,ld", [(1, 1), (7, 7), (16, 16), (30, 30), (47, 48), (48, 48),
+                                  (64, 64), (100, 100)])
+def test_spmm_paired_form_tolerance(cuda, d, ld):
+    """PK_SPMM_PAIRED (the transform-first layers' narrow SpMMs): each row as
+    two interleaved chains added at the row end. Deterministic, within fp32
+    rounding of the reference's single chain, row ranges through the same
+    plan; rows wider than 16 vectors take the plain (bit-identical) form."""
+    k = _k()
+    rng = np.random.default_rng(1000 + d)
+    n_rows, n_cols = 3000, 20000
+    lens = rng.integers(0, 70, size=n_rows)
+    lens[rng.random(n_rows) < 0.3] = 1                 # single-nonzero rows
+    lens[[3, 777, 1500]] = [4500, 9000, 5001]           # hub rows (segments)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    ci = np.concatenate([np.sort(rng.choice(n_cols, size=l, replace=False)) for l in lens])
+    vals = rng.uniform(-1, 1, size=ci.size).astype(np.float32)
+    a = k.DeviceCsr.from_host(n_rows, n_cols, rp, ci.astype(np.uint32), vals)
+    xh = rng.uniform(-1, 1, size=(n_cols, ld)).astype(np.float32)
+    xh[:, d:] = 0
+    x = torch.from_numpy(xh).to(cuda)  # the engine's padded width (47 -> 48, zero columns)
+    want = restate.spmm_rows(rp, ci.astype(np.uint32), vals, xh[:, :ld], 0, n_rows)
+    plan = k.SpmmPlan(a, hub_threshold=4096, mode=k.PK_MODE_FAST)
+    got = k.spmm(a, x, plan=plan, paired=True).cpu().numpy()
+    again = k.spmm(a, x, plan=plan, paired=True).cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), again.view(np.uint32))
+    plain = k.spmm(a, x, plan=plan).cpu().numpy()
+    if ld > 64:
+        assert np.array_equal(got.view(np.uint32), plain.view(np.uint32))
+    # each of the two sums is within (n + 1) u sum|v x| of the exact one
+    bound = 2 * (lens[:, None] + 2) * 2.0 ** -24 * (
+        np.abs(vals)[None, :].max() * np.abs(xh[:, :ld]).max() * lens[:, None])
+    err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+    assert (err <= bound + 1e-30).all(), float((err - bound).max())
+    if ld > d:
+        assert not got[:, d:].any()  # padding columns stay exactly +0
+    part = k.spmm_rows(a, x, 500, 2600, plan=plan, paired=True).cpu().numpy()
+    assert np.array_equal(part.view(np.uint32), got[500:2600].view(np.uint32))
+    exact = k.SpmmPlan(a, hub_threshold=4096, mode=k.PK_MODE_PARITY)
+    with pytest.raises(k.ContractError):
+        k.spmm(a, x, plan=exact, paired=True)
+
+
 @pytest.mark.parametrize("d", [1, 7, 64, 100, 256])
 @pytest.mark.parametrize("mode", ["parity", "fast"])
 def test_spmm_relu_backward_fused(cuda, d, mode):
