@@ -1015,13 +1015,15 @@ int Engine::tf_vec() {
   return v;
 }
 
-// The narrow SpMMs in the paired form (two nonzeros per warp gather,
-// spmm_pair_kernel) where the padded width allows it; PK_TF_PAIR=0 keeps
-// the list kernel.
+// PK_TF_PAIR=1: the narrow SpMMs in the paired form (two nonzeros per warp
+// gather, spmm_pair_kernel). Measured neutral on C2 (3.69-3.73 vs 3.69 ms
+// per 48-wide pass, 5.7 GB DRAM either way: the pass is bound by random
+// 192-B DRAM reads, not by gather instructions), so the list kernel —
+// bit-identical to PARITY on regular rows — stays the default.
 bool Engine::tf_pair() {
   static const bool v = [] {
     const char* e = std::getenv("PK_TF_PAIR");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return v;
 }

@@ -66,6 +66,12 @@ constexpr int kConvRingWarps = kLoaderWarps - 2;  // ring mode: warps 2..7
 // length; 16 stages (512 k) keep the tall dW reduction (K = adjacency rows,
 // up to millions) at fp32-level error (tests/test_gemm_tc_gpu.py).
 constexpr int kSegStages = 16;
+#ifndef PK_TC_RB
+#define PK_TC_RB 2
+#endif
+#ifndef PK_TC_RB_NARROW
+#define PK_TC_RB_NARROW 8  // BN <= 64: the K = 256 weight images stay resident
+#endif
 
 __device__ unsigned g_gemm_watchdog = 0;
 
@@ -464,6 +470,7 @@ struct TcParams {
   float* c;         // output (splits == 1) or partials [split][m][ldc]
   i64 ldc;
   i64 split_stride; // elements between split partials
+  int resident_ok = 1;  // weight-resident ring allowed (PK_TC_RESIDENT=0: off)
   int relu;         // 1: the final value is stored as relu(v) (v > 0 ? v : 0)
   RowMap map;       // output row placement (g == 0: c + row * ldc)
 };
@@ -484,7 +491,9 @@ struct TcConfig {
   // Ring layout (TMA + weight image, single-CTA): the raw A tiles, their lo
   // tiles and the weight images live in three rings of their own depth, so
   // the DRAM-fed raw ring can run far ahead of the L2-fed weight ring.
-  static constexpr int kRB = 2;                 // weight images (hi | lo)
+  // weight images (hi | lo): L2-fed, so a narrow tile's ring needs more
+  // slots in flight to cover the L2 latency (PK_TC_RB / PK_TC_RB_NARROW)
+  static constexpr int kRB = BN <= 64 ? PK_TC_RB_NARROW : PK_TC_RB;
   static constexpr int kRL = 2;                 // converted lo tiles
   static constexpr int kRingBudget = 224 * 1024;
   static constexpr int kRA = std::min(8, (kRingBudget - kRB * 2 * kTileB - kRL * kTileA) / kTileA);
@@ -589,6 +598,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const unsigned tmem = tmem_base;
 
   const int total_tiles = PAIR ? (p.m_tiles + 1) / 2 : p.m_tiles * p.n_tiles * p.splits;
+  // Weight-resident ring: one n tile, no k split, and every k-stage's
+  // weight image fits the ring — each CTA loads the images once and keeps
+  // them (slot = k-stage) instead of re-streaming them from L2 for every m
+  // tile (C2: T = H W3 and dH3 = dT W3^T, where the images were as many
+  // bytes per tile as the A rows).
+  const int nk_all = static_cast<int>((p.k + kBK - 1) / kBK);
+  const bool resident =
+      kRing && !PAIR && p.resident_ok && p.n_tiles == 1 && p.splits == 1 && nk_all > 0 &&
+      nk_all <= kRB;
   // a tile index is live while its cluster leader's is (phantoms beyond)
   auto live = [&](int t) { return PAIR ? t < total_tiles : t - crank < total_tiles; };
   // n tile fastest: the CTAs that share an A row block (several n tiles)
@@ -665,6 +683,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         // ------------------------------------- weight image producer (L2)
         Pos q;
         start(q, tile_first);
+        if (resident) {
+          // every stage's image once, into slot kk, for all of this CTA's tiles
+          if (valid(q))
+            for (int i = 0; i < nk_all; ++i) {
+              mbar_expect_tx(&rb_full[i], 2u * Cfg::kTileB);
+              bulk_copy_g2s(rb_slot(i), p.b_image + static_cast<i64>(i) * 2 * Cfg::kTileB,
+                            2u * Cfg::kTileB, &rb_full[i]);
+              mbar_arrive(&rb_full[i]);
+            }
+        } else
         for (u64 s = 0; valid(q); ++s) {
           const int i = static_cast<int>(s % kRB);
           const unsigned ph = static_cast<unsigned>((s / kRB) & 1);
@@ -916,10 +944,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int kk = k_lo; kk < k_hi; ++kk) {
           if constexpr (kRing) {
             const int ia = static_cast<int>(ring_s % kRA), il = static_cast<int>(ring_s % kRL),
-                      ib = static_cast<int>(ring_s % kRB);
+                      ib = resident ? kk : static_cast<int>(ring_s % kRB);
             TC_PROF_WAIT(2, mbar_wait(&ra_full[ia], static_cast<unsigned>((ring_s / kRA) & 1)));
             TC_PROF_WAIT(6, mbar_wait(&rl_full[il], static_cast<unsigned>((ring_s / kRL) & 1)));
-            mbar_wait(&rb_full[ib], static_cast<unsigned>((ring_s / kRB) & 1));
+            mbar_wait(&rb_full[ib], resident ? 0u : static_cast<unsigned>((ring_s / kRB) & 1));
             tc_fence_after();
             if (lane == 0) {
               const unsigned a_hi = smem_u32(ra_slot(ia)), a_lo = smem_u32(rl_slot(il));
@@ -949,7 +977,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               } else {
                 tc_commit(&ra_empty[ia]);
                 tc_commit(&rl_empty[il]);
-                tc_commit(&rb_empty[ib]);
+                if (!resident) tc_commit(&rb_empty[ib]);
               }
             }
             __syncwarp();
@@ -1276,6 +1304,11 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     attr[variant] = true;
   }
   TcParams p = p0;
+  static const int resident_ok = [] {
+    const char* e = std::getenv("PK_TC_RESIDENT");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  p.resident_ok = resident_ok;
   if (B_PRE) {
     // split the weight once per call into its per-stage tile images
     const i64 stages = (p.k + kBK - 1) / kBK;
