@@ -789,6 +789,11 @@ void Engine::finish_pass(int epoch, double* loss_out, double* acc_out, const dou
   check_device_watchdogs();
   const double* h = sums;
   const u64 count = static_cast<u64>(h[1]), correct = static_cast<u64>(h[2]);
+  if (count == 0 && comms_.solo()) {  // measurement mode: this rank holds no loss rows
+    if (loss_out) *loss_out = 0;
+    if (acc_out) *acc_out = 0;
+    return;
+  }
   if (count == 0)
     throw Error(PK_ERR_TRAINING,
                 "epoch " + std::to_string(epoch) + ": no nodes selected by the training mask");
@@ -798,7 +803,8 @@ void Engine::finish_pass(int epoch, double* loss_out, double* acc_out, const dou
                                      std::to_string(loss) + ")");
   if (loss_out) *loss_out = loss;
   if (acc_out) *acc_out = static_cast<double>(correct) / static_cast<double>(count);
-  check(count == mask_count_, "cross entropy: counted " + std::to_string(count) +
+  // (measurement mode counts only this rank's rows)
+  check(comms_.solo() || count == mask_count_, "cross entropy: counted " + std::to_string(count) +
                                   " masked rows, expected " + std::to_string(mask_count_));
 }
 

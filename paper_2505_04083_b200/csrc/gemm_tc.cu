@@ -69,6 +69,9 @@ constexpr int kSegStages = 16;
 #ifndef PK_TC_RB
 #define PK_TC_RB 2
 #endif
+#ifndef PK_EPI_V8
+#define PK_EPI_V8 1
+#endif
 #ifndef PK_TC_RB_NARROW
 #define PK_TC_RB_NARROW 8  // BN <= 64: the K = 256 weight images fit (resident mode)
 #endif
@@ -1056,6 +1059,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const i64 n0 = static_cast<i64>(nt) * BN;
       float* out = p.c + static_cast<i64>(sp) * p.split_stride;
       const bool vec_out = (p.ldc % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+      // 32-B row pieces as one 256-bit store (a full sector per thread: half
+      // the L2 write requests of two 16-B stores; the epilogue is what bounds
+      // the wide-N small-K tiles, PK_TC_PROF)
+      const bool v8_out = PK_EPI_V8 && p.ldc % 8 == 0 && !p.map.g &&
+                          ((reinterpret_cast<uintptr_t>(out) & 31) == 0);
       // segments of one tile land in order: the first stores, later ones add
       // (fp32 round-to-nearest in registers, fixed order: deterministic); the
       // fused ReLU applies to the last segment's sum (never to split partials)
@@ -1088,7 +1096,30 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           if (gm < p.m) {
             float* dst = p.map.row(out, p.ldc, gm) + n0 + c0;
             const i64 left = p.n - (n0 + c0);
-            if (vec_out && left >= CH) {
+            if (v8_out && left >= CH) {
+#pragma unroll
+              for (int j = 0; j < CH / 8; ++j) {
+                float* d8 = dst + 8 * j;
+                float* w = v + 8 * j;
+                if (sg > 0) {
+                  float o[8];
+                  asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                               : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]), "=f"(o[4]),
+                                 "=f"(o[5]), "=f"(o[6]), "=f"(o[7])
+                               : "l"(d8));
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) w[i] += o[i];
+                }
+                if (relu) {
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) w[i] = w[i] > 0.f ? w[i] : 0.f;
+                }
+                asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d8),
+                             "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]), "f"(w[4]), "f"(w[5]),
+                             "f"(w[6]), "f"(w[7])
+                             : "memory");
+              }
+            } else if (vec_out && left >= CH) {
               float4* d4 = reinterpret_cast<float4*>(dst);
               if (sg > 0) {
                 float4 o[CH / 4];
