@@ -1168,10 +1168,20 @@ void Engine::backward_layer_tf(int l) {
   gemm_launch(true, false, o1 - o0, s.w_cols, s.f_rows, f + o0, ldf, dp, ldp, dw_[l].p(),
               dw_[l].ld, cfg_.mode, st_);
   gemm_flops_ += 2 * static_cast<u64>(o1 - o0) * s.w_cols * s.f_rows;
+  bool masked = false;
   if (l > 0) {
     const i64 lddf = pad4(s.f_cols);
+    // dF is complete here (no reduction follows), so layer l-1's relu'
+    // (kernels.hpp:103-111, mask relu(Q_{l-1}) = this layer's F) can ride
+    // the GEMM epilogue instead of a separate pass over dF (PK_GEMM_RELU_BWD)
+    static const bool fuse_mask = [] {
+      const char* e = std::getenv("PK_GEMM_RELU_BWD");
+      return !(e && e[0] == '0');
+    }();
+    masked = fuse_mask;
     gemm_launch(false, true, s.f_rows, s.f_cols, s.w_cols, dp, ldp, wfull_[l].p(), wfull_[l].ld,
-                df_.p(), lddf, cfg_.mode, st_);
+                df_.p(), lddf, cfg_.mode, st_, false, nullptr, masked ? f : nullptr,
+                masked ? ldf : 0);
     gemm_flops_ += 2 * static_cast<u64>(s.f_rows) * s.f_cols * s.w_cols;
     std::swap(df_.buf, df_prev_.buf);  // becomes dF_out of layer l-1
   } else {
@@ -1182,7 +1192,7 @@ void Engine::backward_layer_tf(int l) {
     gemm_flops_ += 2 * static_cast<u64>(own1 - own0) * s.f_cols * s.w_cols;
   }
   clock_.end(st_);
-  df_masked_ = false;
+  df_masked_ = masked;
 }
 
 // Symmetric scratch for the ordered peer-memory reductions: per axis the

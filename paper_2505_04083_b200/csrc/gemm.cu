@@ -214,8 +214,17 @@ void gemm_simt_dispatch(i64 m, i64 n, i64 k, const float* a, i64 lda, const floa
 
 void gemm_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda, const float* b,
                  i64 ldb, float* c, i64 ldc, int mode, cudaStream_t st, bool relu,
-                 const RowMap* map) {
+                 const RowMap* map, const float* mask, i64 ldm) {
   if (m == 0 || n == 0) return;
+  check(!mask || (!relu && !map), "gemm: a mask epilogue goes without relu / mapped rows");
+  if (mask && k > 0 && mode == PK_MODE_FAST &&
+      gemm_tc_launch(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, st, false, nullptr, mask, ldm))
+    return;
+  if (mask) {  // then the plain product and a separate relu_backward pass
+    gemm_launch(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, mode, st);
+    relu_backward_launch(mask, ldm, c, ldc, m, n, c, ldc, st);
+    return;
+  }
   if (map) {  // a reduction fused into the epilogue: tensor-core path only
     check(mode == PK_MODE_FAST && k > 0 &&
               gemm_tc_launch(ta, tb, m, n, k, a, lda, b, ldb, c, ldc, st, relu, map),

@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "elementwise.cuh"
 #include "gemm.cuh"
 #include "pk_common.cuh"
 
@@ -474,6 +475,8 @@ struct TcParams {
   i64 ldc;
   i64 split_stride; // elements between split partials
   int resident_ok = 0;  // weight-resident ring allowed (PK_TC_RESIDENT=1)
+  const float* mask = nullptr;  // relu_backward epilogue: keep where mask > 0
+  i64 ldm = 0;
   int relu;         // 1: the final value is stored as relu(v) (v > 0 ? v : 0)
   RowMap map;       // output row placement (g == 0: c + row * ldc)
 };
@@ -1063,13 +1066,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       // the L2 write requests of two 16-B stores; the epilogue is what bounds
       // the wide-N small-K tiles, PK_TC_PROF)
       const bool v8_out = PK_EPI_V8 && p.ldc % 8 == 0 && !p.map.g &&
-                          ((reinterpret_cast<uintptr_t>(out) & 31) == 0);
+                          ((reinterpret_cast<uintptr_t>(out) & 31) == 0) &&
+                          (!p.mask || (p.ldm % 8 == 0 &&
+                                       (reinterpret_cast<uintptr_t>(p.mask) & 31) == 0));
       // segments of one tile land in order: the first stores, later ones add
       // (fp32 round-to-nearest in registers, fixed order: deterministic); the
       // fused ReLU applies to the last segment's sum (never to split partials)
       for (int sg = 0; sg < nseg; ++sg) {
         const bool zero = nk == 0;
         const bool relu = p.relu && p.splits == 1 && sg == nseg - 1;
+        // relu_backward (kernels.hpp:103-111) of the finished sum
+        const bool masked = p.mask && p.splits == 1 && sg == nseg - 1;
         TC_PROF_WAIT(4, mbar_wait(&tfull[acc], acc_phase));
         tc_fence_after();
         const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) +
@@ -1114,6 +1121,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                   for (int i = 0; i < 8; ++i) w[i] = w[i] > 0.f ? w[i] : 0.f;
                 }
+                if (masked) {
+                  const float* m8 = p.mask + gm * p.ldm + n0 + c0 + 8 * j;
+                  float q[8];
+                  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                               : "=f"(q[0]), "=f"(q[1]), "=f"(q[2]), "=f"(q[3]), "=f"(q[4]),
+                                 "=f"(q[5]), "=f"(q[6]), "=f"(q[7])
+                               : "l"(m8));
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) w[i] = q[i] > 0.f ? w[i] : 0.f;
+                }
                 asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(d8),
                              "f"(w[0]), "f"(w[1]), "f"(w[2]), "f"(w[3]), "f"(w[4]), "f"(w[5]),
                              "f"(w[6]), "f"(w[7])
@@ -1135,6 +1152,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
                 for (int i = 0; i < CH; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
               }
+              if (masked) {
+                const float* mr = p.mask + gm * p.ldm + n0 + c0;
+#pragma unroll
+                for (int i = 0; i < CH; ++i) v[i] = __ldg(mr + i) > 0.f ? v[i] : 0.f;
+              }
 #pragma unroll
               for (int j = 0; j < CH / 4; ++j)
                 d4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -1143,7 +1165,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               for (int i = 0; i < CH; ++i)
                 if (i < left) {
                   const float x = sg > 0 ? dst[i] + v[i] : v[i];
-                  dst[i] = relu ? (x > 0.f ? x : 0.f) : x;
+                  const float y = relu ? (x > 0.f ? x : 0.f) : x;
+                  dst[i] = masked && !(__ldg(p.mask + gm * p.ldm + n0 + c0 + i) > 0.f) ? 0.f : y;
                 }
             }
           }
@@ -1407,9 +1430,11 @@ bool aligned16(const void* p, i64 ld) {
 
 bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 lda,
                     const float* b, i64 ldb, float* c, i64 ldc, cudaStream_t st, bool relu,
-                    const RowMap* map) {
+                    const RowMap* map, const float* mask, i64 ldm) {
   if (ta && tb) return false;  // not used by the layer
   TcParams p{};
+  p.mask = mask;
+  p.ldm = ldm;
   if (map) {
     p.map = *map;
     c = map->base[0];  // alignment of the slots (all 16-B aligned)
@@ -1473,6 +1498,7 @@ bool gemm_tc_launch(bool ta, bool tb, i64 m, i64 n, i64 k, const float* a, i64 l
     tc_split_reduce_kernel<<<ceil_div(m * n, 256), 256, 0, st>>>(part.p, splits, m, n, p.ldc,
                                                                  p.split_stride, c, ldc, p.relu);
     PK_LAUNCH("gemm tcgen05 split reduce");
+    if (mask) relu_backward_launch(mask, ldm, c, ldc, m, n, c, ldc, st);
   }
   return true;
 }
