@@ -161,6 +161,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// shared -> global tensor store (bulk async group); the box lands clipped
+// to the tensor's bounds
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<u64>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
+
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -477,6 +488,7 @@ struct TcParams {
   int resident_ok = 0;  // weight-resident ring allowed (PK_TC_RESIDENT=1)
   const float* mask = nullptr;  // relu_backward epilogue: keep where mask > 0
   i64 ldm = 0;
+  int tma_store = 0;  // ring kernel: the epilogue stores 32 x 32 boxes by TMA
   int relu;         // 1: the final value is stored as relu(v) (v > 0 ? v : 0)
   RowMap map;       // output row placement (g == 0: c + row * ldc)
 };
@@ -502,9 +514,12 @@ struct TcConfig {
   static constexpr int kRB = BN <= 64 ? PK_TC_RB_NARROW : PK_TC_RB;
   static constexpr int kRL = 2;                 // converted lo tiles
   static constexpr int kRingBudget = 224 * 1024;
-  static constexpr int kRA = std::min(8, (kRingBudget - kRB * 2 * kTileB - kRL * kTileA) / kTileA);
-  static constexpr size_t kSmemRing =
-      static_cast<size_t>(kRA + kRL) * kTileA + static_cast<size_t>(kRB) * 2 * kTileB + 1024;
+  // epilogue staging for the TMA stores: one 32 x 32 fp32 box per epilogue warp
+  static constexpr int kStgBytes = 4 * 4096;
+  static constexpr int kRA =
+      std::min(8, (kRingBudget - kStgBytes - kRB * 2 * kTileB - kRL * kTileA) / kTileA);
+  static constexpr size_t kSmemRing = static_cast<size_t>(kRA + kRL) * kTileA +
+                                      static_cast<size_t>(kRB) * 2 * kTileB + kStgBytes + 1024;
   // CTA-pair rings: each CTA keeps half of every weight image (its N/2 rows)
   static constexpr int kRAPair = std::min(8, (kRingBudget - kRB * kTileB - kRL * kTileA) / kTileA);
   static constexpr size_t kSmemPair =
@@ -534,7 +549,8 @@ struct TcConfig {
 template <bool A_T, bool B_T, int BN, int STAGES, bool B_PRE, bool TMA, int CS, bool PAIR = false>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     gemm_tc_kernel(TcParams p, const __grid_constant__ CUtensorMap tma_a,
-                   const __grid_constant__ CUtensorMap tma_b) {
+                   const __grid_constant__ CUtensorMap tma_b,
+                   const __grid_constant__ CUtensorMap tma_c) {
   using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
   static_assert(!TMA || B_PRE || B_T, "TMA path: a streamed B must be MN-major");
   static_assert(CS == 1 || (TMA && B_PRE), "clusters need the TMA + weight-image path");
@@ -1081,6 +1097,54 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         tc_fence_after();
         const unsigned taddr = tmem + (static_cast<unsigned>(quad * 32) << 16) +
                                static_cast<unsigned>(acc * Cfg::kAccStride);
+        if constexpr (kRing && !PAIR) {
+          // TMA-store epilogue (one k segment, no split, no row map): each
+          // warp stages its 32 rows x 32 columns in shared memory (128-B
+          // swizzle: conflict-free row writes) and one lane stores the box —
+          // full 128-B lines instead of a 32-B piece per thread per row
+          if (p.tma_store && nseg == 1) {
+            unsigned char* stgp = rb_slot(kRB) + quad * 4096;
+            const unsigned stg = smem_u32(stgp);
+            const i64 mrow0 = static_cast<i64>(mt) * kBM + quad * 32;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+              float v[32];
+              tmem_ld32(taddr + static_cast<unsigned>(c0), v);
+              if (relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+              }
+              if (masked && gm < p.m) {
+                const float* mr = p.mask + gm * p.ldm + n0 + c0;
+                const i64 left = p.n - (n0 + c0);
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i < left && !(__ldg(mr + i) > 0.f)) v[i] = 0.f;
+              }
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                 stg + static_cast<unsigned>(lane) * 128u +
+                                 (static_cast<unsigned>(j ^ (lane & 7)) << 4)),
+                             "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]),
+                             "f"(v[4 * j + 3])
+                             : "memory");
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&tma_c, stgp, static_cast<int>(n0 + c0), static_cast<int>(mrow0));
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) acc = 0, acc_phase ^= 1u;
+            continue;
+          }
+        }
         // CH columns per step: one TMEM load and, for a later segment, all
         // CH/4 old-value loads in flight together (RMW latency once per step)
 #ifndef PK_EPI_CH
@@ -1182,6 +1246,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (++acc == 2) acc = 0, acc_phase ^= 1u;
       }
     }
+    // the TMA stores have read their staging (and landed) before the CTA
+    // releases its shared memory
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
 
   tc_fence_before();
@@ -1281,6 +1348,20 @@ bool make_map(CUtensorMap* map, const float* base, i64 rows, i64 cols, i64 ld, i
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the output for the TMA-store epilogue: {n, m}, box {32 cols, 32 rows},
+// 128-B swizzle (the staging layout)
+bool make_c_map(CUtensorMap* map, float* base, i64 rows, i64 cols, i64 ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
+  const cuuint32_t box[2] = {32u, 32u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool tma_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PK_TC_TMA");
@@ -1296,9 +1377,10 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
   using Cfg = TcConfig<A_T, B_T, BN, STAGES, B_PRE>;
   // TMA maps: K-major A {k, m} box {32, 128}; MN-major A {m, k} / B {n, k}
   // box {32, 32} per 32-wide atom. Needs 16-B aligned bases and ld % 4 == 0.
-  CUtensorMap map_a, map_b;
+  CUtensorMap map_a, map_b, map_c;
   std::memset(&map_a, 0, sizeof(map_a));
   std::memset(&map_b, 0, sizeof(map_b));
+  std::memset(&map_c, 0, sizeof(map_c));
   bool tma = tma_enabled() && p0.a.vec && (B_PRE || p0.b.vec);
   if (tma)
     tma = A_T ? make_map(&map_a, p0.a.p, p0.k, p0.a.mn, p0.a.ld, 32, true)
@@ -1324,7 +1406,7 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
   const bool pair = B_PRE && !A_T && BN % 32 == 0 && tma && pair_pref && cs == 1 &&
                     p0.n_tiles == 1 && p0.splits == 1 && p0.m_tiles >= 4;
   if (pair) cs = 2;
-  using KernelT = void (*)(TcParams, const CUtensorMap, const CUtensorMap);
+  using KernelT = void (*)(TcParams, const CUtensorMap, const CUtensorMap, const CUtensorMap);
   KernelT kernel;
   int variant;
   if (!tma) {
@@ -1358,6 +1440,18 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     attr[variant] = true;
   }
   TcParams p = p0;
+  // TMA-store epilogue (PK_TC_TMA_STORE, default on): the single-CTA ring
+  // kernel, one k segment, no split / row map, output boxes that stay inside
+  // the tile (one n tile, or 32-multiple tile widths), 16-B aligned rows
+  static const bool tma_store_pref = [] {
+    const char* e = std::getenv("PK_TC_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  p.tma_store = 0;
+  if (tma_store_pref && B_PRE && !A_T && variant == 1 && p.splits == 1 && !p.map.g &&
+      p.k <= static_cast<i64>(kSegStages) * kBK && (p.n_tiles == 1 || BN % 32 == 0) &&
+      p.ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(p.c) & 15) == 0)
+    p.tma_store = make_c_map(&map_c, p.c, p.m, p.n, p.ldc) ? 1 : 0;
   // measured neutral (C2: NN 2M x 47 x 256 1.05 vs 1.07 ms, NT 2M x 256 x 47
   // 0.88 vs 0.86; epoch within noise): opt-in
   static const int resident_ok = [] {
@@ -1394,9 +1488,9 @@ void launch_bn(const TcParams& p0, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    PK_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, map_a, map_b));
+    PK_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, map_a, map_b, map_c));
   } else {
-    kernel<<<grid, kThreadsTc, smem, st>>>(p, map_a, map_b);
+    kernel<<<grid, kThreadsTc, smem, st>>>(p, map_a, map_b, map_c);
   }
   PK_LAUNCH("gemm tcgen05 kernel");
 }
