@@ -92,7 +92,7 @@ _capi.register(_SIGS)
 
 def _d2h_threads():
     v = os.environ.get("PK_D2H_THREADS")
-    return max(1, int(v)) if v else 8
+    return max(1, int(v)) if v else 1
 
 
 @dataclass
@@ -365,9 +365,9 @@ class RankEngine:
         jobs = []
         for (which, l, _, _), h in zip(self._result_shapes(), self._result_bufs):
             d = self.tensor(which, l)
-            # a copy into pageable memory runs at one host thread's memcpy
-            # rate (~13 GB/s): the big F0 shard goes as row chunks, each on
-            # its own thread and stream (PK_D2H_THREADS)
+            # PK_D2H_THREADS=N copies the big F0 shard as N row chunks, each
+            # on its own thread and stream; measured slower than one copy
+            # (C2: 86.8 vs 67.6 ms for 8 threads), so 1 by default
             n = _d2h_threads() if h.numel() * 4 >= (64 << 20) else 1
             rows = h.shape[0]
             for i in range(n):
