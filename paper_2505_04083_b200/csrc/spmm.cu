@@ -1334,6 +1334,14 @@ void spmm_run(SpmmPlan& plan, const pk_csr& a, i64 r0, i64 r1, const float* x, i
   // the mask is read with y's vector width: it must share y's alignment
   int vec = pick_vec(x, ldx, y, ldy, d, plan.segment || rg.hubs == 0);
   while (vec > max_vec) vec /= 2;
+  // experiment knob: the gather width of mid-width rows (64 < d < 256, e.g.
+  // C2's D = 100), PK_SPMM_MID_VEC = 1 | 2 | 4
+  static const int mid_vec = [] {
+    const char* e = std::getenv("PK_SPMM_MID_VEC");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (mid_vec > 0 && d > 64 && d < 256)
+    while (vec > mid_vec) vec /= 2;
   // the paired narrow form: FAST plans, no epilogue mask, at most 16 vectors
   // of up to 16 B per row
   int pair_vec = 0;
