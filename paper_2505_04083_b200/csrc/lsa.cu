@@ -83,6 +83,62 @@ __device__ void barrier(const LsaPeers& P, int b, unsigned epoch) {
 
 // out[r, c] = sum_j part_j[r, c] in ascending j, rows [r0, r1) of the
 // partial buffers (ld_p) -> out rows starting at out_r0 (ld_o)
+// VEC floats per thread per element group: 1, 4 (128-bit) or 8 (256-bit
+// loads and stores: half the NVLink read requests of 128-bit ones).
+template <int VEC>
+struct LsaVec {
+  float f[VEC];
+};
+template <int VEC>
+__device__ __forceinline__ LsaVec<VEC> lsa_ld(const float* p) {
+  LsaVec<VEC> r;
+  if constexpr (VEC == 8) {
+    asm volatile("ld.global.cg.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(r.f[0]), "=f"(r.f[1]), "=f"(r.f[2]), "=f"(r.f[3]), "=f"(r.f[4]),
+                   "=f"(r.f[5]), "=f"(r.f[6]), "=f"(r.f[7])
+                 : "l"(p));
+  } else if constexpr (VEC == 4) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+    r.f[0] = v.x, r.f[1] = v.y, r.f[2] = v.z, r.f[3] = v.w;
+  } else {
+    r.f[0] = __ldcg(p);
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ LsaVec<VEC> lsa_ld_plain(const float* p) {
+  LsaVec<VEC> r;
+  if constexpr (VEC == 8) {
+    asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(r.f[0]), "=f"(r.f[1]), "=f"(r.f[2]), "=f"(r.f[3]), "=f"(r.f[4]),
+                   "=f"(r.f[5]), "=f"(r.f[6]), "=f"(r.f[7])
+                 : "l"(p));
+  } else if constexpr (VEC == 4) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    r.f[0] = v.x, r.f[1] = v.y, r.f[2] = v.z, r.f[3] = v.w;
+  } else {
+    r.f[0] = *p;
+  }
+  return r;
+}
+template <int VEC>
+__device__ __forceinline__ void lsa_st(float* p, const LsaVec<VEC>& v) {
+  if constexpr (VEC == 8) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p),
+                 "f"(v.f[0]), "f"(v.f[1]), "f"(v.f[2]), "f"(v.f[3]), "f"(v.f[4]), "f"(v.f[5]),
+                 "f"(v.f[6]), "f"(v.f[7])
+                 : "memory");
+  } else if constexpr (VEC == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.f[0], v.f[1], v.f[2], v.f[3]);
+  } else {
+    *p = v.f[0];
+  }
+}
+
+#ifndef PK_LSA_UNROLL
+#define PK_LSA_UNROLL 4
+#endif
+
 template <int VEC, int G>
 __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64 r1, i64 cols,
                                                          i64 ld_p, float* __restrict__ out,
@@ -93,11 +149,11 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
   const i64 cv = cols / VEC;
   const i64 total = (r1 - r0) * cv;
   const i64 stride = static_cast<i64>(gridDim.x) * blockDim.x;
-  using V = typename std::conditional<VEC == 4, float4, float>::type;
+  using V = LsaVec<VEC>;
   // kUnroll grid-stride elements per pass, all members' loads issued before
   // the ordered adds: remote NVLink loads are latency-bound, so each thread
   // keeps kUnroll x g of them in flight
-  constexpr int kUnroll = 4;
+  constexpr int kUnroll = PK_LSA_UNROLL;
   for (i64 base = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; base < total;
        base += stride * kUnroll) {
     V x[kUnroll][G];
@@ -109,7 +165,7 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
       off[u] = i < total ? r * ld_p + c : -1;
 #pragma unroll
       for (int j = 0; j < G; ++j)
-        if (j < P.g && off[u] >= 0) x[u][j] = __ldcg(reinterpret_cast<const V*>(P.data[j] + off[u]));
+        if (j < P.g && off[u] >= 0) x[u][j] = lsa_ld<VEC>(P.data[j] + off[u]);
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
@@ -120,32 +176,20 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
 #pragma unroll
       for (int j = 1; j < G; ++j) {
         if (j >= P.g) break;
-        if constexpr (VEC == 4) {
-          acc.x = __fadd_rn(acc.x, x[u][j].x), acc.y = __fadd_rn(acc.y, x[u][j].y);
-          acc.z = __fadd_rn(acc.z, x[u][j].z), acc.w = __fadd_rn(acc.w, x[u][j].w);
-        } else {
-          acc = __fadd_rn(acc, x[u][j]);
-        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.f[e] = __fadd_rn(acc.f[e], x[u][j].f[e]);
       }
       if (relu) {  // fused relu_forward of the reduced Q (kernels.hpp:94-101)
-        if constexpr (VEC == 4) {
-          acc.x = acc.x > 0.f ? acc.x : 0.f, acc.y = acc.y > 0.f ? acc.y : 0.f;
-          acc.z = acc.z > 0.f ? acc.z : 0.f, acc.w = acc.w > 0.f ? acc.w : 0.f;
-        } else {
-          acc = acc > 0.f ? acc : 0.f;
-        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.f[e] = acc.f[e] > 0.f ? acc.f[e] : 0.f;
       }
       const i64 ro = r - r0 + out_r0;
       if (mask) {  // fused relu_backward: keep where relu(Q) > 0
-        const V m = *reinterpret_cast<const V*>(mask + ro * ldm + c);
-        if constexpr (VEC == 4) {
-          acc.x = m.x > 0.f ? acc.x : 0.f, acc.y = m.y > 0.f ? acc.y : 0.f;
-          acc.z = m.z > 0.f ? acc.z : 0.f, acc.w = m.w > 0.f ? acc.w : 0.f;
-        } else {
-          acc = m > 0.f ? acc : 0.f;
-        }
+        const V m = lsa_ld_plain<VEC>(mask + ro * ldm + c);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.f[e] = m.f[e] > 0.f ? acc.f[e] : 0.f;
       }
-      *reinterpret_cast<V*>(out + ro * ld_o + c) = acc;
+      lsa_st<VEC>(out + ro * ld_o + c, acc);
     }
   }
   barrier(P, blockIdx.x, epoch + 1);
@@ -445,7 +489,17 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   };
   using V4 = std::integral_constant<int, 4>;
   using V1 = std::integral_constant<int, 1>;
-  if (g_ <= 2) {
+  // 256-bit element groups for two-member groups (PK_LSA_VEC=8)
+  static const int vec_pref = [] {
+    const char* e = std::getenv("PK_LSA_VEC");
+    return e ? std::atoi(e) : 4;
+  }();
+  const bool v8 = vec_pref >= 8 && cols % 8 == 0 && ld_p % 8 == 0 && ld_o % 8 == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 31) == 0 &&
+                  (!mask || (ldm % 8 == 0 && (reinterpret_cast<uintptr_t>(mask) & 31) == 0));
+  if (g_ <= 2 && v8) {
+    launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{});
+  } else if (g_ <= 2) {
     if (v4) launch(V4{}, std::integral_constant<int, 2>{});
     else launch(V1{}, std::integral_constant<int, 2>{});
   } else if (g_ <= 4) {
