@@ -95,27 +95,10 @@ ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
        r0 += static_cast<i64>(gridDim.x) * kCeRows) {
     const int nr = static_cast<int>(rows - r0 < kCeRows ? rows - r0 : kCeRows);
     const int elems = nr * classes;
-    // coalesced stage-in: flat element e of the tile -> (row, class), eight
-    // loads in flight per thread before their shared-memory stores (one
-    // load per trip left each thread waiting out a DRAM latency per element)
-    for (int e0 = t; e0 < elems; e0 += 8 * kCeRows) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * kCeRows;
-        if (e < elems) {
-          const int rr = e / classes, c = e - rr * classes;
-          v[u] = __ldcs(logits + (r0 + rr) * ldl + c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + u * kCeRows;
-        if (e < elems) {
-          const int rr = e / classes, c = e - rr * classes;
-          tile[rr * stride + c] = v[u];
-        }
-      }
+    // coalesced stage-in: flat element e of the tile -> (row, class)
+    for (int e = t; e < elems; e += kCeRows) {
+      const int rr = e / classes, c = e - rr * classes;
+      tile[rr * stride + c] = __ldcs(logits + (r0 + rr) * ldl + c);
     }
     const i64 r = r0 + t;
     const bool live = t < nr;
