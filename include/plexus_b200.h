@@ -242,6 +242,18 @@ int pk_philox_permutation_host(uint64_t n, uint64_t seed, uint64_t stream,
 int pk_rmat_edges(int scale, uint64_t edges, double a, double b, double c,
                   uint64_t seed, uint32_t* edges_uv, uint64_t* kept_host,
                   void* stream);
+/* synth_sbm edge draw (graph.hpp:254-274) on the device: pair (u, v), u < v,
+ * in lexicographic order takes the next double of Philox(seed, 5) and is
+ * kept below p_in (same ceil-split community, graph.hpp:151-155) or p_out.
+ * The kept pairs come out in the reference's order as u32 [u, v] pairs.
+ * edges_uv == NULL: count only (*count_host = the edge count); otherwise the
+ * device buffer holds `capacity` pairs (2 * capacity u32). */
+int pk_sbm_edges(uint64_t n, int communities, double p_in, double p_out,
+                 uint64_t seed, uint32_t* edges_uv, uint64_t capacity,
+                 uint64_t* count_host, void* stream);
+/* synth_erdos (graph.hpp:276-289): the same walk with one probability */
+int pk_erdos_edges(uint64_t n, double p, uint64_t seed, uint32_t* edges_uv,
+                   uint64_t capacity, uint64_t* count_host, void* stream);
 /* features (graph.hpp:233-236): (float)next_double() of Philox(seed, 3) */
 int pk_rmat_features(uint64_t seed, int64_t n, int64_t d, float* out,
                      int64_t ldo, void* stream);

@@ -23,7 +23,7 @@ def lib():
             raise RuntimeError(f"reference oracle not built: {REF_LIB}")
         _lib = C.CDLL(REF_LIB)
         _lib.ref_last_error.restype = C.c_char_p
-        for name in ("ref_synth_rmat", "ref_synth_sbm", "ref_graph_from_arrays",
+        for name in ("ref_synth_rmat", "ref_synth_sbm", "ref_synth_erdos", "ref_graph_from_arrays",
                      "ref_normalize", "ref_csr_from_arrays", "ref_csr_transpose",
                      "ref_csr_block", "ref_permute_csr", "ref_preprocess",
                      "ref_pre_csr", "ref_pre_from_arrays", "ref_serial_create"):
@@ -34,6 +34,8 @@ def lib():
         _lib.ref_synth_sbm.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double,
                                        C.c_uint64, C.c_uint32, C.c_uint64, C.c_double,
                                        C.c_int]
+        _lib.ref_synth_erdos.argtypes = [C.c_uint64, C.c_double, C.c_uint64, C.c_uint32,
+                                         C.c_uint64, C.c_double, C.c_int]
         _lib.ref_balance_metric.restype = C.c_double
         _lib.ref_balance_metric.argtypes = [C.c_void_p, C.c_int, C.c_int]
         _lib.ref_predict_comm.restype = C.c_double
@@ -336,6 +338,10 @@ def synth_sbm(n, communities, p_in, p_out, feat, classes, seed, train_fraction=1
               f64=False):
     return Graph(lib().ref_synth_sbm(n, communities, p_in, p_out, feat, classes, seed,
                                      train_fraction, int(f64)), f64)
+
+
+def synth_erdos(n, p, feat, classes, seed, train_fraction=1.0, f64=False):
+    return Graph(lib().ref_synth_erdos(n, p, feat, classes, seed, train_fraction, int(f64)), f64)
 
 
 def graph_from_arrays(n, edges, features, labels, classes, mask, undirected=True):

@@ -143,6 +143,26 @@ void* ref_synth_sbm(u64 n, int communities, double p_in, double p_out, u64 feat,
   return g;
 }
 
+void* ref_synth_erdos(u64 n, double prob, u64 feat, u32 classes, u64 seed,
+                      double train_fraction, int f64) {
+  auto* g = new Graph;
+  g->f64 = f64;
+  int rc = guarded([&] {
+    ErdosParams p;
+    p.n = n;
+    p.p = prob;
+    if (f64)
+      g->d = synth_erdos<double>(p, feat, classes, seed, train_fraction);
+    else
+      g->f = synth_erdos<float>(p, feat, classes, seed, train_fraction);
+  });
+  if (rc) {
+    delete g;
+    return nullptr;
+  }
+  return g;
+}
+
 // Builds a dataset from caller arrays (edges as u,v pairs).
 void* ref_graph_from_arrays(u64 n, u64 num_edges, const u32* uv, int undirected,
                             const void* features, u64 feat, const u32* labels,

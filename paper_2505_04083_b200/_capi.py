@@ -129,6 +129,8 @@ SIGNATURES = {
     "pk_permutation_pair_host": (INT, [U64, U64, P, P]),
     "pk_philox_permutation_host": (INT, [U64, U64, U64, P]),
     "pk_rmat_edges": (INT, [INT, U64, DBL, DBL, DBL, U64, P, U64P, P]),
+    "pk_sbm_edges": (INT, [U64, INT, C.c_double, C.c_double, U64, P, U64, U64P, P]),
+    "pk_erdos_edges": (INT, [U64, C.c_double, U64, P, U64, U64P, P]),
     "pk_rmat_features": (INT, [U64, I64, I64, P, I64, P]),
     "pk_degree_quantile_labels": (INT, [P, U64, I64, U32, P, P]),
     "pk_gather_rows_f32": (INT, [P, I64, P, I64, I64, P, I64, P]),

@@ -56,6 +56,24 @@ def ensure_out_dir(d):
         raise CliError(EXIT_OUTPUT, f"output directory {d} is not writable")
 
 
+def make_synth(kind, p, feat_dim, classes, seed, train_fraction):
+    """make_synth_dataset (tools/main.cpp:70-93): sbm / erdos / rmat with the
+    reference's parameter names and defaults, generated on the GPU."""
+    from . import graph
+    if kind == "sbm":
+        return graph.synth_sbm(int(p.get("n", 1024)), int(p.get("k", 8)), p.get("p_in", 0.1),
+                               p.get("p_out", 0.01), feat_dim, classes, seed,
+                               train_fraction=train_fraction)
+    if kind == "erdos":
+        return graph.synth_erdos(int(p.get("n", 1024)), p.get("p", 0.01), feat_dim, classes,
+                                 seed, train_fraction=train_fraction)
+    if kind == "rmat":
+        return graph.synth_rmat(int(p.get("scale", 10)), int(p.get("edges", 0)), feat_dim,
+                                classes, seed, p.get("a", 0.57), p.get("b", 0.19),
+                                p.get("c", 0.19), train_fraction=train_fraction)
+    raise CliError(EXIT_INPUT, f"unknown synth kind '{kind}' (expected sbm, erdos or rmat)")
+
+
 def cmd_preprocess(a):
     import torch
 
@@ -66,11 +84,7 @@ def cmd_preprocess(a):
         raise CliError(EXIT_INPUT, "this build writes f32 shards (--precision f32)")
     if a.synth:
         kind, p = parse_synth(a.synth)
-        if kind != "rmat":
-            raise CliError(EXIT_INPUT, f"unknown synth kind '{kind}' (this build: rmat)")
-        ds = graph.synth_rmat(int(p.get("scale", 10)), int(p.get("edges", 0)), a.feat_dim,
-                              a.classes, a.seed, p.get("a", 0.57), p.get("b", 0.19),
-                              p.get("c", 0.19), train_fraction=a.train_fraction)
+        ds = make_synth(kind, p, a.feat_dim, a.classes, a.seed, a.train_fraction)
     else:
         ds = load_dataset_files(a)
     ensure_out_dir(a.out)
@@ -298,10 +312,7 @@ def cmd_validate(a):
         pre = shard_io.load_preprocessed(shard_io.load_manifest(a.manifest))
     elif a.synth:
         kind, p = parse_synth(a.synth)
-        if kind != "rmat":
-            raise CliError(EXIT_INPUT, f"unknown synth kind '{kind}' (this build: rmat)")
-        pre = graph.preprocess(graph.synth_rmat(int(p.get("scale", 10)), int(p.get("edges", 0)),
-                                                a.feat_dim, a.classes, a.seed), a.seed)
+        pre = graph.preprocess(make_synth(kind, p, a.feat_dim, a.classes, a.seed, 1.0), a.seed)
     else:
         raise CliError(EXIT_INPUT, "validate needs --manifest or --synth")
     opts = trainer.TrainOptions(hidden_dims=_ints(a.layers), epochs=a.epochs, lr=a.lr,

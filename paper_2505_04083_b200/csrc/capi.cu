@@ -390,6 +390,25 @@ int pk_rmat_edges(int scale, uint64_t edges, double a, double b, double c, uint6
   });
 }
 
+int pk_sbm_edges(uint64_t n, int communities, double p_in, double p_out, uint64_t seed,
+                 uint32_t* edges_uv, uint64_t capacity, uint64_t* count_host, void* stream) {
+  return guard([&] {
+    check(count_host != nullptr, "sbm: null count");
+    *count_host = pair_edges(n, communities, p_in, p_out, seed, edges_uv, capacity,
+                             as_stream(stream));
+  });
+}
+
+int pk_erdos_edges(uint64_t n, double p, uint64_t seed, uint32_t* edges_uv, uint64_t capacity,
+                   uint64_t* count_host, void* stream) {
+  return guard([&] {
+    check(count_host != nullptr, "erdos: null count");
+    check(n >= 1, "erdos: n must be >= 1");
+    check(p >= 0 && p <= 1, "erdos: probability must be in [0,1]");
+    *count_host = pair_edges(n, 1, p, p, seed, edges_uv, capacity, as_stream(stream));
+  });
+}
+
 int pk_rmat_features(uint64_t seed, int64_t n, int64_t d, float* out, int64_t ldo,
                      void* stream) {
   return guard([&] {

@@ -96,6 +96,49 @@ __global__ void assign_labels(const u64* sorted, i64 n, u32 classes, u32* labels
   }
 }
 
+// chunk_index (graph.hpp:151-155): which of `parts` ceil-split chunks of
+// [0, total) holds pos
+__device__ __forceinline__ int chunk_index_dev(u64 total, int parts, u64 pos) {
+  const u64 base = total / parts, rem = total % parts;
+  if (pos < rem * (base + 1)) return static_cast<int>(pos / (base + 1));
+  return static_cast<int>(rem + (pos - rem * (base + 1)) / (base > 0 ? base : 1));
+}
+
+// synth_sbm / synth_erdos (graph.hpp:254-289): pair (u, v), u < v, in
+// lexicographic order consumes u64 draw t(u, v) = sum_{i<u} (n - 1 - i) +
+// (v - u - 1) of Philox(seed, 5) and keeps the edge when the draw's unit
+// double falls below p_in (same community) or p_out. One warp per row u
+// walks v in 32-wide steps; a ballot orders the kept pairs, so the emitted
+// edge list is the reference's, in its order. COUNT pass first (per-row
+// counts -> exclusive scan), then EMIT.
+template <bool EMIT>
+__global__ void pair_rows_kernel(u64 n, int communities, double p_in, double p_out, u64 seed,
+                                 const u64* __restrict__ offsets, u64* __restrict__ counts,
+                                 u64* __restrict__ packed) {
+  const int lane = threadIdx.x % 32;
+  const u64 warps = static_cast<u64>(gridDim.x) * (blockDim.x / 32);
+  for (u64 u = blockIdx.x * static_cast<u64>(blockDim.x / 32) + threadIdx.x / 32; u < n;
+       u += warps) {
+    const u64 base = u * (n - 1) - u * (u - 1) / 2;  // draws of rows 0 .. u-1
+    const int cu = chunk_index_dev(n, communities, u);
+    u64 cnt = 0;
+    const u64 out0 = EMIT ? offsets[u] : 0;
+    for (u64 v0 = u + 1; v0 < n; v0 += 32) {
+      const u64 v = v0 + lane;
+      bool keep = false;
+      if (v < n) {
+        const double r = u64_to_unit(philox_u64_at(seed, 5, base + (v - u - 1)));
+        keep = r < (chunk_index_dev(n, communities, v) == cu ? p_in : p_out);
+      }
+      const unsigned ballot = __ballot_sync(0xffffffffu, keep);
+      if (EMIT && keep)
+        packed[out0 + cnt + __popc(ballot & ((1u << lane) - 1u))] = (v << 32) | u;
+      cnt += static_cast<u64>(__popc(ballot));
+    }
+    if (!EMIT && lane == 0) counts[u] = cnt;
+  }
+}
+
 template <typename F>
 void cub_call(F&& f, cudaStream_t st) {
   size_t bytes = 0;
@@ -128,6 +171,35 @@ u64 rmat_edges(int scale, u64 edges, double a, double b, double c, u64 seed, u32
   PK_CUDA(cudaMemcpyAsync(&kept, nsel.p, sizeof(i64), cudaMemcpyDeviceToHost, st));
   PK_CUDA(cudaStreamSynchronize(st));
   return static_cast<u64>(kept);
+}
+
+u64 pair_edges(u64 n, int communities, double p_in, double p_out, u64 seed, u32* uv,
+               u64 capacity, cudaStream_t st) {
+  check(n >= 1, "sbm: n must be >= 1");
+  check(communities >= 1 && static_cast<u64>(communities) <= n, "sbm: invalid community count");
+  check(p_in >= 0 && p_in <= 1 && p_out >= 0 && p_out <= 1,
+        "sbm: probabilities must be in [0,1]");
+  check(n < (1ull << 32), "sbm: node ids are u32");
+  DevBuf<u64> counts(n), offsets(n);
+  const unsigned grid = static_cast<unsigned>(std::max<u64>(1, std::min<u64>((n + 7) / 8, 1u << 20)));
+  pair_rows_kernel<false><<<grid, 256, 0, st>>>(n, communities, p_in, p_out, seed, nullptr,
+                                                 counts.p, nullptr);
+  PK_LAUNCH("pair edges count");
+  cub_call([&](void* t, size_t& bytes) {
+    return cub::DeviceScan::ExclusiveSum(t, bytes, counts.p, offsets.p, static_cast<i64>(n), st);
+  }, st);
+  u64 last[2] = {0, 0};
+  PK_CUDA(cudaMemcpyAsync(&last[0], offsets.p + (n - 1), sizeof(u64), cudaMemcpyDeviceToHost, st));
+  PK_CUDA(cudaMemcpyAsync(&last[1], counts.p + (n - 1), sizeof(u64), cudaMemcpyDeviceToHost, st));
+  PK_CUDA(cudaStreamSynchronize(st));
+  const u64 total = last[0] + last[1];
+  if (uv == nullptr) return total;
+  check(total <= capacity, "sbm: edge buffer too small (" + std::to_string(total) + " edges)");
+  pair_rows_kernel<true><<<grid, 256, 0, st>>>(n, communities, p_in, p_out, seed, offsets.p,
+                                                nullptr, reinterpret_cast<u64*>(uv));
+  PK_LAUNCH("pair edges emit");
+  PK_CUDA(cudaStreamSynchronize(st));
+  return total;
 }
 
 void rmat_features(u64 seed, i64 n, i64 d, float* out, i64 ldo, cudaStream_t st) {

@@ -19,6 +19,10 @@ void csr_hconcat(const pk_csr* pieces, const u64* col0, int count, u64 c0, u64 c
 
 u64 rmat_edges(int scale, u64 edges, double a, double b, double c, u64 seed, u32* uv,
                cudaStream_t st);
+// synth_sbm / synth_erdos edge lists (graph.hpp:254-289; Erdős = one
+// community): uv == nullptr counts only; returns the edge count
+u64 pair_edges(u64 n, int communities, double p_in, double p_out, u64 seed, u32* uv,
+               u64 capacity, cudaStream_t st);
 void rmat_features(u64 seed, i64 n, i64 d, float* out, i64 ldo, cudaStream_t st);
 void degree_quantile_labels(const u32* uv, u64 m, i64 n, u32 classes, u32* labels,
                             cudaStream_t st);

@@ -112,6 +112,48 @@ def synth_rmat(scale, edges, feat_dim, classes, seed, a=0.57, b=0.19, c=0.19,
     return GraphDataset(n, uv, feats, labels, classes, mask_t, True)
 
 
+def _assemble(n, uv, feat_dim, classes, seed, train_fraction, device):
+    """assemble_synth (graph.hpp:224-249) on the device: Philox(seed, 3)
+    features, degree-quantile labels, Philox(seed, 4) training mask."""
+    if classes < 1:
+        raise ContractError("synth: need at least one class")
+    feats = torch.empty((n, feat_dim), dtype=torch.float32, device=device)
+    call("pk_rmat_features", seed, n, feat_dim, _ptr(feats), feat_dim, _stream())
+    labels = torch.empty(n, dtype=torch.int32, device=device)
+    call("pk_degree_quantile_labels", _ptr(uv), uv.shape[0], n, classes, _ptr(labels),
+         _stream())
+    if train_fraction < 1.0:
+        mask_t = torch.from_numpy(_host_mask(seed, n, train_fraction)).to(device)
+    else:
+        mask_t = torch.ones(n, dtype=torch.uint8, device=device)
+    return GraphDataset(n, uv, feats, labels, classes, mask_t, True)
+
+
+def _pair_graph(fn, args, n, feat_dim, classes, seed, train_fraction, device):
+    if classes < 1:
+        raise ContractError("synth: need at least one class")
+    cnt = C.c_uint64()
+    call(fn, *args, seed, None, 0, C.byref(cnt), _stream())
+    uv = torch.empty((max(cnt.value, 1), 2), dtype=torch.int32, device=device)
+    call(fn, *args, seed, _ptr(uv), cnt.value, C.byref(cnt), _stream())
+    return _assemble(n, uv[:cnt.value], feat_dim, classes, seed, train_fraction, device)
+
+
+def synth_sbm(n, communities, p_in, p_out, feat_dim, classes, seed, train_fraction=1.0,
+              device="cuda") -> GraphDataset:
+    """synth_sbm (graph.hpp:254-274) + assemble_synth on the GPU: bit-exact
+    with the reference (edge order included)."""
+    return _pair_graph("pk_sbm_edges", (n, communities, p_in, p_out), n, feat_dim, classes,
+                       seed, train_fraction, device)
+
+
+def synth_erdos(n, p, feat_dim, classes, seed, train_fraction=1.0,
+                device="cuda") -> GraphDataset:
+    """synth_erdos (graph.hpp:276-289) + assemble_synth on the GPU."""
+    return _pair_graph("pk_erdos_edges", (n, p), n, feat_dim, classes, seed, train_fraction,
+                       device)
+
+
 def _host_mask(seed, n, frac):
     # Philox(seed, 4).next_double() < frac per node; never empty.
     from .philox import philox_doubles

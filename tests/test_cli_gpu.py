@@ -48,3 +48,27 @@ def test_preprocess_then_train(cuda, tmp_path):
         hidden=(16, 16), seed=0).train(3)
     got = [float(r.split(",")[2]) for r in rows[1:] if r.split(",")[1] == "global"]
     assert np.allclose(got, want, rtol=1e-5), (got, want)
+
+
+@pytest.mark.parametrize("spec,want", [
+    ("sbm:n=600,k=4,p_in=0.2,p_out=0.01", lambda: ref.synth_sbm(600, 4, 0.2, 0.01, 9, 5, 4,
+                                                                 train_fraction=0.8)),
+    ("erdos:n=500,p=0.02", lambda: ref.synth_erdos(500, 0.02, 9, 5, 4, train_fraction=0.8)),
+])
+def test_preprocess_sbm_erdos_shards_match_reference(cuda, tmp_path, spec, want):
+    """tools/main.cpp:70-93 synth kinds: the shard set of an SBM / Erdős
+    dataset is byte-identical to the reference's write_shards."""
+    shards, theirs = str(tmp_path / "shards"), str(tmp_path / "theirs")
+    rc, out, err = _cli("preprocess", "--synth", spec, "--feat-dim", "9", "--classes", "5",
+                        "--train-fraction", "0.8", "--p", "2", "--q", "3", "--seed", "4",
+                        "--out", shards, "--name", "pairs")
+    assert rc == 0, err
+    ref.write_shards(want().preprocess(4), 2, 3, theirs, "pairs")
+    for name in sorted(os.listdir(theirs)):
+        assert open(os.path.join(shards, name), "rb").read() == \
+            open(os.path.join(theirs, name), "rb").read(), name
+
+
+def test_preprocess_unknown_synth_kind(cuda, tmp_path):
+    rc, out, err = _cli("preprocess", "--synth", "kron:n=5", "--out", str(tmp_path / "x"))
+    assert rc != 0 and "expected sbm, erdos or rmat" in err

@@ -41,6 +41,46 @@ def test_synth_rmat_bitwise(cuda, scale, edges, a, b, c):
     assert np.array_equal(ds.labels.cpu().numpy().view(np.uint32), want["labels"])
 
 
+# the reference's own SBM / Erdős cases (test_graph.cpp:92, 189-231,
+# test_engine.cpp:16, test_trainer.cpp:15-17, 185, 229) plus a partial mask
+@pytest.mark.parametrize("kind,args,feat,classes,seed,frac", [
+    ("sbm", (4096, 8, 0.2, 0.001), 8, 4, 31, 1.0),
+    ("sbm", (128, 4, 0.2, 0.02), 16, 8, 23, 1.0),
+    ("sbm", (48, 4, 0.3, 0.02), 6, 3, 3, 0.7),
+    ("sbm", (1000, 2, 0.4, 0.1), 5, 3, 9, 1.0),
+    ("sbm", (300, 300, 0.9, 0.0), 2, 2, 4, 1.0),   # every node its own community
+    ("erdos", (50, 0.1), 4, 3, 21, 1.0),
+    ("erdos", (1000, 0.01), 4, 2, 7, 1.0),
+    ("erdos", (8, 0.4), 4, 3, 13, 1.0),
+    ("erdos", (1, 0.5), 2, 1, 1, 1.0),              # no pairs at all
+])
+def test_synth_sbm_erdos_bitwise(cuda, kind, args, feat, classes, seed, frac):
+    g = _g()
+    if kind == "sbm":
+        ds = g.synth_sbm(*args, feat, classes, seed, train_fraction=frac)
+        want = ref.synth_sbm(*args, feat, classes, seed, train_fraction=frac).arrays()
+    else:
+        ds = g.synth_erdos(*args, feat, classes, seed, train_fraction=frac)
+        want = ref.synth_erdos(*args, feat, classes, seed, train_fraction=frac).arrays()
+    assert np.array_equal(ds.edges.cpu().numpy().view(np.uint32).reshape(-1, 2),
+                          want["edges"].reshape(-1, 2))
+    assert np.array_equal(ds.features.cpu().numpy(), want["features"])
+    assert np.array_equal(ds.labels.cpu().numpy().view(np.uint32), want["labels"])
+    assert np.array_equal(ds.train_mask.cpu().numpy(), want["mask"])
+
+
+def test_synth_sbm_erdos_contract_errors(cuda):
+    """test_graph.cpp:230-231"""
+    g = _g()
+    from paper_2505_04083_b200._capi import ContractError
+    with pytest.raises(ContractError):
+        g.synth_erdos(0, 0.5, 2, 2, 1)
+    with pytest.raises(ContractError):
+        g.synth_sbm(10, 0, 0.5, 0.1, 2, 2, 1)
+    with pytest.raises(ContractError):
+        g.synth_sbm(10, 2, 1.5, 0.1, 2, 2, 1)
+
+
 def test_normalize_known_answers(cuda):
     """test_graph.cpp:57-82: K2 -> 0.5 everywhere; star center 1/sqrt(8)."""
     g = _g()
