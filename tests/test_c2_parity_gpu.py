@@ -162,14 +162,18 @@ def test_c2_fast_pass_within_tolerance(c2, ref_pass):
     got = _engine_pass(pre, tr.PK_MODE_FAST)
     # (c) hub segmentation at C2's real degrees: FAST plans cut rows of
     # >= 4096 nonzeros (the automatic threshold max(4096, 64 x mean) at a
-    # mean of 55.6) into 2048-nonzero segments; all other rows stay exact
+    # mean of 55.6) into 2048-nonzero segments; every chain uses fused
+    # multiply-adds, so regular rows differ from the reference by a rounding
+    # per nonzero at most
     rp = pre.a_even.row_ptr.cpu().numpy().astype(np.int64)
     deg = np.diff(rp)
     assert deg.max() >= 150_000, deg.max()
     hub = deg >= 4096
     assert hub.sum() > 0
     h0, w0 = got["h0"], ref_pass["h0"]
-    assert np.array_equal(h0[~hub].view(np.uint32), w0[~hub].view(np.uint32))
+    e_reg = nrel(h0[~hub], w0[~hub])
+    print(f"\nC2 FAST regular rows (fma chains) vs reference: {e_reg:.2e} (normwise)")
+    assert e_reg <= 1e-6, e_reg
     # a hub row's 2048-term segments summed in order differ from the
     # reference's single 155K-term chain by that chain's own rounding
     top = int(np.argmax(deg))
