@@ -1,7 +1,6 @@
 #!/bin/bash
 # One-GPU payload at HEAD: full GPU suite, smoke, the default bench line,
-# an e2e A/B of the threaded TrainResult download (PK_D2H_THREADS=1), and the
-# ncu launch list + traffic JSON (PK_COMMIT).
+# and the ncu launch list + traffic JSON (PK_COMMIT).
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -q -rA > gpurun_out/pytest_gpu_full.log 2>&1
@@ -12,12 +11,5 @@ python - <<'PY'
 import json
 d = json.loads([l for l in open("gpurun_out/bench_final.log") if l.startswith("{")][-1])
 print(d["value"], d["e2e"]["value"], d["phases_ms"], d["roofline"]["spmm_ms_per_epoch"], d["clocks"])
-PY
-PK_D2H_THREADS=1 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-c1-measured > gpurun_out/bench_d2h1.log 2>&1
-python - <<'PY'
-import json
-for f in ("gpurun_out/bench_final.log", "gpurun_out/bench_d2h1.log"):
-    d = json.loads([l for l in open(f) if l.startswith("{")][-1])
-    print(f, "e2e", round(d["e2e"]["value"], 2), {k: round(v, 1) for k, v in d["e2e"]["phases_ms"].items()})
 PY
 PK_COMMIT=${PK_COMMIT} bash scripts/ncu_r2.sh c2 > gpurun_out/ncu_r2.out 2>&1; echo "ncu rc=$?"; cat gpurun_out/ncu_spmm_c2.json
