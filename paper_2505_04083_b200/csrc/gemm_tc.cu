@@ -1117,9 +1117,24 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
               if (masked && gm < p.m) {
                 const float* mr = p.mask + gm * p.ldm + n0 + c0;
                 const i64 left = p.n - (n0 + c0);
+                if (left >= 32 && p.ldm % 8 == 0 &&
+                    (reinterpret_cast<uintptr_t>(p.mask) & 31) == 0) {
+                  // the row's 32 mask values as four 256-bit loads
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                  if (i < left && !(__ldg(mr + i) > 0.f)) v[i] = 0.f;
+                  for (int j = 0; j < 4; ++j) {
+                    float q[8];
+                    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                 : "=f"(q[0]), "=f"(q[1]), "=f"(q[2]), "=f"(q[3]), "=f"(q[4]),
+                                   "=f"(q[5]), "=f"(q[6]), "=f"(q[7])
+                                 : "l"(mr + 8 * j));
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[8 * j + i] = q[i] > 0.f ? v[8 * j + i] : 0.f;
+                  }
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i)
+                    if (i < left && !(__ldg(mr + i) > 0.f)) v[i] = 0.f;
+                }
               }
               if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
               __syncwarp();
