@@ -1173,13 +1173,13 @@ void Engine::backward_layer_tf(int l) {
     const i64 lddf = pad4(s.f_cols);
     // dF is complete here (no reduction follows), so layer l-1's relu'
     // (kernels.hpp:103-111, mask relu(Q_{l-1}) = this layer's F) can ride
-    // the GEMM epilogue instead of a separate pass over dF
-    // (PK_GEMM_RELU_BWD=1). Measured slower on C2 (52.0 vs 49.9 ms with the
-    // TMA-store epilogue, neutral before it): the epilogue is the bound of
-    // this 256-wide K = 48 GEMM, and the per-row mask reads load it further.
+    // the GEMM epilogue instead of a separate pass over dF (bit-identical;
+    // PK_GEMM_RELU_BWD=0: the separate pass). With the mask rows read as
+    // 256-bit loads in the TMA-store epilogue: C2 50.28 / 50.40 vs 50.38 /
+    // 50.55 ms (scalar mask loads were slower: 52.4 vs 50.5)
     static const bool fuse_mask = [] {
       const char* e = std::getenv("PK_GEMM_RELU_BWD");
-      return e && e[0] == '1';
+      return !(e && e[0] == '0');
     }();
     masked = fuse_mask;
     gemm_launch(false, true, s.f_rows, s.f_cols, s.w_cols, dp, ldp, wfull_[l].p(), wfull_[l].ld,

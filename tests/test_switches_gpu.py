@@ -38,7 +38,7 @@ def default(cuda, tmp_path_factory):
 
 
 @pytest.mark.parametrize("env", [{"PK_TC_TMA_STORE": "0"}, {"PK_TC_RESIDENT": "1"},
-                                 {"PK_GEMM_RELU_BWD": "1"}, {"PK_SPMM_MID_VEC": "2"}],
+                                 {"PK_GEMM_RELU_BWD": "0"}, {"PK_SPMM_MID_VEC": "2"}],
                          ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_data_movement_switch_bit_identical(default, tmp_path, env):
     got = _run(tmp_path, "sw", env)
