@@ -458,6 +458,12 @@ int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss_host,
                                double* accuracy_host);
 int pk_engine_optimizer_step(pk_engine* e);
 
+/* SerialTrainer::forward_only (trainer.hpp:126-135) on the engine: the
+ * forward of every layer with the current parameters — no loss, no
+ * gradients, no optimizer step — then the pass's error checks. The logits
+ * are this rank's last-layer output block (pk_engine_tensor PK_T_FOUT of the
+ * last layer; the full n x C matrix on a 1x1x1 grid). Collective. */
+int pk_engine_forward_only(pk_engine* e);
 /* rank_forward_backward one piece at a time (forward_layer, engine.hpp:
  * 158-206; backward_layer, engine.hpp:214-259): begin_pass; forward_layer
  * l = 0..L-1 (fault = EngineOptions.fault_skip_h_allreduce); loss (logits

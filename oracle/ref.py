@@ -311,6 +311,11 @@ class Serial(_Handle):
                     dw=split_weights(dw, d), df0=df0, spmm_flops=sf.value,
                     gemm_flops=gf.value)
 
+    def forward_only(self):
+        logits = np.empty((self.n, self.dims[-1]), _dt(self.f64))
+        _check(lib().ref_serial_forward_only(self.h, _p(logits)))
+        return logits
+
     def train(self, epochs):
         losses, accs = np.empty(epochs), np.empty(epochs)
         _check(lib().ref_serial_train(self.h, C.c_int(epochs), _p(losses), _p(accs)))

@@ -790,6 +790,18 @@ int ref_serial_forward_backward(void* h, int epoch, double* loss, double* acc,
 }
 
 // SerialTrainer::train; per-epoch loss and accuracy.
+// SerialTrainer::forward_only (trainer.hpp:126-135): logits (n x C) of the
+// current parameters, no loss, no gradients.
+int ref_serial_forward_only(void* h, void* logits) {
+  auto* s = static_cast<SerialHolder*>(h);
+  return guarded([&] {
+    if (s->f64)
+      dense_out(s->d->forward_only(), logits);
+    else
+      dense_out(s->f->forward_only(), logits);
+  });
+}
+
 int ref_serial_train(void* h, int epochs, double* losses, double* accs) {
   auto* s = static_cast<SerialHolder*>(h);
   return guarded([&] {

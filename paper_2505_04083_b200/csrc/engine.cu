@@ -778,15 +778,22 @@ void Engine::loss() {
 
 // finalize_loss (trainer.hpp:71-89) and the pass's error checks; the stream
 // has drained.
+// the checks every pass ends with (the stream has drained): a failed peer
+// (its ClusterAborted, not our partial sums), a timed-out peer reduction,
+// a device watchdog
+void Engine::check_after_pass() {
+  comms_.check_alive();
+  if (lsa_ready_ && grid_.size() > 1 && lsa_timed_out())
+    throw Error(PK_ERR_NCCL, "peer-memory reduction: a barrier wait timed out (peer stalled)");
+  check_device_watchdogs();
+}
+
 void Engine::finish_pass(int epoch, double* loss_out, double* acc_out, const double* slot) {
-  comms_.check_alive();  // a peer failed: its ClusterAborted, not our partial sums
+  check_after_pass();
   const i64 C = dims_[L_];
   const double* sums = slot ? slot : sums_host_;
   const u32 bad = *reinterpret_cast<const u32*>(sums + 3);
   check(!bad, "cross entropy: label out of range for " + std::to_string(C) + " classes");
-  if (lsa_ready_ && grid_.size() > 1 && lsa_timed_out())
-    throw Error(PK_ERR_NCCL, "peer-memory reduction: a barrier wait timed out (peer stalled)");
-  check_device_watchdogs();
   const double* h = sums;
   const u64 count = static_cast<u64>(h[1]), correct = static_cast<u64>(h[2]);
   if (count == 0 && comms_.solo()) {  // measurement mode: this rank holds no loss rows
@@ -1556,6 +1563,16 @@ int pk_engine_forward_backward(pk_engine* e, int epoch, double* loss, double* ac
     e->e->forward_backward(epoch);
     PK_CUDA(cudaStreamSynchronize(e->e->stream()));
     e->e->finish_pass(epoch, loss, acc);
+  });
+}
+
+int pk_engine_forward_only(pk_engine* e) {
+  return guard_rank(e, [&] {
+    e->e->reset_clock();
+    e->e->begin_pass();
+    for (int l = 0; l < e->e->num_layers(); ++l) e->e->layer_forward(l, false);
+    PK_CUDA(cudaStreamSynchronize(e->e->stream()));
+    e->e->check_after_pass();
   });
 }
 

@@ -90,6 +90,7 @@ class Engine {
   // After a stream sync: loss, accuracy, error checks of the last pass (or
   // of the pass whose sums went to `slot`).
   void finish_pass(int epoch, double* loss, double* acc, const double* slot = nullptr);
+  void check_after_pass();
   void train_epochs(int first, int count, pk_epoch_metrics* out);
   void optimizer_step();
   void train_epoch(int epoch, pk_epoch_metrics* m);

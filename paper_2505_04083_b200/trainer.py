@@ -78,6 +78,7 @@ _SIGS = {
                                              C.POINTER(C.c_double)]),
     "pk_engine_optimizer_step": (C.c_int, [C.c_void_p]),
     "pk_engine_train_epoch": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(pk_epoch_metrics)]),
+    "pk_engine_forward_only": (C.c_int, [C.c_void_p]),
     "pk_engine_train_epochs": (C.c_int, [C.c_void_p, C.c_int, C.c_int,
                                          C.POINTER(pk_epoch_metrics)]),
     "pk_engine_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(pk_tensor_view)]),
@@ -392,6 +393,13 @@ class RankEngine:
             with cf.ThreadPoolExecutor(max_workers=_d2h_threads()) as ex:
                 list(ex.map(run, jobs))
         return out
+
+    def forward_only(self):
+        """SerialTrainer::forward_only (trainer.hpp:126-135): the forward of
+        every layer with the current parameters, no loss / gradients /
+        optimizer step; returns this rank's logits block (device tensor)."""
+        call("pk_engine_forward_only", self.h)
+        return self.tensor(PK_T_FOUT)
 
     def stream_ptr(self):
         s = C.c_void_p()

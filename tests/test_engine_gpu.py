@@ -207,3 +207,24 @@ def test_train_epochs_batch_equals_single_epochs(cuda):
         assert torch.equal(a.tensor(tr.PK_T_W, l), b.tensor(tr.PK_T_W, l))
     a.close()
     b.close()
+
+
+def test_forward_only_matches_serial_trainer(cuda):
+    """SerialTrainer::forward_only (trainer.hpp:126-135): PARITY logits
+    bit-identical before training, parameters untouched by the call, and
+    after one epoch on both sides within the gradients' 1e-5."""
+    graph, tr = _mods()
+    pre = build(11, 20000, 12, 5, seed=4)
+    rpre = ref.synth_rmat(11, 20000, 12, 5, seed=4).preprocess(4)
+    serial = rpre.serial(hidden=(16, 16), seed=0)
+    opts = tr.TrainOptions(hidden_dims=[16, 16], mode=tr.PK_MODE_PARITY, hub_threshold=64)
+    eng = tr.RankEngine(pre.n, pre.feat_dim, pre.num_classes, tr.GridConfig(1, 1, 1), 0, opts)
+    eng.load(pre)
+    w0 = [eng.tensor(tr.PK_T_W, l).cpu().numpy().copy() for l in range(3)]
+    got = eng.forward_only().cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), serial.forward_only().view(np.uint32))
+    for l in range(3):
+        assert np.array_equal(eng.tensor(tr.PK_T_W, l).cpu().numpy(), w0[l])
+    eng.train_epoch(0)
+    serial.train(1)
+    assert nrel(eng.forward_only().cpu().numpy(), serial.forward_only()) <= 1e-5
