@@ -195,6 +195,116 @@ __global__ void __launch_bounds__(256) lsa_reduce_kernel(LsaPeers P, i64 r0, i64
   barrier(P, blockIdx.x, epoch + 1);
 }
 
+// Two-member all-pull with the peer's partial streamed by the TMA engine
+// (PK_LSA_BULK=1): each CTA walks blocks of whole rows (contiguous in the
+// scratch: rows x ld_p floats), one thread issues 1-D bulk copies of the
+// peer's block into a 4-stage shared-memory ring (mbarrier transaction
+// counts), and every thread adds its own partial (local loads) and the
+// staged peer values in coordinate order. The NVLink reads become a few
+// large transfers per CTA instead of one 16-B load per thread per element.
+// Same row -> CTA assignment on both members, same two barriers as
+// lsa_reduce_kernel, same sums bit for bit.
+constexpr int kBulkStages = 4;
+constexpr int kBulkBytes = 8192;  // per stage (static shared memory: 4 x 8 KB)
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ bool bulk_wait(unsigned long long* bar, unsigned parity,
+                                          const LsaPeers& P) {
+  const unsigned a = smem_addr(bar);
+  const unsigned long long t0 = globaltimer_ns();
+  for (unsigned spins = 0;; ++spins) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return true;
+    if ((spins & 255u) == 255u &&
+        (globaltimer_ns() - t0 > P.timeout_ns || (P.abort && *P.abort))) {
+      atomicExch(&g_lsa_timeout, 1u);
+      return false;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) lsa_reduce2_bulk_kernel(
+    LsaPeers P, i64 r0, i64 r1, i64 cols, i64 ld_p, float* __restrict__ out, i64 out_r0,
+    i64 ld_o, int relu, const float* __restrict__ mask, i64 ldm, unsigned epoch) {
+  __shared__ __align__(128) float stage[kBulkStages][kBulkBytes / 4];
+  __shared__ __align__(8) unsigned long long full[kBulkStages];
+  barrier(P, blockIdx.x, epoch);
+  const int peer = 1 - P.me;
+  const float* own = P.data[P.me];
+  const float* rem = P.data[peer];
+  const i64 rb = std::max<i64>(1, (kBulkBytes / 4) / ld_p);  // rows per block
+  const i64 nblk = (r1 - r0 + rb - 1) / rb;
+  // this CTA's blocks: blockIdx.x, + gridDim.x, ...
+  const i64 mine = blockIdx.x < nblk ? (nblk - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](i64 j) {  // j-th block of this CTA into stage j % S
+    const i64 b = blockIdx.x + j * gridDim.x;
+    const i64 a0 = r0 + b * rb, a1 = std::min<i64>(r1, a0 + rb);
+    const unsigned bytes = static_cast<unsigned>((a1 - a0) * ld_p * 4);
+    const int st = static_cast<int>(j % kBulkStages);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     smem_addr(&full[st])),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(stage[st])),
+        "l"(rem + a0 * ld_p), "r"(bytes), "r"(smem_addr(&full[st]))
+        : "memory");
+  };
+  if (threadIdx.x == 0)
+    for (i64 j = 0; j < std::min<i64>(mine, kBulkStages); ++j) issue(j);
+  __shared__ int s_ok;
+  for (i64 j = 0; j < mine; ++j) {
+    const int st = static_cast<int>(j % kBulkStages);
+    // thread 0 waits for the stage (bounded: a timeout / abort is flagged and
+    // the CTA stops reading); the block barrier hands the data to the rest
+    if (threadIdx.x == 0)
+      s_ok = bulk_wait(&full[st], static_cast<unsigned>((j / kBulkStages) & 1), P) ? 1 : 0;
+    __syncthreads();
+    if (!s_ok) break;
+    const i64 b = blockIdx.x + j * gridDim.x;
+    const i64 a0 = r0 + b * rb, a1 = std::min<i64>(r1, a0 + rb);
+    const i64 cv = cols / 4;
+    const i64 total = (a1 - a0) * cv;
+    for (i64 i = threadIdx.x; i < total; i += blockDim.x) {
+      const i64 rr = i / cv, c = (i % cv) * 4;
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(own + (a0 + rr) * ld_p + c));
+      const float4 y = *reinterpret_cast<const float4*>(&stage[st][rr * ld_p + c]);
+      const float4 s0 = P.me == 0 ? x : y, s1 = P.me == 0 ? y : x;  // coordinate order
+      float4 acc = make_float4(__fadd_rn(s0.x, s1.x), __fadd_rn(s0.y, s1.y),
+                               __fadd_rn(s0.z, s1.z), __fadd_rn(s0.w, s1.w));
+      if (relu) {
+        acc.x = acc.x > 0.f ? acc.x : 0.f, acc.y = acc.y > 0.f ? acc.y : 0.f;
+        acc.z = acc.z > 0.f ? acc.z : 0.f, acc.w = acc.w > 0.f ? acc.w : 0.f;
+      }
+      const i64 ro = a0 + rr - r0 + out_r0;
+      if (mask) {
+        const float4 m = *reinterpret_cast<const float4*>(mask + ro * ldm + c);
+        acc.x = m.x > 0.f ? acc.x : 0.f, acc.y = m.y > 0.f ? acc.y : 0.f;
+        acc.z = m.z > 0.f ? acc.z : 0.f, acc.w = m.w > 0.f ? acc.w : 0.f;
+      }
+      *reinterpret_cast<float4*>(out + ro * ld_o + c) = acc;
+    }
+    __syncthreads();  // the stage is free again
+    if (threadIdx.x == 0 && j + kBulkStages < mine) issue(j + kBulkStages);
+  }
+  barrier(P, blockIdx.x, epoch + 1);
+}
+
 // All-reduce at ring cost: 2 (g - 1) / g x M NVLink bytes per member instead
 // of the all-pull reduce's (g - 1) x M. Rows [r0, r1) are ceil-split over
 // the members; member i
@@ -497,7 +607,14 @@ void LsaGroup::reduce(i64 r0, i64 r1, i64 cols, i64 ld_p, float* out, i64 out_r0
   const bool v8 = vec_pref >= 8 && cols % 8 == 0 && ld_p % 8 == 0 && ld_o % 8 == 0 &&
                   (reinterpret_cast<uintptr_t>(out) & 31) == 0 &&
                   (!mask || (ldm % 8 == 0 && (reinterpret_cast<uintptr_t>(mask) & 31) == 0));
-  if (g_ <= 2 && v8) {
+  static const bool bulk_pref = [] {
+    const char* e = std::getenv("PK_LSA_BULK");
+    return e && e[0] == '1';
+  }();
+  if (g_ == 2 && bulk_pref && v4 && ld_p * 4 <= kBulkBytes && ld_p % 4 == 0) {
+    lsa_reduce2_bulk_kernel<<<ctas, 256, 0, st>>>(peers_, r0, r1, cols, ld_p, out, out_r0, ld_o,
+                                                  relu ? 1 : 0, mask, ldm, epoch);
+  } else if (g_ <= 2 && v8) {
     launch(std::integral_constant<int, 8>{}, std::integral_constant<int, 2>{});
   } else if (g_ <= 2) {
     if (v4) launch(V4{}, std::integral_constant<int, 2>{});
