@@ -164,80 +164,6 @@ ce_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
   }
 }
 
-// FAST form for up to 64 classes: a warp per row (lane j holds classes j and
-// j + 32) instead of a thread per row — the max / argmax (first index on
-// ties, exact) and the denominator are warp trees, so the denominator is
-// another association of the reference's ascending sum (tolerance-level,
-// like the expf / logf ulps the loss is already checked with); everything
-// else is the ce_kernel arithmetic. Deterministic.
-constexpr int kCeWarpRows = 8;  // warps (rows in flight) per CTA
-__global__ void __launch_bounds__(32 * kCeWarpRows)
-ce_warp_kernel(const float* __restrict__ logits, i64 ldl, i64 rows, int classes,
-               const u32* __restrict__ labels, const u8* __restrict__ mask,
-               float* __restrict__ dl, i64 ldd, int dc0, int dc1, double* __restrict__ partial,
-               u32* __restrict__ bad_label, u64 scale_count) {
-  constexpr unsigned kAll = 0xffffffffu;
-  const float s = scale_count ? __fdiv_rn(1.f, static_cast<float>(scale_count)) : 1.f;
-  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  double loss = 0, count = 0, correct = 0;
-  const int c0 = lane, c1 = lane + 32;
-  for (i64 r = static_cast<i64>(blockIdx.x) * kCeWarpRows + warp; r < rows;
-       r += static_cast<i64>(gridDim.x) * kCeWarpRows) {
-    const u8 m = mask[r];
-    const u32 lab = labels[r];
-    float* dr = dl + r * ldd;
-    if (!m || lab >= static_cast<u32>(classes)) {
-      if (m && lane == 0) atomicExch(bad_label, 1u);
-      for (int j = dc0 + lane; j < dc1; j += 32) dr[j - dc0] = 0.f;
-      continue;
-    }
-    const float* lr = logits + r * ldl;
-    const float x0 = c0 < classes ? __ldcs(lr + c0) : -INFINITY;
-    const float x1 = c1 < classes ? __ldcs(lr + c1) : -INFINITY;
-    float bv = x0;
-    int bi = c0;
-    if (x1 > bv) bv = x1, bi = c1;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(kAll, bv, o);
-      const int oi = __shfl_xor_sync(kAll, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
-    }
-    const float mx = bv;
-    const float xl = __shfl_sync(kAll, lab < 32 ? x0 : x1, static_cast<int>(lab % 32));
-    const float e0 = c0 < classes ? expf(x0 - mx) : 0.f;
-    const float e1 = c1 < classes ? expf(x1 - mx) : 0.f;
-    float den = __fadd_rn(e0, e1);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) den = __fadd_rn(den, __shfl_xor_sync(kAll, den, o));
-    if (lane == 0) {
-      loss += static_cast<double>(__fsub_rn(logf(den), __fsub_rn(xl, mx)));
-      count += 1;
-      if (bi == static_cast<int>(lab)) correct += 1;
-    }
-    const float rden = __frcp_rn(den);
-    auto put = [&](int c, float e) {
-      if (c < dc0 || c >= dc1) return;
-      float d = __fmul_rn(e, rden);
-      if (c == static_cast<int>(lab)) d = __fsub_rn(d, 1.f);
-      __stcs(dr + (c - dc0), scale_count ? __fmul_rn(d, s) : d);
-    };
-    put(c0, e0);
-    if (c1 < classes) put(c1, e1);
-  }
-  // fixed-order sums: the warps' lane-0 values in warp order
-  __shared__ double sh[kCeWarpRows][3];
-  if (lane == 0) sh[warp][0] = loss, sh[warp][1] = count, sh[warp][2] = correct;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0, b = 0, c = 0;
-    for (int w = 0; w < kCeWarpRows; ++w) a += sh[w][0], b += sh[w][1], c += sh[w][2];
-    partial[3 * blockIdx.x] = a;
-    partial[3 * blockIdx.x + 1] = b;
-    partial[3 * blockIdx.x + 2] = c;
-  }
-}
-
 // one CTA: thread t sums blocks t, t + 256, ... in order, then a fixed tree
 // (deterministic; the per-block partials were summed in a fixed order too)
 constexpr int kCeFinishThreads = 256;
@@ -345,28 +271,9 @@ void relu_backward_launch(const float* q, i64 ldq, const float* df, i64 lddf, i6
 
 void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
                     const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
-                    cudaStream_t st, u64 scale_count, i64 dc0, i64 dc1, bool fast) {
+                    cudaStream_t st, u64 scale_count, i64 dc0, i64 dc1) {
   if (dc1 < 0) dc1 = classes;
   check(0 <= dc0 && dc0 <= dc1 && dc1 <= classes, "cross entropy: bad class window");
-  if (fast && classes <= 64) {
-    const int blocks = static_cast<int>(
-        std::max<i64>(1, std::min<i64>(static_cast<i64>(sm_count()) * 8,
-                                       (rows + kCeWarpRows - 1) / kCeWarpRows)));
-    ws.partial.ensure(3 * static_cast<size_t>(blocks));
-    ws.bad.ensure(1);
-    PK_CUDA(cudaMemsetAsync(ws.bad.p, 0, sizeof(u32), st));
-    if (rows > 0 && classes > 0) {
-      ce_warp_kernel<<<blocks, 32 * kCeWarpRows, 0, st>>>(
-          logits, ldl, rows, static_cast<int>(classes), labels, mask, dl, ldd,
-          static_cast<int>(dc0), static_cast<int>(dc1), ws.partial.p, ws.bad.p, scale_count);
-      PK_LAUNCH("cross entropy (warp rows)");
-      ce_finish_kernel<<<1, kCeFinishThreads, 0, st>>>(ws.partial.p, blocks, sums);
-    } else {
-      PK_CUDA(cudaMemsetAsync(sums, 0, 3 * sizeof(double), st));
-    }
-    PK_LAUNCH("cross entropy finish");
-    return;
-  }
   const size_t smem = sizeof(float) * kCeRows * ce_stride(static_cast<int>(classes));
   check(classes <= kCeMaxClasses, "cross entropy: at most " + std::to_string(kCeMaxClasses) +
                                       " classes supported");

@@ -23,8 +23,7 @@ struct CeWorkspace {
 // dc1 < 0 = all classes.
 void ce_sums_launch(const float* logits, i64 ldl, i64 rows, i64 classes, const u32* labels,
                     const u8* mask, float* dl, i64 ldd, double* sums, CeWorkspace& ws,
-                    cudaStream_t st, u64 scale_count = 0, i64 dc0 = 0, i64 dc1 = -1,
-                    bool fast = false);
+                    cudaStream_t st, u64 scale_count = 0, i64 dc0 = 0, i64 dc1 = -1);
 void scale_by_count_launch(float* d, i64 ldd, i64 rows, i64 cols, const double* sums,
                            cudaStream_t st);
 

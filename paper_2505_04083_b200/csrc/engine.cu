@@ -763,15 +763,8 @@ void Engine::loss() {
   }
   clock_.begin(2, st_);
   const int gi = comms_.size(last.inner), pi = c_.along(last.inner);
-  // FAST: the warp-per-row form (tolerance-level denominator order;
-  // PK_CE_WARP=0 keeps the reference's sequential sum)
-  static const bool ce_warp = [] {
-    const char* e = std::getenv("PK_CE_WARP");
-    return !(e && e[0] == '0');
-  }();
   ce_sums_launch(logits, ldl, s.a_rows, C, labels_.p, mask_.p, dl_.p(), dl_.ld, sums_.p, ce_ws_,
-                 st_, mask_count_, chunk_start(C, gi, pi), chunk_start(C, gi, pi + 1),
-                 ce_warp && cfg_.mode == PK_MODE_FAST);
+                 st_, mask_count_, chunk_start(C, gi, pi), chunk_start(C, gi, pi + 1));
   clock_.end(st_);
   on_comm([&](cudaStream_t cs) { comms_.all_reduce_f64(sums_.p, 3, last.row, cs); });
   // no host wait here: the sums ride to pinned memory in stream order and
