@@ -30,6 +30,7 @@ def test_rank_configs_stats_matches_reference(capsys, tmp_path):
       "--machine", "/nonexistent.json"], 2),                     # missing machine file
     (["train", "--manifest", "/nonexistent"], 2),                # missing manifest
     (["preprocess", "--out", "/tmp/x"], 2),                      # neither --edges nor --synth
+    (["preprocess", "--synth", "kron:n=5", "--out", "/tmp/x"], 2),  # unknown synth kind
 ])
 def test_exit_codes(argv, code):
     assert cli.main(argv) == code
@@ -39,3 +40,10 @@ def test_parse_synth():
     assert cli.parse_synth("rmat:scale=9,edges=3000") == ("rmat", {"scale": 9.0, "edges": 3000.0})
     with pytest.raises(cli.CliError):
         cli.parse_synth("rmat:scale")
+
+
+def test_parse_synth_pair_kinds():
+    """tools/main.cpp:70-93 parameter names of the sbm / erdos kinds"""
+    assert cli.parse_synth("sbm:n=4096,k=8,p_in=0.2,p_out=0.001") == (
+        "sbm", {"n": 4096.0, "k": 8.0, "p_in": 0.2, "p_out": 0.001})
+    assert cli.parse_synth("erdos:n=50,p=0.1") == ("erdos", {"n": 50.0, "p": 0.1})
