@@ -88,6 +88,39 @@ def synth_rmat(scale, edges, feat, classes, seed, a=0.57, b=0.19, c=0.19,
                 mask=train_mask(seed, n, train_fraction))
 
 
+def chunk_index(total, parts, pos):
+    """graph.hpp:151-155 (ceil-split chunk holding pos), vectorised"""
+    base, rem = total // parts, total % parts
+    pos = np.asarray(pos, np.int64)
+    return np.where(pos < rem * (base + 1), pos // (base + 1),
+                    rem + (pos - rem * (base + 1)) // max(base, 1))
+
+
+def sbm_edges(n, communities, p_in, p_out, seed):
+    """synth_sbm / synth_erdos edge loop, graph.hpp:254-289: pairs (u, v),
+    u < v, in lexicographic order, one next_double() of Philox(seed, 5) each
+    (u64 >> 11 scaled by 2^-53), kept below p_in (same community) or p_out.
+    Small n only (all n(n-1)/2 draws are materialised)."""
+    u, v = np.triu_indices(n, k=1)
+    r = (philox_u64(seed, 5, u.size) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    same = chunk_index(n, communities, u) == chunk_index(n, communities, v)
+    keep = r < np.where(same, p_in, p_out)
+    return np.stack([u[keep], v[keep]], 1).astype(np.uint32)
+
+
+def synth_sbm(n, communities, p_in, p_out, feat, classes, seed, train_fraction=1.0):
+    """synth_sbm + assemble_synth, graph.hpp:224-274"""
+    uv = sbm_edges(n, communities, p_in, p_out, seed)
+    return dict(n=n, edges=uv, features=features(seed, n, feat),
+                labels=degree_quantile_labels(uv, n, classes), classes=classes,
+                mask=train_mask(seed, n, train_fraction))
+
+
+def synth_erdos(n, p, feat, classes, seed, train_fraction=1.0):
+    """synth_erdos + assemble_synth, graph.hpp:224-249, 276-289 (one community)"""
+    return synth_sbm(n, 1, p, p, feat, classes, seed, train_fraction)
+
+
 def normalize(n, edges, undirected=True):
     """normalize_adjacency, graph.hpp:40-76"""
     uv = np.ascontiguousarray(edges, np.uint32)

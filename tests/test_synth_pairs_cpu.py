@@ -1,8 +1,9 @@
-"""The pair-draw indexing the device SBM / Erdős generators use
-(csrc/rmat.cu pair_rows_kernel: pair (u, v), u < v, takes u64 draw
-t = sum_{i<u} (n - 1 - i) + (v - u - 1) of Philox(seed, 5)), restated in
-numpy and pinned to the compiled reference's synth_sbm / synth_erdos
-(graph.hpp:254-289) on CPU."""
+"""The SBM / Erdős restatement (oracle/restate.py sbm_edges / synth_sbm /
+synth_erdos, graph.hpp:254-289) and the closed-form pair-draw indexing the
+device generators use (csrc/rmat.cu pair_rows_kernel: pair (u, v), u < v,
+takes u64 draw t = sum_{i<u} (n - 1 - i) + (v - u - 1) of Philox(seed, 5)),
+pinned to the compiled reference's synth_sbm / synth_erdos on CPU —
+features, labels and mask included."""
 import numpy as np
 import pytest
 
@@ -38,3 +39,23 @@ def test_sbm_pair_indexing_matches_reference(n, c, pi, po, seed):
 def test_erdos_pair_indexing_matches_reference(n, p, seed):
     want = ref.synth_erdos(n, p, 2, 2, seed).arrays()["edges"]
     assert np.array_equal(pair_edges(n, 1, p, p, seed), want)
+
+
+@pytest.mark.parametrize("n,c,pi,po,seed,frac", [(300, 4, 0.2, 0.02, 31, 1.0),
+                                                 (48, 4, 0.3, 0.02, 3, 0.7)])
+def test_restated_synth_sbm_matches_reference(n, c, pi, po, seed, frac):
+    from oracle import restate
+    got = restate.synth_sbm(n, c, pi, po, 6, 3, seed, frac)
+    want = ref.synth_sbm(n, c, pi, po, 6, 3, seed, train_fraction=frac).arrays()
+    assert np.array_equal(got["edges"], want["edges"])
+    assert np.array_equal(got["features"], want["features"])
+    assert np.array_equal(got["labels"], want["labels"])
+    assert np.array_equal(got["mask"], want["mask"])
+
+
+def test_restated_synth_erdos_matches_reference():
+    from oracle import restate
+    got = restate.synth_erdos(200, 0.05, 4, 2, 7)
+    want = ref.synth_erdos(200, 0.05, 4, 2, 7).arrays()
+    assert np.array_equal(got["edges"], want["edges"])
+    assert np.array_equal(got["labels"], want["labels"])
